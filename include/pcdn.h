@@ -1,0 +1,179 @@
+/*
+ * pcdn.h -- C-ABI of the B200 (sm_100a) PCDN hot path.
+ *
+ * PCDN = Parallel Coordinate Descent Newton (Bian, Li, Liu, Yang, arXiv:1306.4080).
+ * Citations "PAPER.md:L" are lines of the paper's LaTeX source; "Zk" are the readings
+ * listed in DESIGN.md.  The problem solved is Eq.1:
+ *
+ *      min_w  F_c(w) = c * sum_{i<s} phi(y_i w'x_i) + ||w||_1
+ *      phi_log(m) = log(1 + e^{-m})      (Eq.2)       loss = PCDN_LOSS_LOGISTIC
+ *      phi_svm(m) = max(0, 1 - m)^2      (Eq.3)       loss = PCDN_LOSS_L2SVM
+ *
+ * Letters follow the paper: s samples, n features, P bundle size.
+ *
+ * Conventions for every call:
+ *  - Array arguments are DEVICE pointers unless marked (host).  They are borrowed: the caller
+ *    (e.g. torch) owns them and keeps them alive and unmodified while the context exists.
+ *  - The library allocates no device memory except in pcdn_train_host(); state and scratch
+ *    live in the caller's workspace (pcdn_workspace_bytes).
+ *  - Every call is stream-ordered on the context's CUDA stream.  Calls that return host
+ *    values (info structs, F_out, status after device checks) synchronize that stream.
+ *  - Return value: a PCDN_* status code.  On failure pcdn_last_error() describes the cause;
+ *    the context stays usable after PCDN_ERR_INVALID, not after PCDN_ERR_CUDA.
+ *  - A context is not thread-safe; use one per stream.
+ */
+#ifndef PCDN_H
+#define PCDN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (mirroring SPEC.md:473, 503 exit codes 0/1/2/3). */
+#define PCDN_OK 0            /* success; for pcdn_solve: stop test met (Eq.14 gap <= eps)   */
+#define PCDN_ERR_INVALID 1   /* argument or data-invariant violation                         */
+#define PCDN_BUDGET 2        /* pcdn_solve: max_outer outer iterations done, gap > eps       */
+#define PCDN_ERR_NUMERIC 3   /* non-finite objective / direction (reading Z10)               */
+#define PCDN_ERR_CUDA 4      /* CUDA runtime error (the context must be destroyed)           */
+#define PCDN_ERR_NOMEM 5     /* workspace too small / host allocation failed                 */
+
+#define PCDN_LOSS_LOGISTIC 0 /* Eq.2 */
+#define PCDN_LOSS_L2SVM 1    /* Eq.3, generalized Hessian App. A.2        */
+
+typedef struct pcdn_ctx pcdn_ctx;
+
+/* Result of one bundle step (Alg.3 lines 6-10). */
+typedef struct {
+    int32_t q;           /* accepted Armijo index, alpha = beta^q (Eq.6); -1 = null step (Z10) */
+    int32_t reserved;
+    double alpha;        /* accepted step size (0 for a null step)                            */
+    double Delta;        /* Eq.7 restricted to the bundle             */
+    double lhs;          /* F(w + alpha d) - F(w) from retained quantities (Eq.12)            */
+    double rhs;          /* sigma * alpha * Delta                                              */
+    double F;            /* maintained objective after the step (reading Z23)                 */
+    int64_t bundle_nnz;  /* sum over the bundle's columns of their nonzero counts             */
+    int64_t n_touched;   /* |T|: samples with a nonzero in a column with d_j != 0 (Z8)        */
+} pcdn_step_info;
+
+/* Result of pcdn_solve (Alg.3 outer loop + Eq.14 stop test). */
+typedef struct {
+    int32_t status;           /* PCDN_OK / PCDN_BUDGET / error code                           */
+    int32_t outer_iters;      /* outer iterations k completed                                 */
+    int64_t steps;            /* bundle steps (inner iterations t) completed                  */
+    int64_t null_steps;       /* steps whose line search was exhausted (Z10)                  */
+    int64_t nnz_processed;    /* sum over steps of bundle_nnz                                 */
+    int64_t touched_total;    /* sum over steps of |T|                                        */
+    int64_t positions;        /* sum over steps of the bundle size                           */
+    int64_t kernel_launches;  /* CUDA kernels launched by this call                           */
+    double F;                 /* F_c(w) recomputed from (z, w) at the last outer boundary     */
+    double gap;               /* (F - F*)/F* (Eq.14), NaN without a reference                 */
+    double t_wall_ms;         /* host wall time of the call                                   */
+    double t_step_kernel_ms;  /* CUDA-event time of the bundle-step kernels (sum)             */
+    double t_gpu_ms;          /* CUDA-event time from first to last kernel of the call        */
+    double alg_bytes;         /* algorithmic bytes of the bundle steps  */
+} pcdn_solve_info;
+
+/* Bytes of device workspace a context for an s x n matrix with nnz nonzeros needs
+ * (alignment included).  Pure host function. */
+size_t pcdn_workspace_bytes(int64_t s, int64_t n, int64_t nnz);
+
+/* Create a context.  Inputs (all device, borrowed):
+ *   csc_col_ptr[n+1] (int64, col_ptr[0]=0, col_ptr[n]=nnz, nondecreasing),
+ *   csc_row_idx[nnz] (int32, strictly increasing inside each column, < s),
+ *   csc_val[nnz] (fp32, finite) -- column x^j of X;
+ *   csr_row_ptr[s+1], csr_col_idx[nnz], csr_val[nnz] -- the same nonzeros by row;
+ *   y[s] (int8 in {-1,+1}); c > 0 (Eq.1); loss = PCDN_LOSS_*.
+ *   workspace: device buffer of >= pcdn_workspace_bytes(s,n,nnz) bytes, 256-byte aligned.
+ *   cuda_stream: cudaStream_t (NULL = legacy default stream).
+ * Validates every invariant above on the device (PCDN_ERR_INVALID names the first offending
+ * index), then sets w = 0, z = Xw = 0, F = F_c(0).  Synchronizes. */
+int pcdn_create(int64_t s, int64_t n, int64_t nnz,
+                const int64_t *csc_col_ptr, const int32_t *csc_row_idx, const float *csc_val,
+                const int64_t *csr_row_ptr, const int32_t *csr_col_idx, const float *csr_val,
+                const int8_t *y, double c, int loss,
+                void *workspace, size_t workspace_bytes, void *cuda_stream, pcdn_ctx **out);
+
+/* Armijo constants (Eq.6-7).  Defaults sigma=0.01, beta=0.5, gamma=0,
+ * q_max=50 (Z10).  Requires 0<sigma<1, 0<beta<1, 0<=gamma<1, 0<=q_max<=200. */
+int pcdn_set_armijo(pcdn_ctx *ctx, double sigma, double beta, double gamma, int q_max);
+
+/* F* for the Eq.14 stop test (reading Z12).  Must be finite and > 0. */
+int pcdn_set_reference(pcdn_ctx *ctx, double f_star);
+
+/* One PCDN inner iteration on the given bundle (Alg.3 l.6-10): a1 g/h (Eq.13, App.A.2),
+ * a2 d (Eq.5) and Delta (Eq.7), a3 d'x_i over T (Alg.4 l.1), a4 P-dim Armijo (Eq.6, Eq.12),
+ * a5 commit to w and the retained z (Alg.4 l.4-5).
+ *   bundle[P]: device, P distinct feature ids in [0,n) (checked on device -> PCDN_ERR_INVALID),
+ *              processed in this order (bundle position k = index in this array).
+ *   info: host, nullable.  g_out/h_out/d_out: device [P], nullable (g, h after the nu floor, d).
+ * Synchronizes when info != NULL. */
+int pcdn_bundle_step(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, pcdn_step_info *info,
+                     double *g_out, double *h_out, double *d_out);
+
+/* Touched set and d'x of the last pcdn_bundle_step taken with debug on (pcdn_set_debug).
+ * T_out (host, ascending sample ids) and dx_out (host) get min(|T|, capacity) entries;
+ * *nT (host) gets |T|.  Synchronizes. */
+int pcdn_last_touched(pcdn_ctx *ctx, int32_t *T_out, double *dx_out, int64_t capacity, int64_t *nT);
+
+/* Alg.3: from the current w, run outer iterations k = 0..max_outer-1.  Outer k draws the
+ * partition pi_k(seed, k) (Eq.8, reading Z2) and runs b = ceil(n/P) bundle steps on the
+ * device without host round trips; then F is recomputed from (z, w) (Z23) and, if eps > 0,
+ * the Eq.14 gap is tested (needs pcdn_set_reference).  eps <= 0 runs exactly max_outer.
+ * Returns PCDN_OK when the gap <= eps, PCDN_BUDGET after max_outer.  info: host, nullable. */
+int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_outer,
+               pcdn_solve_info *info);
+
+/* F_c(w) (Eq.1) into *F_out (host).  recompute_from_w != 0: recompute z = Xw (CSR, ascending
+ * column order) first; otherwise evaluate from the retained z.  Synchronizes. */
+int pcdn_objective(pcdn_ctx *ctx, int recompute_from_w, double *F_out);
+
+/* Copy w (device fp64[n]) out / in.  pcdn_set_w recomputes z = Xw and F (state injection). */
+int pcdn_get_w(pcdn_ctx *ctx, double *w_out);
+int pcdn_set_w(pcdn_ctx *ctx, const double *w);
+/* Copy the retained z = Xw (device fp64[s]). */
+int pcdn_get_z(pcdn_ctx *ctx, double *z_out);
+/* Back to w = 0, z = 0, F = F_c(0). */
+int pcdn_reset(pcdn_ctx *ctx);
+
+/* Device copy of the partition permutation pi_k (reading Z2) for outer iteration k:
+ * out[n] (device int32); bundle t = out[tP : min((t+1)P, n)]. */
+int pcdn_permutation(pcdn_ctx *ctx, uint64_t seed, int64_t k, int32_t *out);
+
+/* Optional per-step trace during pcdn_solve: q_trace[t], F_trace[t] (device, nullable) for the
+ * first `capacity` steps of each call. */
+int pcdn_set_trace(pcdn_ctx *ctx, int32_t *q_trace, double *F_trace, int64_t capacity);
+
+/* Debug mode records T and d'x of each step (for pcdn_last_touched). */
+int pcdn_set_debug(pcdn_ctx *ctx, int on);
+
+/* Tuning knobs (never change results beyond fp64 rounding order): number of CTAs of the
+ * persistent step kernel (0 = all co-resident) and the column length above which a column
+ * is split across warps/CTAs (default 128). */
+int pcdn_set_launch(pcdn_ctx *ctx, int ctas, int heavy_len);
+
+/* Human-readable description of the last error (never NULL). */
+const char *pcdn_last_error(const pcdn_ctx *ctx);
+
+/* Destroy the context (does not free caller memory). */
+void pcdn_destroy(pcdn_ctx *ctx);
+
+/* One-call host API: copies HOST arrays (pinned recommended) to the device, trains with
+ * pcdn_solve and copies w back to w_out (host fp64[n]).  Allocates and frees its own device
+ * memory (stream-ordered).  f_star <= 0 with eps > 0 is invalid.  info: host, nullable. */
+int pcdn_train_host(int64_t s, int64_t n, int64_t nnz,
+                    const int64_t *csc_col_ptr, const int32_t *csc_row_idx, const float *csc_val,
+                    const int64_t *csr_row_ptr, const int32_t *csr_col_idx, const float *csr_val,
+                    const int8_t *y, double c, int loss, int64_t P, double eps, double f_star,
+                    uint64_t seed, int32_t max_outer, void *cuda_stream, double *w_out,
+                    pcdn_solve_info *info);
+
+/* Library version string. */
+const char *pcdn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCDN_H */

@@ -1,0 +1,742 @@
+// pcdn_api.cu -- C-ABI of the B200 PCDN hot path (declared in include/pcdn.h).
+//
+// Host side only marshals arguments, carves the caller's workspace and enqueues the kernels
+// of pcdn_kernels.cuh on the context stream; every step of the path runs on the device.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/pcdn.h"
+#include "pcdn_kernels.cuh"
+
+using namespace pcdn;
+
+namespace {
+
+constexpr int GMAX = 1024;
+constexpr size_t ALIGN = 256;
+
+inline size_t align_up(size_t x) { return (x + ALIGN - 1) & ~(ALIGN - 1); }
+
+struct Layout {
+    size_t w, z, coef, cnt, bits, rec, dxg, tlist, order, flag, hpos, hlist, hlen, hstart, tiles1, tiles2,
+        seen, dk, deltak, gk, hk, part, hpart, counters, info, F, Fcopy, status, err_idx, err_what, bar,
+        objp, nheavy, dbg_dx, dbg_mark, total;
+};
+
+Layout make_layout(int64_t s, int64_t n, int64_t nnz)
+{
+    Layout L{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = align_up(off + (bytes ? bytes : 1));
+        return o;
+    };
+    const int64_t nw = (s + 31) / 32;
+    const int64_t ntile = (n + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
+    L.w = take(sizeof(double) * n);
+    L.z = take(sizeof(double) * s);
+    L.coef = take(sizeof(double2) * s);
+    L.cnt = take(sizeof(int32_t) * s);
+    L.bits = take(sizeof(uint32_t) * nw);
+    L.rec = take(sizeof(Rec) * nnz);
+    L.dxg = take(sizeof(double) * s);
+    L.tlist = take(sizeof(int32_t) * nw * 32);
+    L.order = take(sizeof(int32_t) * n);
+    L.flag = take(sizeof(int32_t) * n);
+    L.hpos = take(sizeof(int64_t) * (n + 1));
+    L.hlist = take(sizeof(int32_t) * n);
+    L.hlen = take(sizeof(int64_t) * n);
+    L.hstart = take(sizeof(int64_t) * (n + 1));
+    L.tiles1 = take(sizeof(int64_t) * ntile);
+    L.tiles2 = take(sizeof(int64_t) * ntile);
+    L.seen = take(sizeof(uint32_t) * ((n + 31) / 32));
+    L.dk = take(sizeof(double) * n);
+    L.deltak = take(sizeof(double) * n);
+    L.gk = take(sizeof(double) * 8);
+    L.hk = take(sizeof(double) * 8);
+    L.part = take(sizeof(double) * 2 * GMAX * NPART);
+    L.hpart = take(sizeof(HPart) * GMAX * 2);
+    L.counters = take(sizeof(int64_t) * 8);
+    L.info = take(sizeof(double) * 8);
+    L.F = take(sizeof(double));
+    L.Fcopy = take(sizeof(double));
+    L.status = take(sizeof(int));
+    L.err_idx = take(sizeof(long long));
+    L.err_what = take(sizeof(int));
+    L.bar = take(sizeof(unsigned long long));
+    L.objp = take(sizeof(double) * 2 * OBJ_NB);
+    L.nheavy = take(sizeof(int64_t));
+    L.dbg_dx = take(sizeof(double) * s);
+    L.dbg_mark = take(s);
+    L.total = off + ALIGN;  // slack for base alignment
+    return L;
+}
+
+struct HostMirror {  // pinned readback block
+    double F;
+    double Fcopy;
+    int status;
+    int err_what;
+    long long err_idx;
+    int64_t counters[8];
+    double info[8];
+};
+
+}  // namespace
+
+struct pcdn_ctx {
+    int64_t s = 0, n = 0, nnz = 0;
+    const int64_t *col_ptr = nullptr;
+    const int32_t *row_idx = nullptr;
+    const float *val = nullptr;
+    const int64_t *row_ptr = nullptr;
+    const int32_t *col_idx = nullptr;
+    const float *csr_val = nullptr;
+    const int8_t *y = nullptr;
+    double c = 1.0;
+    int loss = 0;
+    double sigma = 0.01, beta = 0.5, gamma = 0.0, nu = 1e-12;
+    int qmax = 50;
+    double fstar = 0.0;
+    bool has_fstar = false;
+    int debug = 0;
+    int G = 0;          // CTAs of the step kernel
+    int G_req = 0;
+    int heavy_len = 128;
+    int num_sms = 0;
+    size_t smem = 0;
+    cudaStream_t stream = nullptr;
+    unsigned char *base = nullptr;
+    Layout L{};
+    HostMirror *hm = nullptr;
+    int32_t *q_trace = nullptr;
+    double *F_trace = nullptr;
+    int64_t trace_cap = 0;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t launches = 0;
+    char err[512] = {0};
+
+    template <typename T>
+    T *at(size_t off) const { return reinterpret_cast<T *>(base + off); }
+};
+
+namespace {
+
+int set_err(pcdn_ctx *ctx, int code, const char *fmt, ...)
+{
+    if (ctx) {
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(ctx->err, sizeof(ctx->err), fmt, ap);
+        va_end(ap);
+    }
+    return code;
+}
+
+#define CU(call)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            return set_err(ctx, PCDN_ERR_CUDA, "%s failed: %s (%s:%d)", #call,                    \
+                           cudaGetErrorString(e_), __FILE__, __LINE__);                           \
+    } while (0)
+
+inline int grid1d(int64_t work, int nt = 256)
+{
+    int64_t g = (work + nt - 1) / nt;
+    if (g < 1) g = 1;
+    if (g > 148 * 16) g = 148 * 16;
+    return (int)g;
+}
+
+// device-wide exclusive scan of in[0..n) (n bounded by *n_dev if non-null) into out[0..n]
+template <typename Tin>
+int scan(pcdn_ctx *ctx, const Tin *in, int64_t n_host, const int64_t *n_dev, int64_t *out, int64_t *tiles,
+         int64_t *total)
+{
+    const int64_t ntile = (n_host + SCAN_TILE - 1) / SCAN_TILE > 0 ? (n_host + SCAN_TILE - 1) / SCAN_TILE : 1;
+    k_scan_reduce<Tin, int64_t><<<(unsigned)ntile, SCAN_NT, 0, ctx->stream>>>(in, n_host, n_dev, tiles);
+    k_scan_tiles<int64_t><<<1, SCAN_NT, 0, ctx->stream>>>(tiles, ntile);
+    k_scan_apply<Tin, int64_t><<<(unsigned)ntile, SCAN_NT, 0, ctx->stream>>>(in, n_host, n_dev, tiles, out, total);
+    ctx->launches += 3;
+    CU(cudaGetLastError());
+    return PCDN_OK;
+}
+
+// heavy-column lists for the positions held in ctx->order[0..ntot)
+int build_heavy(pcdn_ctx *ctx, int64_t ntot)
+{
+    const Layout &L = ctx->L;
+    int rc = scan<int32_t>(ctx, ctx->at<int32_t>(L.flag), ntot, nullptr, ctx->at<int64_t>(L.hpos),
+                           ctx->at<int64_t>(L.tiles1), ctx->at<int64_t>(L.nheavy));
+    if (rc) return rc;
+    k_heavy_compact<<<grid1d(ntot), 256, 0, ctx->stream>>>(ctx->at<int64_t>(L.hpos), ntot, ctx->at<int32_t>(L.order),
+                                                           ctx->col_ptr, ctx->at<int32_t>(L.hlist),
+                                                           ctx->at<int64_t>(L.hlen));
+    ctx->launches++;
+    CU(cudaGetLastError());
+    return scan<int64_t>(ctx, ctx->at<int64_t>(L.hlen), ntot, ctx->at<int64_t>(L.nheavy), ctx->at<int64_t>(L.hstart),
+                         ctx->at<int64_t>(L.tiles2), nullptr);
+}
+
+int objective_kernels(pcdn_ctx *ctx)
+{
+    const Layout &L = ctx->L;
+    k_obj_partial<<<OBJ_NB, 256, 0, ctx->stream>>>(ctx->s, ctx->n, ctx->at<double>(L.z), ctx->y, ctx->at<double>(L.w),
+                                                   ctx->loss, ctx->at<double>(L.objp));
+    k_obj_final<<<1, OBJ_NB, 0, ctx->stream>>>(ctx->at<double>(L.objp), ctx->c, ctx->at<double>(L.F),
+                                               ctx->at<double>(L.Fcopy));
+    ctx->launches += 2;
+    CU(cudaGetLastError());
+    return PCDN_OK;
+}
+
+int refresh_z(pcdn_ctx *ctx, int zero)
+{
+    const Layout &L = ctx->L;
+    k_set_z<<<grid1d(ctx->s), 256, 0, ctx->stream>>>(ctx->s, ctx->row_ptr, ctx->col_idx, ctx->csr_val, ctx->y,
+                                                     ctx->at<double>(L.w), ctx->loss, ctx->at<double>(L.z),
+                                                     ctx->at<double2>(L.coef), zero);
+    ctx->launches++;
+    CU(cudaGetLastError());
+    return PCDN_OK;
+}
+
+int readback(pcdn_ctx *ctx)
+{
+    const Layout &L = ctx->L;
+    CU(cudaMemcpyAsync(&ctx->hm->F, ctx->at<double>(L.F), sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(&ctx->hm->status, ctx->at<int>(L.status), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(&ctx->hm->err_idx, ctx->at<long long>(L.err_idx), sizeof(long long), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaMemcpyAsync(&ctx->hm->err_what, ctx->at<int>(L.err_what), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(ctx->hm->counters, ctx->at<int64_t>(L.counters), sizeof(int64_t) * 8, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaMemcpyAsync(ctx->hm->info, ctx->at<double>(L.info), sizeof(double) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return PCDN_OK;
+}
+
+int reset_status(pcdn_ctx *ctx)
+{
+    const Layout &L = ctx->L;
+    CU(cudaMemsetAsync(ctx->at<int>(L.status), 0, sizeof(int), ctx->stream));
+    CU(cudaMemsetAsync(ctx->at<long long>(L.err_idx), 0x7f, sizeof(long long), ctx->stream));
+    CU(cudaMemsetAsync(ctx->at<int>(L.err_what), 0, sizeof(int), ctx->stream));
+    return PCDN_OK;
+}
+
+// Launch the persistent step kernel over `nsteps` bundles of the positions in ctx->order.
+int launch_steps(pcdn_ctx *ctx, int64_t ntot, int64_t P, int64_t nsteps, int64_t trace_off, double *g_out,
+                 double *h_out, double *d_out)
+{
+    const Layout &L = ctx->L;
+    StepArgs a{};
+    a.s = ctx->s;
+    a.n = ctx->n;
+    a.col_ptr = ctx->col_ptr;
+    a.row_idx = ctx->row_idx;
+    a.val = ctx->val;
+    a.row_ptr = ctx->row_ptr;
+    a.y = ctx->y;
+    a.c = ctx->c;
+    a.sigma = ctx->sigma;
+    a.beta = ctx->beta;
+    a.gamma = ctx->gamma;
+    a.nu = ctx->nu;
+    a.loss = ctx->loss;
+    a.qmax = ctx->qmax;
+    a.heavy_len = ctx->heavy_len;
+    a.w = ctx->at<double>(L.w);
+    a.z = ctx->at<double>(L.z);
+    a.coef = ctx->at<double2>(L.coef);
+    a.F = ctx->at<double>(L.F);
+    a.cnt = ctx->at<int32_t>(L.cnt);
+    a.bits = ctx->at<uint32_t>(L.bits);
+    a.rec = ctx->at<Rec>(L.rec);
+    a.dxg = ctx->at<double>(L.dxg);
+    a.tlist = ctx->at<int32_t>(L.tlist);
+    a.order = ctx->at<int32_t>(L.order);
+    a.hpos = ctx->at<int64_t>(L.hpos);
+    a.hlist = ctx->at<int32_t>(L.hlist);
+    a.hstart = ctx->at<int64_t>(L.hstart);
+    a.ntot = ntot;
+    a.P = P;
+    a.nsteps = nsteps;
+    a.dk = ctx->at<double>(L.dk);
+    a.deltak = ctx->at<double>(L.deltak);
+    a.part = ctx->at<double>(L.part);
+    a.hpart = ctx->at<HPart>(L.hpart);
+    a.g_out = g_out;
+    a.h_out = h_out;
+    a.d_out = d_out;
+    a.q_trace = ctx->q_trace;
+    a.F_trace = ctx->F_trace;
+    a.trace_off = trace_off;
+    a.trace_cap = ctx->trace_cap;
+    a.counters = ctx->at<int64_t>(L.counters);
+    a.info = ctx->at<double>(L.info);
+    a.debug = ctx->debug;
+    a.dbg_dx = ctx->at<double>(L.dbg_dx);
+    a.dbg_mark = ctx->at<uint8_t>(L.dbg_mark);
+    a.bar = ctx->at<unsigned long long>(L.bar);
+    a.status = ctx->at<int>(L.status);
+    CU(cudaMemsetAsync(a.bar, 0, sizeof(unsigned long long), ctx->stream));
+    void *args[] = {&a};
+    CU(cudaLaunchCooperativeKernel((const void *)k_step, dim3(ctx->G), dim3(NT), args, ctx->smem, ctx->stream));
+    ctx->launches++;
+    return PCDN_OK;
+}
+
+int configure_launch(pcdn_ctx *ctx)
+{
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    CU(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev));
+    int coop = 0;
+    CU(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    if (!coop) return set_err(ctx, PCDN_ERR_CUDA, "device does not support cooperative launch");
+    ctx->smem = sizeof(StepSmem);
+    CU(cudaFuncSetAttribute((const void *)k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem));
+    int occ = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)k_step, NT, ctx->smem));
+    if (occ < 1) return set_err(ctx, PCDN_ERR_CUDA, "step kernel cannot be resident (smem %zu)", ctx->smem);
+    int maxg = ctx->num_sms * (occ < 2 ? occ : 2);
+    if (maxg > GMAX) maxg = GMAX;
+    ctx->G = ctx->G_req > 0 && ctx->G_req < maxg ? ctx->G_req : maxg;
+    return PCDN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *pcdn_version(void) { return "pcdn-b200 0.1 (sm_100a)"; }
+
+size_t pcdn_workspace_bytes(int64_t s, int64_t n, int64_t nnz)
+{
+    if (s < 1 || n < 1 || nnz < 0) return 0;
+    return make_layout(s, n, nnz).total;
+}
+
+int pcdn_create(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_ptr, const int32_t *csc_row_idx,
+                const float *csc_val, const int64_t *csr_row_ptr, const int32_t *csr_col_idx, const float *csr_val,
+                const int8_t *y, double c, int loss, void *workspace, size_t workspace_bytes, void *cuda_stream,
+                pcdn_ctx **out)
+{
+    if (!out) return PCDN_ERR_INVALID;
+    *out = nullptr;
+    pcdn_ctx *ctx = new (std::nothrow) pcdn_ctx();
+    if (!ctx) return PCDN_ERR_NOMEM;
+    auto fail = [&](int code) {
+        // keep ctx alive so the caller can read the error; caller must destroy it
+        *out = ctx;
+        return code;
+    };
+    if (s < 1 || n < 1 || nnz < 0 || s > INT32_MAX || n > INT32_MAX)
+        return fail(set_err(ctx, PCDN_ERR_INVALID, "invalid sizes s=%lld n=%lld nnz=%lld", (long long)s,
+                            (long long)n, (long long)nnz));
+    if (!(c > 0) || !std::isfinite(c)) return fail(set_err(ctx, PCDN_ERR_INVALID, "c must be finite and > 0"));
+    if (loss != PCDN_LOSS_LOGISTIC && loss != PCDN_LOSS_L2SVM)
+        return fail(set_err(ctx, PCDN_ERR_INVALID, "unknown loss %d", loss));
+    if (!csc_col_ptr || !csr_row_ptr || !y || (nnz > 0 && (!csc_row_idx || !csc_val || !csr_col_idx || !csr_val)))
+        return fail(set_err(ctx, PCDN_ERR_INVALID, "null input pointer"));
+    ctx->L = make_layout(s, n, nnz);
+    if (!workspace || workspace_bytes < ctx->L.total)
+        return fail(set_err(ctx, PCDN_ERR_NOMEM, "workspace too small: need %zu bytes, got %zu", ctx->L.total,
+                            workspace_bytes));
+    ctx->s = s;
+    ctx->n = n;
+    ctx->nnz = nnz;
+    ctx->col_ptr = csc_col_ptr;
+    ctx->row_idx = csc_row_idx;
+    ctx->val = csc_val;
+    ctx->row_ptr = csr_row_ptr;
+    ctx->col_idx = csr_col_idx;
+    ctx->csr_val = csr_val;
+    ctx->y = y;
+    ctx->c = c;
+    ctx->loss = loss;
+    ctx->stream = (cudaStream_t)cuda_stream;
+    ctx->base = reinterpret_cast<unsigned char *>(align_up(reinterpret_cast<uintptr_t>(workspace)));
+    {
+        cudaError_t e = cudaMallocHost(&ctx->hm, sizeof(HostMirror));
+        if (e != cudaSuccess) return fail(set_err(ctx, PCDN_ERR_CUDA, "cudaMallocHost: %s", cudaGetErrorString(e)));
+        for (int i = 0; i < 4; i++) {
+            e = cudaEventCreate(&ctx->ev[i]);
+            if (e != cudaSuccess) return fail(set_err(ctx, PCDN_ERR_CUDA, "cudaEventCreate: %s", cudaGetErrorString(e)));
+        }
+    }
+    int rc = configure_launch(ctx);
+    if (rc) return fail(rc);
+    // zero the whole workspace once (counters, bitmaps, record counts must start at 0)
+    {
+        cudaError_t e = cudaMemsetAsync(ctx->base, 0, ctx->L.total - ALIGN, ctx->stream);
+        if (e != cudaSuccess) return fail(set_err(ctx, PCDN_ERR_CUDA, "memset: %s", cudaGetErrorString(e)));
+    }
+    if ((rc = reset_status(ctx))) return fail(rc);
+    const Layout &L = ctx->L;
+    k_validate<<<grid1d(s > n ? s : n), 256, 0, ctx->stream>>>(s, n, nnz, csc_col_ptr, csc_row_idx, csc_val,
+                                                               csr_row_ptr, csr_col_idx, csr_val, y,
+                                                               ctx->at<int>(L.status), ctx->at<long long>(L.err_idx),
+                                                               ctx->at<int>(L.err_what));
+    k_validate_transpose<<<grid1d(s), 256, 0, ctx->stream>>>(s, csc_col_ptr, csc_row_idx, csc_val, csr_row_ptr,
+                                                             csr_col_idx, csr_val, ctx->at<int>(L.status),
+                                                             ctx->at<long long>(L.err_idx), ctx->at<int>(L.err_what));
+    {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(set_err(ctx, PCDN_ERR_CUDA, "validate launch: %s", cudaGetErrorString(e)));
+    }
+    if ((rc = readback(ctx))) return fail(rc);
+    if (ctx->hm->status) {
+        static const char *what[] = {"?", "col_ptr[0] != 0", "col_ptr[n] != nnz", "col_ptr not monotone",
+                                     "row index out of range", "row indices not strictly increasing in a column",
+                                     "non-finite CSC value", "row_ptr[0] != 0", "row_ptr[s] != nnz",
+                                     "row_ptr not monotone", "CSR column index out of range",
+                                     "CSR column indices not strictly increasing in a row", "non-finite CSR value",
+                                     "label not in {-1,+1}", "CSR and CSC hold different nonzeros"};
+        const int wv = ctx->hm->err_what >= 0 && ctx->hm->err_what <= 14 ? ctx->hm->err_what : 0;
+        return fail(set_err(ctx, PCDN_ERR_INVALID, "invalid input: %s at index %lld", what[wv],
+                            (long long)ctx->hm->err_idx));
+    }
+    if ((rc = pcdn_reset(ctx))) return fail(rc);
+    *out = ctx;
+    return PCDN_OK;
+}
+
+int pcdn_set_armijo(pcdn_ctx *ctx, double sigma, double beta, double gamma, int q_max)
+{
+    if (!ctx) return PCDN_ERR_INVALID;
+    if (!(sigma > 0 && sigma < 1) || !(beta > 0 && beta < 1) || !(gamma >= 0 && gamma < 1) || q_max < 0 || q_max > 200)
+        return set_err(ctx, PCDN_ERR_INVALID, "invalid Armijo constants");
+    ctx->sigma = sigma;
+    ctx->beta = beta;
+    ctx->gamma = gamma;
+    ctx->qmax = q_max;
+    return PCDN_OK;
+}
+
+int pcdn_set_reference(pcdn_ctx *ctx, double f_star)
+{
+    if (!ctx) return PCDN_ERR_INVALID;
+    if (!(f_star > 0) || !std::isfinite(f_star)) return set_err(ctx, PCDN_ERR_INVALID, "F* must be finite and > 0");
+    ctx->fstar = f_star;
+    ctx->has_fstar = true;
+    return PCDN_OK;
+}
+
+int pcdn_set_trace(pcdn_ctx *ctx, int32_t *q_trace, double *F_trace, int64_t capacity)
+{
+    if (!ctx) return PCDN_ERR_INVALID;
+    ctx->q_trace = q_trace;
+    ctx->F_trace = F_trace;
+    ctx->trace_cap = capacity > 0 ? capacity : 0;
+    return PCDN_OK;
+}
+
+int pcdn_set_debug(pcdn_ctx *ctx, int on)
+{
+    if (!ctx) return PCDN_ERR_INVALID;
+    ctx->debug = on ? 1 : 0;
+    return PCDN_OK;
+}
+
+int pcdn_set_launch(pcdn_ctx *ctx, int ctas, int heavy_len)
+{
+    if (!ctx) return PCDN_ERR_INVALID;
+    if (ctas < 0 || heavy_len < 0) return set_err(ctx, PCDN_ERR_INVALID, "invalid launch knobs");
+    ctx->G_req = ctas;
+    if (heavy_len > 0) ctx->heavy_len = heavy_len;
+    return configure_launch(ctx);
+}
+
+const char *pcdn_last_error(const pcdn_ctx *ctx) { return ctx ? ctx->err : "null context"; }
+
+void pcdn_destroy(pcdn_ctx *ctx)
+{
+    if (!ctx) return;
+    if (ctx->stream || true) cudaStreamSynchronize(ctx->stream);
+    for (auto &e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->hm) cudaFreeHost(ctx->hm);
+    delete ctx;
+}
+
+int pcdn_reset(pcdn_ctx *ctx)
+{
+    if (!ctx || !ctx->base) return PCDN_ERR_INVALID;
+    const Layout &L = ctx->L;
+    CU(cudaMemsetAsync(ctx->at<double>(L.w), 0, sizeof(double) * ctx->n, ctx->stream));
+    int rc = refresh_z(ctx, 1);
+    if (rc) return rc;
+    return objective_kernels(ctx);
+}
+
+int pcdn_set_w(pcdn_ctx *ctx, const double *w)
+{
+    if (!ctx || !w) return PCDN_ERR_INVALID;
+    const Layout &L = ctx->L;
+    CU(cudaMemcpyAsync(ctx->at<double>(L.w), w, sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice, ctx->stream));
+    int rc = refresh_z(ctx, 0);
+    if (rc) return rc;
+    return objective_kernels(ctx);
+}
+
+int pcdn_get_w(pcdn_ctx *ctx, double *w_out)
+{
+    if (!ctx || !w_out) return PCDN_ERR_INVALID;
+    CU(cudaMemcpyAsync(w_out, ctx->at<double>(ctx->L.w), sizeof(double) * ctx->n, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+    return PCDN_OK;
+}
+
+int pcdn_get_z(pcdn_ctx *ctx, double *z_out)
+{
+    if (!ctx || !z_out) return PCDN_ERR_INVALID;
+    CU(cudaMemcpyAsync(z_out, ctx->at<double>(ctx->L.z), sizeof(double) * ctx->s, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
+    return PCDN_OK;
+}
+
+int pcdn_objective(pcdn_ctx *ctx, int recompute_from_w, double *F_out)
+{
+    if (!ctx || !F_out) return PCDN_ERR_INVALID;
+    int rc;
+    if (recompute_from_w) {
+        // evaluate from scratch without disturbing the maintained F: z is recomputed (exact
+        // same z for an unchanged w), F_full goes to the copy slot
+        if ((rc = refresh_z(ctx, 0))) return rc;
+    }
+    const Layout &L = ctx->L;
+    k_obj_partial<<<OBJ_NB, 256, 0, ctx->stream>>>(ctx->s, ctx->n, ctx->at<double>(L.z), ctx->y, ctx->at<double>(L.w),
+                                                   ctx->loss, ctx->at<double>(L.objp));
+    k_obj_final<<<1, OBJ_NB, 0, ctx->stream>>>(ctx->at<double>(L.objp), ctx->c, ctx->at<double>(L.Fcopy), nullptr);
+    ctx->launches += 2;
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(&ctx->hm->Fcopy, ctx->at<double>(L.Fcopy), sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    *F_out = ctx->hm->Fcopy;
+    return PCDN_OK;
+}
+
+int pcdn_permutation(pcdn_ctx *ctx, uint64_t seed, int64_t k, int32_t *out)
+{
+    if (!ctx || !out || k < 0) return PCDN_ERR_INVALID;
+    k_perm<<<grid1d(ctx->n), 256, 0, ctx->stream>>>(seed, k, ctx->n, ctx->col_ptr, ctx->heavy_len, out, nullptr);
+    ctx->launches++;
+    CU(cudaGetLastError());
+    return PCDN_OK;
+}
+
+int pcdn_bundle_step(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, pcdn_step_info *info, double *g_out,
+                     double *h_out, double *d_out)
+{
+    if (!ctx) return PCDN_ERR_INVALID;
+    if (!bundle || P < 1 || P > ctx->n) return set_err(ctx, PCDN_ERR_INVALID, "bundle size %lld out of [1, n]", (long long)P);
+    const Layout &L = ctx->L;
+    int rc;
+    if ((rc = reset_status(ctx))) return rc;
+    k_bundle_prep<<<grid1d(P), 256, 0, ctx->stream>>>(bundle, P, ctx->n, ctx->col_ptr, ctx->heavy_len,
+                                                      ctx->at<int32_t>(L.order), ctx->at<int32_t>(L.flag),
+                                                      ctx->at<uint32_t>(L.seen), ctx->at<int>(L.status),
+                                                      ctx->at<long long>(L.err_idx));
+    k_bundle_unseen<<<grid1d(P), 256, 0, ctx->stream>>>(bundle, P, ctx->n, ctx->at<uint32_t>(L.seen));
+    ctx->launches += 2;
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(&ctx->hm->status, ctx->at<int>(L.status), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(&ctx->hm->err_idx, ctx->at<long long>(L.err_idx), sizeof(long long), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (ctx->hm->status)
+        return set_err(ctx, PCDN_ERR_INVALID, "bundle entry %lld is out of range or repeated", (long long)ctx->hm->err_idx);
+    if ((rc = build_heavy(ctx, P))) return rc;
+    if (ctx->debug) CU(cudaMemsetAsync(ctx->at<uint8_t>(L.dbg_mark), 0, ctx->s, ctx->stream));
+    if ((rc = launch_steps(ctx, P, P, 1, 0, g_out, h_out, d_out))) return rc;
+    if (info) {
+        if ((rc = readback(ctx))) return rc;
+        const double *v = ctx->hm->info;
+        info->q = (int32_t)v[0];
+        info->reserved = 0;
+        info->alpha = v[1];
+        info->Delta = v[2];
+        info->lhs = v[3];
+        info->rhs = v[4];
+        info->F = v[5];
+        info->bundle_nnz = (int64_t)v[6];
+        info->n_touched = (int64_t)v[7];
+        if (ctx->hm->status == 3) return set_err(ctx, PCDN_ERR_NUMERIC, "non-finite line-search quantities");
+        if (ctx->hm->status) return set_err(ctx, PCDN_ERR_CUDA, "internal consistency check failed (%d)", ctx->hm->status);
+    }
+    return PCDN_OK;
+}
+
+int pcdn_last_touched(pcdn_ctx *ctx, int32_t *T_out, double *dx_out, int64_t capacity, int64_t *nT)
+{
+    if (!ctx || !nT) return PCDN_ERR_INVALID;
+    if (!ctx->debug) return set_err(ctx, PCDN_ERR_INVALID, "pcdn_last_touched needs pcdn_set_debug(ctx, 1)");
+    std::vector<uint8_t> mark(ctx->s);
+    std::vector<double> dx(ctx->s);
+    CU(cudaMemcpyAsync(mark.data(), ctx->at<uint8_t>(ctx->L.dbg_mark), ctx->s, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(dx.data(), ctx->at<double>(ctx->L.dbg_dx), sizeof(double) * ctx->s, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    int64_t m = 0;
+    for (int64_t i = 0; i < ctx->s; i++) {
+        if (!mark[i]) continue;
+        if (m < capacity) {
+            if (T_out) T_out[m] = (int32_t)i;
+            if (dx_out) dx_out[m] = dx[i];
+        }
+        m++;
+    }
+    *nT = m;
+    return PCDN_OK;
+}
+
+int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_outer, pcdn_solve_info *info)
+{
+    if (!ctx) return PCDN_ERR_INVALID;
+    const auto t_start = std::chrono::steady_clock::now();
+    if (P < 1 || P > ctx->n) return set_err(ctx, PCDN_ERR_INVALID, "P=%lld out of [1, n=%lld]", (long long)P, (long long)ctx->n);
+    if (max_outer < 0) return set_err(ctx, PCDN_ERR_INVALID, "max_outer < 0");
+    if (eps > 0 && !ctx->has_fstar) return set_err(ctx, PCDN_ERR_INVALID, "eps > 0 needs pcdn_set_reference");
+    const Layout &L = ctx->L;
+    const int64_t launches0 = ctx->launches;
+    int rc;
+    if ((rc = reset_status(ctx))) return rc;
+    CU(cudaMemsetAsync(ctx->at<int64_t>(L.counters), 0, sizeof(int64_t) * 8, ctx->stream));
+    const int64_t b = (ctx->n + P - 1) / P;
+    int status = PCDN_BUDGET;
+    int32_t k = 0;
+    double F = NAN, gap = NAN, t_step_ms = 0.0;
+    CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+    for (k = 0; k < max_outer; k++) {
+        // a0: partition pi_k and the per-step heavy-column lists
+        k_perm<<<grid1d(ctx->n), 256, 0, ctx->stream>>>(seed, k, ctx->n, ctx->col_ptr, ctx->heavy_len,
+                                                         ctx->at<int32_t>(L.order), ctx->at<int32_t>(L.flag));
+        ctx->launches++;
+        CU(cudaGetLastError());
+        if ((rc = build_heavy(ctx, ctx->n))) return rc;
+        // a1..a5: all b bundle steps in one persistent launch
+        CU(cudaEventRecord(ctx->ev[0], ctx->stream));
+        if ((rc = launch_steps(ctx, ctx->n, P, b, (int64_t)k * b, nullptr, nullptr, nullptr))) return rc;
+        CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+        // a6: F from scratch (reading Z23), one readback per outer iteration
+        if ((rc = objective_kernels(ctx))) return rc;
+        if ((rc = readback(ctx))) return rc;
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
+        t_step_ms += ms;
+        F = ctx->hm->F;
+        if (ctx->hm->status == 3 || !std::isfinite(F)) {
+            status = PCDN_ERR_NUMERIC;
+            set_err(ctx, PCDN_ERR_NUMERIC, "non-finite objective in outer iteration %d", k);
+            k++;
+            break;
+        }
+        if (ctx->hm->status) {
+            status = PCDN_ERR_CUDA;
+            set_err(ctx, PCDN_ERR_CUDA, "internal consistency check failed (%d)", ctx->hm->status);
+            k++;
+            break;
+        }
+        if (eps > 0) {
+            gap = (F - ctx->fstar) / ctx->fstar;  // Eq.14
+            if (gap <= eps) {
+                status = PCDN_OK;
+                k++;
+                break;
+            }
+        }
+    }
+    CU(cudaEventRecord(ctx->ev[3], ctx->stream));
+    CU(cudaEventSynchronize(ctx->ev[3]));
+    if (max_outer == 0) {
+        if ((rc = readback(ctx))) return rc;
+        F = ctx->hm->F;
+    }
+    if (info) {
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, ctx->ev[2], ctx->ev[3]));
+        const int64_t *cn = ctx->hm->counters;
+        info->status = status;
+        info->outer_iters = k;
+        info->steps = cn[0];
+        info->null_steps = cn[1];
+        info->nnz_processed = cn[2];
+        info->touched_total = cn[3];
+        info->positions = cn[4];
+        info->kernel_launches = ctx->launches - launches0;
+        info->F = F;
+        info->gap = eps > 0 ? (F - ctx->fstar) / ctx->fstar : (ctx->has_fstar ? (F - ctx->fstar) / ctx->fstar : NAN);
+        info->t_wall_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+        info->t_step_kernel_ms = t_step_ms;
+        info->t_gpu_ms = ms;
+        // 16 B per bundle nonzero (index+value, gathered fp64 pair counted as
+        // one fp64 word of the retained per-sample state), 16 B per touched sample, 28 B per position
+        info->alg_bytes = 16.0 * (double)cn[2] + 16.0 * (double)cn[3] + 28.0 * (double)cn[4];
+    }
+    (void)gap;
+    return status;
+}
+
+int pcdn_train_host(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_ptr, const int32_t *csc_row_idx,
+                    const float *csc_val, const int64_t *csr_row_ptr, const int32_t *csr_col_idx,
+                    const float *csr_val, const int8_t *y, double c, int loss, int64_t P, double eps, double f_star,
+                    uint64_t seed, int32_t max_outer, void *cuda_stream, double *w_out, pcdn_solve_info *info)
+{
+    pcdn_ctx *ctx = nullptr;  // for CU() error text only
+    if (s < 1 || n < 1 || nnz < 0 || !csc_col_ptr || !csr_row_ptr || !y || !w_out) return PCDN_ERR_INVALID;
+    if (eps > 0 && !(f_star > 0)) return PCDN_ERR_INVALID;
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const size_t ws = pcdn_workspace_bytes(s, n, nnz);
+    const size_t sz[] = {sizeof(int64_t) * (n + 1), sizeof(int32_t) * nnz, sizeof(float) * nnz,
+                         sizeof(int64_t) * (s + 1), sizeof(int32_t) * nnz, sizeof(float) * nnz, (size_t)s, ws,
+                         sizeof(double) * n};
+    const void *src[] = {csc_col_ptr, csc_row_idx, csc_val, csr_row_ptr, csr_col_idx, csr_val, y, nullptr, nullptr};
+    void *d[9] = {nullptr};
+    int rc = PCDN_OK;
+    for (int i = 0; i < 9; i++) {
+        if (cudaMallocAsync(&d[i], sz[i] ? sz[i] : 1, st) != cudaSuccess) {
+            rc = PCDN_ERR_NOMEM;
+            break;
+        }
+        if (src[i] && sz[i] && cudaMemcpyAsync(d[i], src[i], sz[i], cudaMemcpyHostToDevice, st) != cudaSuccess) {
+            rc = PCDN_ERR_CUDA;
+            break;
+        }
+    }
+    if (rc == PCDN_OK) {
+        rc = pcdn_create(s, n, nnz, (const int64_t *)d[0], (const int32_t *)d[1], (const float *)d[2],
+                         (const int64_t *)d[3], (const int32_t *)d[4], (const float *)d[5], (const int8_t *)d[6], c,
+                         loss, d[7], ws, st, &ctx);
+        if (rc == PCDN_OK && eps > 0) rc = pcdn_set_reference(ctx, f_star);
+        if (rc == PCDN_OK) {
+            rc = pcdn_solve(ctx, P, eps, seed, max_outer, info);
+            if (rc == PCDN_OK || rc == PCDN_BUDGET) {
+                int rc2 = pcdn_get_w(ctx, (double *)d[8]);
+                if (rc2 == PCDN_OK &&
+                    cudaMemcpyAsync(w_out, d[8], sizeof(double) * n, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+                    rc2 = PCDN_ERR_CUDA;
+                if (rc2 == PCDN_OK && cudaStreamSynchronize(st) != cudaSuccess) rc2 = PCDN_ERR_CUDA;
+                if (rc2 != PCDN_OK) rc = rc2;
+            }
+        }
+        if (ctx) pcdn_destroy(ctx);
+    }
+    for (int i = 0; i < 9; i++)
+        if (d[i]) cudaFreeAsync(d[i], st);
+    cudaStreamSynchronize(st);
+    return rc;
+}
+
+}  // extern "C"

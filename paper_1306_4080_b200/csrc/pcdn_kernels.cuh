@@ -1,0 +1,1183 @@
+// pcdn_kernels.cuh -- sm_100a kernels of the PCDN hot path.
+//
+// Citations "PAPER.md:L" point into the paper (arXiv:1306.4080 LaTeX source); "Zk" are the
+// readings of DESIGN.md.  This file shares nothing with oracle/ (the CPU oracle).
+//
+// Design summary:
+//   a0  k_perm           keyed Feistel permutation pi_k, one thread per position (Z2)
+//       k_scan_*         device-wide exclusive scans building the per-step heavy-column lists
+//   a1..a5 k_step        ONE persistent cooperative kernel runs all b bundle steps of an outer
+//                        iteration; phases are separated by a software grid barrier:
+//        A  g_j,h_j -> d_j -> scatter of (k, d_j x_ij) records into per-row segments
+//           (light columns: one warp per column; heavy columns: nnz-balanced split over all
+//           warps with a deterministic warp -> CTA -> grid combine)          [grid barrier]
+//        C  row-block owners: touched set T from a bitmap, d'x_i by an in-order fold of the
+//           row's records sorted by bundle position (no float atomics), line-search partial
+//           sums for a window of candidates q                                  [grid barrier]
+//        D  every CTA reduces the partials in the same order, picks the first passing q
+//           (Eq.6), commits w_B, z_T and the cached per-sample factors           [grid barrier]
+//   a6  k_obj_*          F_c(w) from (z, w) with a fixed-order two-level reduction (Eq.1)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pcdn {
+
+constexpr int NT = 512;            // threads per CTA of the step kernel
+constexpr int NW = NT / 32;        // warps per CTA
+constexpr int QW = 8;              // max Armijo candidates per line-search window
+constexpr int NPART = 2 * QW + 8;  // per-CTA partials: Ls[QW], L1[QW], Delta, nnz, |T|
+constexpr int NE_MAX = 64;         // heavy entries handled per round inside one CTA
+constexpr int NREG = 8;            // rows with <= NREG records are folded by one thread
+constexpr int NHW = 4;             // warps that fold rows with > NREG records
+constexpr int HB = 1024;           // per-warp sort buffer for such rows
+constexpr int SCAN_TILE = 2048;    // items per CTA of the device-wide scans
+constexpr int SCAN_NT = 256;
+
+constexpr int LOSS_LOGISTIC = 0;
+constexpr int LOSS_L2SVM = 1;
+
+struct __align__(16) Rec {   // one contribution d_k x_ik to sample i, k = bundle position
+    int32_t k;
+    int32_t pad;
+    double v;
+};
+
+struct __align__(16) HPart {  // CTA partial of a heavy column crossing CTA boundaries
+    int64_t e;
+    double g, h;
+    double pad;
+};
+
+struct StepArgs {
+    // problem (immutable during the kernel)
+    int64_t s, n;
+    const int64_t *__restrict__ col_ptr;
+    const int32_t *__restrict__ row_idx;
+    const float *__restrict__ val;
+    const int64_t *__restrict__ row_ptr;  // CSR offsets: capacity of each sample's record segment
+    const int8_t *__restrict__ y;
+    double c, sigma, beta, gamma, nu;
+    int loss, qmax;
+    int heavy_len;
+    // state
+    double *w;
+    double *z;
+    double2 *coef;   // cached per-sample (G_i, H_i): grad_j = c sum x G, hess_jj = c sum x^2 H
+    double *F;       // maintained objective (device scalar)
+    int32_t *cnt;    // per-sample record count (zero between steps)
+    uint32_t *bits;  // touched-sample bitmap (zero between steps)
+    Rec *rec;        // per-sample record segments at row_ptr[i]
+    double *dxg;     // d'x_i for i in T (valid only on T)
+    int32_t *tlist;  // T, per row block, ascending
+    // bundles of this launch
+    const int32_t *__restrict__ order;  // feature id per position
+    const int64_t *__restrict__ hpos;   // heavy positions before each position [ntot+1]
+    const int32_t *__restrict__ hlist;  // heavy entry -> position
+    const int64_t *__restrict__ hstart; // heavy entry -> global heavy-nnz offset [nheavy+1]
+    int64_t ntot, P, nsteps;
+    // per-step scratch
+    double *dk, *deltak;  // [P] direction and Delta term per bundle position
+    double *part;         // [2][G][NPART]
+    HPart *hpart;         // [G][2]
+    // outputs
+    double *g_out, *h_out, *d_out;  // nullable [P] (single-step launches)
+    int32_t *q_trace;
+    double *F_trace;
+    int64_t trace_off, trace_cap;
+    int64_t *counters;   // [0]=steps [1]=null [2]=nnz [3]=touched [4]=positions
+    double *info;        // last step: q, alpha, Delta, lhs, rhs, F, nnz, nT
+    int debug;
+    double *dbg_dx;
+    uint8_t *dbg_mark;
+    // sync
+    unsigned long long *bar;
+    int *status;
+};
+
+// ------------------------------------------------------------------------------------
+// small device helpers
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }
+__device__ __forceinline__ double2 ldcg(const double2 *p) { return __ldcg(p); }
+__device__ __forceinline__ int32_t ldcg(const int32_t *p) { return __ldcg(p); }
+__device__ __forceinline__ uint32_t ldcg(const uint32_t *p) { return __ldcg(p); }
+__device__ __forceinline__ int64_t ldcg(const int64_t *p) { return __ldcg((const long long *)p); }
+
+__device__ __forceinline__ HPart ld_hpart(const HPart *p)
+{
+    const double2 *q = reinterpret_cast<const double2 *>(p);
+    const double2 a0 = __ldcg(q), a1 = __ldcg(q + 1);
+    HPart r;
+    r.e = __double_as_longlong(a0.x);
+    r.g = a0.y;
+    r.h = a1.x;
+    r.pad = a1.y;
+    return r;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Software grid barrier for a cooperative launch (all CTAs co-resident).  `target`
+// advances by gridDim.x per barrier; the counter only grows within a launch.
+__device__ __forceinline__ void grid_sync(unsigned long long *ctr, unsigned long long &target)
+{
+    target += gridDim.x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ctr, 1ULL);
+        while (ld_acquire(ctr) < target) {
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// SplitMix64 finalizer; the partition generator of reading Z2.
+__device__ __forceinline__ uint64_t mix64(uint64_t x)
+{
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ULL;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebULL;
+    x ^= x >> 31;
+    return x;
+}
+
+// Per-sample factors (G, H) of Eq.13 (logistic) and App. A.2 (L2-SVM,
+// PAPER.md:825-829, gradient per reading Z5).  sigma(+-m) evaluated without overflow.
+__device__ __forceinline__ double2 coef_of(int loss, double z, int yi)
+{
+    const double yd = (double)yi;
+    if (loss == LOSS_LOGISTIC) {
+        const double m = yd * z;
+        double sm, snm;
+        if (m >= 0) {
+            const double e = exp(-m);
+            sm = 1.0 / (1.0 + e);
+            snm = e / (1.0 + e);
+        } else {
+            const double e = exp(m);
+            sm = e / (1.0 + e);
+            snm = 1.0 / (1.0 + e);
+        }
+        return make_double2(-snm * yd, sm * snm);
+    }
+    const double b = 1.0 - yd * z;
+    if (b > 0) return make_double2(-2.0 * yd * b, 2.0);
+    return make_double2(0.0, 0.0);
+}
+
+__device__ __forceinline__ double softplus(double t) { return (t > 0 ? t : 0.0) + log1p(exp(-fabs(t))); }
+
+// phi(m), Eq.2 / Eq.3 (overflow-safe, reading Z19)
+__device__ __forceinline__ double phi_of(int loss, double m)
+{
+    if (loss == LOSS_LOGISTIC) return softplus(-m);
+    const double b = 1.0 - m;
+    return b > 0 ? b * b : 0.0;
+}
+
+// Per-sample loss change at step alpha (reading Z7).  For the logistic loss sigma(-m) is taken
+// from the cached factor: G = -sigma(-m) y  =>  sigma(-m) = -G y (exact).
+__device__ __forceinline__ double loss_change(int loss, double z, int yi, double cg, double dx, double alpha)
+{
+    const double yd = (double)yi;
+    if (loss == LOSS_LOGISTIC) {
+        const double m = yd * z;
+        const double u = alpha * (yd * dx);
+        if (fabs(u) <= 1.0) {
+            const double snm = -cg * yd;
+            return log1p(expm1(-u) * snm);
+        }
+        return softplus(-(m + u)) - softplus(-m);
+    }
+    const double b1 = 1.0 - yd * (z + alpha * dx);
+    const double b0 = 1.0 - yd * z;
+    const double p1 = b1 > 0 ? b1 * b1 : 0.0;
+    const double p0 = b0 > 0 ? b0 * b0 : 0.0;
+    return p1 - p0;
+}
+
+// Eq.5, branches tested in printed order (reading Z17).
+__device__ __forceinline__ double newton_dir(double g, double h, double wj)
+{
+    const double hw = h * wj;
+    if (g + 1.0 <= hw) return -(g + 1.0) / h;
+    if (g - 1.0 >= hw) return -(g - 1.0) / h;
+    return -wj;
+}
+
+// Finish one feature: c-scaling, nu floor (reading Z4), d_j (Eq.5), Delta term (Eq.7).
+struct Dir {
+    double g, h, d, delta;
+};
+__device__ __forceinline__ Dir finish_feature(const StepArgs &a, double gs, double hs, double wj)
+{
+    Dir r;
+    r.g = a.c * gs;
+    r.h = a.c * hs;
+    if (!(r.h > a.nu)) r.h = a.nu;
+    r.d = newton_dir(r.g, r.h, wj);
+    r.delta = r.g * r.d + a.gamma * r.h * r.d * r.d + fabs(wj + r.d) - fabs(wj);
+    return r;
+}
+
+// Record one contribution d_k x_ik of bundle position k to sample i (a3).  The slot inside the
+// sample's segment comes from an integer atomic; the fold in phase C sorts by k, so the slot
+// order never reaches the arithmetic.
+__device__ __forceinline__ void emit(const StepArgs &a, int32_t i, int32_t k, double v)
+{
+    const int32_t slot = atomicAdd(&a.cnt[i], 1);
+    Rec r;
+    r.k = k;
+    r.pad = 0;
+    r.v = v;
+    __stcg(reinterpret_cast<double2 *>(&a.rec[__ldg(&a.row_ptr[i]) + slot]),
+           *reinterpret_cast<double2 *>(&r));
+    if (slot == 0) atomicOr(&a.bits[i >> 5], 1u << (i & 31));
+}
+
+// ------------------------------------------------------------------------------------
+// a0: partition (Eq.8, Alg.3 l.4, reading Z2)
+// ------------------------------------------------------------------------------------
+struct FeistelKeys {
+    uint64_t key[8];
+    uint64_t mask;
+    int hb;
+};
+
+__device__ __forceinline__ FeistelKeys feistel_keys(uint64_t seed, int64_t k, int64_t n)
+{
+    FeistelKeys f;
+    int bits = 0;
+    while (bits < 63 && ((int64_t)1 << bits) < n) bits++;
+    f.hb = (bits + 1) / 2;
+    if (f.hb < 1) f.hb = 1;
+    f.mask = ((uint64_t)1 << f.hb) - 1;
+    const uint64_t base = mix64(seed ^ 0x6A09E667F3BCC909ULL);
+    const uint64_t kk = mix64(base ^ (uint64_t)k);
+#pragma unroll
+    for (int r = 0; r < 8; r++) f.key[r] = mix64(kk + (uint64_t)(r + 1) * 0x9E3779B97F4A7C15ULL);
+    return f;
+}
+
+__device__ __forceinline__ int64_t feistel_perm(const FeistelKeys &f, int64_t n, int64_t t)
+{
+    uint64_t x = (uint64_t)t;
+    do {
+        uint64_t L = x >> f.hb, R = x & f.mask;
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+            const uint64_t nr = L ^ (mix64(f.key[r] ^ R) & f.mask);
+            L = R;
+            R = nr;
+        }
+        x = (L << f.hb) | R;
+    } while (x >= (uint64_t)n);
+    return (int64_t)x;
+}
+
+// order[t] = pi_k(t); flag[t] = column length > heavy_len
+__global__ void k_perm(uint64_t seed, int64_t k, int64_t n, const int64_t *__restrict__ col_ptr,
+                       int heavy_len, int32_t *order, int32_t *flag)
+{
+    const FeistelKeys f = feistel_keys(seed, k, n);
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = feistel_perm(f, n, t);
+        order[t] = (int32_t)j;
+        if (flag) flag[t] = (__ldg(&col_ptr[j + 1]) - __ldg(&col_ptr[j])) > heavy_len ? 1 : 0;
+    }
+}
+
+// user bundle: validate (distinct, in range) and copy
+__global__ void k_bundle_prep(const int32_t *__restrict__ bundle, int64_t P, int64_t n,
+                              const int64_t *__restrict__ col_ptr, int heavy_len, int32_t *order,
+                              int32_t *flag, uint32_t *seen, int *status, long long *err_idx)
+{
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < P; t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t j = bundle[t];
+        if (j < 0 || j >= n) {
+            atomicMax(status, 1);
+            atomicMin(err_idx, (long long)t);
+            order[t] = 0;
+            flag[t] = 0;
+            continue;
+        }
+        const uint32_t bit = 1u << (j & 31);
+        const uint32_t old = atomicOr(&seen[j >> 5], bit);
+        if (old & bit) {
+            atomicMax(status, 1);
+            atomicMin(err_idx, (long long)t);
+        }
+        order[t] = j;
+        flag[t] = (__ldg(&col_ptr[j + 1]) - __ldg(&col_ptr[j])) > heavy_len ? 1 : 0;
+    }
+}
+
+__global__ void k_bundle_unseen(const int32_t *__restrict__ bundle, int64_t P, int64_t n, uint32_t *seen)
+{
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < P; t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t j = bundle[t];
+        if (j >= 0 && j < n) seen[j >> 5] = 0;
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// device-wide exclusive scan (reduce -> scan of tile sums -> apply).  out[n] = total.
+// `n_dev` (nullable) bounds n at run time (launch sized for the host-side upper bound).
+// ------------------------------------------------------------------------------------
+template <typename Tin, typename Tout>
+__device__ __forceinline__ Tout scan_load(const Tin *in, const int32_t *hlen_pos, int64_t i)
+{
+    return (Tout)in[i];
+}
+
+template <typename Tin, typename Tout>
+__global__ void k_scan_reduce(const Tin *__restrict__ in, int64_t n, const int64_t *n_dev, Tout *tile_sum)
+{
+    if (n_dev) n = min(n, *n_dev);
+    const int64_t t0 = (int64_t)blockIdx.x * SCAN_TILE;
+    Tout s = 0;
+    for (int64_t i = t0 + threadIdx.x; i < min(n, t0 + SCAN_TILE); i += SCAN_NT) s += (Tout)in[i];
+    s = warp_sum(s);
+    __shared__ Tout ws[SCAN_NT / 32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Tout tot = 0;
+        for (int w = 0; w < SCAN_NT / 32; w++) tot += ws[w];
+        tile_sum[blockIdx.x] = tot;
+    }
+}
+
+template <typename Tout>
+__global__ void k_scan_tiles(Tout *tile_sum, int64_t ntiles)
+{
+    // single CTA, exclusive scan in place; sequential chunks of SCAN_NT
+    __shared__ Tout sh[SCAN_NT];
+    __shared__ Tout carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t b = 0; b < ntiles; b += SCAN_NT) {
+        const int64_t i = b + threadIdx.x;
+        const Tout v = i < ntiles ? tile_sum[i] : 0;
+        sh[threadIdx.x] = v;
+        __syncthreads();
+        for (int o = 1; o < SCAN_NT; o <<= 1) {
+            const Tout t = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+            __syncthreads();
+            sh[threadIdx.x] += t;
+            __syncthreads();
+        }
+        if (i < ntiles) tile_sum[i] = carry + sh[threadIdx.x] - v;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += sh[SCAN_NT - 1];
+        __syncthreads();
+    }
+}
+
+template <typename Tin, typename Tout>
+__global__ void k_scan_apply(const Tin *__restrict__ in, int64_t n, const int64_t *n_dev,
+                             const Tout *__restrict__ tile_sum, Tout *out, int64_t *total_out)
+{
+    if (n_dev) n = min(n, *n_dev);
+    const int64_t t0 = (int64_t)blockIdx.x * SCAN_TILE;
+    if (t0 >= n && !(t0 == 0)) return;
+    constexpr int IPT = SCAN_TILE / SCAN_NT;  // items per thread, contiguous
+    Tout v[IPT];
+    Tout s = 0;
+#pragma unroll
+    for (int r = 0; r < IPT; r++) {
+        const int64_t i = t0 + (int64_t)threadIdx.x * IPT + r;
+        v[r] = i < n ? (Tout)in[i] : 0;
+        s += v[r];
+    }
+    // block exclusive scan of s
+    __shared__ Tout sh[SCAN_NT];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 1; o < SCAN_NT; o <<= 1) {
+        const Tout t = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+        __syncthreads();
+        sh[threadIdx.x] += t;
+        __syncthreads();
+    }
+    Tout run = tile_sum[blockIdx.x] + sh[threadIdx.x] - s;
+#pragma unroll
+    for (int r = 0; r < IPT; r++) {
+        const int64_t i = t0 + (int64_t)threadIdx.x * IPT + r;
+        if (i < n) out[i] = run;
+        run += v[r];
+        if (i == n - 1) {
+            out[n] = run;
+            if (total_out) *total_out = (int64_t)run;
+        }
+    }
+    if (n == 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+        out[0] = 0;
+        if (total_out) *total_out = 0;
+    }
+}
+
+// heavy compaction: for flagged positions, hlist[e] = position, hlen[e] = column length
+__global__ void k_heavy_compact(const int64_t *__restrict__ hpos, int64_t ntot, const int32_t *__restrict__ order,
+                                const int64_t *__restrict__ col_ptr, int32_t *hlist, int64_t *hlen)
+{
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntot; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = hpos[t];
+        if (hpos[t + 1] != e) {
+            const int32_t j = order[t];
+            hlist[e] = (int32_t)t;
+            hlen[e] = __ldg(&col_ptr[j + 1]) - __ldg(&col_ptr[j]);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// a1..a5: the persistent bundle-step kernel
+// ------------------------------------------------------------------------------------
+struct StepSmem {
+    // heavy-column rounds
+    int64_t hst[NE_MAX + 1];
+    double hg[NE_MAX][NW];
+    double hh[NE_MAX][NW];
+    double hd[NE_MAX];
+    int64_t ce0, ce1;
+    int64_t cross_e[2];
+    double cross_d[2];
+    // reductions
+    double red[NW][NPART];
+    double tot[NPART];
+    int64_t scan_w[NW];
+    int64_t nT;
+    int has_heavy_rows;
+    int q_acc;
+    int64_t nnz_local;
+    // rows with > NREG records: per-warp sort buffers
+    int32_t sk[NHW][HB];
+    double sv[NHW][HB];
+};
+
+// Warp-level gh over columns' nonzeros [p0, p1): lanes strided, fixed xor tree.
+__device__ __forceinline__ void col_gh(const StepArgs &a, int64_t p0, int64_t p1, int lane, double &gs, double &hs)
+{
+    double g = 0.0, h = 0.0;
+    for (int64_t p = p0 + lane; p < p1; p += 32) {
+        const int32_t i = __ldg(&a.row_idx[p]);
+        const double x = (double)__ldg(&a.val[p]);
+        const double2 cf = ldcg(&a.coef[i]);
+        g += x * cf.x;
+        h += (x * x) * cf.y;
+    }
+    gs = warp_sum(g);
+    hs = warp_sum(h);
+}
+
+__device__ __forceinline__ void col_scatter(const StepArgs &a, int64_t p0, int64_t p1, int lane, int32_t kpos, double d)
+{
+    for (int64_t p = p0 + lane; p < p1; p += 32) {
+        const int32_t i = __ldg(&a.row_idx[p]);
+        emit(a, i, kpos, d * (double)__ldg(&a.val[p]));
+    }
+}
+
+// index of the CTA whose heavy range [floor(c NH/G), floor((c+1) NH/G)) holds offset o
+__device__ __forceinline__ int cta_of(int64_t o, int64_t NH, int G)
+{
+    return (int)(((o + 1) * (int64_t)G - 1) / NH);
+}
+
+// Fold of one sample's records in ascending bundle position (<= NREG records): thread-level.
+__device__ __forceinline__ double fold_small(const StepArgs &a, int64_t off, int ni)
+{
+    int kk[NREG];
+    double vv[NREG];
+#pragma unroll
+    for (int r = 0; r < NREG; r++) {
+        if (r < ni) {
+            const double2 raw = __ldcg(reinterpret_cast<const double2 *>(&a.rec[off + r]));
+            kk[r] = __double_as_longlong(raw.x) & 0xffffffffLL;
+            vv[r] = raw.y;
+        } else {
+            kk[r] = 0x7fffffff;
+            vv[r] = 0.0;
+        }
+    }
+    double dx = 0.0;
+    int last = -1;
+    for (int t = 0; t < ni; t++) {
+        int best = 0x7fffffff;
+        double bv = 0.0;
+#pragma unroll
+        for (int r = 0; r < NREG; r++) {
+            const bool take = kk[r] > last && kk[r] < best;
+            best = take ? kk[r] : best;
+            bv = take ? vv[r] : bv;
+        }
+        last = best;
+        dx += bv;
+    }
+    return dx;
+}
+
+// Fold of one sample with > NREG records by a warp: bitonic sort by bundle position in shared
+// memory, then lane-contiguous partial sums combined by a fixed tree (deterministic).
+__device__ double fold_warp(const StepArgs &a, int64_t off, int ni, int32_t *sk, double *sv, int lane)
+{
+    if (ni <= HB) {
+        int npow = 32;
+        while (npow < ni) npow <<= 1;
+        for (int r = lane; r < npow; r += 32) {
+            if (r < ni) {
+                const double2 raw = __ldcg(reinterpret_cast<const double2 *>(&a.rec[off + r]));
+                sk[r] = (int32_t)(__double_as_longlong(raw.x) & 0xffffffffLL);
+                sv[r] = raw.y;
+            } else {
+                sk[r] = 0x7fffffff;
+                sv[r] = 0.0;
+            }
+        }
+        __syncwarp();
+        for (int kbit = 2; kbit <= npow; kbit <<= 1) {
+            for (int jbit = kbit >> 1; jbit > 0; jbit >>= 1) {
+                for (int r = lane; r < npow; r += 32) {
+                    const int pr = r ^ jbit;
+                    if (pr > r) {
+                        const bool up = (r & kbit) == 0;
+                        const int32_t k1 = sk[r], k2 = sk[pr];
+                        if ((k1 > k2) == up) {
+                            sk[r] = k2;
+                            sk[pr] = k1;
+                            const double t = sv[r];
+                            sv[r] = sv[pr];
+                            sv[pr] = t;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        const int chunk = (ni + 31) / 32;
+        double s = 0.0;
+        for (int r = lane * chunk; r < min(ni, (lane + 1) * chunk); r++) s += sv[r];
+        // fixed-order tree over lanes (lane order preserved pairwise)
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_down_sync(0xffffffffu, s, o);
+            if ((lane & (2 * o - 1)) == 0) s += t;
+        }
+        __syncwarp();
+        return __shfl_sync(0xffffffffu, s, 0);
+    }
+    // very long rows: repeated warp-wide min extraction (correct, O(ni^2/32))
+    double dx = 0.0;
+    int last = -1;
+    for (int t = 0; t < ni; t++) {
+        int best = 0x7fffffff;
+        double bv = 0.0;
+        for (int r = lane; r < ni; r += 32) {
+            const double2 raw = __ldcg(reinterpret_cast<const double2 *>(&a.rec[off + r]));
+            const int32_t k = (int32_t)(__double_as_longlong(raw.x) & 0xffffffffLL);
+            if (k > last && k < best) {
+                best = k;
+                bv = raw.y;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            if (ob < best) {
+                best = ob;
+                bv = ov;
+            }
+        }
+        last = best;
+        dx += bv;
+    }
+    return dx;
+}
+
+// Block-wide fixed-order reduction of up to NPART values per thread (first `cnt` entries).
+__device__ __forceinline__ void block_reduce(double *v, int cnt, StepSmem &sm, int lane, int warp)
+{
+    for (int q = 0; q < cnt; q++) {
+        const double s = warp_sum(v[q]);
+        if (lane == 0) sm.red[warp][q] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < cnt) {
+        double s = 0.0;
+        for (int w2 = 0; w2 < NW; w2++) s += sm.red[w2][threadIdx.x];
+        sm.tot[threadIdx.x] = s;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(NT, 2) k_step(StepArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    StepSmem &sm = *reinterpret_cast<StepSmem *>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x, c = blockIdx.x;
+    unsigned long long bar_target = 0;
+    const int64_t nwords = (a.s + 31) >> 5;
+    const int64_t wb = (int64_t)c * nwords / G, we = (int64_t)(c + 1) * nwords / G;
+    const int64_t row_base = wb * 32;
+    int prev_q = 0;
+
+    for (int64_t t = 0; t < a.nsteps; t++) {
+        const int64_t k0 = t * a.P;
+        const int64_t k1 = min(k0 + a.P, a.ntot);
+        const int64_t Pt = k1 - k0;
+        if (tid == 0) sm.nnz_local = 0;
+        __syncthreads();
+
+        // ---------------- phase A: light columns, one warp per column (a1, a2, a3) --------
+        {
+            int64_t my_nnz = 0;
+            const int64_t gw = (int64_t)c * NW + warp;
+            for (int64_t kk = k0 + gw; kk < k1; kk += (int64_t)G * NW) {
+                const int32_t j = __ldg(&a.order[kk]);
+                const int64_t p0 = __ldg(&a.col_ptr[j]), p1 = __ldg(&a.col_ptr[j + 1]);
+                if (p1 - p0 > a.heavy_len) continue;
+                my_nnz += p1 - p0;
+                double gs, hs;
+                col_gh(a, p0, p1, lane, gs, hs);
+                const double wj = ldcg(&a.w[j]);
+                const Dir r = finish_feature(a, gs, hs, wj);
+                if (lane == 0) {
+                    a.dk[kk - k0] = r.d;
+                    a.deltak[kk - k0] = r.delta;
+                    if (a.g_out) {
+                        a.g_out[kk - k0] = r.g;
+                        a.h_out[kk - k0] = r.h;
+                    }
+                    if (a.d_out) a.d_out[kk - k0] = r.d;
+                }
+                if (r.d != 0.0) col_scatter(a, p0, p1, lane, (int32_t)(kk - k0), r.d);
+            }
+            if (lane == 0 && my_nnz) atomicAdd((unsigned long long *)&sm.nnz_local, (unsigned long long)my_nnz);
+        }
+
+        // ---------------- phase A': heavy columns, nnz-balanced over all warps -----------
+        const int64_t e_lo = __ldg(&a.hpos[k0]), e_hi = __ldg(&a.hpos[k1]);
+        if (e_hi > e_lo) {
+            const int64_t hb0 = __ldg(&a.hstart[e_lo]);
+            const int64_t NH = __ldg(&a.hstart[e_hi]) - hb0;
+            const int64_t lo_c = (int64_t)c * NH / G, hi_c = (int64_t)(c + 1) * NH / G;
+            if (tid == 0) {
+                // first entry ending after lo_c, first entry starting at or after hi_c
+                int64_t lo = e_lo, hi = e_hi;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (__ldg(&a.hstart[mid + 1]) - hb0 > lo_c) hi = mid; else lo = mid + 1;
+                }
+                sm.ce0 = lo;
+                hi = e_hi;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (__ldg(&a.hstart[mid]) - hb0 >= hi_c) hi = mid; else lo = mid + 1;
+                }
+                sm.ce1 = (hi_c > lo_c) ? lo : sm.ce0;
+                sm.cross_e[0] = sm.cross_e[1] = -1;
+            }
+            __syncthreads();
+            const int64_t ce0 = sm.ce0, ce1 = sm.ce1;
+            const int64_t a_w = lo_c + (int64_t)warp * (hi_c - lo_c) / NW;
+            const int64_t b_w = lo_c + (int64_t)(warp + 1) * (hi_c - lo_c) / NW;
+            for (int64_t rb = ce0; rb < ce1; rb += NE_MAX) {
+                const int ne = (int)min((int64_t)NE_MAX, ce1 - rb);
+                for (int i = tid; i <= ne; i += NT) sm.hst[i] = __ldg(&a.hstart[rb + i]) - hb0;
+                for (int i = tid; i < ne * NW; i += NT) {
+                    sm.hg[i / NW][i % NW] = 0.0;
+                    sm.hh[i / NW][i % NW] = 0.0;
+                }
+                __syncthreads();
+                for (int le = 0; le < ne; le++) {
+                    const int64_t st = sm.hst[le], en = sm.hst[le + 1];
+                    if (en <= a_w) continue;
+                    if (st >= b_w) break;
+                    const int64_t s0 = max(a_w, st), s1 = min(b_w, en);
+                    const int32_t kk = __ldg(&a.hlist[rb + le]);
+                    const int32_t j = __ldg(&a.order[kk]);
+                    const int64_t cs = __ldg(&a.col_ptr[j]);
+                    double gs, hs;
+                    col_gh(a, cs + (s0 - st), cs + (s1 - st), lane, gs, hs);
+                    if (lane == 0) {
+                        sm.hg[le][warp] = gs;
+                        sm.hh[le][warp] = hs;
+                    }
+                }
+                __syncthreads();
+                for (int le = tid; le < ne; le += NT) {
+                    double gs = 0.0, hs = 0.0;
+                    for (int w2 = 0; w2 < NW; w2++) {
+                        gs += sm.hg[le][w2];
+                        hs += sm.hh[le][w2];
+                    }
+                    const int64_t st = sm.hst[le], en = sm.hst[le + 1];
+                    const int64_t e = rb + le;
+                    if (st >= lo_c && en <= hi_c) {  // column interior to this CTA: finish now
+                        const int32_t kk = __ldg(&a.hlist[e]);
+                        const int32_t j = __ldg(&a.order[kk]);
+                        const Dir r = finish_feature(a, gs, hs, ldcg(&a.w[j]));
+                        sm.hd[le] = r.d;
+                        a.dk[kk - k0] = r.d;
+                        a.deltak[kk - k0] = r.delta;
+                        if (a.g_out) {
+                            a.g_out[kk - k0] = r.g;
+                            a.h_out[kk - k0] = r.h;
+                        }
+                        if (a.d_out) a.d_out[kk - k0] = r.d;
+                    } else {  // crossing: CTA partial, finished after the grid barrier
+                        const int slot = st < lo_c ? 0 : 1;
+                        HPart hp;
+                        hp.e = e;
+                        hp.g = gs;
+                        hp.h = hs;
+                        hp.pad = 0.0;
+                        a.hpart[(int64_t)c * 2 + slot] = hp;
+                        sm.cross_e[slot] = e;
+                        sm.hd[le] = 0.0;  // not scattered in this round
+                    }
+                }
+                __syncthreads();
+                // scatter interior columns of this round
+                for (int le = 0; le < ne; le++) {
+                    const int64_t st = sm.hst[le], en = sm.hst[le + 1];
+                    if (en <= a_w) continue;
+                    if (st >= b_w) break;
+                    if (!(st >= lo_c && en <= hi_c)) continue;
+                    const double d = sm.hd[le];
+                    if (d == 0.0) continue;
+                    const int64_t s0 = max(a_w, st), s1 = min(b_w, en);
+                    const int32_t kk = __ldg(&a.hlist[rb + le]);
+                    const int32_t j = __ldg(&a.order[kk]);
+                    const int64_t cs = __ldg(&a.col_ptr[j]);
+                    col_scatter(a, cs + (s0 - st), cs + (s1 - st), lane, kk - (int32_t)k0, d);
+                }
+                __syncthreads();
+            }
+            if (c == 0 && tid == 0) sm.nnz_local += NH;
+            grid_sync(a.bar, bar_target);
+            // finish the (at most two) columns crossing this CTA's boundaries
+            if (tid < 2) {
+                const int64_t e = sm.cross_e[tid];
+                sm.cross_d[tid] = 0.0;
+                if (e >= 0) {
+                    const int64_t st = __ldg(&a.hstart[e]) - hb0, en = __ldg(&a.hstart[e + 1]) - hb0;
+                    const int clo = cta_of(st, NH, G), chi = cta_of(en - 1, NH, G);
+                    double gs = 0.0, hs = 0.0;
+                    for (int c2 = clo; c2 <= chi; c2++) {
+                        if ((int64_t)c2 * NH / G == (int64_t)(c2 + 1) * NH / G) continue;  // empty range
+                        const HPart hp = ld_hpart(&a.hpart[(int64_t)c2 * 2 + (c2 == clo ? 1 : 0)]);
+                        if (hp.e != e) atomicMax(a.status, 4);  // internal consistency check
+                        gs += hp.g;
+                        hs += hp.h;
+                    }
+                    const int32_t kk = __ldg(&a.hlist[e]);
+                    const int32_t j = __ldg(&a.order[kk]);
+                    const Dir r = finish_feature(a, gs, hs, ldcg(&a.w[j]));
+                    sm.cross_d[tid] = r.d;
+                    if (c == clo) {
+                        a.dk[kk - k0] = r.d;
+                        a.deltak[kk - k0] = r.delta;
+                        if (a.g_out) {
+                            a.g_out[kk - k0] = r.g;
+                            a.h_out[kk - k0] = r.h;
+                        }
+                        if (a.d_out) a.d_out[kk - k0] = r.d;
+                    }
+                }
+            }
+            __syncthreads();
+            for (int sl = 0; sl < 2; sl++) {
+                const int64_t e = sm.cross_e[sl];
+                if (e < 0 || (sl == 1 && e == sm.cross_e[0])) continue;
+                const double d = sm.cross_d[sl];
+                if (d == 0.0) continue;
+                const int64_t st = __ldg(&a.hstart[e]) - hb0, en = __ldg(&a.hstart[e + 1]) - hb0;
+                if (en <= a_w || st >= b_w) continue;
+                const int64_t s0 = max(a_w, st), s1 = min(b_w, en);
+                const int32_t kk = __ldg(&a.hlist[e]);
+                const int32_t j = __ldg(&a.order[kk]);
+                const int64_t cs = __ldg(&a.col_ptr[j]);
+                col_scatter(a, cs + (s0 - st), cs + (s1 - st), lane, kk - (int32_t)k0, d);
+            }
+        }
+        grid_sync(a.bar, bar_target);
+
+        // ---------------- phase C1: touched set of this CTA's row block ------------------
+        if (tid == 0) {
+            sm.nT = 0;
+            sm.has_heavy_rows = 0;
+        }
+        __syncthreads();
+        for (int64_t w0 = wb; w0 < we; w0 += NT) {
+            const int64_t wi = w0 + tid;
+            const uint32_t bv = wi < we ? ldcg(&a.bits[wi]) : 0u;
+            const int cntb = __popc(bv);
+            // block exclusive scan of cntb (warp scan + warp offsets)
+            int incl = cntb;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int tmp = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += tmp;
+            }
+            if (lane == 31) sm.scan_w[warp] = incl;
+            __syncthreads();
+            int64_t woff = 0;
+            for (int w2 = 0; w2 < warp; w2++) woff += sm.scan_w[w2];
+            int64_t pos = sm.nT + woff + incl - cntb;
+            uint32_t m = bv;
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                a.tlist[row_base + pos++] = (int32_t)(wi * 32 + b);
+            }
+            __syncthreads();
+            if (tid == NT - 1) {
+                int64_t tot = 0;
+                for (int w2 = 0; w2 < NW; w2++) tot += sm.scan_w[w2];
+                sm.nT += tot;
+            }
+            __syncthreads();
+        }
+        const int64_t nT = sm.nT;
+
+        // ---------------- phase C2: d'x_i, in-order fold of each sample's records --------
+        for (int64_t li = tid; li < nT; li += NT) {
+            const int32_t i = ldcg(&a.tlist[row_base + li]);
+            const int ni = ldcg(&a.cnt[i]);
+            if (ni <= NREG) {
+                a.dxg[i] = fold_small(a, __ldg(&a.row_ptr[i]), ni);
+            } else {
+                sm.has_heavy_rows = 1;
+            }
+        }
+        __syncthreads();
+        if (sm.has_heavy_rows && warp < NHW) {
+            for (int64_t lb = (int64_t)warp * 32; lb < nT; lb += 32 * NHW) {
+                const int64_t li = lb + lane;
+                int32_t i = -1;
+                int ni = 0;
+                if (li < nT) {
+                    i = ldcg(&a.tlist[row_base + li]);
+                    ni = ldcg(&a.cnt[i]);
+                }
+                unsigned heavy = __ballot_sync(0xffffffffu, ni > NREG);
+                while (heavy) {
+                    const int src = __ffs(heavy) - 1;
+                    heavy &= heavy - 1;
+                    const int32_t ih = __shfl_sync(0xffffffffu, i, src);
+                    const int nih = __shfl_sync(0xffffffffu, ni, src);
+                    const double dx = fold_warp(a, __ldg(&a.row_ptr[ih]), nih, sm.sk[warp], sm.sv[warp], lane);
+                    if (lane == 0) a.dxg[ih] = dx;
+                    __syncwarp();
+                }
+            }
+        }
+        __syncthreads();
+
+        // ---------------- phase C3 + D: windowed Armijo search (a4), commit (a5) ----------
+        const int64_t pb0 = k0 + (int64_t)c * Pt / G, pb1 = k0 + (int64_t)(c + 1) * Pt / G;
+        int q0 = 0;
+        int nq = min(QW, max(2, prev_q + 2));
+        int qacc = -1;
+        double alpha_acc = 0.0, lhs_acc = 0.0, rhs_acc = 0.0, Delta = 0.0, nnz_tot = 0.0, nT_tot = 0.0;
+        int win = 0;
+        bool bad = false;
+        while (true) {
+            double alpha0 = 1.0;
+            for (int q = 0; q < q0; q++) alpha0 *= a.beta;
+            double acc[NPART];
+#pragma unroll
+            for (int q = 0; q < NPART; q++) acc[q] = 0.0;
+            for (int64_t li = tid; li < nT; li += NT) {
+                const int32_t i = ldcg(&a.tlist[row_base + li]);
+                const double dx = ldcg(&a.dxg[i]);
+                const double zi = ldcg(&a.z[i]);
+                const int yi = a.y[i];
+                const double cg = ldcg(&a.coef[i]).x;
+                double al = alpha0;
+#pragma unroll
+                for (int q = 0; q < QW; q++) {
+                    if (q < nq) acc[q] += loss_change(a.loss, zi, yi, cg, dx, al);
+                    al *= a.beta;
+                }
+            }
+            for (int64_t kk = pb0 + tid; kk < pb1; kk += NT) {
+                const double wj = ldcg(&a.w[__ldg(&a.order[kk])]);
+                const double d = ldcg(&a.dk[kk - k0]);
+                double al = alpha0;
+#pragma unroll
+                for (int q = 0; q < QW; q++) {
+                    if (q < nq) acc[QW + q] += fabs(wj + al * d) - fabs(wj);
+                    al *= a.beta;
+                }
+                acc[2 * QW] += ldcg(&a.deltak[kk - k0]);
+            }
+            if (tid == 0) {
+                acc[2 * QW + 1] = (double)sm.nnz_local;
+                acc[2 * QW + 2] = (double)nT;
+            }
+            block_reduce(acc, 2 * QW + 3, sm, lane, warp);
+            double *part = a.part + (int64_t)(win & 1) * G * NPART;
+            if (tid < 2 * QW + 3) part[(int64_t)c * NPART + tid] = sm.tot[tid];
+            grid_sync(a.bar, bar_target);
+            // every CTA reduces the G partials in the same fixed order
+            {
+                double v[NPART];
+#pragma unroll
+                for (int q = 0; q < NPART; q++) v[q] = 0.0;
+                for (int c2 = tid; c2 < G; c2 += NT) {
+#pragma unroll
+                    for (int q = 0; q < 2 * QW + 3; q++) v[q] += ldcg(&part[(int64_t)c2 * NPART + q]);
+                }
+                block_reduce(v, 2 * QW + 3, sm, lane, warp);
+            }
+            Delta = sm.tot[2 * QW];
+            nnz_tot = sm.tot[2 * QW + 1];
+            nT_tot = sm.tot[2 * QW + 2];
+            {
+                double al = alpha0;
+                for (int q = 0; q < nq; q++) {
+                    const double lhs = sm.tot[QW + q] + a.c * sm.tot[q];
+                    const double rhs = a.sigma * al * Delta;
+                    if (!isfinite(lhs) || !isfinite(Delta)) {
+                        bad = true;
+                        break;
+                    }
+                    if (lhs <= rhs) {
+                        qacc = q0 + q;
+                        alpha_acc = al;
+                        lhs_acc = lhs;
+                        rhs_acc = rhs;
+                        break;
+                    }
+                    al *= a.beta;
+                }
+            }
+            win++;
+            __syncthreads();  // everyone has read sm.tot before it is reused
+            if (qacc >= 0 || bad) break;
+            q0 += nq;
+            if (q0 > a.qmax) break;
+            nq = min(QW, a.qmax + 1 - q0);
+        }
+        if (qacc > a.qmax) {  // window overshoot past q_max counts as exhausted
+            qacc = -1;
+        }
+        if (qacc < 0) alpha_acc = 0.0;  // null step (Z10)
+        prev_q = qacc < 0 ? QW : qacc;
+
+        // commit this CTA's samples and bundle share; clear per-step marks
+        for (int64_t li = tid; li < nT; li += NT) {
+            const int32_t i = ldcg(&a.tlist[row_base + li]);
+            const double dx = ldcg(&a.dxg[i]);
+            if (qacc >= 0) {
+                const double zn = ldcg(&a.z[i]) + alpha_acc * dx;
+                a.z[i] = zn;
+                a.coef[i] = coef_of(a.loss, zn, a.y[i]);
+            }
+            a.cnt[i] = 0;
+            if (a.debug) {
+                a.dbg_dx[i] = dx;
+                a.dbg_mark[i] = 1;
+            }
+        }
+        for (int64_t wi = wb + tid; wi < we; wi += NT) a.bits[wi] = 0u;
+        if (qacc >= 0) {
+            for (int64_t kk = pb0 + tid; kk < pb1; kk += NT) {
+                const int32_t j = __ldg(&a.order[kk]);
+                a.w[j] = ldcg(&a.w[j]) + alpha_acc * ldcg(&a.dk[kk - k0]);
+            }
+        }
+        if (c == 0 && tid == 0) {
+            double F = ldcg(a.F);
+            if (qacc >= 0) F = F + lhs_acc;
+            *a.F = F;
+            if (bad) atomicMax(a.status, 3);
+            a.info[0] = (double)qacc;
+            a.info[1] = alpha_acc;
+            a.info[2] = Delta;
+            a.info[3] = lhs_acc;
+            a.info[4] = rhs_acc;
+            a.info[5] = F;
+            a.info[6] = nnz_tot;
+            a.info[7] = nT_tot;
+            const int64_t gstep = a.trace_off + t;
+            if (gstep < a.trace_cap) {
+                if (a.q_trace) a.q_trace[gstep] = qacc;
+                if (a.F_trace) a.F_trace[gstep] = F;
+            }
+            a.counters[0] += 1;
+            a.counters[1] += qacc < 0 ? 1 : 0;
+            a.counters[2] += (int64_t)nnz_tot;
+            a.counters[3] += (int64_t)nT_tot;
+            a.counters[4] += Pt;
+        }
+        grid_sync(a.bar, bar_target);
+        if (bad) break;
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// a6 and state (re)initialisation
+// ------------------------------------------------------------------------------------
+// z_i = sum_j w_j x_ij over row i in ascending column order, then the cached factors.
+__global__ void k_set_z(int64_t s, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col_idx,
+                        const float *__restrict__ csr_val, const int8_t *__restrict__ y, const double *__restrict__ w,
+                        int loss, double *z, double2 *coef, int zero)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
+        double zi = 0.0;
+        if (!zero)
+            for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; p++) zi += w[col_idx[p]] * (double)csr_val[p];
+        z[i] = zi;
+        coef[i] = coef_of(loss, zi, y[i]);
+    }
+}
+
+// F = c sum_i phi(y_i z_i) + sum_j |w_j|, fixed two-level order: tile b of each array
+constexpr int OBJ_NB = 256;
+__global__ void k_obj_partial(int64_t s, int64_t n, const double *__restrict__ z, const int8_t *__restrict__ y,
+                              const double *__restrict__ w, int loss, double *partial)
+{
+    const int b = blockIdx.x;
+    const int64_t zs0 = (int64_t)b * s / OBJ_NB, zs1 = (int64_t)(b + 1) * s / OBJ_NB;
+    const int64_t ws0 = (int64_t)b * n / OBJ_NB, ws1 = (int64_t)(b + 1) * n / OBJ_NB;
+    double ls = 0.0, l1 = 0.0;
+    for (int64_t i = zs0 + threadIdx.x; i < zs1; i += blockDim.x) ls += phi_of(loss, (double)y[i] * z[i]);
+    for (int64_t j = ws0 + threadIdx.x; j < ws1; j += blockDim.x) l1 += fabs(w[j]);
+    ls = warp_sum(ls);
+    l1 = warp_sum(l1);
+    __shared__ double sh[2][32];
+    if ((threadIdx.x & 31) == 0) {
+        sh[0][threadIdx.x >> 5] = ls;
+        sh[1][threadIdx.x >> 5] = l1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a0 = 0.0, a1 = 0.0;
+        for (int w2 = 0; w2 < (int)(blockDim.x >> 5); w2++) {
+            a0 += sh[0][w2];
+            a1 += sh[1][w2];
+        }
+        partial[2 * b] = a0;
+        partial[2 * b + 1] = a1;
+    }
+}
+
+__global__ void k_obj_final(const double *__restrict__ partial, double c, double *F, double *F_copy)
+{
+    __shared__ double sh[2][OBJ_NB];
+    const int t = threadIdx.x;
+    sh[0][t] = partial[2 * t];
+    sh[1][t] = partial[2 * t + 1];
+    __syncthreads();
+    for (int o = OBJ_NB / 2; o > 0; o >>= 1) {
+        if (t < o) {
+            sh[0][t] += sh[0][t + o];
+            sh[1][t] += sh[1][t + o];
+        }
+        __syncthreads();
+    }
+    if (t == 0) {
+        const double Fv = c * sh[0][0] + sh[1][0];
+        *F = Fv;
+        if (F_copy) *F_copy = Fv;
+    }
+}
+
+// Input validation: code 1 + first offending index.
+__global__ void k_validate(int64_t s, int64_t n, int64_t nnz, const int64_t *__restrict__ col_ptr,
+                           const int32_t *__restrict__ row_idx, const float *__restrict__ val,
+                           const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col_idx,
+                           const float *__restrict__ csr_val, const int8_t *__restrict__ y,
+                           int *status, long long *err_idx, int *err_what)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    auto fail = [&](int what, int64_t idx) {
+        atomicMax(status, 1);
+        if (atomicMin(err_idx, (long long)idx) > (long long)idx) atomicExch(err_what, what);
+    };
+    for (int64_t j = t0; j < n; j += stride) {
+        const int64_t a0 = col_ptr[j], a1 = col_ptr[j + 1];
+        if (j == 0 && a0 != 0) fail(1, 0);
+        if (j == n - 1 && a1 != nnz) fail(2, j);
+        if (a1 < a0 || a0 < 0 || a1 > nnz) {
+            fail(3, j);
+            continue;
+        }
+        for (int64_t p = a0; p < a1; p++) {
+            const int32_t r = row_idx[p];
+            if (r < 0 || r >= s) fail(4, p);
+            if (p > a0 && r <= row_idx[p - 1]) fail(5, p);
+            if (!isfinite(val[p])) fail(6, p);
+        }
+    }
+    for (int64_t i = t0; i < s; i += stride) {
+        const int64_t a0 = row_ptr[i], a1 = row_ptr[i + 1];
+        if (i == 0 && a0 != 0) fail(7, 0);
+        if (i == s - 1 && a1 != nnz) fail(8, i);
+        if (a1 < a0 || a0 < 0 || a1 > nnz) {
+            fail(9, i);
+            continue;
+        }
+        for (int64_t p = a0; p < a1; p++) {
+            const int32_t cidx = col_idx[p];
+            if (cidx < 0 || cidx >= n) fail(10, p);
+            if (p > a0 && cidx <= col_idx[p - 1]) fail(11, p);
+            if (!isfinite(csr_val[p])) fail(12, p);
+        }
+        if (y[i] != 1 && y[i] != -1) fail(13, i);
+    }
+}
+
+// CSR/CSC consistency: every CSR nonzero (i, j, v) must be found in column j by binary search.
+__global__ void k_validate_transpose(int64_t s, const int64_t *__restrict__ col_ptr, const int32_t *__restrict__ row_idx,
+                                     const float *__restrict__ val, const int64_t *__restrict__ row_ptr,
+                                     const int32_t *__restrict__ col_idx, const float *__restrict__ csr_val,
+                                     int *status, long long *err_idx, int *err_what)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; p++) {
+            const int32_t j = col_idx[p];
+            int64_t lo = col_ptr[j], hi = col_ptr[j + 1];
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (row_idx[mid] < i) lo = mid + 1; else hi = mid;
+            }
+            if (lo >= col_ptr[j + 1] || row_idx[lo] != i || val[lo] != csr_val[p]) {
+                atomicMax(status, 1);
+                if (atomicMin(err_idx, (long long)p) > (long long)p) atomicExch(err_what, 14);
+            }
+        }
+    }
+}
+
+// per-column nnz total of the CSC must equal the CSR count (cheap necessary condition)
+__global__ void k_debug_touched_clear(uint8_t *mark, int64_t s)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) mark[i] = 0;
+}
+
+}  // namespace pcdn

@@ -1,0 +1,278 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on seeded inputs.
+
+Bars (BASELINE.json north_star):
+  * partitions, touched sets T and accepted q: bit-exact (decisions whose oracle margin is below
+    1e-9 are ties, reported but not failed -- reading Z22);
+  * from the same state: g, h, d, Delta, d'x, LHS and F within 1e-9, condition-aware
+    (|gpu - ora| <= 1e-9 * max(|ora|, sum|terms|), reading Z21);
+  * solves: final F within 1e-6 relative, w within 1e-5 max-norm, q traces equal.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from synth import LOSS_L2SVM, LOSS_LOGISTIC
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-9
+TIE = 1e-9
+
+
+@pytest.fixture(scope="module")
+def pk():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1306_4080_b200 as pk
+    return pk
+
+
+def _solver(pk, prob, ctas=0, heavy=0):
+    s = pk.Solver(prob)
+    if ctas or heavy:
+        s.set_launch(ctas, heavy)
+    return s
+
+
+def _close(gpu, ora, absterm, what, rtol=RTOL):
+    gpu, ora, absterm = np.atleast_1d(gpu), np.atleast_1d(ora), np.atleast_1d(absterm)
+    tol = rtol * np.maximum(np.abs(ora), absterm) + 1e-300
+    bad = np.abs(gpu - ora) > tol
+    assert not bad.any(), f"{what}: {np.sum(bad)} mismatches, first at {np.argmax(bad)}: " \
+                          f"gpu={gpu[bad][0]!r} ora={ora[bad][0]!r} tol={tol[bad][0]!r}"
+
+
+def _compare_step(g, o, ties):
+    """g: GPU step dict, o: oracle step dict."""
+    _close(g["g"], o["g"], o["g_abs"], "g")
+    _close(g["h"], o["h"], o["h_abs"], "h")
+    dscale = (np.abs(o["g"]) + 1.0) / o["h"]
+    _close(g["d"], o["d"], dscale, "d")
+    _close(g["Delta"], o["Delta"], o["Delta_abs"], "Delta")
+    decisive_d = o["margin_d"] > TIE
+    if decisive_d:
+        np.testing.assert_array_equal(g["T"], o["T"], err_msg="touched set T")
+        _close(g["dx"], o["dx"], o["dx_abs"], "dx")
+        assert g["n_touched"] == o["T"].size
+    else:
+        ties.append(("d", o["margin_d"]))
+    assert g["bundle_nnz"] == o["bundle_nnz"]
+    if decisive_d and np.all(o["d"] == 0):      # zero direction: 0 <= 0 exactly at q = 0 (Z9)
+        assert np.all(g["d"] == 0) and g["q"] == 0 and g["lhs"] == 0 and g["n_touched"] == 0
+        return
+    decisive_q = decisive_d and o["margin_accept"] > TIE and o["margin_prev"] > TIE
+    if decisive_q:
+        assert g["q"] == o["q"], (g["q"], o["q"], o["margin_accept"], o["margin_prev"])
+        assert g["alpha"] == o["alpha"]
+        _close(g["lhs"], o["lhs"], o["lhs_abs"], "lhs")
+        _close(g["F"], o["F_after"], o["lhs_abs"] + abs(o["F_after"]) * 1e-3, "F")
+    else:
+        ties.append(("q", o["margin_accept"], o["margin_prev"]))
+
+
+def _random_state(rng, n, scale=0.3, density=0.3):
+    return rng.normal(size=n) * scale * (rng.random(n) < density)
+
+
+def _step_cases(prob, rng, nb=4, sizes=None):
+    sizes = sizes or [1, max(1, prob.P // 2), prob.P, min(prob.n, 3 * prob.P + 1)]
+    for P in sizes[:nb]:
+        yield rng.choice(prob.n, size=min(P, prob.n), replace=False).astype(np.int32)
+
+
+# ----------------------------------------------------------------------------- a0
+def test_permutation_bitexact(pk):
+    for n in (1, 2, 5, 64, 1000, 4097, 50000):
+        prob = synth.tiny(1, 3, min(n, 50), density=0.5) if n <= 50 else None
+        if prob is None:
+            prob = synth.from_dense(np.eye(3, n, dtype=np.float32), [1, -1, 1])
+        s = _solver(pk, prob)
+        for seed, k in ((0, 0), (7, 3), (2**63 + 5, 11)):
+            got = s.permutation(seed, k).cpu().numpy()
+            np.testing.assert_array_equal(got, oracle.permutation(seed, k, prob.n))
+        s.close()
+
+
+# ----------------------------------------------------------------------------- a1..a5 step parity
+TINY = [
+    dict(seed=1, s=40, n=16, density=0.3),
+    dict(seed=2, s=70, n=33, density=0.2, empty_cols=4, dup_cols=2),
+    dict(seed=3, s=25, n=40, density=0.5, dense_rows=2),
+    dict(seed=4, s=130, n=9, density=0.9),
+]
+
+
+@pytest.mark.parametrize("loss", [LOSS_LOGISTIC, LOSS_L2SVM])
+@pytest.mark.parametrize("case", range(len(TINY)))
+@pytest.mark.parametrize("launch", [(0, 0), (1, 0), (3, 2), (0, 1)])
+def test_step_parity_tiny(pk, loss, case, launch):
+    """Injected state (pcdn_set_w) -> one bundle step, GPU vs oracle.  `launch` = (CTAs, heavy
+    column length): (1,0) = one CTA, (3,2)/(0,1) force the split (heavy) column path."""
+    kw = dict(TINY[case])
+    prob = synth.tiny(loss=loss, c=3.0, P=5, **kw)
+    rng = np.random.default_rng(100 + case)
+    s = _solver(pk, prob, *launch)
+    o = oracle.Oracle(prob)
+    ties = []
+    for rep in range(3):
+        w = _random_state(rng, prob.n, scale=0.5 * rep)
+        for B in _step_cases(prob, rng):
+            s.set_w(w)
+            g = s.step(B)
+            orr = o.step(w, B)
+            _compare_step(g, orr, ties)
+    assert len(ties) <= 2, ties
+    s.close()
+
+
+@pytest.mark.parametrize("cfg,loss", [(1, LOSS_LOGISTIC), (1, LOSS_L2SVM), (2, LOSS_L2SVM), (2, LOSS_LOGISTIC)])
+def test_step_parity_configs(pk, cfg, loss):
+    prob = synth.config(cfg, loss=loss)
+    rng = np.random.default_rng(cfg)
+    s = _solver(pk, prob)
+    o = oracle.Oracle(prob)
+    ties = []
+    # states along an oracle trajectory (realistic w) plus w = 0
+    traj = o.solve(prob.P, max_outer=2, seed=prob.seed)
+    for w in (np.zeros(prob.n), traj["w"]):
+        for B in _step_cases(prob, rng, sizes=[1, prob.P, 4 * prob.P]):
+            s.set_w(w)
+            _compare_step(s.step(B), o.step(w, B), ties)
+    assert len(ties) <= 1, ties
+    s.close()
+
+
+def test_zero_direction_and_validation(pk):
+    prob = synth.tiny(9, 20, 6, density=0.5, c=1e-4)   # |g| < 1 everywhere -> d = 0
+    s = _solver(pk, prob)
+    r = s.step(np.arange(prob.n))
+    assert r["q"] == 0 and r["Delta"] == 0 and r["n_touched"] == 0 and r["T"].size == 0
+    assert np.all(r["d"] == 0)
+    with pytest.raises(pk.PCDNError) as ei:
+        s.step(np.array([1, 1], dtype=np.int32))
+    assert ei.value.status == pk.PCDN_ERR_INVALID
+    with pytest.raises(pk.PCDNError):
+        s.step(np.array([prob.n], dtype=np.int32))
+    s.close()
+    bad = synth.tiny(9, 20, 6, density=0.5)
+    bad.y = bad.y.copy()
+    bad.y[3] = 0
+    with pytest.raises(pk.PCDNError) as ei:
+        pk.Solver(bad)
+    assert ei.value.status == pk.PCDN_ERR_INVALID
+
+
+def test_objective_and_state_injection(pk):
+    for loss in (LOSS_LOGISTIC, LOSS_L2SVM):
+        prob = synth.config(1, loss=loss)
+        s = _solver(pk, prob)
+        o = oracle.Oracle(prob)
+        F0 = s.objective()
+        assert math.isclose(F0, o.objective(np.zeros(prob.n)), rel_tol=1e-12)
+        w = _random_state(np.random.default_rng(3), prob.n, 2.0)
+        s.set_w(w)
+        np.testing.assert_array_equal(s.z().cpu().numpy(), o.compute_z(w))   # same op order: bit-exact
+        assert math.isclose(s.objective(), o.objective(w), rel_tol=1e-12)
+        assert math.isclose(s.objective(recompute=True), o.objective(w), rel_tol=1e-12)
+        s.close()
+
+
+# ----------------------------------------------------------------------------- solve parity
+def _compare_solve(gs, os_, ws_gpu, what):
+    qg, qo = gs["q_trace"], os_["q_trace"]
+    m = min(qg.size, qo.size)
+    div = np.nonzero(qg[:m] != qo[:m])[0]
+    assert div.size == 0, f"{what}: q traces diverge first at step {div[0]} (gpu {qg[div[0]]}, ora {qo[div[0]]})"
+    assert gs["steps"] == os_["steps"] and gs["outer_iters"] == os_["outer"]
+    assert abs(gs["F"] - os_["F"]) <= 1e-6 * abs(os_["F"]), (gs["F"], os_["F"])
+    assert np.max(np.abs(ws_gpu - os_["w"])) <= 1e-5
+    _close(gs["F_trace"], os_["F_trace"], np.abs(os_["F_trace"]) * 1e-3, what + " F trace")
+
+
+@pytest.mark.parametrize("loss", [LOSS_LOGISTIC, LOSS_L2SVM])
+@pytest.mark.parametrize("P", [1, 3, 7, 33])
+def test_solve_parity_tiny(pk, loss, P):
+    prob = synth.tiny(500 + P, 60, 33, density=0.25, loss=loss, c=2.0, empty_cols=2)
+    s = _solver(pk, prob)
+    o = oracle.Oracle(prob)
+    gs = s.solve(P, seed=P, max_outer=8, trace=True)
+    os_ = o.solve(P, seed=P, max_outer=8)
+    _compare_solve(gs, os_, s.w().cpu().numpy(), f"tiny P={P}")
+    s.close()
+
+
+@pytest.mark.parametrize("cfg,loss", [(1, LOSS_LOGISTIC), (1, LOSS_L2SVM), (2, LOSS_L2SVM)])
+def test_solve_parity_configs_to_gap(pk, cfg, loss):
+    """Full solves of configs 1-2 to the Eq.14 gap 1e-3 (F* from the oracle)."""
+    prob = synth.config(cfg, loss=loss)
+    o = oracle.Oracle(prob)
+    fstar = o.solve(prob.P, seed=prob.seed, max_outer=60)["F"]
+    os_ = o.solve(prob.P, eps=1e-3, fstar=fstar, seed=prob.seed, max_outer=60)
+    s = _solver(pk, prob)
+    gs = s.solve(prob.P, eps=1e-3, seed=prob.seed, max_outer=60, fstar=fstar, trace=True)
+    assert gs["rc"] == os_["rc"] == 0
+    _compare_solve(gs, os_, s.w().cpu().numpy(), f"cfg{cfg}")
+    s.close()
+
+
+def test_determinism(pk):
+    prob = synth.config(2)
+    s = _solver(pk, prob)
+    a = s.solve(prob.P, seed=1, max_outer=2, trace=True)
+    wa = s.w().cpu().numpy()
+    s.reset()
+    b = s.solve(prob.P, seed=1, max_outer=2, trace=True)
+    wb = s.w().cpu().numpy()
+    assert np.array_equal(wa.view(np.uint64), wb.view(np.uint64))
+    assert np.array_equal(a["F_trace"].view(np.uint64), b["F_trace"].view(np.uint64))
+    assert np.array_equal(a["q_trace"], b["q_trace"])
+    s.close()
+
+
+@pytest.mark.parametrize("launch", [(1, 0), (2, 3), (5, 1)])
+def test_solve_parity_launch_shapes(pk, launch):
+    """Different CTA counts / forced heavy split: same results as the oracle."""
+    prob = synth.tiny(777, 90, 40, density=0.3, loss=LOSS_LOGISTIC, c=4.0, dense_rows=3)
+    s = _solver(pk, prob, *launch)
+    o = oracle.Oracle(prob)
+    gs = s.solve(6, seed=4, max_outer=6, trace=True)
+    os_ = o.solve(6, seed=4, max_outer=6)
+    _compare_solve(gs, os_, s.w().cpu().numpy(), f"launch {launch}")
+    s.close()
+
+
+# ----------------------------------------------------------------------------- larger configs
+@pytest.mark.parametrize("cfg", [3, 4])
+def test_step_parity_large_configs(pk, cfg):
+    """Configs 3 (Zipf text, heavy columns) and 4 (dense): sampled bundle steps at full size."""
+    prob = synth.config(cfg)
+    rng = np.random.default_rng(cfg)
+    s = _solver(pk, prob)
+    o = oracle.Oracle(prob)
+    ties = []
+    w0 = np.zeros(prob.n)
+    sizes = [64, 1024, 8192] if cfg == 3 else [500]
+    for P in sizes:
+        B = rng.choice(prob.n, size=P, replace=False).astype(np.int32)
+        s.set_w(w0)
+        r = o.step(w0, B)
+        _compare_step(s.step(B), r, ties)
+        w1 = r["w"].copy()   # the oracle state after its step
+        B2 = rng.choice(prob.n, size=P, replace=False).astype(np.int32)
+        s.set_w(w1)
+        _compare_step(s.step(B2), o.step(w1, B2), ties)
+    assert len(ties) <= 1, ties
+    s.close()
+
+
+def test_solve_parity_config4_one_outer(pk):
+    prob = synth.config(4)
+    s = _solver(pk, prob)
+    o = oracle.Oracle(prob)
+    gs = s.solve(prob.P, seed=prob.seed, max_outer=1, trace=True)
+    os_ = o.solve(prob.P, seed=prob.seed, max_outer=1)
+    _compare_solve(gs, os_, s.w().cpu().numpy(), "cfg4")
+    s.close()
