@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""PCDN (arXiv:1306.4080) hot-path benchmark on B200 -- the driver's bench contract.
+
+A "step" is one full PCDN solve of the workload from w0 = 0 (Alg.3) to the
+Eq.14 relative objective gap eps = 1e-3: every row of SURVEY.md 8(a)
+(partition a0, g/h/d a1-a2, d'x a3, Armijo a4, commit a5, outer refresh + stop test a6)
+runs inside it.  Default workload = BASELINE.json configs[1] (config 2: L1-regularized
+L2-loss SVM, 20,000 x 50,000, 50 nnz/row, P=256, seed 1).
+
+value  = bundle nonzeros processed per second (sum over steps of sum_{j in B} nnz(x^j)),
+         whole job (all ranks), inputs resident in HBM, device time from CUDA events.
+e2e    = the same metric through pcdn_train_host() with pinned HOST buffers (H2D of the
+         inputs and D2H of w inside the timed region).
+--impl reference times the CPU oracle (oracle/, fp64, 1 thread) on the same workload.
+
+Multi-GPU: the path does not shard; under torchrun
+every rank solves its own replica; value = all ranks' nonzeros / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PCDN time to rel. obj gap 1e-3; nnz/s and HBM GB/s vs 8 TB/s roofline"
+NOMINAL_HBM_GBS = 8000.0
+
+
+def load_json(path, default=None):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return default
+
+
+def peaks():
+    mp = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json"))
+    if mp and "hbm_gbs" in mp:
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def fstar_for(cfg, loss):
+    g = load_json(os.path.join(ROOT, "tests", "golden", "fstar.json"), {})
+    key = f"cfg{cfg}_{'lr' if loss == 0 else 'svm'}"
+    if key not in g:
+        raise SystemExit(f"no F* for {key} in tests/golden/fstar.json (run scripts/make_fstar.py)")
+    return float(g[key]["F_star"])
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[5 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_oracle(prob, fstar, eps, steps, warmup, budget_s=None):
+    """Time the CPU oracle (single thread) on full solves of the workload."""
+    import oracle
+    try:
+        os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
+        cores = 1
+    except (AttributeError, OSError):
+        cores = 1
+    o = oracle.Oracle(prob)
+    for _ in range(warmup):
+        o.solve(prob.P, eps=eps, fstar=fstar, seed=prob.seed, max_outer=1000, trace_cap=0)
+    times, nnz, outer = [], 0, 0
+    t_all = time.perf_counter()
+    while len(times) < steps or (budget_s and time.perf_counter() - t_all < budget_s and len(times) < 1000):
+        t = time.perf_counter()
+        r = o.solve(prob.P, eps=eps, fstar=fstar, seed=prob.seed, max_outer=1000, trace_cap=0)
+        times.append(time.perf_counter() - t)
+        nnz += r["nnz"]
+        outer = r["outer"]
+    return dict(value=nnz / sum(times), solves=len(times), seconds=sum(times), ms_per_solve=1e3 * np.mean(times),
+                outer=outer, cores=cores, F=r["F"], rc=r["rc"])
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--loss", type=int, default=None)
+    ap.add_argument("--eps", type=float, default=1e-3)
+    ap.add_argument("--P", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    import synth
+    ws, rank, local = dist_setup()
+    prob = synth.config(args.config, loss=args.loss)
+    if args.P:
+        prob.P = args.P
+    fstar = fstar_for(args.config, prob.loss)
+    lossname = "L1-logistic" if prob.loss == 0 else "L1-L2-loss-SVM"
+    workload = (f"cfg{args.config}: {lossname} s={prob.s} x n={prob.n}, nnz={prob.nnz}, c={prob.c}, "
+                f"P={prob.P}, seed={prob.seed}, solve w0=0 -> Eq.14 gap {args.eps:g}")
+    config = {"workload": workload, "config_index": args.config, "s": prob.s, "n": prob.n, "nnz": prob.nnz,
+              "P": prob.P, "c": prob.c, "loss": lossname, "eps": args.eps, "F_star": fstar,
+              "l2": "flushed between timed solves (256 MiB write)", "parallelism": f"replicas x{ws}"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        r = run_oracle(prob, fstar, args.eps, args.steps, args.warmup)
+        line = {"metric": METRIC, "value": r["value"], "unit": "nnz/s", "n_gpus": args.gpus, "steps": r["solves"],
+                "warmup": args.warmup, "ms_per_step": r["ms_per_solve"], "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "impl": "reference",
+                "data": "synthetic (seeded generator synth/, SURVEY.md 8(d) recipe)", "config": config,
+                "time_to_gap_s": r["ms_per_solve"] / 1e3, "outer_iters": r["outer"],
+                "cpu_baseline": {"value": r["value"], "unit": "nnz/s", "cores": r["cores"], "kind": "oracle",
+                                 "sample": f"{r['solves']} full solves of the workload to gap {args.eps:g}",
+                                 "cpu": cpu_model()},
+                "e2e": {"value": r["value"], "unit": "nnz/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    import paper_1306_4080_b200 as pk
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        solver = pk.Solver(prob, device=dev, stream=stream)
+    pk.pcdn_set_reference(solver.ctx, fstar)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def one_solve():
+        pk.pcdn_reset(solver.ctx)
+        st, inf = pk.pcdn_solve(solver.ctx, prob.P, args.eps, prob.seed, 1000)
+        if st != pk.PCDN_OK:
+            raise SystemExit(f"solve did not reach the gap: status {st}")
+        return inf
+
+    for _ in range(args.warmup):
+        one_solve()
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    infos = []
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            ev0[k].record(stream)
+            infos.append(one_solve())
+            ev1[k].record(stream)
+        torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    t_ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))
+    nnz = sum(i.nnz_processed for i in infos)
+    steps_b = sum(i.steps for i in infos)
+    alg_bytes = sum(i.alg_bytes for i in infos)
+    t_kernel = sum(i.t_step_kernel_ms for i in infos)
+    launches = sum(i.kernel_launches for i in infos)
+    outer = infos[-1].outer_iters
+    # step-kernel launches (one per outer iteration) for per-launch roofline numbers
+    step_launches = sum(i.outer_iters for i in infos)
+    if ws > 1:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+        nn = torch.tensor([float(nnz)], dtype=torch.float64, device=dev)
+        dist.all_reduce(nn)
+        nnz_all = float(nn.item())
+    else:
+        nnz_all = float(nnz)
+
+    # end-to-end through the public one-call API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        pin = {}
+        for name, dt in (("col_ptr", np.int64), ("row_idx", np.int32), ("val", np.float32),
+                         ("row_ptr", np.int64), ("col_idx", np.int32), ("csr_val", np.float32), ("y", np.int8)):
+            a = np.ascontiguousarray(getattr(prob, name), dtype=dt)
+            t = torch.empty(a.shape, dtype=getattr(torch, np.dtype(dt).name), pin_memory=True)
+            t.numpy()[...] = a
+            pin[name] = t
+        w_host = torch.empty(prob.n, dtype=torch.float64, pin_memory=True)
+        h2d = sum(t.numel() * t.element_size() for t in pin.values())
+        d2h = w_host.numel() * w_host.element_size()
+
+        def e2e_once():
+            return pk.pcdn_train_host(*(pin[k].numpy() for k in ("col_ptr", "row_idx", "val", "row_ptr", "col_idx",
+                                                                 "csr_val", "y")),
+                                      prob.c, prob.loss, prob.P, args.eps, fstar, prob.seed, 1000, stream=stream,
+                                      w_out=w_host.numpy())
+
+        e2e_once()
+        torch.cuda.synchronize(dev)
+        e_nnz, e_ms = 0, 0.0
+        for k in range(max(1, min(args.steps, 3))):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            st, inf, _ = e2e_once()
+            b.record(stream)
+            b.synchronize()
+            e_ms += a.elapsed_time(b)
+            e_nnz += inf.nnz_processed
+        e2e = {"value": ws * e_nnz / (e_ms / 1e3), "unit": "nnz/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms / max(1, min(args.steps, 3)),
+               "api": "pcdn_train_host (pinned host buffers, includes create/validate/solve/copy-back)"}
+
+    peak, peak_src = peaks()
+    traffic = None
+    prof = load_json(os.path.join(ROOT, "profiles", "k_step_dram.json"), {})
+    if prof.get("workload") == f"cfg{args.config}" and prof.get("P") == prob.P:
+        traffic = prof.get("dram_bytes_per_launch")
+    per_launch_bytes = alg_bytes / max(1, step_launches)
+    per_launch_ms = t_kernel / max(1, step_launches)
+    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "kernel": "pcdn::k_step (persistent, one launch per outer iteration)",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "alg_bytes_per_launch": per_launch_bytes,
+            "launch_ms": per_launch_ms, "peak_source": peak_src,
+            "share_of_step": t_kernel / t_ms if t_ms else None,
+            "frac_of_nominal_8TBs": achieved / NOMINAL_HBM_GBS}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        r = run_oracle(prob, fstar, args.eps, 1, 0, budget_s=10.0)
+        cpu = {"value": r["value"], "unit": "nnz/s", "cores": r["cores"], "kind": "oracle",
+               "sample": f"{r['solves']} full solves of the workload to gap {args.eps:g} "
+                         f"({r['seconds']:.1f} s, {r['ms_per_solve']:.1f} ms/solve)", "cpu": cpu_model()}
+
+    if rank == 0:
+        value = nnz_all / (t_ms / 1e3)
+        line = {"metric": METRIC, "value": value, "unit": "nnz/s", "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded generator synth/, SURVEY.md 8(d) recipe)", "config": config,
+                "time_to_gap_s": t_ms / args.steps / 1e3, "outer_iters": outer,
+                "bundle_steps_per_s": ws * steps_b / (t_ms / 1e3),
+                "hbm_gbs_alg_whole_step": ws * alg_bytes / (t_ms / 1e3) / 1e9,
+                "frac_of_8TBs_whole_step": ws * alg_bytes / (t_ms / 1e3) / 1e9 / NOMINAL_HBM_GBS,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -149,10 +149,20 @@ int pcdn_set_trace(pcdn_ctx *ctx, int32_t *q_trace, double *F_trace, int64_t cap
 /* Debug mode records T and d'x of each step (for pcdn_last_touched). */
 int pcdn_set_debug(pcdn_ctx *ctx, int on);
 
-/* Tuning knobs (never change results beyond fp64 rounding order): number of CTAs of the
- * persistent step kernel (0 = all co-resident) and the column length above which a column
- * is split across warps/CTAs (default 128). */
-int pcdn_set_launch(pcdn_ctx *ctx, int ctas, int heavy_len);
+/* Launch knobs (results stay within fp64 rounding-order differences; for a fixed setting they
+ * are bit-reproducible).  mode: 0 auto (cluster when the mean bundle holds <= 64K nonzeros),
+ * 1 one thread-block cluster of `ctas` <= 16 CTAs with hardware cluster barriers,
+ * 2 cooperative grid of `ctas` CTAs with a software grid barrier (0 = all co-resident).
+ * heavy_len: column length above which a column is split across warps/CTAs (0 = keep; 128 default). */
+int pcdn_set_launch(pcdn_ctx *ctx, int mode, int ctas, int heavy_len);
+
+/* Profiling mode: CTA 0 of the step kernel accumulates clock64() cycles per phase
+ * (0 g/h/d + scatter, 1 barrier after it, 2 touched set, 3 d'x fold, 4 line-search partials,
+ * 5 barrier + decision, 6 commit, 7 end-of-step barrier).  pcdn_set_profile(ctx, 1) zeroes the
+ * counters; pcdn_phase_cycles copies the 16 counters to out (host) and the launch mode used by
+ * the last step launch (1 cluster, 2 grid) to *mode (host, nullable).  Synchronizes. */
+int pcdn_set_profile(pcdn_ctx *ctx, int on);
+int pcdn_phase_cycles(pcdn_ctx *ctx, int64_t *out, int32_t *mode);
 
 /* Human-readable description of the last error (never NULL). */
 const char *pcdn_last_error(const pcdn_ctx *ctx);

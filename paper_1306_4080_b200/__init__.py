@@ -19,7 +19,7 @@ from ._abi import (  # noqa: F401
 __all__ = [
     "pcdn_workspace_bytes", "pcdn_create", "pcdn_set_armijo", "pcdn_set_reference", "pcdn_bundle_step",
     "pcdn_last_touched", "pcdn_solve", "pcdn_objective", "pcdn_get_w", "pcdn_set_w", "pcdn_get_z",
-    "pcdn_reset", "pcdn_permutation", "pcdn_set_trace", "pcdn_set_debug", "pcdn_set_launch",
+    "pcdn_reset", "pcdn_permutation", "pcdn_set_trace", "pcdn_set_debug", "pcdn_set_launch", "pcdn_set_profile", "pcdn_phase_cycles",
     "pcdn_last_error", "pcdn_destroy", "pcdn_train_host", "pcdn_version", "Solver", "PCDNError",
 ]
 
@@ -129,8 +129,19 @@ def pcdn_set_debug(ctx, on):
     return check(ctx, lib().pcdn_set_debug(ctx, 1 if on else 0))
 
 
-def pcdn_set_launch(ctx, ctas=0, heavy_len=0):
-    return check(ctx, lib().pcdn_set_launch(ctx, int(ctas), int(heavy_len)))
+def pcdn_set_launch(ctx, mode=0, ctas=0, heavy_len=0):
+    return check(ctx, lib().pcdn_set_launch(ctx, int(mode), int(ctas), int(heavy_len)))
+
+
+def pcdn_set_profile(ctx, on):
+    return check(ctx, lib().pcdn_set_profile(ctx, 1 if on else 0))
+
+
+def pcdn_phase_cycles(ctx):
+    out = np.zeros(16, dtype=np.int64)
+    mode = C.c_int32()
+    check(ctx, lib().pcdn_phase_cycles(ctx, _ptr(out), C.byref(mode)))
+    return out, mode.value
 
 
 def pcdn_last_error(ctx) -> str:
@@ -253,8 +264,8 @@ class Solver:
             res["F_trace"] = Ft[:ns].cpu().numpy()
         return res
 
-    def set_launch(self, ctas=0, heavy_len=0):
-        pcdn_set_launch(self.ctx, ctas, heavy_len)
+    def set_launch(self, mode=0, ctas=0, heavy_len=0):
+        pcdn_set_launch(self.ctx, mode, ctas, heavy_len)
 
     def close(self):
         if getattr(self, "ctx", None) is not None:

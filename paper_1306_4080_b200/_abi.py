@@ -61,7 +61,9 @@ SIGNATURES = {
     "pcdn_permutation": (C.c_int, [P, C.c_uint64, I64, P]),
     "pcdn_set_trace": (C.c_int, [P, P, P, I64]),
     "pcdn_set_debug": (C.c_int, [P, C.c_int]),
-    "pcdn_set_launch": (C.c_int, [P, C.c_int, C.c_int]),
+    "pcdn_set_launch": (C.c_int, [P, C.c_int, C.c_int, C.c_int]),
+    "pcdn_set_profile": (C.c_int, [P, C.c_int]),
+    "pcdn_phase_cycles": (C.c_int, [P, P, C.POINTER(C.c_int32)]),
     "pcdn_last_error": (C.c_char_p, [P]),
     "pcdn_destroy": (None, [P]),
     "pcdn_train_host": (C.c_int, [I64, I64, I64, P, P, P, P, P, P, P, C.c_double, C.c_int, I64, C.c_double,

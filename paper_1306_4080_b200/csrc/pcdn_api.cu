@@ -27,7 +27,7 @@ inline size_t align_up(size_t x) { return (x + ALIGN - 1) & ~(ALIGN - 1); }
 struct Layout {
     size_t w, z, coef, cnt, bits, rec, dxg, tlist, order, flag, hpos, hlist, hlen, hstart, tiles1, tiles2,
         seen, dk, deltak, gk, hk, part, hpart, counters, info, F, Fcopy, status, err_idx, err_what, bar,
-        objp, nheavy, dbg_dx, dbg_mark, total;
+        objp, nheavy, prof, dbg_dx, dbg_mark, total;
 };
 
 Layout make_layout(int64_t s, int64_t n, int64_t nnz)
@@ -74,6 +74,7 @@ Layout make_layout(int64_t s, int64_t n, int64_t nnz)
     L.bar = take(sizeof(unsigned long long));
     L.objp = take(sizeof(double) * 2 * OBJ_NB);
     L.nheavy = take(sizeof(int64_t));
+    L.prof = take(sizeof(long long) * 16);
     L.dbg_dx = take(sizeof(double) * s);
     L.dbg_mark = take(s);
     L.total = off + ALIGN;  // slack for base alignment
@@ -108,8 +109,12 @@ struct pcdn_ctx {
     double fstar = 0.0;
     bool has_fstar = false;
     int debug = 0;
-    int G = 0;          // CTAs of the step kernel
+    int profile = 0;
+    int G = 0;          // CTAs of the grid-mode step kernel (cooperative launch)
+    int Gc = 0;         // CTAs of the cluster-mode step kernel (one cluster)
     int G_req = 0;
+    int mode_req = 0;   // 0 auto, 1 cluster, 2 grid
+    int last_mode = 0;
     int heavy_len = 128;
     int num_sms = 0;
     size_t smem = 0;
@@ -285,13 +290,39 @@ int launch_steps(pcdn_ctx *ctx, int64_t ntot, int64_t P, int64_t nsteps, int64_t
     a.counters = ctx->at<int64_t>(L.counters);
     a.info = ctx->at<double>(L.info);
     a.debug = ctx->debug;
+    a.prof = ctx->profile ? ctx->at<long long>(L.prof) : nullptr;
     a.dbg_dx = ctx->at<double>(L.dbg_dx);
     a.dbg_mark = ctx->at<uint8_t>(L.dbg_mark);
     a.bar = ctx->at<unsigned long long>(L.bar);
     a.status = ctx->at<int>(L.status);
     CU(cudaMemsetAsync(a.bar, 0, sizeof(unsigned long long), ctx->stream));
-    void *args[] = {&a};
-    CU(cudaLaunchCooperativeKernel((const void *)k_step, dim3(ctx->G), dim3(NT), args, ctx->smem, ctx->stream));
+    // cluster mode for steps small enough that 16 SMs keep up (hardware barrier, ~0.2 us);
+    // grid mode (all SMs, software barrier) for large steps
+    int mode = ctx->mode_req;
+    if (mode == 0) {
+        const double est_nb = (double)ctx->nnz * (double)P / (double)ctx->n;
+        mode = (ctx->Gc >= 2 && est_nb <= 65536.0) ? 1 : 2;
+    }
+    ctx->last_mode = mode;
+    if (mode == 1) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(ctx->Gc);
+        cfg.blockDim = dim3(NT);
+        cfg.dynamicSmemBytes = ctx->smem;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = ctx->Gc;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CU(cudaLaunchKernelEx(&cfg, k_step<ClusterSync>, a));
+    } else {
+        void *args[] = {&a};
+        CU(cudaLaunchCooperativeKernel((const void *)k_step<GridSync>, dim3(ctx->G), dim3(NT), args, ctx->smem,
+                                       ctx->stream));
+    }
     ctx->launches++;
     return PCDN_OK;
 }
@@ -305,13 +336,41 @@ int configure_launch(pcdn_ctx *ctx)
     CU(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
     if (!coop) return set_err(ctx, PCDN_ERR_CUDA, "device does not support cooperative launch");
     ctx->smem = sizeof(StepSmem);
-    CU(cudaFuncSetAttribute((const void *)k_step, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem));
+    const void *kg = (const void *)k_step<GridSync>;
+    const void *kc = (const void *)k_step<ClusterSync>;
+    CU(cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem));
+    CU(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem));
+    CU(cudaFuncSetAttribute(kc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     int occ = 0;
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void *)k_step, NT, ctx->smem));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kg, NT, ctx->smem));
     if (occ < 1) return set_err(ctx, PCDN_ERR_CUDA, "step kernel cannot be resident (smem %zu)", ctx->smem);
-    int maxg = ctx->num_sms * (occ < 2 ? occ : 2);
+    int maxg = ctx->num_sms * occ;
     if (maxg > GMAX) maxg = GMAX;
-    ctx->G = ctx->G_req > 0 && ctx->G_req < maxg ? ctx->G_req : maxg;
+    // largest cluster the device can co-schedule with this footprint (<= 16, non-portable)
+    int maxc = 0;
+    {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(16);
+        cfg.blockDim = dim3(NT);
+        cfg.dynamicSmemBytes = ctx->smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 16;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (cudaOccupancyMaxPotentialClusterSize(&maxc, k_step<ClusterSync>, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            maxc = 0;
+        }
+        if (maxc > 16) maxc = 16;
+    }
+    const bool want_cluster = ctx->mode_req == 1;
+    ctx->G = (!want_cluster && ctx->G_req > 0 && ctx->G_req < maxg) ? ctx->G_req : maxg;
+    ctx->Gc = (want_cluster && ctx->G_req > 0 && ctx->G_req < maxc) ? ctx->G_req : maxc;
+    if (ctx->mode_req == 1 && ctx->Gc < 1)
+        return set_err(ctx, PCDN_ERR_INVALID, "cluster mode unavailable (max cluster size %d)", maxc);
     return PCDN_OK;
 }
 
@@ -449,13 +508,33 @@ int pcdn_set_debug(pcdn_ctx *ctx, int on)
     return PCDN_OK;
 }
 
-int pcdn_set_launch(pcdn_ctx *ctx, int ctas, int heavy_len)
+int pcdn_set_launch(pcdn_ctx *ctx, int mode, int ctas, int heavy_len)
 {
     if (!ctx) return PCDN_ERR_INVALID;
-    if (ctas < 0 || heavy_len < 0) return set_err(ctx, PCDN_ERR_INVALID, "invalid launch knobs");
+    if (mode < 0 || mode > 2 || ctas < 0 || heavy_len < 0 || (mode == 1 && ctas > 16))
+        return set_err(ctx, PCDN_ERR_INVALID, "invalid launch knobs");
+    ctx->mode_req = mode;
     ctx->G_req = ctas;
     if (heavy_len > 0) ctx->heavy_len = heavy_len;
     return configure_launch(ctx);
+}
+
+int pcdn_set_profile(pcdn_ctx *ctx, int on)
+{
+    if (!ctx) return PCDN_ERR_INVALID;
+    ctx->profile = on ? 1 : 0;
+    CU(cudaMemsetAsync(ctx->at<long long>(ctx->L.prof), 0, sizeof(long long) * 16, ctx->stream));
+    return PCDN_OK;
+}
+
+int pcdn_phase_cycles(pcdn_ctx *ctx, int64_t *out, int32_t *mode)
+{
+    if (!ctx || !out) return PCDN_ERR_INVALID;
+    CU(cudaMemcpyAsync(out, ctx->at<long long>(ctx->L.prof), sizeof(long long) * 16, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (mode) *mode = ctx->last_mode;
+    return PCDN_OK;
 }
 
 const char *pcdn_last_error(const pcdn_ctx *ctx) { return ctx ? ctx->err : "null context"; }
@@ -544,10 +623,12 @@ int pcdn_bundle_step(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, pcdn_step_
     const Layout &L = ctx->L;
     int rc;
     if ((rc = reset_status(ctx))) return rc;
+    CU(cudaMemsetAsync(ctx->at<int64_t>(L.counters), 0, sizeof(int64_t) * 8, ctx->stream));
     k_bundle_prep<<<grid1d(P), 256, 0, ctx->stream>>>(bundle, P, ctx->n, ctx->col_ptr, ctx->heavy_len,
                                                       ctx->at<int32_t>(L.order), ctx->at<int32_t>(L.flag),
                                                       ctx->at<uint32_t>(L.seen), ctx->at<int>(L.status),
-                                                      ctx->at<long long>(L.err_idx));
+                                                      ctx->at<long long>(L.err_idx),
+                                                      (unsigned long long *)(ctx->at<int64_t>(L.counters) + 2));
     k_bundle_unseen<<<grid1d(P), 256, 0, ctx->stream>>>(bundle, P, ctx->n, ctx->at<uint32_t>(L.seen));
     ctx->launches += 2;
     CU(cudaGetLastError());
@@ -570,7 +651,7 @@ int pcdn_bundle_step(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, pcdn_step_
         info->lhs = v[3];
         info->rhs = v[4];
         info->F = v[5];
-        info->bundle_nnz = (int64_t)v[6];
+        info->bundle_nnz = ctx->hm->counters[2];
         info->n_touched = (int64_t)v[7];
         if (ctx->hm->status == 3) return set_err(ctx, PCDN_ERR_NUMERIC, "non-finite line-search quantities");
         if (ctx->hm->status) return set_err(ctx, PCDN_ERR_CUDA, "internal consistency check failed (%d)", ctx->hm->status);
@@ -671,7 +752,7 @@ int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_
         info->outer_iters = k;
         info->steps = cn[0];
         info->null_steps = cn[1];
-        info->nnz_processed = cn[2];
+        info->nnz_processed = ctx->nnz * (int64_t)k;   // every column once per outer iteration
         info->touched_total = cn[3];
         info->positions = cn[4];
         info->kernel_launches = ctx->launches - launches0;
@@ -683,7 +764,7 @@ int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_
         info->t_gpu_ms = ms;
         // 16 B per bundle nonzero (index+value, gathered fp64 pair counted as
         // one fp64 word of the retained per-sample state), 16 B per touched sample, 28 B per position
-        info->alg_bytes = 16.0 * (double)cn[2] + 16.0 * (double)cn[3] + 28.0 * (double)cn[4];
+        info->alg_bytes = 16.0 * (double)info->nnz_processed + 16.0 * (double)cn[3] + 28.0 * (double)cn[4];
     }
     (void)gap;
     return status;

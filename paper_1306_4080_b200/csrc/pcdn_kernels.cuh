@@ -25,12 +25,14 @@ namespace pcdn {
 
 constexpr int NT = 512;            // threads per CTA of the step kernel
 constexpr int NW = NT / 32;        // warps per CTA
-constexpr int QW = 8;              // max Armijo candidates per line-search window
-constexpr int NPART = 2 * QW + 8;  // per-CTA partials: Ls[QW], L1[QW], Delta, nnz, |T|
+constexpr int QW = 6;              // Armijo candidates of a wide line-search window
+constexpr int NPART = 32;          // per-CTA partial slots (packed: Ls[nq], L1[nq], Delta, |T|)
+constexpr int WREG = 4;            // bitmap words per thread kept in registers in phase C1
 constexpr int NE_MAX = 64;         // heavy entries handled per round inside one CTA
 constexpr int NREG = 8;            // rows with <= NREG records are folded by one thread
 constexpr int NHW = 4;             // warps that fold rows with > NREG records
 constexpr int HB = 1024;           // per-warp sort buffer for such rows
+constexpr int TSM = 4096;          // touched samples of a row block kept in shared memory
 constexpr int SCAN_TILE = 2048;    // items per CTA of the device-wide scans
 constexpr int SCAN_NT = 256;
 
@@ -88,6 +90,7 @@ struct StepArgs {
     int64_t *counters;   // [0]=steps [1]=null [2]=nnz [3]=touched [4]=positions
     double *info;        // last step: q, alpha, Delta, lhs, rhs, F, nnz, nT
     int debug;
+    long long *prof;     // nullable: per-phase clock64 cycles of CTA 0 (profiling mode)
     double *dbg_dx;
     uint8_t *dbg_mark;
     // sync
@@ -138,6 +141,27 @@ __device__ __forceinline__ void grid_sync(unsigned long long *ctr, unsigned long
     }
     __syncthreads();
 }
+
+// Sync policies of the persistent step kernel.  GridSync: cooperative launch of G CTAs (up to
+// 2 per SM), software barrier through an L2 counter.  ClusterSync: one thread-block cluster of
+// G <= 16 CTAs, hardware cluster barrier (release/acquire at cluster scope covers the global
+// memory the phases exchange).
+struct GridSync {
+    static constexpr int kMinBlocks = 1;
+    unsigned long long *ctr;
+    unsigned long long target;
+    __device__ __forceinline__ explicit GridSync(unsigned long long *c) : ctr(c), target(0) {}
+    __device__ __forceinline__ void sync() { grid_sync(ctr, target); }
+};
+
+struct ClusterSync {
+    static constexpr int kMinBlocks = 1;
+    __device__ __forceinline__ explicit ClusterSync(unsigned long long *) {}
+    __device__ __forceinline__ void sync()
+    {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
+};
 
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v)
@@ -307,7 +331,8 @@ __global__ void k_perm(uint64_t seed, int64_t k, int64_t n, const int64_t *__res
 // user bundle: validate (distinct, in range) and copy
 __global__ void k_bundle_prep(const int32_t *__restrict__ bundle, int64_t P, int64_t n,
                               const int64_t *__restrict__ col_ptr, int heavy_len, int32_t *order,
-                              int32_t *flag, uint32_t *seen, int *status, long long *err_idx)
+                              int32_t *flag, uint32_t *seen, int *status, long long *err_idx,
+                              unsigned long long *bundle_nnz)
 {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < P; t += (int64_t)gridDim.x * blockDim.x) {
         const int32_t j = bundle[t];
@@ -325,7 +350,9 @@ __global__ void k_bundle_prep(const int32_t *__restrict__ bundle, int64_t P, int
             atomicMin(err_idx, (long long)t);
         }
         order[t] = j;
-        flag[t] = (__ldg(&col_ptr[j + 1]) - __ldg(&col_ptr[j])) > heavy_len ? 1 : 0;
+        const int64_t len = __ldg(&col_ptr[j + 1]) - __ldg(&col_ptr[j]);
+        flag[t] = len > heavy_len ? 1 : 0;
+        atomicAdd(bundle_nnz, (unsigned long long)len);   // integer: order-independent
     }
 }
 
@@ -461,13 +488,21 @@ struct StepSmem {
     int64_t cross_e[2];
     double cross_d[2];
     // reductions
-    double red[NW][NPART];
-    double tot[NPART];
+    double red[NW][32];
+    double tot[32];
     int64_t scan_w[NW];
     int64_t nT;
     int has_heavy_rows;
     int q_acc;
-    int64_t nnz_local;
+    // CTA 0 bookkeeping (maintained F, step counters) and profile counters
+    double F;
+    long long cnt[4];
+    long long pacc[8];
+    // line-search decision broadcast
+    int dec_q, dec_bad;
+    double dec_alpha, dec_lhs, dec_rhs, dec_Delta, dec_nT;
+    // touched samples of the row block (when they fit)
+    int32_t tl[TSM];
     // rows with > NREG records: per-warp sort buffers
     int32_t sk[NHW][HB];
     double sv[NHW][HB];
@@ -613,53 +648,347 @@ __device__ double fold_warp(const StepArgs &a, int64_t off, int ni, int32_t *sk,
     return dx;
 }
 
-// Block-wide fixed-order reduction of up to NPART values per thread (first `cnt` entries).
-__device__ __forceinline__ void block_reduce(double *v, int cnt, StepSmem &sm, int lane, int warp)
+// ------------------------------------------------------------------------------------
+// register-resident per-step data (prefetch / reuse across phases)
+// ------------------------------------------------------------------------------------
+constexpr int PF = 4;  // nonzeros per lane of a light column prefetched into registers
+
+// Immutable data of a warp's first light column of the NEXT step (order, col_ptr, row_idx,
+// val) plus w_j, loaded while the current step finishes: after the end-of-step barrier only
+// the cached per-sample factors still have to be gathered.  w_j is safe to load early: the
+// bundles of one launch are disjoint, so the current step never writes it.
+struct ColPref {
+    int64_t kk;  // position, -1 = none
+    int64_t p0, p1;
+    double wj;
+    int32_t j;
+    int32_t r[PF];
+    float x[PF];
+};
+
+__device__ __forceinline__ void prefetch_col(const StepArgs &a, ColPref &pf, int64_t kk, int64_t k1, int lane)
 {
-    for (int q = 0; q < cnt; q++) {
-        const double s = warp_sum(v[q]);
-        if (lane == 0) sm.red[warp][q] = s;
+    pf.kk = -1;
+    if (kk >= k1) return;
+    pf.kk = kk;
+    pf.j = __ldg(&a.order[kk]);
+    pf.p0 = __ldg(&a.col_ptr[pf.j]);
+    pf.p1 = __ldg(&a.col_ptr[pf.j + 1]);
+    if (pf.p1 - pf.p0 > a.heavy_len) return;
+    pf.wj = ldcg(&a.w[pf.j]);
+#pragma unroll
+    for (int m = 0; m < PF; m++) {
+        const int64_t p = pf.p0 + lane + 32 * m;
+        if (p < pf.p1) {
+            pf.r[m] = __ldg(&a.row_idx[p]);
+            pf.x[m] = __ldg(&a.val[p]);
+        }
     }
-    __syncthreads();
-    if (threadIdx.x < cnt) {
-        double s = 0.0;
-        for (int w2 = 0; w2 < NW; w2++) s += sm.red[w2][threadIdx.x];
-        sm.tot[threadIdx.x] = s;
-    }
-    __syncthreads();
 }
 
-__global__ void __launch_bounds__(NT, 2) k_step(StepArgs a)
+// The CTA's first bundle-share position (L1 term, Delta, w commit) and the thread's first
+// touched sample (loss change, commit), kept in registers from the line search to the commit.
+struct ShareReg {
+    int64_t kk;  // -1 = none
+    int32_t j;
+    double wj, d, delta;
+};
+struct RowReg {
+    int32_t i;  // -1 = none
+    int yi;
+    int has_dx;  // 0 when the sample had > NREG records (folded by a warp into dxg)
+    double zi, dx;
+};
+
+// ------------------------------------------------------------------------------------
+// line-search window helpers
+// ------------------------------------------------------------------------------------
+// Transpose-reduce of W values per lane across a warp: after the call, lane l holds the warp
+// total of slot l / (32 / W).  Fixed tree (deterministic); log2(W) halving levels exchange
+// W/2, W/4, .. values, then single-value xor levels: W=8 costs 9 shuffles instead of 40.
+template <int W>
+__device__ __forceinline__ double xreduce(double (&v)[W], int lane)
 {
+    constexpr int LOGW = W == 2 ? 1 : W == 4 ? 2 : W == 8 ? 3 : W == 16 ? 4 : 5;
+#pragma unroll
+    for (int lvl = 0; lvl < 5; lvl++) {
+        const int o = 16 >> lvl;
+        if (lvl < LOGW) {
+            const int half = W >> (lvl + 1);
+            const bool up = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < W / 2; i++) {
+                if (i < half) {
+                    const double send = up ? v[i] : v[i + half];
+                    const double keep = up ? v[i + half] : v[i];
+                    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
+            }
+        } else {
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+        }
+    }
+    return v[0];
+}
+
+struct WinState {
+    int q0, nq, qacc, bad, win;
+    double alpha, lhs, rhs, Delta, nT_tot;
+};
+
+template <int NQ>
+struct WinLayout {  // packed partial slots: Ls[0,NQ) L1[NQ,2NQ) Delta |T|
+    static constexpr int W = 2 * NQ + 2 <= 8 ? 8 : (2 * NQ + 2 <= 16 ? 16 : 32);
+    static constexpr int DELTA = 2 * NQ, NTOUCH = 2 * NQ + 1;
+};
+
+// One Armijo window over candidates q0 .. q0+NQ-1 (Eq.6 with Eq.12 from retained quantities):
+// per-sample loss changes over this CTA's touched samples (window 0 also folds d'x_i), the L1
+// term and Delta over this CTA's bundle share, a fixed-order CTA partial, a barrier, then every
+// CTA reduces the G partials in the same order and takes the same decision.
+template <int NQ, class Sync>
+__device__ __forceinline__ void window(const StepArgs &a, StepSmem &sm, Sync &sy, WinState &ws, const int32_t *Tl,
+                                      int64_t nT, int64_t k0, int64_t pb0, int64_t pb1, int G, int c, int tid,
+                                      int lane, int warp, const ShareReg &sh, RowReg &rr)
+{
+    using LY = WinLayout<NQ>;
+    constexpr int W = LY::W;
+    double alpha0 = 1.0;
+    for (int q = 0; q < ws.q0; q++) alpha0 *= a.beta;
+    double acc[W];
+#pragma unroll
+    for (int q = 0; q < W; q++) acc[q] = 0.0;
+    if (ws.win == 0) {
+        for (int64_t li = tid; li < nT; li += NT) {
+            const int32_t i = Tl[li];
+            const int ni = ldcg(&a.cnt[i]);
+            const int64_t off = __ldg(&a.row_ptr[i]);
+            const double zi = ldcg(&a.z[i]);
+            const double cg = ldcg(&a.coef[i]).x;
+            const int yi = a.y[i];
+            if (li == tid) {
+                rr.i = i;
+                rr.yi = yi;
+                rr.zi = zi;
+                rr.has_dx = ni <= NREG;
+            }
+            if (ni <= NREG) {
+                const double dx = fold_small(a, off, ni);
+                a.dxg[i] = dx;
+                if (li == tid) rr.dx = dx;
+                double al = alpha0;
+#pragma unroll
+                for (int q = 0; q < NQ; q++) {
+                    acc[q] += loss_change(a.loss, zi, yi, cg, dx, al);
+                    al *= a.beta;
+                }
+            } else {
+                sm.has_heavy_rows = 1;
+            }
+        }
+        __syncthreads();
+        if (sm.has_heavy_rows && warp < NHW) {
+            // samples with > NREG records: one warp each, fixed warp assignment
+            for (int64_t lb = (int64_t)warp * 32; lb < nT; lb += 32 * NHW) {
+                const int64_t li = lb + lane;
+                int32_t i = -1;
+                int ni = 0;
+                if (li < nT) {
+                    i = Tl[li];
+                    ni = ldcg(&a.cnt[i]);
+                }
+                unsigned heavy = __ballot_sync(0xffffffffu, ni > NREG);
+                while (heavy) {
+                    const int src = __ffs(heavy) - 1;
+                    heavy &= heavy - 1;
+                    const int32_t ih = __shfl_sync(0xffffffffu, i, src);
+                    const int nih = __shfl_sync(0xffffffffu, ni, src);
+                    const double dx = fold_warp(a, __ldg(&a.row_ptr[ih]), nih, sm.sk[warp], sm.sv[warp], lane);
+                    if (lane == 0) {
+                        a.dxg[ih] = dx;
+                        const double zi = ldcg(&a.z[ih]);
+                        const double cg = ldcg(&a.coef[ih]).x;
+                        const int yi = a.y[ih];
+                        double al = alpha0;
+#pragma unroll
+                        for (int q = 0; q < NQ; q++) {
+                            acc[q] += loss_change(a.loss, zi, yi, cg, dx, al);
+                            al *= a.beta;
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+    } else {
+        for (int64_t li = tid; li < nT; li += NT) {
+            const int32_t i = Tl[li];
+            const double dx = ldcg(&a.dxg[i]);
+            const double zi = ldcg(&a.z[i]);
+            const double cg = ldcg(&a.coef[i]).x;
+            const int yi = a.y[i];
+            double al = alpha0;
+#pragma unroll
+            for (int q = 0; q < NQ; q++) {
+                acc[q] += loss_change(a.loss, zi, yi, cg, dx, al);
+                al *= a.beta;
+            }
+        }
+    }
+    // L1 part of Eq.12 and Delta over this CTA's share of the bundle
+    for (int64_t kk = pb0 + tid; kk < pb1; kk += NT) {
+        const bool reg = kk == sh.kk;
+        const double wj = reg ? sh.wj : ldcg(&a.w[__ldg(&a.order[kk])]);
+        const double d = reg ? sh.d : ldcg(&a.dk[kk - k0]);
+        double al = alpha0;
+#pragma unroll
+        for (int q = 0; q < NQ; q++) {
+            acc[NQ + q] += fabs(wj + al * d) - fabs(wj);
+            al *= a.beta;
+        }
+        acc[LY::DELTA] += reg ? sh.delta : ldcg(&a.deltak[kk - k0]);
+    }
+    if (tid == 0) acc[LY::NTOUCH] = (double)nT;
+    // CTA partial: transpose-reduce per warp, warps combined in order by warp 0
+    constexpr int SPL = 32 / W;  // lanes per slot after xreduce
+    {
+        const double tot = xreduce<W>(acc, lane);
+        if ((lane % SPL) == 0) sm.red[warp][lane / SPL] = tot;
+    }
+    double *part = a.part + (int64_t)(ws.win & 1) * G * NPART;
+    __syncthreads();
+    if (warp == 0 && lane < W) {
+        double s = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < NW; w2++) s += sm.red[w2][lane];
+        part[(int64_t)c * NPART + lane] = s;
+    }
+    sy.sync();
+    // every CTA reduces the G partials in the same fixed order (warp 0) and decides
+    if (warp == 0) {
+        double v[W];
+#pragma unroll
+        for (int q = 0; q < W; q++) v[q] = 0.0;
+        for (int c2 = lane; c2 < G; c2 += 32) {
+#pragma unroll
+            for (int q = 0; q < W; q++) v[q] += ldcg(&part[(int64_t)c2 * NPART + q]);
+        }
+        const double tot = xreduce<W>(v, lane);
+        if ((lane % SPL) == 0) sm.tot[lane / SPL] = tot;
+        __syncwarp();
+        if (lane == 0) {
+            const double Dl = sm.tot[LY::DELTA];
+            int qa = -1, badl = 0;
+            double al = alpha0, la = 0.0, ra = 0.0, alpha_a = 0.0;
+#pragma unroll
+            for (int q = 0; q < NQ; q++) {
+                if (qa < 0 && !badl) {
+                    const double lhs = sm.tot[NQ + q] + a.c * sm.tot[q];
+                    const double rhs = a.sigma * al * Dl;
+                    if (!isfinite(lhs) || !isfinite(Dl)) {
+                        badl = 1;
+                    } else if (lhs <= rhs) {
+                        qa = ws.q0 + q;
+                        alpha_a = al;
+                        la = lhs;
+                        ra = rhs;
+                    }
+                    al *= a.beta;
+                }
+            }
+            sm.dec_q = qa;
+            sm.dec_bad = badl;
+            sm.dec_alpha = alpha_a;
+            sm.dec_lhs = la;
+            sm.dec_rhs = ra;
+            sm.dec_Delta = Dl;
+            sm.dec_nT = sm.tot[LY::NTOUCH];
+        }
+    }
+    __syncthreads();
+    ws.qacc = sm.dec_q;
+    ws.bad = sm.dec_bad;
+    ws.alpha = sm.dec_alpha;
+    ws.lhs = sm.dec_lhs;
+    ws.rhs = sm.dec_rhs;
+    ws.Delta = sm.dec_Delta;
+    ws.nT_tot = sm.dec_nT;
+    ws.win++;
+    __syncthreads();  // sm.dec_* / sm.red / sm.tot are reused by the next window
+}
+
+template <class Sync>
+__global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
+{
+    Sync sy(a.bar);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     StepSmem &sm = *reinterpret_cast<StepSmem *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, c = blockIdx.x;
-    unsigned long long bar_target = 0;
     const int64_t nwords = (a.s + 31) >> 5;
     const int64_t wb = (int64_t)c * nwords / G, we = (int64_t)(c + 1) * nwords / G;
     const int64_t row_base = wb * 32;
     int prev_q = 0;
+    const int64_t pbs0 = (int64_t)c * a.P / G, pbs1 = (int64_t)(c + 1) * a.P / G;
 
+    long long tprev = 0;
+    const bool prof = a.prof != nullptr && c == 0 && tid == 0;
+    if (tid < 8) sm.pacc[tid] = 0;
+#define PROF_MARK(i)                              \
+    do {                                          \
+        if (prof) {                               \
+            const long long now_ = clock64();     \
+            sm.pacc[i] += now_ - tprev;           \
+            tprev = now_;                         \
+        }                                         \
+    } while (0)
+    const int64_t gw = (int64_t)c * NW + warp;
+    ColPref pf;
+    prefetch_col(a, pf, gw, min(a.P, a.ntot), lane);
+    if (c == 0 && tid == 0) {
+        sm.F = ldcg(a.F);
+        for (int i = 0; i < 4; i++) sm.cnt[i] = 0;
+    }
     for (int64_t t = 0; t < a.nsteps; t++) {
+        if (prof) tprev = clock64();
         const int64_t k0 = t * a.P;
         const int64_t k1 = min(k0 + a.P, a.ntot);
         const int64_t Pt = k1 - k0;
-        if (tid == 0) sm.nnz_local = 0;
-        __syncthreads();
 
         // ---------------- phase A: light columns, one warp per column (a1, a2, a3) --------
         {
-            int64_t my_nnz = 0;
-            const int64_t gw = (int64_t)c * NW + warp;
             for (int64_t kk = k0 + gw; kk < k1; kk += (int64_t)G * NW) {
-                const int32_t j = __ldg(&a.order[kk]);
-                const int64_t p0 = __ldg(&a.col_ptr[j]), p1 = __ldg(&a.col_ptr[j + 1]);
+                const bool pre = kk == pf.kk;
+                const int32_t j = pre ? pf.j : __ldg(&a.order[kk]);
+                const int64_t p0 = pre ? pf.p0 : __ldg(&a.col_ptr[j]);
+                const int64_t p1 = pre ? pf.p1 : __ldg(&a.col_ptr[j + 1]);
                 if (p1 - p0 > a.heavy_len) continue;
-                my_nnz += p1 - p0;
                 double gs, hs;
-                col_gh(a, p0, p1, lane, gs, hs);
-                const double wj = ldcg(&a.w[j]);
+                if (pre) {
+                    // prefetched column: only the cached factors are gathered here
+                    double g = 0.0, h = 0.0;
+#pragma unroll
+                    for (int m = 0; m < PF; m++) {
+                        if (p0 + lane + 32 * m < p1) {
+                            const double x = (double)pf.x[m];
+                            const double2 cf = ldcg(&a.coef[pf.r[m]]);
+                            g += x * cf.x;
+                            h += (x * x) * cf.y;
+                        }
+                    }
+                    for (int64_t p = p0 + lane + 32 * PF; p < p1; p += 32) {
+                        const int32_t i = __ldg(&a.row_idx[p]);
+                        const double x = (double)__ldg(&a.val[p]);
+                        const double2 cf = ldcg(&a.coef[i]);
+                        g += x * cf.x;
+                        h += (x * x) * cf.y;
+                    }
+                    gs = warp_sum(g);
+                    hs = warp_sum(h);
+                } else {
+                    col_gh(a, p0, p1, lane, gs, hs);
+                }
+                const double wj = pre ? pf.wj : ldcg(&a.w[j]);
                 const Dir r = finish_feature(a, gs, hs, wj);
                 if (lane == 0) {
                     a.dk[kk - k0] = r.d;
@@ -670,9 +999,17 @@ __global__ void __launch_bounds__(NT, 2) k_step(StepArgs a)
                     }
                     if (a.d_out) a.d_out[kk - k0] = r.d;
                 }
-                if (r.d != 0.0) col_scatter(a, p0, p1, lane, (int32_t)(kk - k0), r.d);
+                if (r.d != 0.0) {
+                    if (pre) {
+#pragma unroll
+                        for (int m = 0; m < PF; m++)
+                            if (p0 + lane + 32 * m < p1) emit(a, pf.r[m], (int32_t)(kk - k0), r.d * (double)pf.x[m]);
+                        col_scatter(a, p0 + 32 * PF, p1, lane, (int32_t)(kk - k0), r.d);
+                    } else {
+                        col_scatter(a, p0, p1, lane, (int32_t)(kk - k0), r.d);
+                    }
+                }
             }
-            if (lane == 0 && my_nnz) atomicAdd((unsigned long long *)&sm.nnz_local, (unsigned long long)my_nnz);
         }
 
         // ---------------- phase A': heavy columns, nnz-balanced over all warps -----------
@@ -774,8 +1111,7 @@ __global__ void __launch_bounds__(NT, 2) k_step(StepArgs a)
                 }
                 __syncthreads();
             }
-            if (c == 0 && tid == 0) sm.nnz_local += NH;
-            grid_sync(a.bar, bar_target);
+            sy.sync();
             // finish the (at most two) columns crossing this CTA's boundaries
             if (tid < 2) {
                 const int64_t e = sm.cross_e[tid];
@@ -821,180 +1157,118 @@ __global__ void __launch_bounds__(NT, 2) k_step(StepArgs a)
                 col_scatter(a, cs + (s0 - st), cs + (s1 - st), lane, kk - (int32_t)k0, d);
             }
         }
-        grid_sync(a.bar, bar_target);
+        PROF_MARK(0);
+        sy.sync();
+        PROF_MARK(1);
+        const bool full = Pt == a.P;
+        const int64_t pb0 = k0 + (full ? pbs0 : (int64_t)c * Pt / G);
+        const int64_t pb1 = k0 + (full ? pbs1 : (int64_t)(c + 1) * Pt / G);
+        ShareReg sh;
+        sh.kk = -1;
+        if (pb0 + tid < pb1) {  // loads issued here, consumed by the line search
+            sh.kk = pb0 + tid;
+            sh.j = __ldg(&a.order[sh.kk]);
+            sh.wj = ldcg(&a.w[sh.j]);
+            sh.d = ldcg(&a.dk[sh.kk - k0]);
+            sh.delta = ldcg(&a.deltak[sh.kk - k0]);
+        }
+        RowReg rr;
+        rr.i = -1;
 
         // ---------------- phase C1: touched set of this CTA's row block ------------------
-        if (tid == 0) {
-            sm.nT = 0;
-            sm.has_heavy_rows = 0;
-        }
-        __syncthreads();
-        for (int64_t w0 = wb; w0 < we; w0 += NT) {
-            const int64_t wi = w0 + tid;
-            const uint32_t bv = wi < we ? ldcg(&a.bits[wi]) : 0u;
-            const int cntb = __popc(bv);
-            // block exclusive scan of cntb (warp scan + warp offsets)
-            int incl = cntb;
+        // each thread owns a contiguous run of bitmap words; a ballot-based warp scan plus
+        // warp totals gives every touched sample its slot in T (ascending sample order)
+        {
+            const int64_t nwc = we - wb;
+            const int64_t wpt = (nwc + NT - 1) / NT;
+            const int64_t w0 = wb + (int64_t)tid * wpt, w1 = min(we, w0 + wpt);
+            uint32_t wv[WREG];
+            unsigned cntb = 0;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int tmp = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += tmp;
+            for (int r = 0; r < WREG; r++) {
+                wv[r] = (w0 + r < w1) ? ldcg(&a.bits[w0 + r]) : 0u;
+                cntb += __popc(wv[r]);
             }
-            if (lane == 31) sm.scan_w[warp] = incl;
-            __syncthreads();
-            int64_t woff = 0;
-            for (int w2 = 0; w2 < warp; w2++) woff += sm.scan_w[w2];
-            int64_t pos = sm.nT + woff + incl - cntb;
-            uint32_t m = bv;
-            while (m) {
-                const int b = __ffs(m) - 1;
-                m &= m - 1;
-                a.tlist[row_base + pos++] = (int32_t)(wi * 32 + b);
+            for (int64_t wi = w0 + WREG; wi < w1; wi++) cntb += __popc(ldcg(&a.bits[wi]));
+            unsigned incl = 0;
+            const unsigned lemask = 0xffffffffu >> (31 - lane);
+#pragma unroll
+            for (int b = 0; b < 16; b++) {
+                const unsigned m = __ballot_sync(0xffffffffu, (cntb >> b) & 1u);
+                if (!m && (b >= 8)) break;
+                incl += (unsigned)__popc(m & lemask) << b;
             }
+            const unsigned wtot = __reduce_add_sync(0xffffffffu, cntb);
+            if (lane == 0) sm.scan_w[warp] = wtot;
             __syncthreads();
-            if (tid == NT - 1) {
-                int64_t tot = 0;
-                for (int w2 = 0; w2 < NW; w2++) tot += sm.scan_w[w2];
-                sm.nT += tot;
+            const unsigned sw = lane < NW ? (unsigned)sm.scan_w[lane] : 0u;
+            const unsigned woff = __reduce_add_sync(0xffffffffu, lane < warp ? sw : 0u);
+            const unsigned total = __reduce_add_sync(0xffffffffu, sw);
+            int32_t *Tw = total <= (unsigned)TSM ? sm.tl : a.tlist + row_base;
+            if (cntb) {
+                int64_t pos = (int64_t)woff + incl - cntb;
+#pragma unroll
+                for (int r = 0; r < WREG; r++) {
+                    uint32_t m = wv[r];
+                    while (m) {
+                        const int b = __ffs(m) - 1;
+                        m &= m - 1;
+                        Tw[pos++] = (int32_t)((w0 + r) * 32 + b);
+                    }
+                }
+                for (int64_t wi = w0 + WREG; wi < w1; wi++) {
+                    uint32_t m = ldcg(&a.bits[wi]);
+                    while (m) {
+                        const int b = __ffs(m) - 1;
+                        m &= m - 1;
+                        Tw[pos++] = (int32_t)(wi * 32 + b);
+                    }
+                }
+            }
+            if (tid == 0) {
+                sm.nT = total;
+                sm.has_heavy_rows = 0;
             }
             __syncthreads();
         }
         const int64_t nT = sm.nT;
+        const int32_t *Tl = nT <= TSM ? sm.tl : a.tlist + row_base;
+        PROF_MARK(2);
 
-        // ---------------- phase C2: d'x_i, in-order fold of each sample's records --------
-        for (int64_t li = tid; li < nT; li += NT) {
-            const int32_t i = ldcg(&a.tlist[row_base + li]);
-            const int ni = ldcg(&a.cnt[i]);
-            if (ni <= NREG) {
-                a.dxg[i] = fold_small(a, __ldg(&a.row_ptr[i]), ni);
-            } else {
-                sm.has_heavy_rows = 1;
-            }
-        }
-        __syncthreads();
-        if (sm.has_heavy_rows && warp < NHW) {
-            for (int64_t lb = (int64_t)warp * 32; lb < nT; lb += 32 * NHW) {
-                const int64_t li = lb + lane;
-                int32_t i = -1;
-                int ni = 0;
-                if (li < nT) {
-                    i = ldcg(&a.tlist[row_base + li]);
-                    ni = ldcg(&a.cnt[i]);
-                }
-                unsigned heavy = __ballot_sync(0xffffffffu, ni > NREG);
-                while (heavy) {
-                    const int src = __ffs(heavy) - 1;
-                    heavy &= heavy - 1;
-                    const int32_t ih = __shfl_sync(0xffffffffu, i, src);
-                    const int nih = __shfl_sync(0xffffffffu, ni, src);
-                    const double dx = fold_warp(a, __ldg(&a.row_ptr[ih]), nih, sm.sk[warp], sm.sv[warp], lane);
-                    if (lane == 0) a.dxg[ih] = dx;
-                    __syncwarp();
-                }
-            }
-        }
-        __syncthreads();
-
-        // ---------------- phase C3 + D: windowed Armijo search (a4), commit (a5) ----------
-        const int64_t pb0 = k0 + (int64_t)c * Pt / G, pb1 = k0 + (int64_t)(c + 1) * Pt / G;
-        int q0 = 0;
-        int nq = min(QW, max(2, prev_q + 2));
-        int qacc = -1;
-        double alpha_acc = 0.0, lhs_acc = 0.0, rhs_acc = 0.0, Delta = 0.0, nnz_tot = 0.0, nT_tot = 0.0;
-        int win = 0;
-        bool bad = false;
+        // ---------------- phase C2+C3: fold d'x_i (a3) and the Armijo windows (a4) ----------
+        WinState ws;
+        ws.q0 = 0;
+        ws.nq = prev_q <= 1 ? 2 : QW;
+        ws.qacc = -1;
+        ws.bad = 0;
+        ws.win = 0;
         while (true) {
-            double alpha0 = 1.0;
-            for (int q = 0; q < q0; q++) alpha0 *= a.beta;
-            double acc[NPART];
-#pragma unroll
-            for (int q = 0; q < NPART; q++) acc[q] = 0.0;
-            for (int64_t li = tid; li < nT; li += NT) {
-                const int32_t i = ldcg(&a.tlist[row_base + li]);
-                const double dx = ldcg(&a.dxg[i]);
-                const double zi = ldcg(&a.z[i]);
-                const int yi = a.y[i];
-                const double cg = ldcg(&a.coef[i]).x;
-                double al = alpha0;
-#pragma unroll
-                for (int q = 0; q < QW; q++) {
-                    if (q < nq) acc[q] += loss_change(a.loss, zi, yi, cg, dx, al);
-                    al *= a.beta;
-                }
-            }
-            for (int64_t kk = pb0 + tid; kk < pb1; kk += NT) {
-                const double wj = ldcg(&a.w[__ldg(&a.order[kk])]);
-                const double d = ldcg(&a.dk[kk - k0]);
-                double al = alpha0;
-#pragma unroll
-                for (int q = 0; q < QW; q++) {
-                    if (q < nq) acc[QW + q] += fabs(wj + al * d) - fabs(wj);
-                    al *= a.beta;
-                }
-                acc[2 * QW] += ldcg(&a.deltak[kk - k0]);
-            }
-            if (tid == 0) {
-                acc[2 * QW + 1] = (double)sm.nnz_local;
-                acc[2 * QW + 2] = (double)nT;
-            }
-            block_reduce(acc, 2 * QW + 3, sm, lane, warp);
-            double *part = a.part + (int64_t)(win & 1) * G * NPART;
-            if (tid < 2 * QW + 3) part[(int64_t)c * NPART + tid] = sm.tot[tid];
-            grid_sync(a.bar, bar_target);
-            // every CTA reduces the G partials in the same fixed order
-            {
-                double v[NPART];
-#pragma unroll
-                for (int q = 0; q < NPART; q++) v[q] = 0.0;
-                for (int c2 = tid; c2 < G; c2 += NT) {
-#pragma unroll
-                    for (int q = 0; q < 2 * QW + 3; q++) v[q] += ldcg(&part[(int64_t)c2 * NPART + q]);
-                }
-                block_reduce(v, 2 * QW + 3, sm, lane, warp);
-            }
-            Delta = sm.tot[2 * QW];
-            nnz_tot = sm.tot[2 * QW + 1];
-            nT_tot = sm.tot[2 * QW + 2];
-            {
-                double al = alpha0;
-                for (int q = 0; q < nq; q++) {
-                    const double lhs = sm.tot[QW + q] + a.c * sm.tot[q];
-                    const double rhs = a.sigma * al * Delta;
-                    if (!isfinite(lhs) || !isfinite(Delta)) {
-                        bad = true;
-                        break;
-                    }
-                    if (lhs <= rhs) {
-                        qacc = q0 + q;
-                        alpha_acc = al;
-                        lhs_acc = lhs;
-                        rhs_acc = rhs;
-                        break;
-                    }
-                    al *= a.beta;
-                }
-            }
-            win++;
-            __syncthreads();  // everyone has read sm.tot before it is reused
-            if (qacc >= 0 || bad) break;
-            q0 += nq;
-            if (q0 > a.qmax) break;
-            nq = min(QW, a.qmax + 1 - q0);
+            if (ws.nq <= 2) window<2>(a, sm, sy, ws, Tl, nT, k0, pb0, pb1, G, c, tid, lane, warp, sh, rr);
+            else window<QW>(a, sm, sy, ws, Tl, nT, k0, pb0, pb1, G, c, tid, lane, warp, sh, rr);
+            PROF_MARK(5);
+            if (ws.qacc >= 0 || ws.bad) break;
+            ws.q0 += ws.nq;
+            if (ws.q0 > a.qmax) break;
+            ws.nq = QW;
         }
-        if (qacc > a.qmax) {  // window overshoot past q_max counts as exhausted
-            qacc = -1;
-        }
-        if (qacc < 0) alpha_acc = 0.0;  // null step (Z10)
+        int qacc = ws.qacc;
+        const bool bad = ws.bad != 0;
+        if (qacc > a.qmax) qacc = -1;   // window overshoot past q_max counts as exhausted
+        const double alpha_acc = qacc < 0 ? 0.0 : ws.alpha;   // null step (Z10)
         prev_q = qacc < 0 ? QW : qacc;
 
-        // commit this CTA's samples and bundle share; clear per-step marks
+        // ---------------- commit (a5): this CTA's samples and bundle share; clear marks -----
+        // prefetch the next step's first light column of this warp (immutable data + w_j)
+        prefetch_col(a, pf, k1 + gw, min(k1 + a.P, a.ntot), lane);
         for (int64_t li = tid; li < nT; li += NT) {
-            const int32_t i = ldcg(&a.tlist[row_base + li]);
-            const double dx = ldcg(&a.dxg[i]);
+            // the heavy-row fold may have produced dx for the register row: take dxg then
+            const bool reg = li == tid && rr.has_dx;
+            const int32_t i = li == tid ? rr.i : Tl[li];
+            const double dx = reg ? rr.dx : ldcg(&a.dxg[i]);
             if (qacc >= 0) {
-                const double zn = ldcg(&a.z[i]) + alpha_acc * dx;
+                const double zn = (li == tid ? rr.zi : ldcg(&a.z[i])) + alpha_acc * dx;
                 a.z[i] = zn;
-                a.coef[i] = coef_of(a.loss, zn, a.y[i]);
+                a.coef[i] = coef_of(a.loss, zn, li == tid ? rr.yi : (int)a.y[i]);
             }
             a.cnt[i] = 0;
             if (a.debug) {
@@ -1005,37 +1279,51 @@ __global__ void __launch_bounds__(NT, 2) k_step(StepArgs a)
         for (int64_t wi = wb + tid; wi < we; wi += NT) a.bits[wi] = 0u;
         if (qacc >= 0) {
             for (int64_t kk = pb0 + tid; kk < pb1; kk += NT) {
-                const int32_t j = __ldg(&a.order[kk]);
-                a.w[j] = ldcg(&a.w[j]) + alpha_acc * ldcg(&a.dk[kk - k0]);
+                if (kk == sh.kk) {
+                    a.w[sh.j] = sh.wj + alpha_acc * sh.d;
+                } else {
+                    const int32_t j = __ldg(&a.order[kk]);
+                    a.w[j] = ldcg(&a.w[j]) + alpha_acc * ldcg(&a.dk[kk - k0]);
+                }
             }
         }
+        PROF_MARK(6);
         if (c == 0 && tid == 0) {
-            double F = ldcg(a.F);
-            if (qacc >= 0) F = F + lhs_acc;
+            double F = sm.F;
+            if (qacc >= 0) F = F + ws.lhs;
+            sm.F = F;
             *a.F = F;
             if (bad) atomicMax(a.status, 3);
             a.info[0] = (double)qacc;
             a.info[1] = alpha_acc;
-            a.info[2] = Delta;
-            a.info[3] = lhs_acc;
-            a.info[4] = rhs_acc;
+            a.info[2] = ws.Delta;
+            a.info[3] = ws.lhs;
+            a.info[4] = ws.rhs;
             a.info[5] = F;
-            a.info[6] = nnz_tot;
-            a.info[7] = nT_tot;
+            a.info[7] = ws.nT_tot;
             const int64_t gstep = a.trace_off + t;
             if (gstep < a.trace_cap) {
                 if (a.q_trace) a.q_trace[gstep] = qacc;
                 if (a.F_trace) a.F_trace[gstep] = F;
             }
-            a.counters[0] += 1;
-            a.counters[1] += qacc < 0 ? 1 : 0;
-            a.counters[2] += (int64_t)nnz_tot;
-            a.counters[3] += (int64_t)nT_tot;
-            a.counters[4] += Pt;
+            sm.cnt[0] += 1;
+            sm.cnt[1] += qacc < 0 ? 1 : 0;
+            sm.cnt[2] += (int64_t)ws.nT_tot;
+            sm.cnt[3] += Pt;
         }
-        grid_sync(a.bar, bar_target);
+        sy.sync();
+        PROF_MARK(7);
         if (bad) break;
     }
+    if (c == 0 && tid == 0) {
+        a.counters[0] += sm.cnt[0];
+        a.counters[1] += sm.cnt[1];
+        a.counters[3] += sm.cnt[2];
+        a.counters[4] += sm.cnt[3];
+    }
+    if (prof)
+        for (int i = 0; i < 8; i++) a.prof[i] += sm.pacc[i];
+#undef PROF_MARK
 }
 
 // ------------------------------------------------------------------------------------

@@ -30,10 +30,10 @@ def pk():
     return pk
 
 
-def _solver(pk, prob, ctas=0, heavy=0):
+def _solver(pk, prob, mode=0, ctas=0, heavy=0):
     s = pk.Solver(prob)
-    if ctas or heavy:
-        s.set_launch(ctas, heavy)
+    if mode or ctas or heavy:
+        s.set_launch(mode, ctas, heavy)
     return s
 
 
@@ -105,12 +105,16 @@ TINY = [
 ]
 
 
+LAUNCH = [(0, 0, 0), (1, 1, 0), (1, 16, 0), (1, 4, 1), (2, 3, 2), (2, 0, 1), (2, 1, 0)]
+
+
 @pytest.mark.parametrize("loss", [LOSS_LOGISTIC, LOSS_L2SVM])
 @pytest.mark.parametrize("case", range(len(TINY)))
-@pytest.mark.parametrize("launch", [(0, 0), (1, 0), (3, 2), (0, 1)])
+@pytest.mark.parametrize("launch", LAUNCH)
 def test_step_parity_tiny(pk, loss, case, launch):
-    """Injected state (pcdn_set_w) -> one bundle step, GPU vs oracle.  `launch` = (CTAs, heavy
-    column length): (1,0) = one CTA, (3,2)/(0,1) force the split (heavy) column path."""
+    """Injected state (pcdn_set_w) -> one bundle step, GPU vs oracle.  `launch` = (mode, CTAs,
+    heavy column length): mode 1 = one thread-block cluster, 2 = cooperative grid; a small
+    heavy length forces the split (heavy) column path with CTA-crossing columns."""
     kw = dict(TINY[case])
     prob = synth.tiny(loss=loss, c=3.0, P=5, **kw)
     rng = np.random.default_rng(100 + case)
@@ -218,9 +222,10 @@ def test_solve_parity_configs_to_gap(pk, cfg, loss):
     s.close()
 
 
-def test_determinism(pk):
+@pytest.mark.parametrize("mode", [1, 2])
+def test_determinism(pk, mode):
     prob = synth.config(2)
-    s = _solver(pk, prob)
+    s = _solver(pk, prob, mode)
     a = s.solve(prob.P, seed=1, max_outer=2, trace=True)
     wa = s.w().cpu().numpy()
     s.reset()
@@ -232,7 +237,7 @@ def test_determinism(pk):
     s.close()
 
 
-@pytest.mark.parametrize("launch", [(1, 0), (2, 3), (5, 1)])
+@pytest.mark.parametrize("launch", [(1, 1, 0), (1, 16, 3), (2, 2, 3), (2, 5, 1), (2, 0, 0)])
 def test_solve_parity_launch_shapes(pk, launch):
     """Different CTA counts / forced heavy split: same results as the oracle."""
     prob = synth.tiny(777, 90, 40, density=0.3, loss=LOSS_LOGISTIC, c=4.0, dense_rows=3)
@@ -245,12 +250,13 @@ def test_solve_parity_launch_shapes(pk, launch):
 
 
 # ----------------------------------------------------------------------------- larger configs
-@pytest.mark.parametrize("cfg", [3, 4])
-def test_step_parity_large_configs(pk, cfg):
-    """Configs 3 (Zipf text, heavy columns) and 4 (dense): sampled bundle steps at full size."""
+@pytest.mark.parametrize("cfg,mode", [(3, 1), (3, 2), (4, 1), (4, 2)])
+def test_step_parity_large_configs(pk, cfg, mode):
+    """Configs 3 (Zipf text, heavy columns) and 4 (dense): sampled bundle steps at full size,
+    in both launch modes."""
     prob = synth.config(cfg)
     rng = np.random.default_rng(cfg)
-    s = _solver(pk, prob)
+    s = _solver(pk, prob, mode)
     o = oracle.Oracle(prob)
     ties = []
     w0 = np.zeros(prob.n)
