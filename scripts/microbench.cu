@@ -87,6 +87,56 @@ __global__ void warp_shfl(int iters, long long *cyc, double *out)
     if (threadIdx.x == 0) cyc[0] = t1 - t0;
 }
 
+
+// DSMEM: dependent loads from a peer CTA's shared memory (cluster of 2), and returning atomics
+__global__ void dsmem_chase(int hops, long long *cyc, unsigned *out)
+{
+    __shared__ unsigned buf[1024];
+    cg::cluster_group cl = cg::this_cluster();
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) buf[i] = (i * 389 + 7) & 1023;
+    cl.sync();
+    if (cl.block_rank() == 0 && threadIdx.x == 0) {
+        unsigned *peer = cl.map_shared_rank(buf, 1);
+        unsigned x = 0;
+        long long t0 = clock64();
+        for (int h = 0; h < hops; h++) x = peer[x];
+        long long t1 = clock64();
+        out[0] = x;
+        cyc[0] = t1 - t0;
+        x = 0;
+        t0 = clock64();
+        for (int h = 0; h < hops; h++) x = atomicAdd(peer + (x & 1023), 0u) & 1023;
+        t1 = clock64();
+        out[1] = x;
+        cyc[1] = t1 - t0;
+        x = 0;
+        t0 = clock64();
+        for (int h = 0; h < hops; h++) x = buf[x];
+        t1 = clock64();
+        out[2] = x;
+        cyc[2] = t1 - t0;
+    }
+    cl.sync();
+}
+// remote store then cluster barrier (the exchange pattern of a broadcast partial)
+__global__ void dsmem_bcast_bar(int iters, long long *cyc)
+{
+    __shared__ double part[16][32];
+    cg::cluster_group cl = cg::this_cluster();
+    const int G = cl.num_blocks(), me = cl.block_rank();
+    long long t0 = clock64();
+    for (int i = 0; i < iters; i++) {
+        if (threadIdx.x < 32 * G) {
+            const int dst = threadIdx.x >> 5, slot = threadIdx.x & 31;
+            double *pp = cl.map_shared_rank(&part[me][slot], dst);
+            *pp = (double)i;
+        }
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
+    long long t1 = clock64();
+    if (threadIdx.x == 0 && me == 0) cyc[0] = t1 - t0;
+}
+
 int main()
 {
     int dev = 0, clk = 0;
@@ -166,6 +216,42 @@ int main()
             CK(cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost));
             printf("grid barrier %3d CTAs x %4d thr: %.1f cycles\n", g, nt, (double)c / iters);
         }
+    }
+
+    {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(2);
+        cfg.blockDim = dim3(128);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, dsmem_chase, 4096, cyc, out));
+        CK(cudaDeviceSynchronize());
+        long long cc[3];
+        CK(cudaMemcpy(cc, cyc, 24, cudaMemcpyDeviceToHost));
+        printf("DSMEM load latency: %.1f cycles; DSMEM returning atomic: %.1f; local smem: %.1f\n",
+               cc[0] / 4096.0, cc[1] / 4096.0, cc[2] / 4096.0);
+    }
+    CK(cudaFuncSetAttribute(dsmem_bcast_bar, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    for (int cs : {2, 8, 16}) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(cs);
+        cfg.blockDim = dim3(512);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, dsmem_bcast_bar, 10000, cyc));
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost));
+        printf("DSMEM broadcast + cluster barrier %2d CTAs x 512: %.1f cycles\n", cs, (double)c / 10000);
     }
     printf("SM clock attribute %d kHz, %d SMs\n", clk, nsm);
     return 0;
