@@ -150,11 +150,20 @@ int pcdn_set_trace(pcdn_ctx *ctx, int32_t *q_trace, double *F_trace, int64_t cap
 int pcdn_set_debug(pcdn_ctx *ctx, int on);
 
 /* Launch knobs (results stay within fp64 rounding-order differences; for a fixed setting they
- * are bit-reproducible).  mode: 0 auto (cluster when the mean bundle holds <= 64K nonzeros),
- * 1 one thread-block cluster of `ctas` <= 16 CTAs with hardware cluster barriers,
- * 2 cooperative grid of `ctas` CTAs with a software grid barrier (0 = all co-resident).
+ * are bit-reproducible).  mode: 0 auto (cluster-resident when the mean bundle holds <= 64K
+ * nonzeros and the samples fit the cluster's shared memory, else cluster / grid as below),
+ * 1 one thread-block cluster of `ctas` <= 16 CTAs with hardware cluster barriers, per-sample
+ *   state in HBM/L2,
+ * 2 cooperative grid of `ctas` CTAs with a software grid barrier (0 = all co-resident),
+ * 3 cluster-resident: one cluster of `ctas` CTAs (power of two <= 16; 0 = largest that fits)
+ *   holding the per-sample state and the step's d'x records in distributed shared memory
+ *   (DESIGN.md 7); PCDN_ERR_INVALID if the samples do not fit.
  * heavy_len: column length above which a column is split across warps/CTAs (0 = keep; 128 default). */
 int pcdn_set_launch(pcdn_ctx *ctx, int mode, int ctas, int heavy_len);
+
+/* Testing knob of mode 3: cap the records a CTA keeps in shared memory per step (0 = as many as
+ * fit); the rest spill to the CTA's HBM overflow region.  Results are unchanged. */
+int pcdn_set_resident_cap(pcdn_ctx *ctx, int cap);
 
 /* Profiling mode: CTA 0 of the step kernel accumulates clock64() cycles per phase
  * (0 g/h/d + scatter, 1 barrier after it, 2 touched set, 3 d'x fold, 4 line-search partials,

@@ -1,6 +1,7 @@
 """Build libpcdn.so in-tree for sm_100a (nvcc -gencode arch=compute_100a,code=sm_100a)."""
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
@@ -8,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", "pcdn_api.cu")]
-DEPS = SRC + [os.path.join(HERE, "csrc", "pcdn_kernels.cuh"), os.path.join(ROOT, "include", "pcdn.h")]
+DEPS = SRC + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [os.path.join(ROOT, "include", "pcdn.h"), __file__]
 LIB = os.path.join(HERE, "libpcdn.so")
 
 NVCC_FLAGS = [

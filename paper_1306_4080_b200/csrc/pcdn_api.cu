@@ -14,6 +14,7 @@
 
 #include "../../include/pcdn.h"
 #include "pcdn_kernels.cuh"
+#include "pcdn_resident.cuh"
 
 using namespace pcdn;
 
@@ -25,9 +26,9 @@ constexpr size_t ALIGN = 256;
 inline size_t align_up(size_t x) { return (x + ALIGN - 1) & ~(ALIGN - 1); }
 
 struct Layout {
-    size_t w, z, coef, cnt, bits, rec, dxg, tlist, order, flag, hpos, hlist, hlen, hstart, tiles1, tiles2,
+    size_t w, z, coef, cnt, bits, rec, dxg, tlist, order, flag, colinfo, hpos, hlist, hlen, hstart, tiles1, tiles2,
         seen, dk, deltak, gk, hk, part, hpart, counters, info, F, Fcopy, status, err_idx, err_what, bar,
-        objp, nheavy, prof, dbg_dx, dbg_mark, total;
+        objp, nheavy, prof, dbg_dx, dbg_mark, rec2, rslot, ovf_cnt, total;
 };
 
 Layout make_layout(int64_t s, int64_t n, int64_t nnz)
@@ -51,6 +52,7 @@ Layout make_layout(int64_t s, int64_t n, int64_t nnz)
     L.tlist = take(sizeof(int32_t) * nw * 32);
     L.order = take(sizeof(int32_t) * n);
     L.flag = take(sizeof(int32_t) * n);
+    L.colinfo = take(sizeof(int4) * n);
     L.hpos = take(sizeof(int64_t) * (n + 1));
     L.hlist = take(sizeof(int32_t) * n);
     L.hlen = take(sizeof(int64_t) * n);
@@ -77,6 +79,9 @@ Layout make_layout(int64_t s, int64_t n, int64_t nnz)
     L.prof = take(sizeof(long long) * 16);
     L.dbg_dx = take(sizeof(double) * s);
     L.dbg_mark = take(s);
+    L.rec2 = take(sizeof(Rec) * nnz);
+    L.rslot = take(sizeof(uint32_t) * nnz);
+    L.ovf_cnt = take(sizeof(int) * 16);
     L.total = off + ALIGN;  // slack for base alignment
     return L;
 }
@@ -113,7 +118,10 @@ struct pcdn_ctx {
     int G = 0;          // CTAs of the grid-mode step kernel (cooperative launch)
     int Gc = 0;         // CTAs of the cluster-mode step kernel (one cluster)
     int G_req = 0;
-    int mode_req = 0;   // 0 auto, 1 cluster, 2 grid
+    int mode_req = 0;   // 0 auto, 1 cluster, 2 grid, 3 cluster-resident
+    int res_G = 0;      // CTAs of the cluster-resident kernel (power of two; 0 = unavailable)
+    int res_lg = 0, res_Bs = 0, res_cap = 0, res_cap_req = 0;
+    size_t res_smem = 0;
     int last_mode = 0;
     int heavy_len = 128;
     int num_sms = 0;
@@ -270,6 +278,7 @@ int launch_steps(pcdn_ctx *ctx, int64_t ntot, int64_t P, int64_t nsteps, int64_t
     a.dxg = ctx->at<double>(L.dxg);
     a.tlist = ctx->at<int32_t>(L.tlist);
     a.order = ctx->at<int32_t>(L.order);
+    a.colinfo = ctx->at<int4>(L.colinfo);
     a.hpos = ctx->at<int64_t>(L.hpos);
     a.hlist = ctx->at<int32_t>(L.hlist);
     a.hstart = ctx->at<int64_t>(L.hstart);
@@ -295,16 +304,48 @@ int launch_steps(pcdn_ctx *ctx, int64_t ntot, int64_t P, int64_t nsteps, int64_t
     a.dbg_mark = ctx->at<uint8_t>(L.dbg_mark);
     a.bar = ctx->at<unsigned long long>(L.bar);
     a.status = ctx->at<int>(L.status);
+    a.res_lg = ctx->res_lg;
+    a.res_Bs = ctx->res_Bs;
+    a.res_cap = ctx->res_cap;
+    {
+        const ResLayout RL = res_layout(ctx->res_Bs > 0 ? ctx->res_Bs : 1, ctx->res_cap);
+        a.res_off[0] = (int)RL.zd;
+        a.res_off[1] = (int)RL.coef;
+        a.res_off[2] = (int)RL.head;
+        a.res_off[3] = (int)RL.lq;
+        a.res_off[4] = (int)RL.y;
+        a.res_off[5] = (int)RL.recin;
+        a.res_off[6] = 0;
+        a.res_off[7] = (int)RL.total;
+    }
+    a.rec2 = ctx->at<Rec>(L.rec2);
+    a.rslot = ctx->at<uint32_t>(L.rslot);
+    a.ovf_cnt = ctx->at<int>(L.ovf_cnt);
     CU(cudaMemsetAsync(a.bar, 0, sizeof(unsigned long long), ctx->stream));
     // cluster mode for steps small enough that 16 SMs keep up (hardware barrier, ~0.2 us);
     // grid mode (all SMs, software barrier) for large steps
     int mode = ctx->mode_req;
     if (mode == 0) {
         const double est_nb = (double)ctx->nnz * (double)P / (double)ctx->n;
-        mode = (ctx->Gc >= 2 && est_nb <= 65536.0) ? 1 : 2;
+        if (ctx->res_G >= 2 && est_nb <= 65536.0) mode = 3;
+        else mode = (ctx->Gc >= 2 && est_nb <= 65536.0) ? 1 : 2;
     }
     ctx->last_mode = mode;
-    if (mode == 1) {
+    if (mode == 3) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(ctx->res_G);
+        cfg.blockDim = dim3(NT);
+        cfg.dynamicSmemBytes = ctx->res_smem;
+        cfg.stream = ctx->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = ctx->res_G;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CU(cudaLaunchKernelEx(&cfg, k_step_res, a));
+    } else if (mode == 1) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(ctx->Gc);
         cfg.blockDim = dim3(NT);
@@ -365,6 +406,55 @@ int configure_launch(pcdn_ctx *ctx)
             maxc = 0;
         }
         if (maxc > 16) maxc = 16;
+    }
+    // cluster-resident kernel: the largest power-of-two cluster whose CTAs hold ceil(s/G)
+    // samples plus a record buffer of >= 256 records in shared memory
+    {
+        int optin = 0;
+        CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        const void *kr = (const void *)k_step_res;
+        CU(cudaFuncSetAttribute(kr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        ctx->res_G = 0;
+        const int greq = ctx->mode_req == 3 ? ctx->G_req : 0;
+        for (int lg = 4; lg >= 0; lg--) {
+            const int G = 1 << lg;
+            if (greq > 0 && G != greq) continue;
+            const int64_t Bs = (ctx->s + G - 1) / G;
+            if (Bs > 32 * NT) continue;   // <= 32 owned samples per thread
+            const ResLayout L0 = res_layout((int)Bs, 0);
+            if ((int64_t)L0.total + 64 > optin) continue;
+            int cap = (int)(((int64_t)optin - (int64_t)L0.total - 64) / (int64_t)R_BYTES_PER_RECORD);
+            if (ctx->res_cap_req > 0 && ctx->res_cap_req < cap) cap = ctx->res_cap_req;
+            while (cap > 0 && res_layout((int)Bs, cap).total > (size_t)optin) cap--;
+            if (cap < (ctx->res_cap_req > 0 ? 1 : 256)) continue;
+            const size_t sm = res_layout((int)Bs, cap).total;
+            CU(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(G);
+            cfg.blockDim = dim3(NT);
+            cfg.dynamicSmemBytes = sm;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = G;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int nclu = 0;
+            if (cudaOccupancyMaxActiveClusters(&nclu, kr, &cfg) != cudaSuccess) {
+                cudaGetLastError();
+                nclu = 0;
+            }
+            if (nclu < 1) continue;
+            ctx->res_G = G;
+            ctx->res_lg = lg;
+            ctx->res_Bs = (int)Bs;
+            ctx->res_cap = cap;
+            ctx->res_smem = sm;
+            break;
+        }
+        if (ctx->mode_req == 3 && ctx->res_G < 1)
+            return set_err(ctx, PCDN_ERR_INVALID, "cluster-resident mode unavailable for s=%lld", (long long)ctx->s);
     }
     const bool want_cluster = ctx->mode_req == 1;
     ctx->G = (!want_cluster && ctx->G_req > 0 && ctx->G_req < maxg) ? ctx->G_req : maxg;
@@ -511,11 +601,20 @@ int pcdn_set_debug(pcdn_ctx *ctx, int on)
 int pcdn_set_launch(pcdn_ctx *ctx, int mode, int ctas, int heavy_len)
 {
     if (!ctx) return PCDN_ERR_INVALID;
-    if (mode < 0 || mode > 2 || ctas < 0 || heavy_len < 0 || (mode == 1 && ctas > 16))
+    if (mode < 0 || mode > 3 || ctas < 0 || heavy_len < 0 || (mode == 1 && ctas > 16) ||
+        (mode == 3 && (ctas > 16 || (ctas & (ctas - 1)) != 0)))
         return set_err(ctx, PCDN_ERR_INVALID, "invalid launch knobs");
     ctx->mode_req = mode;
     ctx->G_req = ctas;
     if (heavy_len > 0) ctx->heavy_len = heavy_len;
+    return configure_launch(ctx);
+}
+
+int pcdn_set_resident_cap(pcdn_ctx *ctx, int cap)
+{
+    if (!ctx) return PCDN_ERR_INVALID;
+    if (cap < 0) return set_err(ctx, PCDN_ERR_INVALID, "negative record capacity");
+    ctx->res_cap_req = cap;
     return configure_launch(ctx);
 }
 
@@ -609,7 +708,8 @@ int pcdn_objective(pcdn_ctx *ctx, int recompute_from_w, double *F_out)
 int pcdn_permutation(pcdn_ctx *ctx, uint64_t seed, int64_t k, int32_t *out)
 {
     if (!ctx || !out || k < 0) return PCDN_ERR_INVALID;
-    k_perm<<<grid1d(ctx->n), 256, 0, ctx->stream>>>(seed, k, ctx->n, ctx->col_ptr, ctx->heavy_len, out, nullptr);
+    k_perm<<<grid1d(ctx->n), 256, 0, ctx->stream>>>(seed, k, ctx->n, ctx->col_ptr, ctx->heavy_len, out, nullptr,
+                                                     nullptr);
     ctx->launches++;
     CU(cudaGetLastError());
     return PCDN_OK;
@@ -628,7 +728,8 @@ int pcdn_bundle_step(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, pcdn_step_
                                                       ctx->at<int32_t>(L.order), ctx->at<int32_t>(L.flag),
                                                       ctx->at<uint32_t>(L.seen), ctx->at<int>(L.status),
                                                       ctx->at<long long>(L.err_idx),
-                                                      (unsigned long long *)(ctx->at<int64_t>(L.counters) + 2));
+                                                      (unsigned long long *)(ctx->at<int64_t>(L.counters) + 2),
+                                                      ctx->at<int4>(L.colinfo));
     k_bundle_unseen<<<grid1d(P), 256, 0, ctx->stream>>>(bundle, P, ctx->n, ctx->at<uint32_t>(L.seen));
     ctx->launches += 2;
     CU(cudaGetLastError());
@@ -702,7 +803,8 @@ int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_
     for (k = 0; k < max_outer; k++) {
         // a0: partition pi_k and the per-step heavy-column lists
         k_perm<<<grid1d(ctx->n), 256, 0, ctx->stream>>>(seed, k, ctx->n, ctx->col_ptr, ctx->heavy_len,
-                                                         ctx->at<int32_t>(L.order), ctx->at<int32_t>(L.flag));
+                                                         ctx->at<int32_t>(L.order), ctx->at<int32_t>(L.flag),
+                                                         ctx->at<int4>(L.colinfo));
         ctx->launches++;
         CU(cudaGetLastError());
         if ((rc = build_heavy(ctx, ctx->n))) return rc;

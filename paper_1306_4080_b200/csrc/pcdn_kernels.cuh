@@ -74,6 +74,7 @@ struct StepArgs {
     int32_t *tlist;  // T, per row block, ascending
     // bundles of this launch
     const int32_t *__restrict__ order;  // feature id per position
+    const int4 *__restrict__ colinfo;   // packed (j, length, col_ptr[j]) per position
     const int64_t *__restrict__ hpos;   // heavy positions before each position [ntot+1]
     const int32_t *__restrict__ hlist;  // heavy entry -> position
     const int64_t *__restrict__ hstart; // heavy entry -> global heavy-nnz offset [nheavy+1]
@@ -93,6 +94,14 @@ struct StepArgs {
     long long *prof;     // nullable: per-phase clock64 cycles of CTA 0 (profiling mode)
     double *dbg_dx;
     uint8_t *dbg_mark;
+    // cluster-resident variant (pcdn_resident.cuh): cluster of 2^res_lg CTAs, res_Bs samples
+    // per CTA, res_cap records per CTA in shared memory; rec (as the overflow of received
+    // records), rec2 (overflow segments) and rslot (overflow slots) are global spill regions
+    int res_lg, res_Bs, res_cap;
+    int res_off[8];   // byte offsets of the dynamic shared-memory arrays (ResLayout)
+    Rec *rec2;
+    uint32_t *rslot;
+    int *ovf_cnt;   // [16] overflow records received per CTA in the current step
     // sync
     unsigned long long *bar;
     int *status;
@@ -316,15 +325,30 @@ __device__ __forceinline__ int64_t feistel_perm(const FeistelKeys &f, int64_t n,
     return (int64_t)x;
 }
 
-// order[t] = pi_k(t); flag[t] = column length > heavy_len
+// packed per-position column descriptor: (feature j, column length, col_ptr[j] lo, hi) -- one
+// 16-byte load gives the step kernel everything it needs to issue a column's loads
+__device__ __forceinline__ int4 make_colinfo(int32_t j, int64_t p0, int64_t len)
+{
+    return make_int4(j, (int)len, (int)(uint32_t)(p0 & 0xffffffffLL), (int)(p0 >> 32));
+}
+__device__ __forceinline__ int64_t colinfo_p0(const int4 &ci)
+{
+    return (int64_t)(((uint64_t)(uint32_t)ci.w << 32) | (uint64_t)(uint32_t)ci.z);
+}
+
+// order[t] = pi_k(t); flag[t] = column length > heavy_len; colinfo[t] (nullable)
 __global__ void k_perm(uint64_t seed, int64_t k, int64_t n, const int64_t *__restrict__ col_ptr,
-                       int heavy_len, int32_t *order, int32_t *flag)
+                       int heavy_len, int32_t *order, int32_t *flag, int4 *colinfo)
 {
     const FeistelKeys f = feistel_keys(seed, k, n);
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = feistel_perm(f, n, t);
         order[t] = (int32_t)j;
-        if (flag) flag[t] = (__ldg(&col_ptr[j + 1]) - __ldg(&col_ptr[j])) > heavy_len ? 1 : 0;
+        if (flag) {
+            const int64_t p0 = __ldg(&col_ptr[j]), len = __ldg(&col_ptr[j + 1]) - p0;
+            flag[t] = len > heavy_len ? 1 : 0;
+            if (colinfo) colinfo[t] = make_colinfo((int32_t)j, p0, len);
+        }
     }
 }
 
@@ -332,7 +356,7 @@ __global__ void k_perm(uint64_t seed, int64_t k, int64_t n, const int64_t *__res
 __global__ void k_bundle_prep(const int32_t *__restrict__ bundle, int64_t P, int64_t n,
                               const int64_t *__restrict__ col_ptr, int heavy_len, int32_t *order,
                               int32_t *flag, uint32_t *seen, int *status, long long *err_idx,
-                              unsigned long long *bundle_nnz)
+                              unsigned long long *bundle_nnz, int4 *colinfo)
 {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < P; t += (int64_t)gridDim.x * blockDim.x) {
         const int32_t j = bundle[t];
@@ -341,6 +365,7 @@ __global__ void k_bundle_prep(const int32_t *__restrict__ bundle, int64_t P, int
             atomicMin(err_idx, (long long)t);
             order[t] = 0;
             flag[t] = 0;
+            colinfo[t] = make_colinfo(0, 0, 0);
             continue;
         }
         const uint32_t bit = 1u << (j & 31);
@@ -350,8 +375,9 @@ __global__ void k_bundle_prep(const int32_t *__restrict__ bundle, int64_t P, int
             atomicMin(err_idx, (long long)t);
         }
         order[t] = j;
-        const int64_t len = __ldg(&col_ptr[j + 1]) - __ldg(&col_ptr[j]);
+        const int64_t p0 = __ldg(&col_ptr[j]), len = __ldg(&col_ptr[j + 1]) - p0;
         flag[t] = len > heavy_len ? 1 : 0;
+        colinfo[t] = make_colinfo(j, p0, len);
         atomicAdd(bundle_nnz, (unsigned long long)len);   // integer: order-independent
     }
 }

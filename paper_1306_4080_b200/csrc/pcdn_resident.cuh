@@ -1,0 +1,1160 @@
+// pcdn_resident.cuh -- the cluster-resident bundle-step kernel.
+//
+// Small bundle steps (the configured P of configs 1-3) are bound by the latency of the
+// exchanges between phases, not by HBM.  This variant keeps ALL per-sample state
+// in the distributed shared memory of one thread-block cluster for the whole launch (one launch =
+// all b bundle steps of an outer iteration), and synchronises the steps with point-to-point
+// DSMEM messages instead of cluster barriers: every `barrier.cluster.arrive.release` costs a
+// GPU-scope memory drain (MEMBAR.ALL.GPU + ERRBAR in SASS), while `st.async` stores that
+// complete a transaction count on the receiver's mbarrier need no fence at all.
+//
+//   CTA c of the G-CTA cluster (G = 2^lg <= 16) owns samples i = li*G + c:
+//     zd[li] = (z_i, dx_i): retained w'x_i and the d'x_i of the LAST step (0 if
+//     the sample was not touched), coef[li] = (G_i, H_i) (Eq.13 / App. A.2 factors), y[li].
+//
+//   phase A   warp per light column (split over all warps for heavy columns): coalesced
+//             row-index/value loads from HBM; gather of (z_i, dx_i) from the owner's shared
+//             memory and coef(z_i + alpha_prev dx_i) -- the previous step's commit applied on the
+//             fly (the owner commits it lazily, below); g/h -> d (Eq.5) -> Delta term; if
+//             d_j != 0 each nonzero sends the record (li, k, d_j x_ij) with st.async into this
+//             CTA's fixed region of the owner's buffer.  Then one st.async per owner carries the
+//             record count (mbarrier M0).
+//   phase C   every CTA, locally: wait M0 (every producer has finished its gathers), commit the
+//             previous step to its own samples (z += alpha_prev dx, coef, dx = 0), wait M1 (the
+//             records: expected bytes = 16 x the counts), link each record into its sample's
+//             list (one atomicExch), fold each list in ascending bundle position k (registers;
+//             long lists by a warp) -> d'x_i (a3), deterministic, no float atomics; per-sample
+//             loss changes for a window of Armijo candidates (Eq.12, a4) plus the L1 term and
+//             Delta over the CTA's own bundle positions -> one partial row, sent with st.async to
+//             every CTA (M2); every CTA sums the G rows in the same fixed order and takes the
+//             same decision (first q with LHS <= sigma alpha Delta).
+//   commit    w_B in HBM, F (a5); z/coef of the touched samples are committed lazily by their
+//             owners at the next step (and at the end of the launch).
+//
+// Records that do not fit a producer's region spill to the owner's HBM overflow region sized
+// by the nonzeros of the owner's samples (an upper bound on what a step can send it), so every
+// step size is handled; z and coef are written back to HBM at the end of the launch.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "pcdn_kernels.cuh"
+
+namespace pcdn {
+
+namespace cgx = cooperative_groups;
+
+constexpr int R_HB = 256;  // per-warp bitonic buffer for samples with many records in one step
+constexpr int R_CPW = 8;   // own bundle positions per warp whose column results stay in smem
+constexpr int R_WMAX = 16; // partial-row slots (WinLayout<QW>::W)
+
+struct __align__(16) RRec {  // a record: sample (then: next record of the sample's list), k, value
+    int32_t li;
+    int32_t k;
+    double v;
+};
+
+struct ResFixed {
+    // mbarriers: M0 record counts, M1 records, M2/M3 line-search partial rows of even/odd
+    // windows (two: a fast CTA's next-window row must not complete this window's phase)
+    uint64_t mb[4];
+    int64_t hst[NE_MAX + 1];
+    double hg[NE_MAX][NW];
+    double hh[NE_MAX][NW];
+    double hd[NE_MAX];
+    int64_t ce0, ce1;
+    int64_t cross_e[2];
+    double cross_d[2];
+    double red[NW][32];
+    __align__(16) double part_in[2][16][R_WMAX];   // partial rows from every CTA, by window parity
+    // the CTA's own bundle positions kk = k0 + c*NW + warp + m*G*NW, m < R_CPW: the column
+    // results of phase A kept for the line search's L1 term and the w commit (slot m*NW + warp)
+    int32_t colj[R_CPW * NW];
+    int32_t colf[R_CPW * NW];    // 1 = light column computed by the slot's warp, 0 = heavy (HBM)
+    double colw[R_CPW * NW];
+    double cold[R_CPW * NW];
+    double coldl[R_CPW * NW];
+    unsigned long long scan_w[NW];
+    int64_t ovf_base[16];        // HBM overflow base of every CTA of the cluster
+    int64_t own_nnz;
+    int sendcnt[16];             // records this CTA sent to each owner in the current step
+    uint32_t recvcnt[16];        // records each producer CTA sent to this CTA (st.async, M0)
+    int spilled;                 // this CTA wrote overflow records to HBM in the current step
+    int nlong;                   // samples whose list is longer than NREG (queued in lq)
+    int stage_n;                 // HBM staging used by long lists in the current step
+    int dec_q[2], dec_bad[2];    // the decision of the window, by window parity
+    double dec_alpha[2], dec_lhs[2], dec_rhs[2], dec_Delta[2], dec_nT[2];
+    double F;
+    long long cnt[4];
+    long long pacc[8];
+    int32_t sk[NHW][R_HB];
+    double sv[NHW][R_HB];
+};
+
+// byte layout of the dynamic shared memory of one CTA (identical in every CTA of the cluster)
+struct ResLayout {
+    int Bs, cap;
+    size_t zd, coef, head, lq, y, recin, total;
+};
+
+__host__ __device__ inline size_t r_align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+__host__ __device__ inline ResLayout res_layout(int Bs, int cap)
+{
+    ResLayout L;
+    L.Bs = Bs;
+    L.cap = cap;
+    size_t o = r_align16(sizeof(ResFixed));
+    L.zd = o;   o = r_align16(o + sizeof(double2) * Bs);
+    L.coef = o; o = r_align16(o + sizeof(double2) * Bs);
+    L.head = o; o = r_align16(o + sizeof(int32_t) * Bs);
+    L.lq = o;   o = r_align16(o + sizeof(int32_t) * Bs);
+    L.y = o;    o = r_align16(o + Bs);
+    L.recin = o; o = r_align16(o + sizeof(RRec) * cap);
+    L.total = o;
+    return L;
+}
+constexpr int R_BYTES_PER_RECORD = 16;
+
+struct ResCtx {
+    ResFixed *fx;
+    double2 *zd, *coef;
+    int32_t *head, *lq;
+    int8_t *y;
+    RRec *recin;
+    int lg, G, c, Bs, Bsc, cap, capP, per;
+    int64_t my_ovf;
+    double alpha_prev;   // the accepted step of the previous bundle step (0: none / null step)
+};
+
+// ---------------------------------------------------------------------------------------
+// DSMEM / mbarrier primitives (sm_90+ PTX)
+// ---------------------------------------------------------------------------------------
+#ifdef PCDN_ALIGN_CHECK
+#include <cstdio>
+#define RCHK(p, al, site)                                                                          \
+    do {                                                                                           \
+        if (((uintptr_t)(p)) & ((al)-1)) {                                                         \
+            printf("PCDN misaligned site %d ptr %p (cta %d tid %d)\n", site, (void *)(p), (int)blockIdx.x, (int)threadIdx.x); \
+            __trap();                                                                              \
+        }                                                                                          \
+    } while (0)
+#else
+#define RCHK(p, al, site) do {} while (0)
+#endif
+template <typename T>
+__device__ __forceinline__ T *remote(T *p, int rank)
+{
+    T *r = cgx::this_cluster().map_shared_rank(p, (unsigned)rank);
+    RCHK(r, alignof(T), 1);
+    return r;
+}
+__device__ __forceinline__ uint32_t s_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int rank)
+{
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_u32(uint32_t raddr, uint32_t v, uint32_t rbar)
+{
+    RCHK(raddr, 4, 4);
+    RCHK(rbar, 8, 5);
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];"
+                 :: "r"(raddr), "r"(v), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void st_async_f64x2(uint32_t raddr, double a0, double a1, uint32_t rbar)
+{
+    RCHK(raddr, 16, 2);
+    RCHK(rbar, 8, 3);
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+                 :: "r"(raddr), "d"(a0), "d"(a1), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, int count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+}
+// Wait for the phase with the given parity (acquire, cluster scope).  A phase that does not
+// complete within ~4 s of SM clock means a broken protocol: trap instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
+{
+    uint32_t done;
+    const long long t0 = clock64();
+    do {
+        asm volatile("{\n\t.reg .pred P;\n\t"
+                     "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, P;\n\t}"
+                     : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+        if (!done && clock64() - t0 > 8000000000LL) __trap();
+    } while (!done);
+}
+// orders this CTA's shared-memory writes before a later cluster-scope signal (MEMBAR.CTA only)
+__device__ __forceinline__ void fence_smem_release_cluster()
+{
+    asm volatile("fence.release.sync_restrict::shared::cta.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_sync_all()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// coef of sample i after the previous step: from the owner's (z_i, dx_i) and alpha_prev; a
+// sample the previous step did not touch has dx_i = 0 and its stored coef is used as is
+__device__ __forceinline__ double2 res_coef(const StepArgs &a, const ResCtx &R, int32_t i)
+{
+    const int owner = i & (R.G - 1);
+    const int li = i >> R.lg;
+    const double2 zd = *remote(&R.zd[li], owner);
+    const double2 cf = *remote(&R.coef[li], owner);
+    if (zd.y == 0.0) return cf;
+    return coef_of(a.loss, zd.x + R.alpha_prev * zd.y, (int)__ldg(&a.y[i]));
+}
+
+// Send the records (sample i, bundle position k, d_k x_ik) of the warp's valid lanes to their
+// owners.  Every producer CTA p has a fixed region [p*capP, (p+1)*capP) of each owner's record
+// buffer; the slot comes from a LOCAL shared-memory counter per owner (one atomic per group of
+// lanes with the same owner), the record travels by st.async and completes 16 bytes on the
+// owner's M1.  Records beyond the region go to the owner's HBM overflow (global atomic slot;
+// rare).  All 32 lanes must call.
+__device__ __forceinline__ void res_emit_warp(const StepArgs &a, const ResCtx &R, bool valid, int32_t i, int32_t k,
+                                              double v, int lane)
+{
+    const int owner = valid ? (i & (R.G - 1)) : -1;
+    const unsigned grp = __match_any_sync(0xffffffffu, owner);
+    const int leader = __ffs(grp) - 1;
+    int base = 0;
+    if (valid && lane == leader) base = atomicAdd(&R.fx->sendcnt[owner], __popc(grp));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (!valid) return;
+    const int slot = base + __popc(grp & ((1u << lane) - 1u));
+    RRec r;
+    r.li = i >> R.lg;
+    r.k = k;
+    r.v = v;
+    const double2 raw = *reinterpret_cast<const double2 *>(&r);
+    if (slot < R.capP) {
+        st_async_f64x2(mapa_u32(s_addr(&R.recin[R.c * R.capP + slot]), owner), raw.x, raw.y,
+                       mapa_u32(s_addr(&R.fx->mb[1]), owner));
+    } else {
+        const int gs = atomicAdd(&a.ovf_cnt[owner], 1);
+        __stcg(reinterpret_cast<double2 *>(&a.rec[R.fx->ovf_base[owner] + gs]), raw);
+        R.fx->spilled = 1;
+    }
+}
+
+__device__ __forceinline__ void res_col_gh(const StepArgs &a, const ResCtx &R, int64_t p0, int64_t p1, int lane,
+                                           double &gs, double &hs)
+{
+    double g = 0.0, h = 0.0;
+    for (int64_t p = p0 + lane; p < p1; p += 32) {
+        const int32_t i = __ldg(&a.row_idx[p]);
+        const double x = (double)__ldg(&a.val[p]);
+        const double2 cf = res_coef(a, R, i);
+        g += x * cf.x;
+        h += (x * x) * cf.y;
+    }
+    gs = warp_sum(g);
+    hs = warp_sum(h);
+}
+
+__device__ __forceinline__ void res_col_scatter(const StepArgs &a, const ResCtx &R, int64_t p0, int64_t p1, int lane,
+                                                int32_t kpos, double d)
+{
+    for (int64_t pb = p0; pb < p1; pb += 32) {
+        const int64_t p = pb + lane;
+        const bool ok = p < p1;
+        const int32_t i = ok ? __ldg(&a.row_idx[p]) : 0;
+        const double v = ok ? d * (double)__ldg(&a.val[p]) : 0.0;
+        res_emit_warp(a, R, ok, i, kpos, v, lane);
+    }
+}
+
+// a received record by slot index: the shared buffer below cap, the CTA's HBM overflow above
+__device__ __forceinline__ RRec res_rec(const StepArgs &a, const ResCtx &R, int phys)
+{
+    double2 raw;
+    RCHK(&R.recin[phys], 16, 6);
+    if (phys < R.cap) raw = *reinterpret_cast<const double2 *>(&R.recin[phys]);
+    else raw = __ldcg(reinterpret_cast<const double2 *>(&a.rec[R.my_ovf + (phys - R.cap)]));
+    return *reinterpret_cast<const RRec *>(&raw);
+}
+
+// Fold of one long list (> NREG records) by a warp.  Lane 0 walks the list into HBM staging
+// (the CTA's rec2 region); <= R_HB records are bitonic-sorted by k in shared memory and summed
+// by lane-contiguous partials combined in a fixed tree; longer lists by repeated warp-wide
+// minimum extraction.  The k of one sample's records are distinct (one record per column).
+__device__ double res_fold_long(const StepArgs &a, const ResCtx &R, int h, int lane, int32_t *sk, double *sv)
+{
+    int n = 0;
+    long long base = 0;
+    RRec *stage = reinterpret_cast<RRec *>(a.rec2);
+    if (lane == 0) {
+        for (int p = h; p >= 0; p = res_rec(a, R, p).li) n++;
+        base = R.my_ovf + atomicAdd(&R.fx->stage_n, n);
+        int t = 0;
+        for (int p = h; p >= 0;) {
+            const RRec r = res_rec(a, R, p);
+            __stcg(reinterpret_cast<double2 *>(&stage[base + t]), *reinterpret_cast<const double2 *>(&r));
+            t++;
+            p = r.li;
+        }
+    }
+    n = __shfl_sync(0xffffffffu, n, 0);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    __syncwarp();
+    const RRec *seg = stage + base;
+    auto ld = [&](int r, int32_t &k, double &v) {
+        const double2 raw = __ldcg(reinterpret_cast<const double2 *>(&seg[r]));
+        k = (int32_t)(__double_as_longlong(raw.x) >> 32);
+        v = raw.y;
+    };
+    if (n <= R_HB) {
+        int npow = 32;
+        while (npow < n) npow <<= 1;
+        for (int r = lane; r < npow; r += 32) {
+            if (r < n) {
+                ld(r, sk[r], sv[r]);
+            } else {
+                sk[r] = 0x7fffffff;
+                sv[r] = 0.0;
+            }
+        }
+        __syncwarp();
+        for (int kbit = 2; kbit <= npow; kbit <<= 1) {
+            for (int jbit = kbit >> 1; jbit > 0; jbit >>= 1) {
+                for (int r = lane; r < npow; r += 32) {
+                    const int pr = r ^ jbit;
+                    if (pr > r) {
+                        const bool up = (r & kbit) == 0;
+                        const int32_t k1 = sk[r], k2 = sk[pr];
+                        if ((k1 > k2) == up) {
+                            sk[r] = k2;
+                            sk[pr] = k1;
+                            const double t = sv[r];
+                            sv[r] = sv[pr];
+                            sv[pr] = t;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        const int chunk = (n + 31) / 32;
+        double s = 0.0;
+        for (int r = lane * chunk; r < min(n, (lane + 1) * chunk); r++) s += sv[r];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_down_sync(0xffffffffu, s, o);
+            if ((lane & (2 * o - 1)) == 0) s += t;
+        }
+        __syncwarp();
+        return __shfl_sync(0xffffffffu, s, 0);
+    }
+    double dx = 0.0;
+    int last = -1;
+    for (int t = 0; t < n; t++) {
+        int best = 0x7fffffff;
+        double bv = 0.0;
+        for (int r = lane; r < n; r += 32) {
+            int32_t k;
+            double v;
+            ld(r, k, v);
+            if (k > last && k < best) {
+                best = k;
+                bv = v;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            if (ob < best) {
+                best = ob;
+                bv = ov;
+            }
+        }
+        last = best;
+        dx += bv;
+    }
+    return dx;
+}
+
+struct ResProf {   // profiling mode: CTA 0 thread 0 accumulates clock64 cycles per phase
+    bool on;
+    long long t;
+    __device__ __forceinline__ void start() { if (on) t = clock64(); }
+    __device__ __forceinline__ void mark(ResFixed &fx, int i)
+    {
+        if (on) {
+            const long long now = clock64();
+            fx.pacc[i] += now - t;
+            t = now;
+        }
+    }
+};
+
+// Commit the previous step to this CTA's own touched samples (lazily: every producer has
+// finished gathering them): z += alpha dx (Alg.4 l.5 with additive retained z), coef, dx = 0.
+__device__ __forceinline__ void res_lazy_commit(const StepArgs &a, const ResCtx &R, int tid)
+{
+    for (int r = 0; r < R.per; r++) {
+        const int li = tid + r * NT;
+        if (li >= R.Bsc) break;
+        if (R.head[li] < 0) continue;
+        const double2 zd = R.zd[li];
+        const double zn = zd.x + R.alpha_prev * zd.y;
+        R.zd[li] = make_double2(zn, 0.0);
+        R.coef[li] = coef_of(a.loss, zn, R.y[li]);
+        R.head[li] = -1;
+        if (a.debug) {
+            const int64_t i = (int64_t)li * R.G + R.c;
+            a.dbg_dx[i] = zd.y;
+            a.dbg_mark[i] = 1;
+        }
+    }
+}
+
+// One Armijo window over candidates q0 .. q0+NQ-1 (Eq.6 with Eq.12 from retained quantities):
+// per-sample loss changes over this CTA's touched samples (window 0 also folds d'x_i), the L1
+// term and Delta over the CTA's own bundle positions, a fixed-order CTA partial row, sent to
+// every CTA of the cluster (st.async, M2); each CTA sums the G rows in the same fixed order and
+// takes the same decision.
+template <int NQ>
+__device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, WinState &ws, int64_t k0, int64_t k1,
+                                          int tid, int lane, int warp, ResProf &pr, int wcount)
+{
+    using LY = WinLayout<NQ>;
+    constexpr int W = LY::W;
+    ResFixed &fx = *R.fx;
+    double alpha0 = 1.0;
+    for (int q = 0; q < ws.q0; q++) alpha0 *= a.beta;
+    double acc[W];
+#pragma unroll
+    for (int q = 0; q < W; q++) acc[q] = 0.0;
+    int ntouch = 0;
+    unsigned longmask = 0;   // owned samples (bit r) whose list is longer than NREG
+    if (ws.win == 0) {
+        for (int r = 0; r < R.per; r++) {
+            const int li = tid + r * NT;
+            if (li >= R.Bsc) break;
+            const int h = R.head[li];
+            if (h < 0) continue;
+            ntouch++;
+            RRec rc = res_rec(a, R, h);
+            double dx;
+            if (rc.li < 0) {   // one record: the common case
+                dx = rc.v;
+            } else {
+                // up to NREG records: gather, then add in ascending k (selection in registers)
+                int kk[NREG];
+                double vv[NREG];
+                kk[0] = rc.k;
+                vv[0] = rc.v;
+                int ni = 1, p = rc.li;
+#pragma unroll
+                for (int e = 1; e < NREG; e++) {
+                    kk[e] = 0x7fffffff;
+                    vv[e] = 0.0;
+                    if (p >= 0) {
+                        rc = res_rec(a, R, p);
+                        kk[e] = rc.k;
+                        vv[e] = rc.v;
+                        p = rc.li;
+                        ni++;
+                    }
+                }
+                if (p >= 0) {   // long list: folded by a warp after the CTA reduction below
+                    longmask |= 1u << r;
+                    R.lq[atomicAdd(&fx.nlong, 1)] = li;
+                    continue;
+                }
+                dx = 0.0;
+                int last = -1;
+                for (int t = 0; t < ni; t++) {
+                    int best = 0x7fffffff;
+                    double bv = 0.0;
+#pragma unroll
+                    for (int e = 0; e < NREG; e++) {
+                        const bool take = kk[e] > last && kk[e] < best;
+                        best = take ? kk[e] : best;
+                        bv = take ? vv[e] : bv;
+                    }
+                    last = best;
+                    dx += bv;
+                }
+            }
+            const double zi = R.zd[li].x;
+            R.zd[li].y = dx;
+            const double cg = R.coef[li].x;
+            const int yi = R.y[li];
+            double al = alpha0;
+#pragma unroll
+            for (int q = 0; q < NQ; q++) {
+                acc[q] += loss_change(a.loss, zi, yi, cg, dx, al);
+                al *= a.beta;
+            }
+        }
+    } else {
+        for (int r = 0; r < R.per; r++) {
+            const int li = tid + r * NT;
+            if (li >= R.Bsc) break;
+            if (R.head[li] < 0) continue;
+            ntouch++;
+            const double2 zd = R.zd[li];
+            const double cg = R.coef[li].x;
+            const int yi = R.y[li];
+            double al = alpha0;
+#pragma unroll
+            for (int q = 0; q < NQ; q++) {
+                acc[q] += loss_change(a.loss, zd.x, yi, cg, zd.y, al);
+                al *= a.beta;
+            }
+        }
+    }
+    // L1 part of Eq.12 and Delta over this CTA's own bundle positions (monotone in s2)
+    for (int s2 = tid;; s2 += NT) {
+        const int m = s2 / NW, wq = s2 - m * NW;
+        const int64_t kk = k0 + (int64_t)R.c * NW + wq + (int64_t)m * R.G * NW;
+        if (kk >= k1) break;
+        double wj, d, dl;
+        if (m < R_CPW && fx.colf[s2]) {
+            wj = fx.colw[s2];
+            d = fx.cold[s2];
+            dl = fx.coldl[s2];
+        } else {
+            wj = ldcg(&a.w[__ldg(&a.order[kk])]);
+            d = ldcg(&a.dk[kk - k0]);
+            dl = ldcg(&a.deltak[kk - k0]);
+        }
+        double al = alpha0;
+#pragma unroll
+        for (int q = 0; q < NQ; q++) {
+            acc[NQ + q] += fabs(wj + al * d) - fabs(wj);
+            al *= a.beta;
+        }
+        acc[LY::DELTA] += dl;
+    }
+    acc[LY::NTOUCH] = (double)ntouch;
+    pr.mark(fx, 3);
+    constexpr int SPL = 32 / W;
+    {
+        const double tot = xreduce<W>(acc, lane);
+        if ((lane % SPL) == 0) fx.red[warp][lane / SPL] = tot;
+    }
+    __syncthreads();
+    if (ws.win == 0 && fx.nlong > 0) {
+        // rare: samples with more than NREG records in this step.  Warps fold their lists, the
+        // owning threads add their loss changes, and the per-warp rows get a second fixed-order
+        // contribution (the structure depends only on the data, so results stay deterministic).
+        const int nl = fx.nlong;
+        if (warp < NHW) {
+            for (int e = warp; e < nl; e += NHW) {
+                const int li = R.lq[e];
+                const double dx = res_fold_long(a, R, R.head[li], lane, fx.sk[warp], fx.sv[warp]);
+                if (lane == 0) R.zd[li].y = dx;
+            }
+        }
+        __syncthreads();
+        double acc2[W];
+#pragma unroll
+        for (int q = 0; q < W; q++) acc2[q] = 0.0;
+        for (int r = 0; r < R.per; r++) {   // each owner thread, in its own fixed order
+            if (!((longmask >> r) & 1u)) continue;
+            const int li = tid + r * NT;
+            const double2 zd = R.zd[li];
+            const double cg = R.coef[li].x;
+            const int yi = R.y[li];
+            double al = alpha0;
+#pragma unroll
+            for (int q = 0; q < NQ; q++) {
+                acc2[q] += loss_change(a.loss, zd.x, yi, cg, zd.y, al);
+                al *= a.beta;
+            }
+        }
+        const double tot2 = xreduce<W>(acc2, lane);
+        if ((lane % SPL) == 0) fx.red[warp][lane / SPL] += tot2;
+        __syncthreads();
+    }
+    const int buf = wcount & 1;
+    const uint32_t mb2 = s_addr(&fx.mb[2 + buf]);
+    if (warp == 0) {
+        // this CTA's partial row -> part_in[buf][c][*] of every CTA (st.async, M2)
+        double sv = 0.0;
+        if (lane < W) {
+#pragma unroll
+            for (int w2 = 0; w2 < NW; w2++) sv += fx.red[w2][lane];
+        }
+        fence_smem_release_cluster();   // zd (dx, lazy commit) must be visible to the gathers
+        constexpr int HW = W / 2;
+        for (int base = 0; base < R.G * HW; base += 32) {
+            const int idx = base + lane;
+            const int q = idx % HW;
+            const double v0 = __shfl_sync(0xffffffffu, sv, 2 * q);
+            const double v1 = __shfl_sync(0xffffffffu, sv, 2 * q + 1);
+            if (idx < R.G * HW) {
+                const int dst = idx / HW;
+                st_async_f64x2(mapa_u32(s_addr(&fx.part_in[buf][R.c][2 * q]), dst), v0, v1, mapa_u32(mb2, dst));
+            }
+        }
+        if (lane == 0) mbar_arrive_tx(mb2, (uint32_t)(8 * W * R.G));
+    }
+    mbar_wait(mb2, (uint32_t)((wcount >> 1) & 1));
+    pr.mark(fx, 4);
+    // warp 0: the G partial rows (local now), fixed-order tree, decision; broadcast in the CTA
+    // (every CTA computes the identical decision)
+    if (warp == 0) {
+        double tot;
+        {
+            double v[W];
+#pragma unroll
+            for (int q = 0; q < W; q++) v[q] = lane < R.G ? fx.part_in[buf][lane][q] : 0.0;
+            tot = xreduce<W>(v, lane);   // lane l holds slot l / SPL
+        }
+        const double Dl = __shfl_sync(0xffffffffu, tot, LY::DELTA * SPL);
+        const double nTt = __shfl_sync(0xffffffffu, tot, LY::NTOUCH * SPL);
+        int qa = -1, badl = 0;
+        double al = alpha0, la = 0.0, ra = 0.0, alpha_a = 0.0;
+#pragma unroll
+        for (int q = 0; q < NQ; q++) {
+            const double Ls = __shfl_sync(0xffffffffu, tot, q * SPL);
+            const double L1 = __shfl_sync(0xffffffffu, tot, (NQ + q) * SPL);
+            if (qa < 0 && !badl) {
+                const double lhs = L1 + a.c * Ls;
+                const double rhs = a.sigma * al * Dl;
+                if (!isfinite(lhs) || !isfinite(Dl)) {
+                    badl = 1;
+                } else if (lhs <= rhs) {
+                    qa = ws.q0 + q;
+                    alpha_a = al;
+                    la = lhs;
+                    ra = rhs;
+                }
+                al *= a.beta;
+            }
+        }
+        if (lane == 0) {
+            fx.dec_q[buf] = qa;
+            fx.dec_bad[buf] = badl;
+            fx.dec_alpha[buf] = alpha_a;
+            fx.dec_lhs[buf] = la;
+            fx.dec_rhs[buf] = ra;
+            fx.dec_Delta[buf] = Dl;
+            fx.dec_nT[buf] = nTt;
+        }
+    }
+    __syncthreads();   // dec_*[buf] is rewritten two windows later, after two more syncs
+    ws.qacc = fx.dec_q[buf];
+    ws.bad = fx.dec_bad[buf];
+    ws.alpha = fx.dec_alpha[buf];
+    ws.lhs = fx.dec_lhs[buf];
+    ws.rhs = fx.dec_rhs[buf];
+    ws.Delta = fx.dec_Delta[buf];
+    ws.nT_tot = fx.dec_nT[buf];
+    ws.win++;
+    pr.mark(fx, 5);
+}
+
+// Prefetch state of a warp's first own column of the next step: the packed descriptor is loaded
+// a step ahead, the row indices / values / w_j are issued at the end of the step.
+struct ResPref {
+    int64_t kk;  // position, -1 = none
+    int64_t p0;
+    int32_t j, len;
+    double wj;
+    int32_t r[PF];
+    float x[PF];
+};
+
+__device__ __forceinline__ void res_issue_col(const StepArgs &a, ResPref &pf, int64_t kk, const int4 &ci, int lane)
+{
+    pf.kk = kk;
+    if (kk < 0) return;
+    pf.j = ci.x;
+    pf.len = ci.y;
+    pf.p0 = colinfo_p0(ci);
+    if (pf.len > a.heavy_len) return;
+    pf.wj = ldcg(&a.w[pf.j]);
+#pragma unroll
+    for (int m = 0; m < PF; m++) {
+        if (lane + 32 * m < pf.len) {
+            pf.r[m] = __ldg(&a.row_idx[pf.p0 + lane + 32 * m]);
+            pf.x[m] = __ldg(&a.val[pf.p0 + lane + 32 * m]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x, c = blockIdx.x;   // one cluster = the whole grid
+    ResCtx R;
+    {
+        // array offsets come from the kernel parameters (constant bank): cheap to rematerialize
+        R.fx = reinterpret_cast<ResFixed *>(smem_raw);
+        R.zd = reinterpret_cast<double2 *>(smem_raw + a.res_off[0]);
+        R.coef = reinterpret_cast<double2 *>(smem_raw + a.res_off[1]);
+        R.head = reinterpret_cast<int32_t *>(smem_raw + a.res_off[2]);
+        R.lq = reinterpret_cast<int32_t *>(smem_raw + a.res_off[3]);
+        R.y = reinterpret_cast<int8_t *>(smem_raw + a.res_off[4]);
+        R.recin = reinterpret_cast<RRec *>(smem_raw + a.res_off[5]);
+        R.lg = a.res_lg;
+        R.G = G;
+        R.c = c;
+        R.Bs = a.res_Bs;
+        R.cap = a.res_cap;
+        R.capP = a.res_cap / G;
+        R.Bsc = (int)((a.s - c + G - 1) / G);   // samples owned by this CTA
+        R.per = (R.Bsc + NT - 1) / NT;          // owned samples per thread (interleaved)
+        R.alpha_prev = 0.0;
+    }
+    ResFixed &fx = *R.fx;
+    RCHK(R.zd, 16, 7);
+    RCHK(R.coef, 16, 8);
+    RCHK(R.recin, 16, 9);
+    RCHK(&fx.part_in[0][0][0], 16, 10);
+    const int64_t GN = (int64_t)G * NW;
+    const int64_t gw = (int64_t)c * NW + warp;
+    const uint32_t mb0 = s_addr(&fx.mb[0]), mb1 = s_addr(&fx.mb[1]);
+
+    // ---------------- prologue: owned per-sample state into shared memory, mbarriers --------
+    long long own = 0;
+    for (int li = tid; li < R.Bsc; li += NT) {
+        const int64_t i = (int64_t)li * G + c;
+        R.zd[li] = make_double2(ldcg(&a.z[i]), 0.0);
+        R.coef[li] = ldcg(&a.coef[i]);
+        R.y[li] = a.y[i];
+        R.head[li] = -1;
+        own += __ldg(&a.row_ptr[i + 1]) - __ldg(&a.row_ptr[i]);
+    }
+    own = warp_sum(own);
+    if (lane == 0) fx.scan_w[warp] = (unsigned long long)own;
+    if (tid < 8) fx.pacc[tid] = 0;
+    if (tid < 16) {
+        fx.sendcnt[tid] = 0;
+        fx.recvcnt[tid] = 0;
+    }
+    if (tid == 0) {
+        for (int b = 0; b < 4; b++) mbar_init(s_addr(&fx.mb[b]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fx.nlong = 0;
+        fx.stage_n = 0;
+        fx.spilled = 0;
+        fx.F = ldcg(a.F);
+        for (int i = 0; i < 4; i++) fx.cnt[i] = 0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        long long t = 0;
+        for (int w2 = 0; w2 < NW; w2++) t += (long long)fx.scan_w[w2];
+        fx.own_nnz = t;
+    }
+    cluster_sync_all();   // every CTA's state and mbarriers are initialised
+    if (warp == 0) {
+        const long long mine = lane < G ? (long long)*remote(&fx.own_nnz, lane) : 0;
+        long long incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane < G) fx.ovf_base[lane] = incl - mine;
+    }
+    __syncthreads();
+    R.my_ovf = fx.ovf_base[c];
+
+    ResProf pr;
+    pr.on = a.prof != nullptr && c == 0 && tid == 0;
+    pr.t = 0;
+    const bool prof = pr.on;
+#define PROF_MARK(i) pr.mark(fx, i)
+    int prev_q = 0;
+    int wcount = 0;            // windows so far in this launch (M2 phase parity)
+    uint32_t ph = 0;           // bit 0: M0 parity, bit 1: M1 parity
+    ResPref pf;
+    {
+        const int64_t kk = gw < min(a.P, a.ntot) ? gw : -1;
+        const int4 ci = kk >= 0 ? __ldg(&a.colinfo[kk]) : make_int4(0, 0, 0, 0);
+        res_issue_col(a, pf, kk, ci, lane);
+    }
+    int64_t h_lo = __ldg(&a.hpos[0]), h_hi = __ldg(&a.hpos[min(a.P, a.ntot)]);
+    for (int64_t t = 0; t < a.nsteps; t++) {
+        pr.start();
+        const int64_t k0 = t * a.P;
+        const int64_t k1 = min(k0 + a.P, a.ntot);
+        const int64_t Pt = k1 - k0;
+        const int64_t kn = k1 + gw, kn1 = min(k1 + a.P, a.ntot);
+        const int4 ci_next = kn < kn1 ? __ldg(&a.colinfo[kn]) : make_int4(0, 0, 0, 0);
+        const int64_t hn_lo = __ldg(&a.hpos[k1]), hn_hi = __ldg(&a.hpos[kn1]);
+
+        // ---------------- phase A: light columns, one warp per column (a1, a2, a3) --------
+        {
+            int m = 0;
+            for (int64_t kk = k0 + gw; kk < k1; kk += GN, m++) {
+                const bool pre = kk == pf.kk;
+                int32_t j, len;
+                int64_t p0;
+                if (pre) {
+                    j = pf.j;
+                    len = pf.len;
+                    p0 = pf.p0;
+                } else {
+                    const int4 ci = __ldg(&a.colinfo[kk]);
+                    j = ci.x;
+                    len = ci.y;
+                    p0 = colinfo_p0(ci);
+                }
+                const int slot = m * NW + warp;
+                if (len > a.heavy_len) {
+                    if (lane == 0 && m < R_CPW) fx.colf[slot] = 0;
+                    continue;
+                }
+                const int64_t p1 = p0 + len;
+                double gs, hs;
+                if (pre) {
+                    double g = 0.0, h = 0.0;
+#pragma unroll
+                    for (int mm = 0; mm < PF; mm++) {
+                        if (lane + 32 * mm < len) {
+                            const double x = (double)pf.x[mm];
+                            const double2 cf = res_coef(a, R, pf.r[mm]);
+                            g += x * cf.x;
+                            h += (x * x) * cf.y;
+                        }
+                    }
+                    for (int64_t p = p0 + lane + 32 * PF; p < p1; p += 32) {
+                        const int32_t i = __ldg(&a.row_idx[p]);
+                        const double x = (double)__ldg(&a.val[p]);
+                        const double2 cf = res_coef(a, R, i);
+                        g += x * cf.x;
+                        h += (x * x) * cf.y;
+                    }
+                    gs = warp_sum(g);
+                    hs = warp_sum(h);
+                } else {
+                    res_col_gh(a, R, p0, p1, lane, gs, hs);
+                }
+                const double wj = pre ? pf.wj : ldcg(&a.w[j]);
+                const Dir r = finish_feature(a, gs, hs, wj);
+                if (lane == 0) {
+                    if (m >= R_CPW || a.d_out) {
+                        a.dk[kk - k0] = r.d;
+                        a.deltak[kk - k0] = r.delta;
+                    }
+                    if (a.g_out) {
+                        a.g_out[kk - k0] = r.g;
+                        a.h_out[kk - k0] = r.h;
+                    }
+                    if (a.d_out) a.d_out[kk - k0] = r.d;
+                    if (m < R_CPW) {
+                        fx.colf[slot] = 1;
+                        fx.colj[slot] = j;
+                        fx.colw[slot] = wj;
+                        fx.cold[slot] = r.d;
+                        fx.coldl[slot] = r.delta;
+                    }
+                }
+                if (r.d != 0.0) {
+                    if (pre) {
+#pragma unroll
+                        for (int mm = 0; mm < PF; mm++)
+                            if (32 * mm < len) {
+                                const bool ok = lane + 32 * mm < len;
+                                res_emit_warp(a, R, ok, pf.r[mm], (int32_t)(kk - k0), ok ? r.d * (double)pf.x[mm] : 0.0, lane);
+                            }
+                        res_col_scatter(a, R, p0 + 32 * PF, p1, lane, (int32_t)(kk - k0), r.d);
+                    } else {
+                        res_col_scatter(a, R, p0, p1, lane, (int32_t)(kk - k0), r.d);
+                    }
+                }
+            }
+        }
+
+        // ---------------- phase A': heavy columns, nnz-balanced over all warps -----------
+        const int64_t e_lo = h_lo, e_hi = h_hi;
+        if (e_hi > e_lo) {
+            const int64_t hb0 = __ldg(&a.hstart[e_lo]);
+            const int64_t NH = __ldg(&a.hstart[e_hi]) - hb0;
+            const int64_t lo_c = (int64_t)c * NH / G, hi_c = (int64_t)(c + 1) * NH / G;
+            if (tid == 0) {
+                int64_t lo = e_lo, hi = e_hi;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (__ldg(&a.hstart[mid + 1]) - hb0 > lo_c) hi = mid; else lo = mid + 1;
+                }
+                fx.ce0 = lo;
+                hi = e_hi;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (__ldg(&a.hstart[mid]) - hb0 >= hi_c) hi = mid; else lo = mid + 1;
+                }
+                fx.ce1 = (hi_c > lo_c) ? lo : fx.ce0;
+                fx.cross_e[0] = fx.cross_e[1] = -1;
+            }
+            __syncthreads();
+            const int64_t ce0 = fx.ce0, ce1 = fx.ce1;
+            const int64_t a_w = lo_c + (int64_t)warp * (hi_c - lo_c) / NW;
+            const int64_t b_w = lo_c + (int64_t)(warp + 1) * (hi_c - lo_c) / NW;
+            for (int64_t rb = ce0; rb < ce1; rb += NE_MAX) {
+                const int ne = (int)min((int64_t)NE_MAX, ce1 - rb);
+                for (int i = tid; i <= ne; i += NT) fx.hst[i] = __ldg(&a.hstart[rb + i]) - hb0;
+                for (int i = tid; i < ne * NW; i += NT) {
+                    fx.hg[i / NW][i % NW] = 0.0;
+                    fx.hh[i / NW][i % NW] = 0.0;
+                }
+                __syncthreads();
+                for (int le = 0; le < ne; le++) {
+                    const int64_t st = fx.hst[le], en = fx.hst[le + 1];
+                    if (en <= a_w) continue;
+                    if (st >= b_w) break;
+                    const int64_t s0 = max(a_w, st), s1 = min(b_w, en);
+                    const int32_t kk = __ldg(&a.hlist[rb + le]);
+                    const int32_t j = __ldg(&a.order[kk]);
+                    const int64_t cs = __ldg(&a.col_ptr[j]);
+                    double gs, hs;
+                    res_col_gh(a, R, cs + (s0 - st), cs + (s1 - st), lane, gs, hs);
+                    if (lane == 0) {
+                        fx.hg[le][warp] = gs;
+                        fx.hh[le][warp] = hs;
+                    }
+                }
+                __syncthreads();
+                for (int le = tid; le < ne; le += NT) {
+                    double gs = 0.0, hs = 0.0;
+                    for (int w2 = 0; w2 < NW; w2++) {
+                        gs += fx.hg[le][w2];
+                        hs += fx.hh[le][w2];
+                    }
+                    const int64_t st = fx.hst[le], en = fx.hst[le + 1];
+                    const int64_t e = rb + le;
+                    if (st >= lo_c && en <= hi_c) {
+                        const int32_t kk = __ldg(&a.hlist[e]);
+                        const int32_t j = __ldg(&a.order[kk]);
+                        const Dir r = finish_feature(a, gs, hs, ldcg(&a.w[j]));
+                        fx.hd[le] = r.d;
+                        a.dk[kk - k0] = r.d;
+                        a.deltak[kk - k0] = r.delta;
+                        if (a.g_out) {
+                            a.g_out[kk - k0] = r.g;
+                            a.h_out[kk - k0] = r.h;
+                        }
+                        if (a.d_out) a.d_out[kk - k0] = r.d;
+                    } else {
+                        const int slot = st < lo_c ? 0 : 1;
+                        HPart hp;
+                        hp.e = e;
+                        hp.g = gs;
+                        hp.h = hs;
+                        hp.pad = 0.0;
+                        a.hpart[(int64_t)c * 2 + slot] = hp;
+                        fx.cross_e[slot] = e;
+                        fx.hd[le] = 0.0;
+                    }
+                }
+                __syncthreads();
+                for (int le = 0; le < ne; le++) {
+                    const int64_t st = fx.hst[le], en = fx.hst[le + 1];
+                    if (en <= a_w) continue;
+                    if (st >= b_w) break;
+                    if (!(st >= lo_c && en <= hi_c)) continue;
+                    const double d = fx.hd[le];
+                    if (d == 0.0) continue;
+                    const int64_t s0 = max(a_w, st), s1 = min(b_w, en);
+                    const int32_t kk = __ldg(&a.hlist[rb + le]);
+                    const int32_t j = __ldg(&a.order[kk]);
+                    const int64_t cs = __ldg(&a.col_ptr[j]);
+                    res_col_scatter(a, R, cs + (s0 - st), cs + (s1 - st), lane, kk - (int32_t)k0, d);
+                }
+                __syncthreads();
+            }
+            cluster_sync_all();
+            if (tid < 2) {
+                const int64_t e = fx.cross_e[tid];
+                fx.cross_d[tid] = 0.0;
+                if (e >= 0) {
+                    const int64_t st = __ldg(&a.hstart[e]) - hb0, en = __ldg(&a.hstart[e + 1]) - hb0;
+                    const int clo = cta_of(st, NH, G), chi = cta_of(en - 1, NH, G);
+                    double gs = 0.0, hs = 0.0;
+                    for (int c2 = clo; c2 <= chi; c2++) {
+                        if ((int64_t)c2 * NH / G == (int64_t)(c2 + 1) * NH / G) continue;
+                        const HPart hp = ld_hpart(&a.hpart[(int64_t)c2 * 2 + (c2 == clo ? 1 : 0)]);
+                        if (hp.e != e) atomicMax(a.status, 4);
+                        gs += hp.g;
+                        hs += hp.h;
+                    }
+                    const int32_t kk = __ldg(&a.hlist[e]);
+                    const int32_t j = __ldg(&a.order[kk]);
+                    const Dir r = finish_feature(a, gs, hs, ldcg(&a.w[j]));
+                    fx.cross_d[tid] = r.d;
+                    if (c == clo) {
+                        a.dk[kk - k0] = r.d;
+                        a.deltak[kk - k0] = r.delta;
+                        if (a.g_out) {
+                            a.g_out[kk - k0] = r.g;
+                            a.h_out[kk - k0] = r.h;
+                        }
+                        if (a.d_out) a.d_out[kk - k0] = r.d;
+                    }
+                }
+            }
+            __syncthreads();
+            for (int sl = 0; sl < 2; sl++) {
+                const int64_t e = fx.cross_e[sl];
+                if (e < 0 || (sl == 1 && e == fx.cross_e[0])) continue;
+                const double d = fx.cross_d[sl];
+                if (d == 0.0) continue;
+                const int64_t st = __ldg(&a.hstart[e]) - hb0, en = __ldg(&a.hstart[e + 1]) - hb0;
+                if (en <= a_w || st >= b_w) continue;
+                const int64_t s0 = max(a_w, st), s1 = min(b_w, en);
+                const int32_t kk = __ldg(&a.hlist[e]);
+                const int32_t j = __ldg(&a.order[kk]);
+                const int64_t cs = __ldg(&a.col_ptr[j]);
+                res_col_scatter(a, R, cs + (s0 - st), cs + (s1 - st), lane, kk - (int32_t)k0, d);
+            }
+        }
+        // ---------------- record counts to every owner (st.async, M0) ----------------------
+        __syncthreads();   // every warp's records are sent and the counters are final
+        if (tid < G) {
+            // HBM data other CTAs read in this step (overflow records, heavy-column results,
+            // dk/deltak of positions beyond R_CPW) is made visible before the count signal
+            if (fx.spilled || e_hi > e_lo || Pt > GN * R_CPW) __threadfence();
+            st_async_u32(mapa_u32(s_addr(&fx.recvcnt[c]), tid), (uint32_t)fx.sendcnt[tid], mapa_u32(mb0, tid));
+            fx.sendcnt[tid] = 0;
+        }
+        if (tid == 0) mbar_arrive_tx(mb0, (uint32_t)(4 * G));
+        PROF_MARK(0);
+        mbar_wait(mb0, ph & 1u);
+        ph ^= 1u;
+        PROF_MARK(1);
+
+        // ---------------- phase C1: lazy commit of the previous step, link the records --------
+        res_lazy_commit(a, R, tid);
+        int n_ovf;
+        {
+            const int ex = lane < G ? max(0, (int)fx.recvcnt[lane] - R.capP) : 0;
+            n_ovf = __reduce_add_sync(0xffffffffu, ex);
+            const int nin = lane < G ? min((int)fx.recvcnt[lane], R.capP) : 0;
+            const int tot_in = __reduce_add_sync(0xffffffffu, nin);
+            if (tid == 0) mbar_arrive_tx(mb1, (uint32_t)(16 * tot_in));
+        }
+        __syncthreads();   // heads reset by the lazy commit
+        if (tid == 0) fx.spilled = 0;
+        mbar_wait(mb1, (ph >> 1) & 1u);
+        ph ^= 2u;
+        if (warp < G) {   // warp p links the records of producer region p
+            const int np = min((int)fx.recvcnt[warp], R.capP);
+            for (int r = lane; r < np; r += 32) {
+                const int phys = warp * R.capP + r;
+                const int li = R.recin[phys].li;
+                R.recin[phys].li = atomicExch(&R.head[li], phys);
+            }
+        }
+        for (int o = tid; o < n_ovf; o += NT) {
+            int32_t *lip = reinterpret_cast<int32_t *>(&a.rec[R.my_ovf + o]);
+            const int li = __ldcg(lip);
+            __stcg(lip, atomicExch(&R.head[li], R.cap + o));
+        }
+        if (tid == 0 && n_ovf) {
+            a.ovf_cnt[c] = 0;
+            __threadfence();   // the reset is visible before this CTA's partial row is sent
+        }
+        __syncthreads();
+        PROF_MARK(2);
+
+        // ---------------- phase C2+C3: fold d'x_i (a3) and the Armijo windows (a4) ----------
+        WinState ws;
+        ws.q0 = 0;
+        ws.nq = prev_q <= 1 ? 2 : QW;
+        ws.qacc = -1;
+        ws.bad = 0;
+        ws.win = 0;
+        while (true) {
+            if (ws.nq <= 2) res_window<2>(a, R, ws, k0, k1, tid, lane, warp, pr, wcount);
+            else res_window<QW>(a, R, ws, k0, k1, tid, lane, warp, pr, wcount);
+            wcount++;
+            if (ws.qacc >= 0 || ws.bad) break;
+            ws.q0 += ws.nq;
+            if (ws.q0 > a.qmax) break;
+            ws.nq = QW;
+        }
+        int qacc = ws.qacc;
+        const bool bad = ws.bad != 0;
+        if (qacc > a.qmax) qacc = -1;
+        const double alpha_acc = qacc < 0 ? 0.0 : ws.alpha;
+        prev_q = qacc < 0 ? QW : qacc;
+        R.alpha_prev = alpha_acc;   // z/coef of the touched samples: committed lazily
+
+        // ---------------- commit (a5): w_B, F ---------------------------------------------
+        if (qacc >= 0) {
+            for (int s2 = tid;; s2 += NT) {
+                const int m = s2 / NW, wq = s2 - m * NW;
+                const int64_t kk = k0 + (int64_t)c * NW + wq + (int64_t)m * GN;
+                if (kk >= k1) break;
+                if (m < R_CPW && fx.colf[s2]) {
+                    a.w[fx.colj[s2]] = fx.colw[s2] + alpha_acc * fx.cold[s2];
+                } else {
+                    const int32_t j = __ldg(&a.order[kk]);
+                    a.w[j] = ldcg(&a.w[j]) + alpha_acc * ldcg(&a.dk[kk - k0]);
+                }
+            }
+        }
+        if (tid == 0) {
+            fx.nlong = 0;
+            fx.stage_n = 0;
+        }
+        if (c == 0 && tid == 0) {
+            double F = fx.F;
+            if (qacc >= 0) F = F + ws.lhs;
+            fx.F = F;
+            *a.F = F;
+            if (bad) atomicMax(a.status, 3);
+            a.info[0] = (double)qacc;
+            a.info[1] = alpha_acc;
+            a.info[2] = ws.Delta;
+            a.info[3] = ws.lhs;
+            a.info[4] = ws.rhs;
+            a.info[5] = F;
+            a.info[7] = ws.nT_tot;
+            const int64_t gstep = a.trace_off + t;
+            if (gstep < a.trace_cap) {
+                if (a.q_trace) a.q_trace[gstep] = qacc;
+                if (a.F_trace) a.F_trace[gstep] = F;
+            }
+            fx.cnt[0] += 1;
+            fx.cnt[1] += qacc < 0 ? 1 : 0;
+            fx.cnt[2] += (int64_t)ws.nT_tot;
+            fx.cnt[3] += Pt;
+        }
+        // next step's first own column (w_j is safe to read: the bundles of a launch are disjoint;
+        // colf/colw of this step were read above by the same threads that rewrite them next)
+        res_issue_col(a, pf, kn < kn1 ? kn : -1, ci_next, lane);
+        h_lo = hn_lo;
+        h_hi = hn_hi;
+        __syncthreads();   // colf/colj/colw of this step are read before the next phase A writes
+        PROF_MARK(6);
+        if (bad) break;
+    }
+    // ---------------- epilogue: last lazy commit, owned per-sample state back to HBM -------
+    res_lazy_commit(a, R, tid);
+    __syncthreads();
+    for (int li = tid; li < R.Bsc; li += NT) {
+        const int64_t i = (int64_t)li * G + c;
+        a.z[i] = R.zd[li].x;
+        a.coef[i] = R.coef[li];
+    }
+    if (c == 0 && tid == 0) {
+        a.counters[0] += fx.cnt[0];
+        a.counters[1] += fx.cnt[1];
+        a.counters[3] += fx.cnt[2];
+        a.counters[4] += fx.cnt[3];
+    }
+    if (prof)
+        for (int i = 0; i < 8; i++) a.prof[i] += fx.pacc[i];
+#undef PROF_MARK
+    cluster_sync_all();   // no CTA exits while another may still read its shared memory
+}
+
+}  // namespace pcdn

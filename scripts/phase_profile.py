@@ -11,7 +11,7 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 import paper_1306_4080_b200 as pk  # noqa: E402
 
-NAMES = ["A g/h/d+scatter", "sync1", "C1 touched set", "C2 dx fold", "C3 LS partials", "sync2+decide",
+NAMES = ["A g/h/d+scatter", "sync1", "C1 touched set", "C2 fold+LS loops", "C3 reduce+xbar", "decide",
          "commit", "sync3"]
 
 ap = argparse.ArgumentParser()

@@ -30,10 +30,10 @@ def pk():
     return pk
 
 
-def _solver(pk, prob, mode=0, ctas=0, heavy=0):
+def _solver(pk, prob, mode=0, ctas=0, heavy=0, res_cap=None):
     s = pk.Solver(prob)
-    if mode or ctas or heavy:
-        s.set_launch(mode, ctas, heavy)
+    if mode or ctas or heavy or res_cap:
+        s.set_launch(mode, ctas, heavy, res_cap)
     return s
 
 
@@ -105,7 +105,11 @@ TINY = [
 ]
 
 
-LAUNCH = [(0, 0, 0), (1, 1, 0), (1, 16, 0), (1, 4, 1), (2, 3, 2), (2, 0, 1), (2, 1, 0)]
+# (mode, CTAs, heavy column length[, records kept in shared memory per CTA]): mode 1 = one
+# cluster, state in HBM; 2 = cooperative grid; 3 = cluster-resident (state in distributed shared
+# memory; a tiny record capacity forces the HBM overflow path)
+LAUNCH = [(0, 0, 0), (1, 1, 0), (1, 16, 0), (1, 4, 1), (2, 3, 2), (2, 0, 1), (2, 1, 0),
+          (3, 0, 0), (3, 1, 0), (3, 16, 0), (3, 4, 1), (3, 2, 2, 3), (3, 16, 0, 1)]
 
 
 @pytest.mark.parametrize("loss", [LOSS_LOGISTIC, LOSS_L2SVM])
@@ -222,7 +226,7 @@ def test_solve_parity_configs_to_gap(pk, cfg, loss):
     s.close()
 
 
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode", [1, 2, 3])
 def test_determinism(pk, mode):
     prob = synth.config(2)
     s = _solver(pk, prob, mode)
@@ -237,7 +241,8 @@ def test_determinism(pk, mode):
     s.close()
 
 
-@pytest.mark.parametrize("launch", [(1, 1, 0), (1, 16, 3), (2, 2, 3), (2, 5, 1), (2, 0, 0)])
+@pytest.mark.parametrize("launch", [(1, 1, 0), (1, 16, 3), (2, 2, 3), (2, 5, 1), (2, 0, 0), (3, 16, 3),
+                                    (3, 4, 0, 2), (3, 1, 1), (3, 8, 0)])
 def test_solve_parity_launch_shapes(pk, launch):
     """Different CTA counts / forced heavy split: same results as the oracle."""
     prob = synth.tiny(777, 90, 40, density=0.3, loss=LOSS_LOGISTIC, c=4.0, dense_rows=3)
@@ -250,7 +255,7 @@ def test_solve_parity_launch_shapes(pk, launch):
 
 
 # ----------------------------------------------------------------------------- larger configs
-@pytest.mark.parametrize("cfg,mode", [(3, 1), (3, 2), (4, 1), (4, 2)])
+@pytest.mark.parametrize("cfg,mode", [(3, 1), (3, 2), (3, 3), (4, 1), (4, 2), (4, 3)])
 def test_step_parity_large_configs(pk, cfg, mode):
     """Configs 3 (Zipf text, heavy columns) and 4 (dense): sampled bundle steps at full size,
     in both launch modes."""
