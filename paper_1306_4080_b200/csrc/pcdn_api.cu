@@ -26,7 +26,7 @@ constexpr size_t ALIGN = 256;
 inline size_t align_up(size_t x) { return (x + ALIGN - 1) & ~(ALIGN - 1); }
 
 struct Layout {
-    size_t w, z, coef, cnt, bits, rec, dxg, tlist, order, flag, colinfo, hpos, hlist, hlen, hstart, tiles1, tiles2,
+    size_t w, z, coef, cnt, bits, rec, dxg, tlist, order, flag, fflag, fpos, flist, tiles3, colinfo, hpos, hlist, hlen, hstart, tiles1, tiles2,
         seen, dk, deltak, gk, hk, part, hpart, counters, info, F, Fcopy, status, err_idx, err_what, bar,
         objp, nheavy, prof, dbg_dx, dbg_mark, rec2, rslot, ovf_cnt, total;
 };
@@ -52,6 +52,10 @@ Layout make_layout(int64_t s, int64_t n, int64_t nnz)
     L.tlist = take(sizeof(int32_t) * nw * 32);
     L.order = take(sizeof(int32_t) * n);
     L.flag = take(sizeof(int32_t) * n);
+    L.fflag = take(sizeof(int32_t) * n);
+    L.fpos = take(sizeof(int64_t) * (n + 1));
+    L.flist = take(sizeof(int32_t) * n);
+    L.tiles3 = take(sizeof(int64_t) * ntile);
     L.colinfo = take(sizeof(int4) * n);
     L.hpos = take(sizeof(int64_t) * (n + 1));
     L.hlist = take(sizeof(int32_t) * n);
@@ -196,8 +200,17 @@ int build_heavy(pcdn_ctx *ctx, int64_t ntot)
                                                            ctx->at<int64_t>(L.hlen));
     ctx->launches++;
     CU(cudaGetLastError());
-    return scan<int64_t>(ctx, ctx->at<int64_t>(L.hlen), ntot, ctx->at<int64_t>(L.nheavy), ctx->at<int64_t>(L.hstart),
-                         ctx->at<int64_t>(L.tiles2), nullptr);
+    rc = scan<int64_t>(ctx, ctx->at<int64_t>(L.hlen), ntot, ctx->at<int64_t>(L.nheavy), ctx->at<int64_t>(L.hstart),
+                       ctx->at<int64_t>(L.tiles2), nullptr);
+    if (rc) return rc;
+    // full columns (a nonzero in every row): their d'x contribution is folded straight from CSC
+    rc = scan<int32_t>(ctx, ctx->at<int32_t>(L.fflag), ntot, nullptr, ctx->at<int64_t>(L.fpos),
+                       ctx->at<int64_t>(L.tiles3), nullptr);
+    if (rc) return rc;
+    k_full_compact<<<grid1d(ntot), 256, 0, ctx->stream>>>(ctx->at<int64_t>(L.fpos), ntot, ctx->at<int32_t>(L.flist));
+    ctx->launches++;
+    CU(cudaGetLastError());
+    return PCDN_OK;
 }
 
 int objective_kernels(pcdn_ctx *ctx)
@@ -282,6 +295,8 @@ int launch_steps(pcdn_ctx *ctx, int64_t ntot, int64_t P, int64_t nsteps, int64_t
     a.hpos = ctx->at<int64_t>(L.hpos);
     a.hlist = ctx->at<int32_t>(L.hlist);
     a.hstart = ctx->at<int64_t>(L.hstart);
+    a.fpos = ctx->at<int64_t>(L.fpos);
+    a.flist = ctx->at<int32_t>(L.flist);
     a.ntot = ntot;
     a.P = P;
     a.nsteps = nsteps;
@@ -708,8 +723,8 @@ int pcdn_objective(pcdn_ctx *ctx, int recompute_from_w, double *F_out)
 int pcdn_permutation(pcdn_ctx *ctx, uint64_t seed, int64_t k, int32_t *out)
 {
     if (!ctx || !out || k < 0) return PCDN_ERR_INVALID;
-    k_perm<<<grid1d(ctx->n), 256, 0, ctx->stream>>>(seed, k, ctx->n, ctx->col_ptr, ctx->heavy_len, out, nullptr,
-                                                     nullptr);
+    k_perm<<<grid1d(ctx->n), 256, 0, ctx->stream>>>(seed, k, ctx->n, ctx->s, ctx->col_ptr, ctx->heavy_len, out,
+                                                     nullptr, nullptr, nullptr);
     ctx->launches++;
     CU(cudaGetLastError());
     return PCDN_OK;
@@ -724,8 +739,9 @@ int pcdn_bundle_step(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, pcdn_step_
     int rc;
     if ((rc = reset_status(ctx))) return rc;
     CU(cudaMemsetAsync(ctx->at<int64_t>(L.counters), 0, sizeof(int64_t) * 8, ctx->stream));
-    k_bundle_prep<<<grid1d(P), 256, 0, ctx->stream>>>(bundle, P, ctx->n, ctx->col_ptr, ctx->heavy_len,
+    k_bundle_prep<<<grid1d(P), 256, 0, ctx->stream>>>(bundle, P, ctx->n, ctx->s, ctx->col_ptr, ctx->heavy_len,
                                                       ctx->at<int32_t>(L.order), ctx->at<int32_t>(L.flag),
+                                                      ctx->at<int32_t>(L.fflag),
                                                       ctx->at<uint32_t>(L.seen), ctx->at<int>(L.status),
                                                       ctx->at<long long>(L.err_idx),
                                                       (unsigned long long *)(ctx->at<int64_t>(L.counters) + 2),
@@ -802,8 +818,9 @@ int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_
     CU(cudaEventRecord(ctx->ev[2], ctx->stream));
     for (k = 0; k < max_outer; k++) {
         // a0: partition pi_k and the per-step heavy-column lists
-        k_perm<<<grid1d(ctx->n), 256, 0, ctx->stream>>>(seed, k, ctx->n, ctx->col_ptr, ctx->heavy_len,
+        k_perm<<<grid1d(ctx->n), 256, 0, ctx->stream>>>(seed, k, ctx->n, ctx->s, ctx->col_ptr, ctx->heavy_len,
                                                          ctx->at<int32_t>(L.order), ctx->at<int32_t>(L.flag),
+                                                         ctx->at<int32_t>(L.fflag),
                                                          ctx->at<int4>(L.colinfo));
         ctx->launches++;
         CU(cudaGetLastError());

@@ -34,6 +34,7 @@ constexpr int NHW = 4;             // warps that fold rows with > NREG records
 constexpr int HB = 1024;           // per-warp sort buffer for such rows
 constexpr int TSM = 4096;          // touched samples of a row block kept in shared memory
 constexpr int SCAN_TILE = 2048;    // items per CTA of the device-wide scans
+constexpr int FMAX = 256;          // full columns of a step staged in shared memory
 constexpr int SCAN_NT = 256;
 
 constexpr int LOSS_LOGISTIC = 0;
@@ -78,6 +79,8 @@ struct StepArgs {
     const int64_t *__restrict__ hpos;   // heavy positions before each position [ntot+1]
     const int32_t *__restrict__ hlist;  // heavy entry -> position
     const int64_t *__restrict__ hstart; // heavy entry -> global heavy-nnz offset [nheavy+1]
+    const int64_t *__restrict__ fpos;   // full columns before each position [ntot+1]
+    const int32_t *__restrict__ flist;  // full-column entry -> position
     int64_t ntot, P, nsteps;
     // per-step scratch
     double *dk, *deltak;  // [P] direction and Delta term per bundle position
@@ -336,9 +339,10 @@ __device__ __forceinline__ int64_t colinfo_p0(const int4 &ci)
     return (int64_t)(((uint64_t)(uint32_t)ci.w << 32) | (uint64_t)(uint32_t)ci.z);
 }
 
-// order[t] = pi_k(t); flag[t] = column length > heavy_len; colinfo[t] (nullable)
-__global__ void k_perm(uint64_t seed, int64_t k, int64_t n, const int64_t *__restrict__ col_ptr,
-                       int heavy_len, int32_t *order, int32_t *flag, int4 *colinfo)
+// order[t] = pi_k(t); flag[t] = column length > heavy_len; fflag[t] = column is full (holds a
+// nonzero in every row: its entry for row i sits at col_ptr[j] + i); colinfo[t] (nullable)
+__global__ void k_perm(uint64_t seed, int64_t k, int64_t n, int64_t s, const int64_t *__restrict__ col_ptr,
+                       int heavy_len, int32_t *order, int32_t *flag, int32_t *fflag, int4 *colinfo)
 {
     const FeistelKeys f = feistel_keys(seed, k, n);
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
@@ -347,15 +351,23 @@ __global__ void k_perm(uint64_t seed, int64_t k, int64_t n, const int64_t *__res
         if (flag) {
             const int64_t p0 = __ldg(&col_ptr[j]), len = __ldg(&col_ptr[j + 1]) - p0;
             flag[t] = len > heavy_len ? 1 : 0;
+            fflag[t] = len == s ? 1 : 0;
             if (colinfo) colinfo[t] = make_colinfo((int32_t)j, p0, len);
         }
     }
 }
 
+// full-column compaction: flist[e] = position of the e-th full column (fpos = exclusive scan)
+__global__ void k_full_compact(const int64_t *__restrict__ fpos, int64_t ntot, int32_t *flist)
+{
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntot; t += (int64_t)gridDim.x * blockDim.x)
+        if (fpos[t + 1] != fpos[t]) flist[fpos[t]] = (int32_t)t;
+}
+
 // user bundle: validate (distinct, in range) and copy
-__global__ void k_bundle_prep(const int32_t *__restrict__ bundle, int64_t P, int64_t n,
+__global__ void k_bundle_prep(const int32_t *__restrict__ bundle, int64_t P, int64_t n, int64_t s,
                               const int64_t *__restrict__ col_ptr, int heavy_len, int32_t *order,
-                              int32_t *flag, uint32_t *seen, int *status, long long *err_idx,
+                              int32_t *flag, int32_t *fflag, uint32_t *seen, int *status, long long *err_idx,
                               unsigned long long *bundle_nnz, int4 *colinfo)
 {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < P; t += (int64_t)gridDim.x * blockDim.x) {
@@ -365,6 +377,7 @@ __global__ void k_bundle_prep(const int32_t *__restrict__ bundle, int64_t P, int
             atomicMin(err_idx, (long long)t);
             order[t] = 0;
             flag[t] = 0;
+            fflag[t] = 0;
             colinfo[t] = make_colinfo(0, 0, 0);
             continue;
         }
@@ -377,6 +390,7 @@ __global__ void k_bundle_prep(const int32_t *__restrict__ bundle, int64_t P, int
         order[t] = j;
         const int64_t p0 = __ldg(&col_ptr[j]), len = __ldg(&col_ptr[j + 1]) - p0;
         flag[t] = len > heavy_len ? 1 : 0;
+        fflag[t] = len == s ? 1 : 0;
         colinfo[t] = make_colinfo(j, p0, len);
         atomicAdd(bundle_nnz, (unsigned long long)len);   // integer: order-independent
     }
@@ -527,6 +541,12 @@ struct StepSmem {
     // line-search decision broadcast
     int dec_q, dec_bad;
     double dec_alpha, dec_lhs, dec_rhs, dec_Delta, dec_nT;
+    // full columns of the step (d, col_ptr[j]), the first FMAX of them, and their d'x part for the
+    // rows of the block (dense pass, when the block has <= TSM rows)
+    double fd[FMAX];
+    int64_t fcp[FMAX];
+    double dxd[TSM];
+    int64_t row_base;
     // touched samples of the row block (when they fit)
     int32_t tl[TSM];
     // rows with > NREG records: per-warp sort buffers
@@ -762,11 +782,51 @@ struct WinState {
     double alpha, lhs, rhs, Delta, nT_tot;
 };
 
+// The step's full columns (a nonzero in every row, so x_ij sits at col_ptr[j] + i): their d'x_i
+// terms are read straight from CSC in bundle order instead of travelling as records (dense
+// workloads would otherwise send every sample one record per bundle column).
+struct DenseInfo {
+    int64_t f_lo, nf;   // entries [f_lo, f_lo + nf) of flist
+    bool any;           // some full column of the step has d_j != 0 (then every sample is in T)
+};
+
+__device__ __forceinline__ double dense_dx(const StepArgs &a, const double *fd, const int64_t *fcp, const DenseInfo &di,
+                                           int64_t k0, int64_t i)
+{
+    double dx = 0.0;
+    for (int64_t e = 0; e < di.nf; e++) {
+        double d;
+        int64_t cp;
+        if (e < FMAX) {
+            d = fd[e];
+            cp = fcp[e];
+        } else {
+            const int32_t kk = __ldg(&a.flist[di.f_lo + e]);
+            d = ldcg(&a.dk[kk - k0]);
+            cp = __ldg(&a.col_ptr[__ldg(&a.order[kk])]);
+        }
+        if (d != 0.0) dx += d * (double)__ldg(&a.val[cp + i]);
+    }
+    return dx;
+}
+
 template <int NQ>
 struct WinLayout {  // packed partial slots: Ls[0,NQ) L1[NQ,2NQ) Delta |T|
     static constexpr int W = 2 * NQ + 2 <= 8 ? 8 : (2 * NQ + 2 <= 16 ? 16 : 32);
     static constexpr int DELTA = 2 * NQ, NTOUCH = 2 * NQ + 1;
 };
+
+// the full columns' d'x part of sample i: from the dense pass (the block's rows are T when a
+// full column has d != 0, so T[li] = row_base + li) or computed here for big blocks
+__device__ __forceinline__ double dense_part(const StepArgs &a, const StepSmem &sm, const DenseInfo &di, int64_t k0,
+                                            int64_t i, int64_t nT)
+{
+    if (nT <= TSM) {
+        const int64_t li = i - sm.row_base;
+        return sm.dxd[li];
+    }
+    return dense_dx(a, sm.fd, sm.fcp, di, k0, i);
+}
 
 // One Armijo window over candidates q0 .. q0+NQ-1 (Eq.6 with Eq.12 from retained quantities):
 // per-sample loss changes over this CTA's touched samples (window 0 also folds d'x_i), the L1
@@ -775,7 +835,7 @@ struct WinLayout {  // packed partial slots: Ls[0,NQ) L1[NQ,2NQ) Delta |T|
 template <int NQ, class Sync>
 __device__ __forceinline__ void window(const StepArgs &a, StepSmem &sm, Sync &sy, WinState &ws, const int32_t *Tl,
                                       int64_t nT, int64_t k0, int64_t pb0, int64_t pb1, int G, int c, int tid,
-                                      int lane, int warp, const ShareReg &sh, RowReg &rr)
+                                      int lane, int warp, const ShareReg &sh, RowReg &rr, const DenseInfo &di)
 {
     using LY = WinLayout<NQ>;
     constexpr int W = LY::W;
@@ -799,7 +859,7 @@ __device__ __forceinline__ void window(const StepArgs &a, StepSmem &sm, Sync &sy
                 rr.has_dx = ni <= NREG;
             }
             if (ni <= NREG) {
-                const double dx = fold_small(a, off, ni);
+                const double dx = (di.any ? dense_part(a, sm, di, k0, i, nT) : 0.0) + fold_small(a, off, ni);
                 a.dxg[i] = dx;
                 if (li == tid) rr.dx = dx;
                 double al = alpha0;
@@ -829,8 +889,9 @@ __device__ __forceinline__ void window(const StepArgs &a, StepSmem &sm, Sync &sy
                     heavy &= heavy - 1;
                     const int32_t ih = __shfl_sync(0xffffffffu, i, src);
                     const int nih = __shfl_sync(0xffffffffu, ni, src);
-                    const double dx = fold_warp(a, __ldg(&a.row_ptr[ih]), nih, sm.sk[warp], sm.sv[warp], lane);
+                    const double dxr = fold_warp(a, __ldg(&a.row_ptr[ih]), nih, sm.sk[warp], sm.sv[warp], lane);
                     if (lane == 0) {
+                        const double dx = (di.any ? dense_part(a, sm, di, k0, ih, nT) : 0.0) + dxr;
                         a.dxg[ih] = dx;
                         const double zi = ldcg(&a.z[ih]);
                         const double cg = ldcg(&a.coef[ih]).x;
@@ -954,6 +1015,7 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
     const int64_t nwords = (a.s + 31) >> 5;
     const int64_t wb = (int64_t)c * nwords / G, we = (int64_t)(c + 1) * nwords / G;
     const int64_t row_base = wb * 32;
+    if (tid == 0) sm.row_base = row_base;
     int prev_q = 0;
     const int64_t pbs0 = (int64_t)c * a.P / G, pbs1 = (int64_t)(c + 1) * a.P / G;
 
@@ -1025,7 +1087,7 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
                     }
                     if (a.d_out) a.d_out[kk - k0] = r.d;
                 }
-                if (r.d != 0.0) {
+                if (r.d != 0.0 && p1 - p0 != a.s) {   // full columns are folded from CSC (dense_dx)
                     if (pre) {
 #pragma unroll
                         for (int m = 0; m < PF; m++)
@@ -1128,7 +1190,7 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
                     if (st >= b_w) break;
                     if (!(st >= lo_c && en <= hi_c)) continue;
                     const double d = sm.hd[le];
-                    if (d == 0.0) continue;
+                    if (d == 0.0 || en - st == a.s) continue;   // full columns: dense_dx
                     const int64_t s0 = max(a_w, st), s1 = min(b_w, en);
                     const int32_t kk = __ldg(&a.hlist[rb + le]);
                     const int32_t j = __ldg(&a.order[kk]);
@@ -1175,7 +1237,7 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
                 const double d = sm.cross_d[sl];
                 if (d == 0.0) continue;
                 const int64_t st = __ldg(&a.hstart[e]) - hb0, en = __ldg(&a.hstart[e + 1]) - hb0;
-                if (en <= a_w || st >= b_w) continue;
+                if (en <= a_w || st >= b_w || en - st == a.s) continue;
                 const int64_t s0 = max(a_w, st), s1 = min(b_w, en);
                 const int32_t kk = __ldg(&a.hlist[e]);
                 const int32_t j = __ldg(&a.order[kk]);
@@ -1201,10 +1263,39 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
         RowReg rr;
         rr.i = -1;
 
+        // ---------------- the step's full columns (dense_dx) -----------------------------
+        DenseInfo di;
+        di.f_lo = __ldg(&a.fpos[k0]);
+        di.nf = __ldg(&a.fpos[k1]) - di.f_lo;
+        di.any = false;
+        if (di.nf > 0) {
+            int any = 0;
+            for (int64_t e = tid; e < di.nf; e += NT) {
+                const int32_t kk = __ldg(&a.flist[di.f_lo + e]);
+                const double d = ldcg(&a.dk[kk - k0]);
+                if (e < FMAX) {
+                    sm.fd[e] = d;
+                    sm.fcp[e] = __ldg(&a.col_ptr[__ldg(&a.order[kk])]);
+                }
+                any |= d != 0.0;
+            }
+            di.any = __syncthreads_or(any) != 0;
+        }
+
         // ---------------- phase C1: touched set of this CTA's row block ------------------
         // each thread owns a contiguous run of bitmap words; a ballot-based warp scan plus
-        // warp totals gives every touched sample its slot in T (ascending sample order)
-        {
+        // warp totals gives every touched sample its slot in T (ascending sample order).  A full
+        // column with d_j != 0 touches every sample (reading Z8): T = the whole block.
+        if (di.any) {
+            const int64_t nrows = min(a.s, we * 32) - row_base;
+            int32_t *Tw = nrows <= TSM ? sm.tl : a.tlist + row_base;
+            for (int64_t li = tid; li < nrows; li += NT) Tw[li] = (int32_t)(row_base + li);
+            if (tid == 0) {
+                sm.nT = nrows > 0 ? nrows : 0;
+                sm.has_heavy_rows = 0;
+            }
+            __syncthreads();
+        } else {
             const int64_t nwc = we - wb;
             const int64_t wpt = (nwc + NT - 1) / NT;
             const int64_t w0 = wb + (int64_t)tid * wpt, w1 = min(we, w0 + wpt);
@@ -1259,6 +1350,49 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
         }
         const int64_t nT = sm.nT;
         const int32_t *Tl = nT <= TSM ? sm.tl : a.tlist + row_base;
+        if (di.any && nT <= TSM) {
+            // dense pass: the full columns' d'x part of every row of the block, split over all
+            // threads as (row, column chunk) so the loads of a column are coalesced over rows;
+            // chunk partials are added in chunk order (a fixed order)
+            const int R = (int)nT;
+            const int C = R >= NT ? 1 : (int)min((int64_t)(NT / max(R, 1)), di.nf);
+            double *dpart = &sm.red[0][0];   // NW*32 = NT doubles
+            for (int r0 = 0; r0 < R; r0 += NT) {
+                const int t = tid;
+                if (C == 1) {
+                    if (r0 + t < R) sm.dxd[r0 + t] = dense_dx(a, sm.fd, sm.fcp, di, k0, row_base + r0 + t);
+                } else if (t < R * C) {
+                    const int r = t % R, ch = t / R;
+                    const int64_t e0 = (int64_t)ch * di.nf / C, e1 = (int64_t)(ch + 1) * di.nf / C;
+                    const int64_t i = row_base + r;
+                    double part = 0.0;
+#pragma unroll 4
+                    for (int64_t e = e0; e < e1; e++) {
+                        double d;
+                        int64_t cp;
+                        if (e < FMAX) {
+                            d = sm.fd[e];
+                            cp = sm.fcp[e];
+                        } else {
+                            const int32_t kk = __ldg(&a.flist[di.f_lo + e]);
+                            d = ldcg(&a.dk[kk - k0]);
+                            cp = __ldg(&a.col_ptr[__ldg(&a.order[kk])]);
+                        }
+                        if (d != 0.0) part += d * (double)__ldg(&a.val[cp + i]);
+                    }
+                    dpart[t] = part;
+                }
+            }
+            if (C > 1) {
+                __syncthreads();
+                for (int r = tid; r < R; r += NT) {
+                    double x = 0.0;
+                    for (int ch = 0; ch < C; ch++) x += dpart[ch * R + r];
+                    sm.dxd[r] = x;
+                }
+            }
+            __syncthreads();
+        }
         PROF_MARK(2);
 
         // ---------------- phase C2+C3: fold d'x_i (a3) and the Armijo windows (a4) ----------
@@ -1269,8 +1403,8 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
         ws.bad = 0;
         ws.win = 0;
         while (true) {
-            if (ws.nq <= 2) window<2>(a, sm, sy, ws, Tl, nT, k0, pb0, pb1, G, c, tid, lane, warp, sh, rr);
-            else window<QW>(a, sm, sy, ws, Tl, nT, k0, pb0, pb1, G, c, tid, lane, warp, sh, rr);
+            if (ws.nq <= 2) window<2>(a, sm, sy, ws, Tl, nT, k0, pb0, pb1, G, c, tid, lane, warp, sh, rr, di);
+            else window<QW>(a, sm, sy, ws, Tl, nT, k0, pb0, pb1, G, c, tid, lane, warp, sh, rr, di);
             PROF_MARK(5);
             if (ws.qacc >= 0 || ws.bad) break;
             ws.q0 += ws.nq;

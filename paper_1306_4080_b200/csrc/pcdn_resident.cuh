@@ -65,6 +65,8 @@ struct ResFixed {
     int64_t cross_e[2];
     double cross_d[2];
     double red[NW][32];
+    double fd[FMAX];             // the step's full columns: d_j and col_ptr[j] (dense_dx)
+    int64_t fcp[FMAX];
     __align__(16) double part_in[2][16][R_WMAX];   // partial rows from every CTA, by window parity
     // the CTA's own bundle positions kk = k0 + c*NW + warp + m*G*NW, m < R_CPW: the column
     // results of phase A kept for the line search's L1 term and the w commit (slot m*NW + warp)
@@ -124,6 +126,7 @@ struct ResCtx {
     int lg, G, c, Bs, Bsc, cap, capP, per;
     int64_t my_ovf;
     double alpha_prev;   // the accepted step of the previous bundle step (0: none / null step)
+    bool dense_prev;     // the previous step touched every sample (a full column with d != 0)
 };
 
 // ---------------------------------------------------------------------------------------
@@ -403,7 +406,7 @@ __device__ __forceinline__ void res_lazy_commit(const StepArgs &a, const ResCtx 
     for (int r = 0; r < R.per; r++) {
         const int li = tid + r * NT;
         if (li >= R.Bsc) break;
-        if (R.head[li] < 0) continue;
+        if (R.head[li] < 0 && !R.dense_prev) continue;
         const double2 zd = R.zd[li];
         const double zn = zd.x + R.alpha_prev * zd.y;
         R.zd[li] = make_double2(zn, 0.0);
@@ -424,7 +427,7 @@ __device__ __forceinline__ void res_lazy_commit(const StepArgs &a, const ResCtx 
 // takes the same decision.
 template <int NQ>
 __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, WinState &ws, int64_t k0, int64_t k1,
-                                          int tid, int lane, int warp, ResProf &pr, int wcount)
+                                          int tid, int lane, int warp, ResProf &pr, int wcount, const DenseInfo &di)
 {
     using LY = WinLayout<NQ>;
     constexpr int W = LY::W;
@@ -441,11 +444,15 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
             const int li = tid + r * NT;
             if (li >= R.Bsc) break;
             const int h = R.head[li];
-            if (h < 0) continue;
+            if (h < 0 && !di.any) continue;
             ntouch++;
-            RRec rc = res_rec(a, R, h);
+            // full columns first (bundle order), then the records (ascending k): a fixed order
+            const double dxd = di.any ? dense_dx(a, fx.fd, fx.fcp, di, k0, (int64_t)li * R.G + R.c) : 0.0;
             double dx;
-            if (rc.li < 0) {   // one record: the common case
+            RRec rc;
+            if (h < 0) {
+                dx = 0.0;
+            } else if ((rc = res_rec(a, R, h)).li < 0) {   // one record: the common case
                 dx = rc.v;
             } else {
                 // up to NREG records: gather, then add in ascending k (selection in registers)
@@ -468,6 +475,7 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
                 }
                 if (p >= 0) {   // long list: folded by a warp after the CTA reduction below
                     longmask |= 1u << r;
+                    R.zd[li].y = dxd;
                     R.lq[atomicAdd(&fx.nlong, 1)] = li;
                     continue;
                 }
@@ -486,6 +494,7 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
                     dx += bv;
                 }
             }
+            dx = dxd + dx;
             const double zi = R.zd[li].x;
             R.zd[li].y = dx;
             const double cg = R.coef[li].x;
@@ -501,7 +510,7 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
         for (int r = 0; r < R.per; r++) {
             const int li = tid + r * NT;
             if (li >= R.Bsc) break;
-            if (R.head[li] < 0) continue;
+            if (R.head[li] < 0 && !di.any) continue;
             ntouch++;
             const double2 zd = R.zd[li];
             const double cg = R.coef[li].x;
@@ -553,8 +562,8 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
         if (warp < NHW) {
             for (int e = warp; e < nl; e += NHW) {
                 const int li = R.lq[e];
-                const double dx = res_fold_long(a, R, R.head[li], lane, fx.sk[warp], fx.sv[warp]);
-                if (lane == 0) R.zd[li].y = dx;
+                const double dxr = res_fold_long(a, R, R.head[li], lane, fx.sk[warp], fx.sv[warp]);
+                if (lane == 0) R.zd[li].y = R.zd[li].y + dxr;   // dense part + records
             }
         }
         __syncthreads();
@@ -710,6 +719,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         R.Bsc = (int)((a.s - c + G - 1) / G);   // samples owned by this CTA
         R.per = (R.Bsc + NT - 1) / NT;          // owned samples per thread (interleaved)
         R.alpha_prev = 0.0;
+        R.dense_prev = false;
     }
     ResFixed &fx = *R.fx;
     RCHK(R.zd, 16, 7);
@@ -840,9 +850,10 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
                 const double wj = pre ? pf.wj : ldcg(&a.w[j]);
                 const Dir r = finish_feature(a, gs, hs, wj);
                 if (lane == 0) {
-                    if (m >= R_CPW || a.d_out) {
+                    if (m >= R_CPW || a.d_out || len == a.s) {
                         a.dk[kk - k0] = r.d;
                         a.deltak[kk - k0] = r.delta;
+                        if (len == a.s) fx.spilled = 1;   // read by other CTAs: fence before the counts
                     }
                     if (a.g_out) {
                         a.g_out[kk - k0] = r.g;
@@ -857,7 +868,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
                         fx.coldl[slot] = r.delta;
                     }
                 }
-                if (r.d != 0.0) {
+                if (r.d != 0.0 && len != a.s) {   // full columns are folded from CSC (dense_dx)
                     if (pre) {
 #pragma unroll
                         for (int mm = 0; mm < PF; mm++)
@@ -961,7 +972,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
                     if (st >= b_w) break;
                     if (!(st >= lo_c && en <= hi_c)) continue;
                     const double d = fx.hd[le];
-                    if (d == 0.0) continue;
+                    if (d == 0.0 || en - st == a.s) continue;   // full columns: dense_dx
                     const int64_t s0 = max(a_w, st), s1 = min(b_w, en);
                     const int32_t kk = __ldg(&a.hlist[rb + le]);
                     const int32_t j = __ldg(&a.order[kk]);
@@ -1007,7 +1018,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
                 const double d = fx.cross_d[sl];
                 if (d == 0.0) continue;
                 const int64_t st = __ldg(&a.hstart[e]) - hb0, en = __ldg(&a.hstart[e + 1]) - hb0;
-                if (en <= a_w || st >= b_w) continue;
+                if (en <= a_w || st >= b_w || en - st == a.s) continue;
                 const int64_t s0 = max(a_w, st), s1 = min(b_w, en);
                 const int32_t kk = __ldg(&a.hlist[e]);
                 const int32_t j = __ldg(&a.order[kk]);
@@ -1061,7 +1072,24 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
             a.ovf_cnt[c] = 0;
             __threadfence();   // the reset is visible before this CTA's partial row is sent
         }
-        __syncthreads();
+        // the step's full columns (dense_dx): staged, and whether they touch every sample
+        DenseInfo di;
+        di.f_lo = __ldg(&a.fpos[k0]);
+        di.nf = __ldg(&a.fpos[k1]) - di.f_lo;
+        di.any = false;
+        {
+            int any = 0;
+            for (int64_t e = tid; e < di.nf; e += NT) {
+                const int32_t kk = __ldg(&a.flist[di.f_lo + e]);
+                const double d = ldcg(&a.dk[kk - k0]);
+                if (e < FMAX) {
+                    fx.fd[e] = d;
+                    fx.fcp[e] = __ldg(&a.col_ptr[__ldg(&a.order[kk])]);
+                }
+                any |= d != 0.0;
+            }
+            di.any = __syncthreads_or(any) != 0;
+        }
         PROF_MARK(2);
 
         // ---------------- phase C2+C3: fold d'x_i (a3) and the Armijo windows (a4) ----------
@@ -1072,8 +1100,8 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         ws.bad = 0;
         ws.win = 0;
         while (true) {
-            if (ws.nq <= 2) res_window<2>(a, R, ws, k0, k1, tid, lane, warp, pr, wcount);
-            else res_window<QW>(a, R, ws, k0, k1, tid, lane, warp, pr, wcount);
+            if (ws.nq <= 2) res_window<2>(a, R, ws, k0, k1, tid, lane, warp, pr, wcount, di);
+            else res_window<QW>(a, R, ws, k0, k1, tid, lane, warp, pr, wcount, di);
             wcount++;
             if (ws.qacc >= 0 || ws.bad) break;
             ws.q0 += ws.nq;
@@ -1086,6 +1114,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         const double alpha_acc = qacc < 0 ? 0.0 : ws.alpha;
         prev_q = qacc < 0 ? QW : qacc;
         R.alpha_prev = alpha_acc;   // z/coef of the touched samples: committed lazily
+        R.dense_prev = di.any;
 
         // ---------------- commit (a5): w_B, F ---------------------------------------------
         if (qacc >= 0) {

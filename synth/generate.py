@@ -350,9 +350,9 @@ def from_dense(X, y, c=1.0, loss=LOSS_LOGISTIC, P=1, name="dense", seed=0, keep_
 def tiny(seed: int, s: int, n: int, density: float = 0.2, loss: int = LOSS_LOGISTIC,
          c: float = 1.0, P: int = 4, positive: bool = False, empty_cols: int = 0,
          dup_cols: int = 0, dense_rows: int = 0, planted: bool = True,
-         flip: float = 0.1, scale: float = 1.0) -> Problem:
+         flip: float = 0.1, scale: float = 1.0, full_cols: int = 0) -> Problem:
     """Random small problem with optional nasty structure (empty columns,
-    duplicated columns, fully dense rows)."""
+    duplicated columns, fully dense rows, full columns = a nonzero in every row)."""
     rng = np.random.default_rng(seed)
     mask = rng.random((s, n)) < density
     vals = rng.normal(size=(s, n)) * scale
@@ -367,6 +367,10 @@ def tiny(seed: int, s: int, n: int, density: float = 0.2, loss: int = LOSS_LOGIS
             X[:, b] = X[:, a]
     if empty_cols:
         X[:, rng.choice(n, size=min(empty_cols, n), replace=False)] = 0.0
+    if full_cols:
+        fc = rng.choice(n, size=min(full_cols, n), replace=False)
+        v = rng.normal(size=(s, fc.size)) * scale
+        X[:, fc] = np.where(v == 0.0, 1.0, v)
     X = X.astype(np.float32)
     if planted:
         wstar = rng.normal(size=n) * (rng.random(n) < 0.3)

@@ -102,6 +102,7 @@ TINY = [
     dict(seed=2, s=70, n=33, density=0.2, empty_cols=4, dup_cols=2),
     dict(seed=3, s=25, n=40, density=0.5, dense_rows=2),
     dict(seed=4, s=130, n=9, density=0.9),
+    dict(seed=5, s=150, n=30, density=0.1, full_cols=6, dense_rows=1),   # full columns: dense_dx
 ]
 
 
@@ -244,8 +245,9 @@ def test_determinism(pk, mode):
 @pytest.mark.parametrize("launch", [(1, 1, 0), (1, 16, 3), (2, 2, 3), (2, 5, 1), (2, 0, 0), (3, 16, 3),
                                     (3, 4, 0, 2), (3, 1, 1), (3, 8, 0)])
 def test_solve_parity_launch_shapes(pk, launch):
-    """Different CTA counts / forced heavy split: same results as the oracle."""
-    prob = synth.tiny(777, 90, 40, density=0.3, loss=LOSS_LOGISTIC, c=4.0, dense_rows=3)
+    """Different CTA counts / forced heavy split: same results as the oracle (two full columns
+    exercise the dense d'x path)."""
+    prob = synth.tiny(777, 90, 40, density=0.3, loss=LOSS_LOGISTIC, c=4.0, dense_rows=3, full_cols=2)
     s = _solver(pk, prob, *launch)
     o = oracle.Oracle(prob)
     gs = s.solve(6, seed=4, max_outer=6, trace=True)
