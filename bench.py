@@ -107,6 +107,21 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def aggregate_over_ranks(t_ms, totals, dist=None, device="cpu"):
+    """Whole-job numbers of a replicas-only run: the timed region of the job is the
+    slowest rank's (max over ranks), work counters add up over ranks.  Without a process group
+    (N=1) the inputs are returned as they are."""
+    import torch
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(t_ms), {k: float(v) for k, v in totals.items()}
+    tt = torch.tensor([float(t_ms)], dtype=torch.float64, device=device)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    keys = sorted(totals)
+    vv = torch.tensor([float(totals[k]) for k in keys], dtype=torch.float64, device=device)
+    dist.all_reduce(vv, op=dist.ReduceOp.SUM)
+    return float(tt.item()), {k: float(x) for k, x in zip(keys, vv.tolist())}
+
+
 def dist_setup():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -157,6 +172,10 @@ def main():
     ap.add_argument("--loss", type=int, default=None)
     ap.add_argument("--eps", type=float, default=1e-3)
     ap.add_argument("--P", type=int, default=None)
+    ap.add_argument("--outer", type=int, default=0,
+                    help="run exactly this many outer iterations per solve (no Eq.14 stop test; for configs "
+                         "without a committed F*)")
+    ap.add_argument("--mode", type=int, default=0, help="step-kernel launch mode (pcdn_set_launch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -166,10 +185,11 @@ def main():
     prob = synth.config(args.config, loss=args.loss)
     if args.P:
         prob.P = args.P
-    fstar = fstar_for(args.config, prob.loss)
+    fstar = fstar_for(args.config, prob.loss) if args.outer <= 0 else None
     lossname = "L1-logistic" if prob.loss == 0 else "L1-L2-loss-SVM"
+    stop = f"Eq.14 gap {args.eps:g}" if args.outer <= 0 else f"{args.outer} outer iterations"
     workload = (f"cfg{args.config}: {lossname} s={prob.s} x n={prob.n}, nnz={prob.nnz}, c={prob.c}, "
-                f"P={prob.P}, seed={prob.seed}, solve w0=0 -> Eq.14 gap {args.eps:g}")
+                f"P={prob.P}, seed={prob.seed}, solve w0=0 -> {stop}")
     config = {"workload": workload, "config_index": args.config, "s": prob.s, "n": prob.n, "nnz": prob.nnz,
               "P": prob.P, "c": prob.c, "loss": lossname, "eps": args.eps, "F_star": fstar,
               "l2": "flushed between timed solves (256 MiB write)", "parallelism": f"replicas x{ws}"}
@@ -177,6 +197,8 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
+        if fstar is None:
+            raise SystemExit("--impl reference needs the Eq.14 stop test (no --outer)")
         r = run_oracle(prob, fstar, args.eps, args.steps, args.warmup)
         line = {"metric": METRIC, "value": r["value"], "unit": "nnz/s", "n_gpus": args.gpus, "steps": r["solves"],
                 "warmup": args.warmup, "ms_per_step": r["ms_per_solve"], "higher_is_better": True,
@@ -200,13 +222,17 @@ def main():
     stream = torch.cuda.Stream(dev)
     with torch.cuda.stream(stream):
         solver = pk.Solver(prob, device=dev, stream=stream)
-    pk.pcdn_set_reference(solver.ctx, fstar)
+    if fstar is not None:
+        pk.pcdn_set_reference(solver.ctx, fstar)
+    if args.mode:
+        solver.set_launch(args.mode)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    eps_run, max_outer = (args.eps, 1000) if args.outer <= 0 else (0.0, args.outer)
 
     def one_solve():
         pk.pcdn_reset(solver.ctx)
-        st, inf = pk.pcdn_solve(solver.ctx, prob.P, args.eps, prob.seed, 1000)
-        if st != pk.PCDN_OK:
+        st, inf = pk.pcdn_solve(solver.ctx, prob.P, eps_run, prob.seed, max_outer)
+        if st != (pk.PCDN_OK if args.outer <= 0 else pk.PCDN_BUDGET):
             raise SystemExit(f"solve did not reach the gap: status {st}")
         return inf
 
@@ -237,19 +263,13 @@ def main():
     outer = infos[-1].outer_iters
     # step-kernel launches (one per outer iteration) for per-launch roofline numbers
     step_launches = sum(i.outer_iters for i in infos)
-    if ws > 1:
-        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
-        nn = torch.tensor([float(nnz)], dtype=torch.float64, device=dev)
-        dist.all_reduce(nn)
-        nnz_all = float(nn.item())
-    else:
-        nnz_all = float(nnz)
+    t_ms, tot = aggregate_over_ranks(t_ms, {"nnz": nnz, "steps": steps_b, "alg_bytes": alg_bytes},
+                                     dist if ws > 1 else None, dev)
+    nnz_all, steps_all, bytes_all = tot["nnz"], tot["steps"], tot["alg_bytes"]
 
     # end-to-end through the public one-call API with pinned host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and fstar is not None:
         pin = {}
         for name, dt in (("col_ptr", np.int64), ("row_idx", np.int32), ("val", np.float32),
                          ("row_ptr", np.int64), ("col_idx", np.int32), ("csr_val", np.float32), ("y", np.int8)):
@@ -280,7 +300,8 @@ def main():
             b.synchronize()
             e_ms += a.elapsed_time(b)
             e_nnz += inf.nnz_processed
-        e2e = {"value": ws * e_nnz / (e_ms / 1e3), "unit": "nnz/s", "h2d_bytes_per_step": int(h2d),
+        e_ms, e_tot = aggregate_over_ranks(e_ms, {"nnz": e_nnz}, dist if ws > 1 else None, dev)
+        e2e = {"value": e_tot["nnz"] / (e_ms / 1e3), "unit": "nnz/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e_ms / max(1, min(args.steps, 3)),
                "api": "pcdn_train_host (pinned host buffers, includes create/validate/solve/copy-back)"}
 
@@ -300,7 +321,7 @@ def main():
             "frac_of_nominal_8TBs": achieved / NOMINAL_HBM_GBS}
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and fstar is not None:
         r = run_oracle(prob, fstar, args.eps, 1, 0, budget_s=10.0)
         cpu = {"value": r["value"], "unit": "nnz/s", "cores": r["cores"], "kind": "oracle",
                "sample": f"{r['solves']} full solves of the workload to gap {args.eps:g} "
@@ -313,9 +334,10 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded generator synth/, SURVEY.md 8(d) recipe)", "config": config,
                 "time_to_gap_s": t_ms / args.steps / 1e3, "outer_iters": outer,
-                "bundle_steps_per_s": ws * steps_b / (t_ms / 1e3),
-                "hbm_gbs_alg_whole_step": ws * alg_bytes / (t_ms / 1e3) / 1e9,
-                "frac_of_8TBs_whole_step": ws * alg_bytes / (t_ms / 1e3) / 1e9 / NOMINAL_HBM_GBS,
+                "bundle_steps_per_s": steps_all / (t_ms / 1e3),
+                "step_us": 1e3 * t_kernel / max(1, steps_b), "step_launch_mode": pk.pcdn_phase_cycles(solver.ctx)[1],
+                "hbm_gbs_alg_whole_step": bytes_all / (t_ms / 1e3) / 1e9,
+                "frac_of_8TBs_whole_step": bytes_all / (t_ms / 1e3) / 1e9 / NOMINAL_HBM_GBS,
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)

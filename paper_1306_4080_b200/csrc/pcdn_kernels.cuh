@@ -537,7 +537,7 @@ struct StepSmem {
     // CTA 0 bookkeeping (maintained F, step counters) and profile counters
     double F;
     long long cnt[4];
-    long long pacc[8];
+    long long pacc[16];
     // line-search decision broadcast
     int dec_q, dec_bad;
     double dec_alpha, dec_lhs, dec_rhs, dec_Delta, dec_nT;
@@ -554,12 +554,16 @@ struct StepSmem {
     double sv[NHW][HB];
 };
 
-// Warp-level gh over columns' nonzeros [p0, p1): lanes strided, fixed xor tree.
-__device__ __forceinline__ void col_gh(const StepArgs &a, int64_t p0, int64_t p1, int lane, double &gs, double &hs)
+// Warp-level gh over columns' nonzeros [p0, p1): lanes strided, fixed xor tree.  The loop is
+// unrolled so several independent gathers are in flight per lane (the per-lane summation order is
+// unchanged).  full_base >= 0: the column is full, its row index is p - full_base (no index load).
+__device__ __forceinline__ void col_gh(const StepArgs &a, int64_t p0, int64_t p1, int lane, double &gs, double &hs,
+                                       int64_t full_base = -1)
 {
     double g = 0.0, h = 0.0;
+#pragma unroll 8
     for (int64_t p = p0 + lane; p < p1; p += 32) {
-        const int32_t i = __ldg(&a.row_idx[p]);
+        const int32_t i = full_base >= 0 ? (int32_t)(p - full_base) : __ldg(&a.row_idx[p]);
         const double x = (double)__ldg(&a.val[p]);
         const double2 cf = ldcg(&a.coef[i]);
         g += x * cf.x;
@@ -575,6 +579,31 @@ __device__ __forceinline__ void col_scatter(const StepArgs &a, int64_t p0, int64
         const int32_t i = __ldg(&a.row_idx[p]);
         emit(a, i, kpos, d * (double)__ldg(&a.val[p]));
     }
+}
+
+// First e in [lo, hi) with pred(e) true (pred monotone: false..false true..true), hi if none.
+// All 32 lanes probe evenly spaced candidates, so each round narrows the range 32-fold.
+template <class Pred>
+__device__ __forceinline__ int64_t warp_first(int64_t lo, int64_t hi, int lane, Pred pred)
+{
+    while (hi - lo > 32) {
+        const int64_t step = (hi - lo + 31) / 32;
+        const int64_t e = lo + (int64_t)lane * step;
+        const unsigned m = __ballot_sync(0xffffffffu, e < hi ? pred(e) : true);
+        if (m == 0) {               // false up to lo + 31*step
+            lo = lo + 31 * step + 1;
+            continue;
+        }
+        const int f = __ffs(m) - 1;
+        if (f == 0) return lo;      // pred(lo)
+        // false at lo + (f-1)*step, true at lo + f*step (or beyond hi)
+        const int64_t nhi = min(hi, lo + (int64_t)f * step);
+        lo = lo + (int64_t)(f - 1) * step + 1;
+        hi = nhi;
+    }
+    const int64_t e = lo + lane;
+    const unsigned m = __ballot_sync(0xffffffffu, e < hi ? pred(e) : true);
+    return m == 0 ? hi : min(hi, lo + (int64_t)(__ffs(m) - 1));
 }
 
 // index of the CTA whose heavy range [floor(c NH/G), floor((c+1) NH/G)) holds offset o
@@ -1021,7 +1050,7 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
 
     long long tprev = 0;
     const bool prof = a.prof != nullptr && c == 0 && tid == 0;
-    if (tid < 8) sm.pacc[tid] = 0;
+    if (tid < 16) sm.pacc[tid] = 0;
 #define PROF_MARK(i)                              \
     do {                                          \
         if (prof) {                               \
@@ -1100,29 +1129,28 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
             }
         }
 
+        PROF_MARK(8);
         // ---------------- phase A': heavy columns, nnz-balanced over all warps -----------
         const int64_t e_lo = __ldg(&a.hpos[k0]), e_hi = __ldg(&a.hpos[k1]);
         if (e_hi > e_lo) {
             const int64_t hb0 = __ldg(&a.hstart[e_lo]);
             const int64_t NH = __ldg(&a.hstart[e_hi]) - hb0;
             const int64_t lo_c = (int64_t)c * NH / G, hi_c = (int64_t)(c + 1) * NH / G;
-            if (tid == 0) {
-                // first entry ending after lo_c, first entry starting at or after hi_c
-                int64_t lo = e_lo, hi = e_hi;
-                while (lo < hi) {
-                    const int64_t mid = (lo + hi) >> 1;
-                    if (__ldg(&a.hstart[mid + 1]) - hb0 > lo_c) hi = mid; else lo = mid + 1;
+            if (warp == 0) {
+                // first entry ending after lo_c, first entry starting at or after hi_c: 32-ary
+                // warp searches (one dependent load round per 32x narrowing)
+                const int64_t ce0 = warp_first(e_lo, e_hi, lane,
+                                               [&](int64_t e) { return __ldg(&a.hstart[e + 1]) - hb0 > lo_c; });
+                int64_t ce1 = warp_first(ce0, e_hi, lane, [&](int64_t e) { return __ldg(&a.hstart[e]) - hb0 >= hi_c; });
+                if (!(hi_c > lo_c)) ce1 = ce0;
+                if (lane == 0) {
+                    sm.ce0 = ce0;
+                    sm.ce1 = ce1;
+                    sm.cross_e[0] = sm.cross_e[1] = -1;
                 }
-                sm.ce0 = lo;
-                hi = e_hi;
-                while (lo < hi) {
-                    const int64_t mid = (lo + hi) >> 1;
-                    if (__ldg(&a.hstart[mid]) - hb0 >= hi_c) hi = mid; else lo = mid + 1;
-                }
-                sm.ce1 = (hi_c > lo_c) ? lo : sm.ce0;
-                sm.cross_e[0] = sm.cross_e[1] = -1;
             }
             __syncthreads();
+            PROF_MARK(9);
             const int64_t ce0 = sm.ce0, ce1 = sm.ce1;
             const int64_t a_w = lo_c + (int64_t)warp * (hi_c - lo_c) / NW;
             const int64_t b_w = lo_c + (int64_t)(warp + 1) * (hi_c - lo_c) / NW;
@@ -1143,7 +1171,7 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
                     const int32_t j = __ldg(&a.order[kk]);
                     const int64_t cs = __ldg(&a.col_ptr[j]);
                     double gs, hs;
-                    col_gh(a, cs + (s0 - st), cs + (s1 - st), lane, gs, hs);
+                    col_gh(a, cs + (s0 - st), cs + (s1 - st), lane, gs, hs, en - st == a.s ? cs : -1);
                     if (lane == 0) {
                         sm.hg[le][warp] = gs;
                         sm.hh[le][warp] = hs;
@@ -1199,7 +1227,9 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
                 }
                 __syncthreads();
             }
+            PROF_MARK(10);
             sy.sync();
+            PROF_MARK(11);
             // finish the (at most two) columns crossing this CTA's boundaries
             if (tid < 2) {
                 const int64_t e = sm.cross_e[tid];
@@ -1366,7 +1396,7 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
                     const int64_t e0 = (int64_t)ch * di.nf / C, e1 = (int64_t)(ch + 1) * di.nf / C;
                     const int64_t i = row_base + r;
                     double part = 0.0;
-#pragma unroll 4
+#pragma unroll 16
                     for (int64_t e = e0; e < e1; e++) {
                         double d;
                         int64_t cp;
@@ -1482,7 +1512,7 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
         a.counters[4] += sm.cnt[3];
     }
     if (prof)
-        for (int i = 0; i < 8; i++) a.prof[i] += sm.pacc[i];
+        for (int i = 0; i < 16; i++) a.prof[i] += sm.pacc[i];
 #undef PROF_MARK
 }
 

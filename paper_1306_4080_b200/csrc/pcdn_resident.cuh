@@ -252,6 +252,7 @@ __device__ __forceinline__ void res_col_gh(const StepArgs &a, const ResCtx &R, i
                                            double &gs, double &hs)
 {
     double g = 0.0, h = 0.0;
+#pragma unroll 4
     for (int64_t p = p0 + lane; p < p1; p += 32) {
         const int32_t i = __ldg(&a.row_idx[p]);
         const double x = (double)__ldg(&a.val[p]);

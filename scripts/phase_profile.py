@@ -11,8 +11,8 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 import paper_1306_4080_b200 as pk  # noqa: E402
 
-NAMES = ["A g/h/d+scatter", "sync1", "C1 touched set", "C2 fold+LS loops", "C3 reduce+xbar", "decide",
-         "commit", "sync3"]
+NAMES = ["A rest", "sync1", "C1 touched set", "C2 fold+LS loops", "C3 reduce+xbar", "decide",
+         "commit", "sync3", "A light", "A' search", "A' rounds", "A' gridsync"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
@@ -39,7 +39,7 @@ for mode in [int(m) for m in args.modes.split(",")]:
         cyc, m = pk.pcdn_phase_cycles(s.ctx)
         pk.pcdn_set_profile(s.ctx, 0)
         steps = r["steps"]
-        us = cyc[:8] / steps / args.mhz
+        us = cyc[:len(NAMES)] / steps / args.mhz
         key = f"mode{m}_ctas{ctas}"
         res[key] = dict(step_us_kernel=r["t_step_kernel_ms"] * 1e3 / steps, phases_us=dict(zip(NAMES, us.round(3).tolist())),
                         steps=steps)
