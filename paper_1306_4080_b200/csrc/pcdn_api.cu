@@ -341,9 +341,12 @@ int launch_steps(pcdn_ctx *ctx, int64_t ntot, int64_t P, int64_t nsteps, int64_t
     // grid mode (all SMs, software barrier) for large steps
     int mode = ctx->mode_req;
     if (mode == 0) {
+        // cluster-resident when the samples fit the cluster's shared memory and the bundles are
+        // small; else the HBM-state kernel as one cluster only while each of its warps has few
+        // columns per step (they are processed one after another), otherwise over the whole grid
         const double est_nb = (double)ctx->nnz * (double)P / (double)ctx->n;
         if (ctx->res_G >= 2 && est_nb <= 65536.0) mode = 3;
-        else mode = (ctx->Gc >= 2 && est_nb <= 65536.0) ? 1 : 2;
+        else mode = (ctx->Gc >= 2 && est_nb <= 16384.0 && P <= 2 * NW * ctx->Gc) ? 1 : 2;
     }
     ctx->last_mode = mode;
     if (mode == 3) {

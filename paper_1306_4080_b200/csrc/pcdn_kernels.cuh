@@ -1231,32 +1231,36 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
             sy.sync();
             PROF_MARK(11);
             // finish the (at most two) columns crossing this CTA's boundaries
-            if (tid < 2) {
-                const int64_t e = sm.cross_e[tid];
-                sm.cross_d[tid] = 0.0;
+            if (warp < 2) {   // one warp per crossing column, lanes over the CTA partials
+                const int64_t e = sm.cross_e[warp];
+                if (lane == 0) sm.cross_d[warp] = 0.0;
                 if (e >= 0) {
                     const int64_t st = __ldg(&a.hstart[e]) - hb0, en = __ldg(&a.hstart[e + 1]) - hb0;
                     const int clo = cta_of(st, NH, G), chi = cta_of(en - 1, NH, G);
                     double gs = 0.0, hs = 0.0;
-                    for (int c2 = clo; c2 <= chi; c2++) {
+                    for (int c2 = clo + lane; c2 <= chi; c2 += 32) {
                         if ((int64_t)c2 * NH / G == (int64_t)(c2 + 1) * NH / G) continue;  // empty range
                         const HPart hp = ld_hpart(&a.hpart[(int64_t)c2 * 2 + (c2 == clo ? 1 : 0)]);
                         if (hp.e != e) atomicMax(a.status, 4);  // internal consistency check
                         gs += hp.g;
                         hs += hp.h;
                     }
-                    const int32_t kk = __ldg(&a.hlist[e]);
-                    const int32_t j = __ldg(&a.order[kk]);
-                    const Dir r = finish_feature(a, gs, hs, ldcg(&a.w[j]));
-                    sm.cross_d[tid] = r.d;
-                    if (c == clo) {
-                        a.dk[kk - k0] = r.d;
-                        a.deltak[kk - k0] = r.delta;
-                        if (a.g_out) {
-                            a.g_out[kk - k0] = r.g;
-                            a.h_out[kk - k0] = r.h;
+                    gs = warp_sum(gs);
+                    hs = warp_sum(hs);
+                    if (lane == 0) {
+                        const int32_t kk = __ldg(&a.hlist[e]);
+                        const int32_t j = __ldg(&a.order[kk]);
+                        const Dir r = finish_feature(a, gs, hs, ldcg(&a.w[j]));
+                        sm.cross_d[warp] = r.d;
+                        if (c == clo) {
+                            a.dk[kk - k0] = r.d;
+                            a.deltak[kk - k0] = r.delta;
+                            if (a.g_out) {
+                                a.g_out[kk - k0] = r.g;
+                                a.h_out[kk - k0] = r.h;
+                            }
+                            if (a.d_out) a.d_out[kk - k0] = r.d;
                         }
-                        if (a.d_out) a.d_out[kk - k0] = r.d;
                     }
                 }
             }
