@@ -19,7 +19,7 @@ from ._abi import (  # noqa: F401
 __all__ = [
     "pcdn_workspace_bytes", "pcdn_create", "pcdn_set_armijo", "pcdn_set_reference", "pcdn_bundle_step",
     "pcdn_last_touched", "pcdn_solve", "pcdn_objective", "pcdn_get_w", "pcdn_set_w", "pcdn_get_z",
-    "pcdn_reset", "pcdn_permutation", "pcdn_set_trace", "pcdn_set_debug", "pcdn_set_launch", "pcdn_set_resident_cap", "pcdn_set_profile", "pcdn_phase_cycles",
+    "pcdn_reset", "pcdn_permutation", "pcdn_set_trace", "pcdn_set_debug", "pcdn_set_launch", "pcdn_set_resident_cap", "pcdn_set_profile", "pcdn_phase_cycles", "pcdn_warp_timeline",
     "pcdn_last_error", "pcdn_destroy", "pcdn_train_host", "pcdn_version", "Solver", "PCDNError",
 ]
 
@@ -138,7 +138,8 @@ def pcdn_set_resident_cap(ctx, cap):
 
 
 def pcdn_set_profile(ctx, on):
-    return check(ctx, lib().pcdn_set_profile(ctx, 1 if on else 0))
+    """on: 0 off, 1 per-phase cycle counters, 2 also the per-warp timeline."""
+    return check(ctx, lib().pcdn_set_profile(ctx, int(on)))
 
 
 def pcdn_phase_cycles(ctx):
@@ -146,6 +147,12 @@ def pcdn_phase_cycles(ctx):
     mode = C.c_int32()
     check(ctx, lib().pcdn_phase_cycles(ctx, _ptr(out), C.byref(mode)))
     return out, mode.value
+
+
+def pcdn_warp_timeline(ctx):
+    out = np.zeros(16 * 16 * 16, dtype=np.int64)
+    check(ctx, lib().pcdn_warp_timeline(ctx, _ptr(out)))
+    return out.reshape(16, 16, 16)
 
 
 def pcdn_last_error(ctx) -> str:

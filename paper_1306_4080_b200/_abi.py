@@ -65,6 +65,7 @@ SIGNATURES = {
     "pcdn_set_resident_cap": (C.c_int, [P, C.c_int]),
     "pcdn_set_profile": (C.c_int, [P, C.c_int]),
     "pcdn_phase_cycles": (C.c_int, [P, P, C.POINTER(C.c_int32)]),
+    "pcdn_warp_timeline": (C.c_int, [P, P]),
     "pcdn_last_error": (C.c_char_p, [P]),
     "pcdn_destroy": (None, [P]),
     "pcdn_train_host": (C.c_int, [I64, I64, I64, P, P, P, P, P, P, P, C.c_double, C.c_int, I64, C.c_double,

@@ -26,9 +26,9 @@ constexpr size_t ALIGN = 256;
 inline size_t align_up(size_t x) { return (x + ALIGN - 1) & ~(ALIGN - 1); }
 
 struct Layout {
-    size_t w, z, coef, cnt, bits, rec, dxg, tlist, order, flag, fflag, fpos, flist, tiles3, colinfo, hpos, hlist, hlen, hstart, tiles1, tiles2,
+    size_t w, z, coef, cnt, bits, rec, dxg, tlist, order, hdesc, flag, fflag, fpos, flist, tiles3, colinfo, hpos, hlist, hlen, hstart, tiles1, tiles2,
         seen, dk, deltak, gk, hk, part, hpart, counters, info, F, Fcopy, status, err_idx, err_what, bar,
-        objp, nheavy, prof, dbg_dx, dbg_mark, rec2, rslot, ovf_cnt, total;
+        objp, nheavy, prof, tl, dbg_dx, dbg_mark, rec2, rslot, ovf_cnt, total;
 };
 
 Layout make_layout(int64_t s, int64_t n, int64_t nnz)
@@ -51,6 +51,7 @@ Layout make_layout(int64_t s, int64_t n, int64_t nnz)
     L.dxg = take(sizeof(double) * s);
     L.tlist = take(sizeof(int32_t) * nw * 32);
     L.order = take(sizeof(int32_t) * n);
+    L.hdesc = take(sizeof(int4) * n);
     L.flag = take(sizeof(int32_t) * n);
     L.fflag = take(sizeof(int32_t) * n);
     L.fpos = take(sizeof(int64_t) * (n + 1));
@@ -81,6 +82,7 @@ Layout make_layout(int64_t s, int64_t n, int64_t nnz)
     L.objp = take(sizeof(double) * 2 * OBJ_NB);
     L.nheavy = take(sizeof(int64_t));
     L.prof = take(sizeof(long long) * 16);
+    L.tl = take(sizeof(long long) * TL_STEPS * NW * TL_PTS);
     L.dbg_dx = take(sizeof(double) * s);
     L.dbg_mark = take(s);
     L.rec2 = take(sizeof(Rec) * nnz);
@@ -197,7 +199,7 @@ int build_heavy(pcdn_ctx *ctx, int64_t ntot)
     if (rc) return rc;
     k_heavy_compact<<<grid1d(ntot), 256, 0, ctx->stream>>>(ctx->at<int64_t>(L.hpos), ntot, ctx->at<int32_t>(L.order),
                                                            ctx->col_ptr, ctx->at<int32_t>(L.hlist),
-                                                           ctx->at<int64_t>(L.hlen));
+                                                           ctx->at<int64_t>(L.hlen), ctx->at<int4>(L.hdesc));
     ctx->launches++;
     CU(cudaGetLastError());
     rc = scan<int64_t>(ctx, ctx->at<int64_t>(L.hlen), ntot, ctx->at<int64_t>(L.nheavy), ctx->at<int64_t>(L.hstart),
@@ -294,6 +296,7 @@ int launch_steps(pcdn_ctx *ctx, int64_t ntot, int64_t P, int64_t nsteps, int64_t
     a.colinfo = ctx->at<int4>(L.colinfo);
     a.hpos = ctx->at<int64_t>(L.hpos);
     a.hlist = ctx->at<int32_t>(L.hlist);
+    a.hdesc = ctx->at<int4>(L.hdesc);
     a.hstart = ctx->at<int64_t>(L.hstart);
     a.fpos = ctx->at<int64_t>(L.fpos);
     a.flist = ctx->at<int32_t>(L.flist);
@@ -315,6 +318,7 @@ int launch_steps(pcdn_ctx *ctx, int64_t ntot, int64_t P, int64_t nsteps, int64_t
     a.info = ctx->at<double>(L.info);
     a.debug = ctx->debug;
     a.prof = ctx->profile ? ctx->at<long long>(L.prof) : nullptr;
+    a.tl = ctx->profile == 2 ? ctx->at<long long>(L.tl) : nullptr;
     a.dbg_dx = ctx->at<double>(L.dbg_dx);
     a.dbg_mark = ctx->at<uint8_t>(L.dbg_mark);
     a.bar = ctx->at<unsigned long long>(L.bar);
@@ -639,8 +643,18 @@ int pcdn_set_resident_cap(pcdn_ctx *ctx, int cap)
 int pcdn_set_profile(pcdn_ctx *ctx, int on)
 {
     if (!ctx) return PCDN_ERR_INVALID;
-    ctx->profile = on ? 1 : 0;
+    ctx->profile = on == 2 ? 2 : (on ? 1 : 0);
     CU(cudaMemsetAsync(ctx->at<long long>(ctx->L.prof), 0, sizeof(long long) * 16, ctx->stream));
+    CU(cudaMemsetAsync(ctx->at<long long>(ctx->L.tl), 0, sizeof(long long) * TL_STEPS * NW * TL_PTS, ctx->stream));
+    return PCDN_OK;
+}
+
+int pcdn_warp_timeline(pcdn_ctx *ctx, int64_t *out)
+{
+    if (!ctx || !out) return PCDN_ERR_INVALID;
+    CU(cudaMemcpyAsync(out, ctx->at<long long>(ctx->L.tl), sizeof(long long) * TL_STEPS * NW * TL_PTS,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
     return PCDN_OK;
 }
 

@@ -35,6 +35,8 @@ constexpr int HB = 1024;           // per-warp sort buffer for such rows
 constexpr int TSM = 4096;          // touched samples of a row block kept in shared memory
 constexpr int SCAN_TILE = 2048;    // items per CTA of the device-wide scans
 constexpr int FMAX = 256;          // full columns of a step staged in shared memory
+constexpr int TL_STEPS = 16;       // per-warp timeline (profiling mode 2): first steps of a launch
+constexpr int TL_PTS = 16;         //   and points per step
 constexpr int SCAN_NT = 256;
 
 constexpr int LOSS_LOGISTIC = 0;
@@ -78,6 +80,7 @@ struct StepArgs {
     const int4 *__restrict__ colinfo;   // packed (j, length, col_ptr[j]) per position
     const int64_t *__restrict__ hpos;   // heavy positions before each position [ntot+1]
     const int32_t *__restrict__ hlist;  // heavy entry -> position
+    const int4 *__restrict__ hdesc;     // heavy entry -> (position, j, col_ptr[j] lo, hi)
     const int64_t *__restrict__ hstart; // heavy entry -> global heavy-nnz offset [nheavy+1]
     const int64_t *__restrict__ fpos;   // full columns before each position [ntot+1]
     const int32_t *__restrict__ flist;  // full-column entry -> position
@@ -95,6 +98,7 @@ struct StepArgs {
     double *info;        // last step: q, alpha, Delta, lhs, rhs, F, nnz, nT
     int debug;
     long long *prof;     // nullable: per-phase clock64 cycles of CTA 0 (profiling mode)
+    long long *tl;       // nullable: per-warp timeline of CTA 0, [TL_STEPS][NW][TL_PTS] (profile 2)
     double *dbg_dx;
     uint8_t *dbg_mark;
     // cluster-resident variant (pcdn_resident.cuh): cluster of 2^res_lg CTAs, res_Bs samples
@@ -502,15 +506,18 @@ __global__ void k_scan_apply(const Tin *__restrict__ in, int64_t n, const int64_
 }
 
 // heavy compaction: for flagged positions, hlist[e] = position, hlen[e] = column length
+// hdesc[e] = packed (position, feature j, col_ptr[j]) of heavy entry e: one load in the kernels
 __global__ void k_heavy_compact(const int64_t *__restrict__ hpos, int64_t ntot, const int32_t *__restrict__ order,
-                                const int64_t *__restrict__ col_ptr, int32_t *hlist, int64_t *hlen)
+                                const int64_t *__restrict__ col_ptr, int32_t *hlist, int64_t *hlen, int4 *hdesc)
 {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntot; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t e = hpos[t];
         if (hpos[t + 1] != e) {
             const int32_t j = order[t];
+            const int64_t cs = __ldg(&col_ptr[j]);
             hlist[e] = (int32_t)t;
-            hlen[e] = __ldg(&col_ptr[j + 1]) - __ldg(&col_ptr[j]);
+            hlen[e] = __ldg(&col_ptr[j + 1]) - cs;
+            hdesc[e] = make_int4((int)t, j, (int)(uint32_t)(cs & 0xffffffffLL), (int)(cs >> 32));
         }
     }
 }
@@ -604,6 +611,34 @@ __device__ __forceinline__ int64_t warp_first(int64_t lo, int64_t hi, int lane, 
     const int64_t e = lo + lane;
     const unsigned m = __ballot_sync(0xffffffffu, e < hi ? pred(e) : true);
     return m == 0 ? hi : min(hi, lo + (int64_t)(__ffs(m) - 1));
+}
+
+// The heavy-column work of one CTA in one step: entries [e_lo, e_hi) of the step, heavy nonzero
+// offsets relative to hb0, NH in total, this CTA's range [lo_c, hi_c) and the entries [ce0, ce1)
+// overlapping it.  Static per launch, so it is computed a step ahead by an otherwise idle warp.
+struct HeavyPlan {
+    int64_t e_lo, e_hi, hb0, NH, ce0, ce1;
+};
+
+__device__ __forceinline__ void heavy_plan_warp(const StepArgs &a, int64_t k0, int64_t k1, int c, int G, int lane,
+                                                HeavyPlan *out)
+{
+    HeavyPlan hp;
+    hp.e_lo = __ldg(&a.hpos[k0]);
+    hp.e_hi = __ldg(&a.hpos[k1]);
+    hp.hb0 = 0;
+    hp.NH = 0;
+    hp.ce0 = hp.ce1 = hp.e_lo;
+    if (hp.e_hi > hp.e_lo) {
+        hp.hb0 = __ldg(&a.hstart[hp.e_lo]);
+        hp.NH = __ldg(&a.hstart[hp.e_hi]) - hp.hb0;
+        const int64_t lo_c = (int64_t)c * hp.NH / G, hi_c = (int64_t)(c + 1) * hp.NH / G;
+        const int64_t hb0 = hp.hb0;
+        hp.ce0 = warp_first(hp.e_lo, hp.e_hi, lane, [&](int64_t e) { return __ldg(&a.hstart[e + 1]) - hb0 > lo_c; });
+        hp.ce1 = warp_first(hp.ce0, hp.e_hi, lane, [&](int64_t e) { return __ldg(&a.hstart[e]) - hb0 >= hi_c; });
+        if (!(hi_c > lo_c)) hp.ce1 = hp.ce0;
+    }
+    if (lane == 0) *out = hp;
 }
 
 // index of the CTA whose heavy range [floor(c NH/G), floor((c+1) NH/G)) holds offset o
@@ -808,6 +843,7 @@ __device__ __forceinline__ double xreduce(double (&v)[W], int lane)
 
 struct WinState {
     int q0, nq, qacc, bad, win;
+    unsigned tmask;   // cluster-resident kernel: owned samples (bit r) touched in this step
     double alpha, lhs, rhs, Delta, nT_tot;
 };
 

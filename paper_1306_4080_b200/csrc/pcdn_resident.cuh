@@ -46,6 +46,7 @@ namespace cgx = cooperative_groups;
 constexpr int R_HB = 256;  // per-warp bitonic buffer for samples with many records in one step
 constexpr int R_CPW = 8;   // own bundle positions per warp whose column results stay in smem
 constexpr int R_WMAX = 16; // partial-row slots (WinLayout<QW>::W)
+constexpr int R_RP = 4;    // own light columns per warp staged a step ahead
 
 struct __align__(16) RRec {  // a record: sample (then: next record of the sample's list), k, value
     int32_t li;
@@ -64,17 +65,32 @@ struct ResFixed {
     int64_t ce0, ce1;
     int64_t cross_e[2];
     double cross_d[2];
+    HPart hpo[2];                // this CTA's partials of the columns crossing its range (DSMEM-read)
+    int64_t cross_st[2], cross_en[2], cross_cs[2];
+    int32_t cross_kk[2];
+    double cross_w[2];
+    int32_t hkk[NE_MAX], hj[NE_MAX];   // staged heavy-entry descriptors of a round
+    int64_t hcs[NE_MAX];
+    double hw[NE_MAX];
+    HeavyPlan plan[2];           // heavy-column plan of this and the next step
+    // the next step's first R_RP own light columns of every warp, staged while the CTA waits for
+    // the line-search exchange: descriptor, w_j and the first 32 (row, value) pairs
+    int4 stg_ci[NW][R_RP];
+    double stg_w[NW][R_RP];
+    int32_t stg_r[NW][R_RP][32];
+    float stg_x[NW][R_RP][32];
     double red[NW][32];
     double fd[FMAX];             // the step's full columns: d_j and col_ptr[j] (dense_dx)
     int64_t fcp[FMAX];
     __align__(16) double part_in[2][16][R_WMAX];   // partial rows from every CTA, by window parity
     // the CTA's own bundle positions kk = k0 + c*NW + warp + m*G*NW, m < R_CPW: the column
     // results of phase A kept for the line search's L1 term and the w commit (slot m*NW + warp)
-    int32_t colj[R_CPW * NW];
-    int32_t colf[R_CPW * NW];    // 1 = light column computed by the slot's warp, 0 = heavy (HBM)
-    double colw[R_CPW * NW];
-    double cold[R_CPW * NW];
-    double coldl[R_CPW * NW];
+    // (double-buffered by step parity: the next step's phase A may write while the commit reads)
+    int32_t colj[2][R_CPW * NW];
+    int32_t colf[2][R_CPW * NW]; // 1 = light column computed by the slot's warp, 0 = heavy (HBM)
+    double colw[2][R_CPW * NW];
+    double cold[2][R_CPW * NW];
+    double coldl[2][R_CPW * NW];
     unsigned long long scan_w[NW];
     int64_t ovf_base[16];        // HBM overflow base of every CTA of the cluster
     int64_t own_nnz;
@@ -87,7 +103,7 @@ struct ResFixed {
     double dec_alpha[2], dec_lhs[2], dec_rhs[2], dec_Delta[2], dec_nT[2];
     double F;
     long long cnt[4];
-    long long pacc[8];
+    long long pacc[16];
     int32_t sk[NHW][R_HB];
     double sv[NHW][R_HB];
 };
@@ -126,7 +142,8 @@ struct ResCtx {
     int lg, G, c, Bs, Bsc, cap, capP, per;
     int64_t my_ovf;
     double alpha_prev;   // the accepted step of the previous bundle step (0: none / null step)
-    bool dense_prev;     // the previous step touched every sample (a full column with d != 0)
+    int cb;              // column-slot buffer of the current step (step parity)
+    long long *tl;       // per-warp timeline slot of the current step (profiling mode 2), or null
 };
 
 // ---------------------------------------------------------------------------------------
@@ -386,6 +403,12 @@ __device__ double res_fold_long(const StepArgs &a, const ResCtx &R, int h, int l
     return dx;
 }
 
+// per-warp timeline point (profiling mode 2)
+#define RTL(R, pt)                                                    \
+    do {                                                              \
+        if ((R).tl && (threadIdx.x & 31) == 0) (R).tl[pt] = clock64(); \
+    } while (0)
+
 struct ResProf {   // profiling mode: CTA 0 thread 0 accumulates clock64 cycles per phase
     bool on;
     long long t;
@@ -400,25 +423,63 @@ struct ResProf {   // profiling mode: CTA 0 thread 0 accumulates clock64 cycles 
     }
 };
 
-// Commit the previous step to this CTA's own touched samples (lazily: every producer has
-// finished gathering them): z += alpha dx (Alg.4 l.5 with additive retained z), coef, dx = 0.
+// Commit the previous step to this CTA's own samples (lazily: every producer has finished
+// gathering them): z += alpha_prev dx (Alg.4 l.5 with additive retained z), coef, dx = 0.  A
+// sample the previous step did not touch has dx = 0 (a no-op, as is a touched one whose dx
+// cancelled to 0).  Used at the end of a launch; inside the step loop the commit is fused into
+// the first fold pass of the next step.
 __device__ __forceinline__ void res_lazy_commit(const StepArgs &a, const ResCtx &R, int tid)
 {
     for (int r = 0; r < R.per; r++) {
         const int li = tid + r * NT;
         if (li >= R.Bsc) break;
-        if (R.head[li] < 0 && !R.dense_prev) continue;
         const double2 zd = R.zd[li];
+        if (zd.y == 0.0) continue;
         const double zn = zd.x + R.alpha_prev * zd.y;
         R.zd[li] = make_double2(zn, 0.0);
         R.coef[li] = coef_of(a.loss, zn, R.y[li]);
-        R.head[li] = -1;
-        if (a.debug) {
-            const int64_t i = (int64_t)li * R.G + R.c;
-            a.dbg_dx[i] = zd.y;
-            a.dbg_mark[i] = 1;
-        }
     }
+}
+
+// Stage the first R_RP own light columns of the step [kb, ke) for this warp (its own slots only,
+// so no CTA-level synchronisation): all descriptor loads first, then all data loads, then stores.
+// w_j may be read early: the bundles of a launch are disjoint.
+__device__ __forceinline__ void res_stage_cols(const StepArgs &a, ResFixed &fx, int64_t kb, int64_t ke, int64_t gw,
+                                               int64_t GN, int warp, int lane)
+{
+    int4 ci[R_RP];
+#pragma unroll
+    for (int m = 0; m < R_RP; m++) {
+        const int64_t kk = kb + gw + (int64_t)m * GN;
+        ci[m] = kk < ke ? __ldg(&a.colinfo[kk]) : make_int4(0, -1, 0, 0);
+    }
+    int32_t r[R_RP];
+    float x[R_RP];
+    double w[R_RP];
+#pragma unroll
+    for (int m = 0; m < R_RP; m++) {
+        const int len = ci[m].y;
+        const bool light = len >= 0 && len <= a.heavy_len;
+        r[m] = 0;
+        x[m] = 0.f;
+        w[m] = 0.0;
+        if (light && lane < len) {
+            const int64_t p = colinfo_p0(ci[m]) + lane;
+            r[m] = __ldg(&a.row_idx[p]);
+            x[m] = __ldg(&a.val[p]);
+        }
+        if (light && lane == 0) w[m] = ldcg(&a.w[ci[m].x]);
+    }
+#pragma unroll
+    for (int m = 0; m < R_RP; m++) {
+        if (lane == 0) {
+            fx.stg_ci[warp][m] = ci[m];
+            fx.stg_w[warp][m] = w[m];
+        }
+        fx.stg_r[warp][m][lane] = r[m];
+        fx.stg_x[warp][m][lane] = x[m];
+    }
+    __syncwarp();
 }
 
 // One Armijo window over candidates q0 .. q0+NQ-1 (Eq.6 with Eq.12 from retained quantities):
@@ -428,7 +489,8 @@ __device__ __forceinline__ void res_lazy_commit(const StepArgs &a, const ResCtx 
 // takes the same decision.
 template <int NQ>
 __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, WinState &ws, int64_t k0, int64_t k1,
-                                          int tid, int lane, int warp, ResProf &pr, int wcount, const DenseInfo &di)
+                                          int tid, int lane, int warp, ResProf &pr, int wcount, const DenseInfo &di,
+                                          int64_t kn0, int64_t kn1)
 {
     using LY = WinLayout<NQ>;
     constexpr int W = LY::W;
@@ -441,11 +503,26 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
     int ntouch = 0;
     unsigned longmask = 0;   // owned samples (bit r) whose list is longer than NREG
     if (ws.win == 0) {
+        unsigned tm = 0;
         for (int r = 0; r < R.per; r++) {
             const int li = tid + r * NT;
             if (li >= R.Bsc) break;
+            // lazy commit of the previous step (fused): z += alpha_prev dx_prev, coef
+            double2 zd = R.zd[li];
+            double2 cf;
+            bool cf_new = false;
+            if (zd.y != 0.0) {
+                zd.x = zd.x + R.alpha_prev * zd.y;
+                cf = coef_of(a.loss, zd.x, R.y[li]);
+                R.coef[li] = cf;
+                cf_new = true;
+            }
             const int h = R.head[li];
-            if (h < 0 && !di.any) continue;
+            if (h < 0 && !di.any) {
+                if (zd.y != 0.0) R.zd[li] = make_double2(zd.x, 0.0);
+                continue;
+            }
+            tm |= 1u << r;
             ntouch++;
             // full columns first (bundle order), then the records (ascending k): a fixed order
             const double dxd = di.any ? dense_dx(a, fx.fd, fx.fcp, di, k0, (int64_t)li * R.G + R.c) : 0.0;
@@ -455,6 +532,7 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
                 dx = 0.0;
             } else if ((rc = res_rec(a, R, h)).li < 0) {   // one record: the common case
                 dx = rc.v;
+                R.head[li] = -1;
             } else {
                 // up to NREG records: gather, then add in ascending k (selection in registers)
                 int kk[NREG];
@@ -476,10 +554,11 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
                 }
                 if (p >= 0) {   // long list: folded by a warp after the CTA reduction below
                     longmask |= 1u << r;
-                    R.zd[li].y = dxd;
+                    R.zd[li] = make_double2(zd.x, dxd);
                     R.lq[atomicAdd(&fx.nlong, 1)] = li;
                     continue;
                 }
+                R.head[li] = -1;
                 dx = 0.0;
                 int last = -1;
                 for (int t = 0; t < ni; t++) {
@@ -496,22 +575,26 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
                 }
             }
             dx = dxd + dx;
-            const double zi = R.zd[li].x;
-            R.zd[li].y = dx;
-            const double cg = R.coef[li].x;
+            R.zd[li] = make_double2(zd.x, dx);
+            if (a.debug) {
+                const int64_t i = (int64_t)li * R.G + R.c;
+                a.dbg_dx[i] = dx;
+                a.dbg_mark[i] = 1;
+            }
+            const double cg = cf_new ? cf.x : R.coef[li].x;
             const int yi = R.y[li];
             double al = alpha0;
 #pragma unroll
             for (int q = 0; q < NQ; q++) {
-                acc[q] += loss_change(a.loss, zi, yi, cg, dx, al);
+                acc[q] += loss_change(a.loss, zd.x, yi, cg, dx, al);
                 al *= a.beta;
             }
         }
+        ws.tmask = tm;
     } else {
         for (int r = 0; r < R.per; r++) {
+            if (!((ws.tmask >> r) & 1u)) continue;
             const int li = tid + r * NT;
-            if (li >= R.Bsc) break;
-            if (R.head[li] < 0 && !di.any) continue;
             ntouch++;
             const double2 zd = R.zd[li];
             const double cg = R.coef[li].x;
@@ -530,10 +613,10 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
         const int64_t kk = k0 + (int64_t)R.c * NW + wq + (int64_t)m * R.G * NW;
         if (kk >= k1) break;
         double wj, d, dl;
-        if (m < R_CPW && fx.colf[s2]) {
-            wj = fx.colw[s2];
-            d = fx.cold[s2];
-            dl = fx.coldl[s2];
+        if (m < R_CPW && fx.colf[R.cb][s2]) {
+            wj = fx.colw[R.cb][s2];
+            d = fx.cold[R.cb][s2];
+            dl = fx.coldl[R.cb][s2];
         } else {
             wj = ldcg(&a.w[__ldg(&a.order[kk])]);
             d = ldcg(&a.dk[kk - k0]);
@@ -549,12 +632,14 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
     }
     acc[LY::NTOUCH] = (double)ntouch;
     pr.mark(fx, 3);
+    if (ws.win == 0) RTL(R, 8);
     constexpr int SPL = 32 / W;
     {
         const double tot = xreduce<W>(acc, lane);
         if ((lane % SPL) == 0) fx.red[warp][lane / SPL] = tot;
     }
     __syncthreads();
+    if (ws.win == 0) RTL(R, 9);
     if (ws.win == 0 && fx.nlong > 0) {
         // rare: samples with more than NREG records in this step.  Warps fold their lists, the
         // owning threads add their loss changes, and the per-warp rows get a second fixed-order
@@ -564,7 +649,15 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
             for (int e = warp; e < nl; e += NHW) {
                 const int li = R.lq[e];
                 const double dxr = res_fold_long(a, R, R.head[li], lane, fx.sk[warp], fx.sv[warp]);
-                if (lane == 0) R.zd[li].y = R.zd[li].y + dxr;   // dense part + records
+                if (lane == 0) {
+                    R.zd[li].y = R.zd[li].y + dxr;   // dense part + records
+                    R.head[li] = -1;
+                    if (a.debug) {
+                        const int64_t i = (int64_t)li * R.G + R.c;
+                        a.dbg_dx[i] = R.zd[li].y;
+                        a.dbg_mark[i] = 1;
+                    }
+                }
             }
         }
         __syncthreads();
@@ -611,7 +704,9 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
         }
         if (lane == 0) mbar_arrive_tx(mb2, (uint32_t)(8 * W * R.G));
     }
+    if (ws.win == 0) RTL(R, 10);
     mbar_wait(mb2, (uint32_t)((wcount >> 1) & 1));
+    if (ws.win == 0) RTL(R, 11);
     pr.mark(fx, 4);
     // warp 0: the G partial rows (local now), fixed-order tree, decision; broadcast in the CTA
     // (every CTA computes the identical decision)
@@ -664,36 +759,8 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
     ws.Delta = fx.dec_Delta[buf];
     ws.nT_tot = fx.dec_nT[buf];
     ws.win++;
+    if (ws.win == 0) RTL(R, 12);
     pr.mark(fx, 5);
-}
-
-// Prefetch state of a warp's first own column of the next step: the packed descriptor is loaded
-// a step ahead, the row indices / values / w_j are issued at the end of the step.
-struct ResPref {
-    int64_t kk;  // position, -1 = none
-    int64_t p0;
-    int32_t j, len;
-    double wj;
-    int32_t r[PF];
-    float x[PF];
-};
-
-__device__ __forceinline__ void res_issue_col(const StepArgs &a, ResPref &pf, int64_t kk, const int4 &ci, int lane)
-{
-    pf.kk = kk;
-    if (kk < 0) return;
-    pf.j = ci.x;
-    pf.len = ci.y;
-    pf.p0 = colinfo_p0(ci);
-    if (pf.len > a.heavy_len) return;
-    pf.wj = ldcg(&a.w[pf.j]);
-#pragma unroll
-    for (int m = 0; m < PF; m++) {
-        if (lane + 32 * m < pf.len) {
-            pf.r[m] = __ldg(&a.row_idx[pf.p0 + lane + 32 * m]);
-            pf.x[m] = __ldg(&a.val[pf.p0 + lane + 32 * m]);
-        }
-    }
 }
 
 __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
@@ -720,7 +787,8 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         R.Bsc = (int)((a.s - c + G - 1) / G);   // samples owned by this CTA
         R.per = (R.Bsc + NT - 1) / NT;          // owned samples per thread (interleaved)
         R.alpha_prev = 0.0;
-        R.dense_prev = false;
+        R.tl = nullptr;
+        R.cb = 0;
     }
     ResFixed &fx = *R.fx;
     RCHK(R.zd, 16, 7);
@@ -743,7 +811,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
     }
     own = warp_sum(own);
     if (lane == 0) fx.scan_w[warp] = (unsigned long long)own;
-    if (tid < 8) fx.pacc[tid] = 0;
+    if (tid < 16) fx.pacc[tid] = 0;
     if (tid < 16) {
         fx.sendcnt[tid] = 0;
         fx.recvcnt[tid] = 0;
@@ -774,6 +842,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         }
         if (lane < G) fx.ovf_base[lane] = incl - mine;
     }
+    if (warp == 1) heavy_plan_warp(a, 0, min(a.P, a.ntot), c, G, lane, &fx.plan[0]);
     __syncthreads();
     R.my_ovf = fx.ovf_base[c];
 
@@ -785,58 +854,46 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
     int prev_q = 0;
     int wcount = 0;            // windows so far in this launch (M2 phase parity)
     uint32_t ph = 0;           // bit 0: M0 parity, bit 1: M1 parity
-    ResPref pf;
-    {
-        const int64_t kk = gw < min(a.P, a.ntot) ? gw : -1;
-        const int4 ci = kk >= 0 ? __ldg(&a.colinfo[kk]) : make_int4(0, 0, 0, 0);
-        res_issue_col(a, pf, kk, ci, lane);
-    }
-    int64_t h_lo = __ldg(&a.hpos[0]), h_hi = __ldg(&a.hpos[min(a.P, a.ntot)]);
+    res_stage_cols(a, fx, 0, min(a.P, a.ntot), gw, GN, warp, lane);
     for (int64_t t = 0; t < a.nsteps; t++) {
         pr.start();
+        R.cb = (int)(t & 1);
+        R.tl = (a.tl && c == 0 && t < TL_STEPS) ? a.tl + (t * NW + warp) * TL_PTS : nullptr;
+        RTL(R, 0);
         const int64_t k0 = t * a.P;
         const int64_t k1 = min(k0 + a.P, a.ntot);
         const int64_t Pt = k1 - k0;
-        const int64_t kn = k1 + gw, kn1 = min(k1 + a.P, a.ntot);
-        const int4 ci_next = kn < kn1 ? __ldg(&a.colinfo[kn]) : make_int4(0, 0, 0, 0);
-        const int64_t hn_lo = __ldg(&a.hpos[k1]), hn_hi = __ldg(&a.hpos[kn1]);
+        const int64_t kn1 = min(k1 + a.P, a.ntot);
 
         // ---------------- phase A: light columns, one warp per column (a1, a2, a3) --------
         {
             int m = 0;
             for (int64_t kk = k0 + gw; kk < k1; kk += GN, m++) {
-                const bool pre = kk == pf.kk;
-                int32_t j, len;
-                int64_t p0;
-                if (pre) {
-                    j = pf.j;
-                    len = pf.len;
-                    p0 = pf.p0;
-                } else {
-                    const int4 ci = __ldg(&a.colinfo[kk]);
-                    j = ci.x;
-                    len = ci.y;
-                    p0 = colinfo_p0(ci);
-                }
+                const bool stg = m < R_RP;   // staged during the previous step (res_stage_cols)
+                const int4 ci = stg ? fx.stg_ci[warp][m] : __ldg(&a.colinfo[kk]);
+                const int32_t j = ci.x, len = ci.y;
+                const int64_t p0 = colinfo_p0(ci);
                 const int slot = m * NW + warp;
                 if (len > a.heavy_len) {
-                    if (lane == 0 && m < R_CPW) fx.colf[slot] = 0;
+                    if (lane == 0 && m < R_CPW) fx.colf[R.cb][slot] = 0;
                     continue;
                 }
                 const int64_t p1 = p0 + len;
                 double gs, hs;
-                if (pre) {
+                {
                     double g = 0.0, h = 0.0;
-#pragma unroll
-                    for (int mm = 0; mm < PF; mm++) {
-                        if (lane + 32 * mm < len) {
-                            const double x = (double)pf.x[mm];
-                            const double2 cf = res_coef(a, R, pf.r[mm]);
+                    int64_t pr0 = p0;
+                    if (stg) {
+                        if (lane < len) {
+                            const double x = (double)fx.stg_x[warp][m][lane];
+                            const double2 cf = res_coef(a, R, fx.stg_r[warp][m][lane]);
                             g += x * cf.x;
                             h += (x * x) * cf.y;
                         }
+                        pr0 = p0 + 32;
                     }
-                    for (int64_t p = p0 + lane + 32 * PF; p < p1; p += 32) {
+#pragma unroll 4
+                    for (int64_t p = pr0 + lane; p < p1; p += 32) {
                         const int32_t i = __ldg(&a.row_idx[p]);
                         const double x = (double)__ldg(&a.val[p]);
                         const double2 cf = res_coef(a, R, i);
@@ -845,10 +902,8 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
                     }
                     gs = warp_sum(g);
                     hs = warp_sum(h);
-                } else {
-                    res_col_gh(a, R, p0, p1, lane, gs, hs);
                 }
-                const double wj = pre ? pf.wj : ldcg(&a.w[j]);
+                const double wj = stg ? fx.stg_w[warp][m] : ldcg(&a.w[j]);
                 const Dir r = finish_feature(a, gs, hs, wj);
                 if (lane == 0) {
                     if (m >= R_CPW || a.d_out || len == a.s) {
@@ -862,22 +917,19 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
                     }
                     if (a.d_out) a.d_out[kk - k0] = r.d;
                     if (m < R_CPW) {
-                        fx.colf[slot] = 1;
-                        fx.colj[slot] = j;
-                        fx.colw[slot] = wj;
-                        fx.cold[slot] = r.d;
-                        fx.coldl[slot] = r.delta;
+                        fx.colf[R.cb][slot] = 1;
+                        fx.colj[R.cb][slot] = j;
+                        fx.colw[R.cb][slot] = wj;
+                        fx.cold[R.cb][slot] = r.d;
+                        fx.coldl[R.cb][slot] = r.delta;
                     }
                 }
                 if (r.d != 0.0 && len != a.s) {   // full columns are folded from CSC (dense_dx)
-                    if (pre) {
-#pragma unroll
-                        for (int mm = 0; mm < PF; mm++)
-                            if (32 * mm < len) {
-                                const bool ok = lane + 32 * mm < len;
-                                res_emit_warp(a, R, ok, pf.r[mm], (int32_t)(kk - k0), ok ? r.d * (double)pf.x[mm] : 0.0, lane);
-                            }
-                        res_col_scatter(a, R, p0 + 32 * PF, p1, lane, (int32_t)(kk - k0), r.d);
+                    if (stg) {
+                        const bool ok = lane < len;
+                        res_emit_warp(a, R, ok, fx.stg_r[warp][m][lane], (int32_t)(kk - k0),
+                                      ok ? r.d * (double)fx.stg_x[warp][m][lane] : 0.0, lane);
+                        res_col_scatter(a, R, p0 + 32, p1, lane, (int32_t)(kk - k0), r.d);
                     } else {
                         res_col_scatter(a, R, p0, p1, lane, (int32_t)(kk - k0), r.d);
                     }
@@ -885,34 +937,32 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
             }
         }
 
+        RTL(R, 1);
+        PROF_MARK(8);
         // ---------------- phase A': heavy columns, nnz-balanced over all warps -----------
-        const int64_t e_lo = h_lo, e_hi = h_hi;
+        const HeavyPlan hpl = fx.plan[t & 1];   // computed a step ahead (see the count exchange)
+        const int64_t e_lo = hpl.e_lo, e_hi = hpl.e_hi;
         if (e_hi > e_lo) {
-            const int64_t hb0 = __ldg(&a.hstart[e_lo]);
-            const int64_t NH = __ldg(&a.hstart[e_hi]) - hb0;
+            const int64_t hb0 = hpl.hb0, NH = hpl.NH;
             const int64_t lo_c = (int64_t)c * NH / G, hi_c = (int64_t)(c + 1) * NH / G;
-            if (tid == 0) {
-                int64_t lo = e_lo, hi = e_hi;
-                while (lo < hi) {
-                    const int64_t mid = (lo + hi) >> 1;
-                    if (__ldg(&a.hstart[mid + 1]) - hb0 > lo_c) hi = mid; else lo = mid + 1;
-                }
-                fx.ce0 = lo;
-                hi = e_hi;
-                while (lo < hi) {
-                    const int64_t mid = (lo + hi) >> 1;
-                    if (__ldg(&a.hstart[mid]) - hb0 >= hi_c) hi = mid; else lo = mid + 1;
-                }
-                fx.ce1 = (hi_c > lo_c) ? lo : fx.ce0;
-                fx.cross_e[0] = fx.cross_e[1] = -1;
-            }
-            __syncthreads();
-            const int64_t ce0 = fx.ce0, ce1 = fx.ce1;
+            if (tid == 0) fx.cross_e[0] = fx.cross_e[1] = -1;
+            PROF_MARK(9);
+            const int64_t ce0 = hpl.ce0, ce1 = hpl.ce1;
             const int64_t a_w = lo_c + (int64_t)warp * (hi_c - lo_c) / NW;
             const int64_t b_w = lo_c + (int64_t)(warp + 1) * (hi_c - lo_c) / NW;
             for (int64_t rb = ce0; rb < ce1; rb += NE_MAX) {
                 const int ne = (int)min((int64_t)NE_MAX, ce1 - rb);
-                for (int i = tid; i <= ne; i += NT) fx.hst[i] = __ldg(&a.hstart[rb + i]) - hb0;
+                // entry offsets and descriptors (position, j, col_ptr[j]) and w_j, one round trip
+                for (int i = tid; i <= ne; i += NT) {
+                    fx.hst[i] = __ldg(&a.hstart[rb + i]) - hb0;
+                    if (i < ne) {
+                        const int4 hd = __ldg(&a.hdesc[rb + i]);
+                        fx.hkk[i] = hd.x;
+                        fx.hj[i] = hd.y;
+                        fx.hcs[i] = colinfo_p0(hd);
+                        fx.hw[i] = ldcg(&a.w[hd.y]);
+                    }
+                }
                 for (int i = tid; i < ne * NW; i += NT) {
                     fx.hg[i / NW][i % NW] = 0.0;
                     fx.hh[i / NW][i % NW] = 0.0;
@@ -923,9 +973,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
                     if (en <= a_w) continue;
                     if (st >= b_w) break;
                     const int64_t s0 = max(a_w, st), s1 = min(b_w, en);
-                    const int32_t kk = __ldg(&a.hlist[rb + le]);
-                    const int32_t j = __ldg(&a.order[kk]);
-                    const int64_t cs = __ldg(&a.col_ptr[j]);
+                    const int64_t cs = fx.hcs[le];
                     double gs, hs;
                     res_col_gh(a, R, cs + (s0 - st), cs + (s1 - st), lane, gs, hs);
                     if (lane == 0) {
@@ -943,9 +991,8 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
                     const int64_t st = fx.hst[le], en = fx.hst[le + 1];
                     const int64_t e = rb + le;
                     if (st >= lo_c && en <= hi_c) {
-                        const int32_t kk = __ldg(&a.hlist[e]);
-                        const int32_t j = __ldg(&a.order[kk]);
-                        const Dir r = finish_feature(a, gs, hs, ldcg(&a.w[j]));
+                        const int32_t kk = fx.hkk[le];
+                        const Dir r = finish_feature(a, gs, hs, fx.hw[le]);
                         fx.hd[le] = r.d;
                         a.dk[kk - k0] = r.d;
                         a.deltak[kk - k0] = r.delta;
@@ -961,8 +1008,13 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
                         hp.g = gs;
                         hp.h = hs;
                         hp.pad = 0.0;
-                        a.hpart[(int64_t)c * 2 + slot] = hp;
+                        fx.hpo[slot] = hp;
                         fx.cross_e[slot] = e;
+                        fx.cross_st[slot] = st;
+                        fx.cross_en[slot] = en;
+                        fx.cross_kk[slot] = fx.hkk[le];
+                        fx.cross_cs[slot] = fx.hcs[le];
+                        fx.cross_w[slot] = fx.hw[le];
                         fx.hd[le] = 0.0;
                     }
                 }
@@ -975,24 +1027,27 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
                     const double d = fx.hd[le];
                     if (d == 0.0 || en - st == a.s) continue;   // full columns: dense_dx
                     const int64_t s0 = max(a_w, st), s1 = min(b_w, en);
-                    const int32_t kk = __ldg(&a.hlist[rb + le]);
-                    const int32_t j = __ldg(&a.order[kk]);
-                    const int64_t cs = __ldg(&a.col_ptr[j]);
-                    res_col_scatter(a, R, cs + (s0 - st), cs + (s1 - st), lane, kk - (int32_t)k0, d);
+                    const int64_t cs = fx.hcs[le];
+                    res_col_scatter(a, R, cs + (s0 - st), cs + (s1 - st), lane, fx.hkk[le] - (int32_t)k0, d);
                 }
                 __syncthreads();
             }
-            cluster_sync_all();
+            PROF_MARK(10);
+            // the crossing partials live in shared memory: a relaxed cluster barrier after a
+            // shared-memory-only release fence (no GPU-scope drain) makes them readable
+            fence_smem_release_cluster();
+            asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+            PROF_MARK(11);
             if (warp < 2) {   // one warp per crossing column, lanes over the CTA partials
                 const int64_t e = fx.cross_e[warp];
                 if (lane == 0) fx.cross_d[warp] = 0.0;
                 if (e >= 0) {
-                    const int64_t st = __ldg(&a.hstart[e]) - hb0, en = __ldg(&a.hstart[e + 1]) - hb0;
+                    const int64_t st = fx.cross_st[warp], en = fx.cross_en[warp];
                     const int clo = cta_of(st, NH, G), chi = cta_of(en - 1, NH, G);
                     double gs = 0.0, hs = 0.0;
                     for (int c2 = clo + lane; c2 <= chi; c2 += 32) {
                         if ((int64_t)c2 * NH / G == (int64_t)(c2 + 1) * NH / G) continue;  // empty range
-                        const HPart hp = ld_hpart(&a.hpart[(int64_t)c2 * 2 + (c2 == clo ? 1 : 0)]);
+                        const HPart hp = *remote(&fx.hpo[c2 == clo ? 1 : 0], c2);
                         if (hp.e != e) atomicMax(a.status, 4);  // internal consistency check
                         gs += hp.g;
                         hs += hp.h;
@@ -1000,9 +1055,8 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
                     gs = warp_sum(gs);
                     hs = warp_sum(hs);
                     if (lane == 0) {
-                        const int32_t kk = __ldg(&a.hlist[e]);
-                        const int32_t j = __ldg(&a.order[kk]);
-                        const Dir r = finish_feature(a, gs, hs, ldcg(&a.w[j]));
+                        const int32_t kk = fx.cross_kk[warp];
+                        const Dir r = finish_feature(a, gs, hs, fx.cross_w[warp]);
                         fx.cross_d[warp] = r.d;
                         if (c == clo) {
                             a.dk[kk - k0] = r.d;
@@ -1022,16 +1076,15 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
                 if (e < 0 || (sl == 1 && e == fx.cross_e[0])) continue;
                 const double d = fx.cross_d[sl];
                 if (d == 0.0) continue;
-                const int64_t st = __ldg(&a.hstart[e]) - hb0, en = __ldg(&a.hstart[e + 1]) - hb0;
+                const int64_t st = fx.cross_st[sl], en = fx.cross_en[sl];
                 if (en <= a_w || st >= b_w || en - st == a.s) continue;
                 const int64_t s0 = max(a_w, st), s1 = min(b_w, en);
-                const int32_t kk = __ldg(&a.hlist[e]);
-                const int32_t j = __ldg(&a.order[kk]);
-                const int64_t cs = __ldg(&a.col_ptr[j]);
-                res_col_scatter(a, R, cs + (s0 - st), cs + (s1 - st), lane, kk - (int32_t)k0, d);
+                const int64_t cs = fx.cross_cs[sl];
+                res_col_scatter(a, R, cs + (s0 - st), cs + (s1 - st), lane, fx.cross_kk[sl] - (int32_t)k0, d);
             }
         }
         // ---------------- record counts to every owner (st.async, M0) ----------------------
+        RTL(R, 2);
         __syncthreads();   // every warp's records are sent and the counters are final
         if (tid < G) {
             // HBM data other CTAs read in this step (overflow records, heavy-column results,
@@ -1041,13 +1094,21 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
             fx.sendcnt[tid] = 0;
         }
         if (tid == 0) mbar_arrive_tx(mb0, (uint32_t)(4 * G));
+        // while the counts travel: the next step's heavy plan (one warp) and every warp's next
+        // own light columns (descriptor, w_j, first 32 nonzeros) into shared memory
+        if (k1 < a.ntot) {
+            if (warp == NW - 1) heavy_plan_warp(a, k1, kn1, c, G, lane, &fx.plan[(t + 1) & 1]);
+            res_stage_cols(a, fx, k1, kn1, gw, GN, warp, lane);
+        }
         PROF_MARK(0);
+        RTL(R, 3);
         mbar_wait(mb0, ph & 1u);
+        RTL(R, 4);
         ph ^= 1u;
         PROF_MARK(1);
 
         // ---------------- phase C1: lazy commit of the previous step, link the records --------
-        res_lazy_commit(a, R, tid);
+        RTL(R, 5);
         int n_ovf;
         {
             const int ex = lane < G ? max(0, (int)fx.recvcnt[lane] - R.capP) : 0;
@@ -1059,6 +1120,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         __syncthreads();   // heads reset by the lazy commit
         if (tid == 0) fx.spilled = 0;
         mbar_wait(mb1, (ph >> 1) & 1u);
+        RTL(R, 6);
         ph ^= 2u;
         if (warp < G) {   // warp p links the records of producer region p
             const int np = min((int)fx.recvcnt[warp], R.capP);
@@ -1096,6 +1158,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
             di.any = __syncthreads_or(any) != 0;
         }
         PROF_MARK(2);
+        RTL(R, 7);
 
         // ---------------- phase C2+C3: fold d'x_i (a3) and the Armijo windows (a4) ----------
         WinState ws;
@@ -1105,8 +1168,8 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         ws.bad = 0;
         ws.win = 0;
         while (true) {
-            if (ws.nq <= 2) res_window<2>(a, R, ws, k0, k1, tid, lane, warp, pr, wcount, di);
-            else res_window<QW>(a, R, ws, k0, k1, tid, lane, warp, pr, wcount, di);
+            if (ws.nq <= 2) res_window<2>(a, R, ws, k0, k1, tid, lane, warp, pr, wcount, di, k1, kn1);
+            else res_window<QW>(a, R, ws, k0, k1, tid, lane, warp, pr, wcount, di, k1, kn1);
             wcount++;
             if (ws.qacc >= 0 || ws.bad) break;
             ws.q0 += ws.nq;
@@ -1119,7 +1182,6 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         const double alpha_acc = qacc < 0 ? 0.0 : ws.alpha;
         prev_q = qacc < 0 ? QW : qacc;
         R.alpha_prev = alpha_acc;   // z/coef of the touched samples: committed lazily
-        R.dense_prev = di.any;
 
         // ---------------- commit (a5): w_B, F ---------------------------------------------
         if (qacc >= 0) {
@@ -1127,8 +1189,8 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
                 const int m = s2 / NW, wq = s2 - m * NW;
                 const int64_t kk = k0 + (int64_t)c * NW + wq + (int64_t)m * GN;
                 if (kk >= k1) break;
-                if (m < R_CPW && fx.colf[s2]) {
-                    a.w[fx.colj[s2]] = fx.colw[s2] + alpha_acc * fx.cold[s2];
+                if (m < R_CPW && fx.colf[R.cb][s2]) {
+                    a.w[fx.colj[R.cb][s2]] = fx.colw[R.cb][s2] + alpha_acc * fx.cold[R.cb][s2];
                 } else {
                     const int32_t j = __ldg(&a.order[kk]);
                     a.w[j] = ldcg(&a.w[j]) + alpha_acc * ldcg(&a.dk[kk - k0]);
@@ -1143,15 +1205,17 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
             double F = fx.F;
             if (qacc >= 0) F = F + ws.lhs;
             fx.F = F;
-            *a.F = F;
-            if (bad) atomicMax(a.status, 3);
-            a.info[0] = (double)qacc;
-            a.info[1] = alpha_acc;
-            a.info[2] = ws.Delta;
-            a.info[3] = ws.lhs;
-            a.info[4] = ws.rhs;
-            a.info[5] = F;
-            a.info[7] = ws.nT_tot;
+            if (bad || t == a.nsteps - 1) {   // the maintained F and the last step's info
+                *a.F = F;
+                if (bad) atomicMax(a.status, 3);
+                a.info[0] = (double)qacc;
+                a.info[1] = alpha_acc;
+                a.info[2] = ws.Delta;
+                a.info[3] = ws.lhs;
+                a.info[4] = ws.rhs;
+                a.info[5] = F;
+                a.info[7] = ws.nT_tot;
+            }
             const int64_t gstep = a.trace_off + t;
             if (gstep < a.trace_cap) {
                 if (a.q_trace) a.q_trace[gstep] = qacc;
@@ -1162,13 +1226,8 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
             fx.cnt[2] += (int64_t)ws.nT_tot;
             fx.cnt[3] += Pt;
         }
-        // next step's first own column (w_j is safe to read: the bundles of a launch are disjoint;
-        // colf/colw of this step were read above by the same threads that rewrite them next)
-        res_issue_col(a, pf, kn < kn1 ? kn : -1, ci_next, lane);
-        h_lo = hn_lo;
-        h_hi = hn_hi;
-        __syncthreads();   // colf/colj/colw of this step are read before the next phase A writes
         PROF_MARK(6);
+        RTL(R, 13);
         if (bad) break;
     }
     // ---------------- epilogue: last lazy commit, owned per-sample state back to HBM -------
@@ -1186,7 +1245,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         a.counters[4] += fx.cnt[3];
     }
     if (prof)
-        for (int i = 0; i < 8; i++) a.prof[i] += fx.pacc[i];
+        for (int i = 0; i < 16; i++) a.prof[i] += fx.pacc[i];
 #undef PROF_MARK
     cluster_sync_all();   // no CTA exits while another may still read its shared memory
 }
