@@ -618,6 +618,7 @@ __device__ __forceinline__ int64_t warp_first(int64_t lo, int64_t hi, int lane, 
 // overlapping it.  Static per launch, so it is computed a step ahead by an otherwise idle warp.
 struct HeavyPlan {
     int64_t e_lo, e_hi, hb0, NH, ce0, ce1;
+    int64_t f_lo, nf;   // the step's full columns: entries [f_lo, f_lo + nf) of flist
 };
 
 __device__ __forceinline__ void heavy_plan_warp(const StepArgs &a, int64_t k0, int64_t k1, int c, int G, int lane,
@@ -626,6 +627,8 @@ __device__ __forceinline__ void heavy_plan_warp(const StepArgs &a, int64_t k0, i
     HeavyPlan hp;
     hp.e_lo = __ldg(&a.hpos[k0]);
     hp.e_hi = __ldg(&a.hpos[k1]);
+    hp.f_lo = __ldg(&a.fpos[k0]);
+    hp.nf = __ldg(&a.fpos[k1]) - hp.f_lo;
     hp.hb0 = 0;
     hp.NH = 0;
     hp.ce0 = hp.ce1 = hp.e_lo;

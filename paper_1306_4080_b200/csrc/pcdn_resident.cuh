@@ -704,6 +704,8 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
         }
         if (lane == 0) mbar_arrive_tx(mb2, (uint32_t)(8 * W * R.G));
     }
+    // while the partial rows travel: stage the next step's own light columns (window 0 only)
+    if (ws.win == 0 && kn0 < kn1) res_stage_cols(a, fx, kn0, kn1, (int64_t)R.c * NW + warp, (int64_t)R.G * NW, warp, lane);
     if (ws.win == 0) RTL(R, 10);
     mbar_wait(mb2, (uint32_t)((wcount >> 1) & 1));
     if (ws.win == 0) RTL(R, 11);
@@ -1096,10 +1098,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         if (tid == 0) mbar_arrive_tx(mb0, (uint32_t)(4 * G));
         // while the counts travel: the next step's heavy plan (one warp) and every warp's next
         // own light columns (descriptor, w_j, first 32 nonzeros) into shared memory
-        if (k1 < a.ntot) {
-            if (warp == NW - 1) heavy_plan_warp(a, k1, kn1, c, G, lane, &fx.plan[(t + 1) & 1]);
-            res_stage_cols(a, fx, k1, kn1, gw, GN, warp, lane);
-        }
+        if (k1 < a.ntot && warp == NW - 1) heavy_plan_warp(a, k1, kn1, c, G, lane, &fx.plan[(t + 1) & 1]);
         PROF_MARK(0);
         RTL(R, 3);
         mbar_wait(mb0, ph & 1u);
@@ -1141,8 +1140,8 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         }
         // the step's full columns (dense_dx): staged, and whether they touch every sample
         DenseInfo di;
-        di.f_lo = __ldg(&a.fpos[k0]);
-        di.nf = __ldg(&a.fpos[k1]) - di.f_lo;
+        di.f_lo = hpl.f_lo;   // from the plan computed a step ahead
+        di.nf = hpl.nf;
         di.any = false;
         {
             int any = 0;

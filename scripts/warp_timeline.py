@@ -42,3 +42,7 @@ print(f"{'point':22s} {'min':>8s} {'median':>8s} {'max':>8s}   (cycles since ste
 for p, name in enumerate(PTS):
     v = rel[:, :, p]
     print(f"{name:22s} {np.nanmean(np.nanmin(v, 1)):8.0f} {np.nanmean(np.nanmedian(v, 1)):8.0f} {np.nanmean(np.nanmax(v, 1)):8.0f}")
+d78 = np.nanmedian(rel[:, :, 8] - rel[:, :, 7], 0)
+d01 = np.nanmedian(rel[:, :, 1] - rel[:, :, 0], 0)
+print("per-warp median cycles, fold+LS pass (7->8):", " ".join(f"{v:.0f}" for v in d78))
+print("per-warp median cycles, light columns (0->1):", " ".join(f"{v:.0f}" for v in d01))
