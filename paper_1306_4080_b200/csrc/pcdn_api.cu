@@ -15,12 +15,14 @@
 #include "../../include/pcdn.h"
 #include "pcdn_kernels.cuh"
 #include "pcdn_resident.cuh"
+#include "pcdn_dense.cuh"
 
 using namespace pcdn;
 
 namespace {
 
 constexpr int GMAX = 1024;
+constexpr int DENSE_GMAX = 512;   // CTAs of the dense step kernel (<= 2 per SM on 148 SMs)
 constexpr size_t ALIGN = 256;
 
 inline size_t align_up(size_t x) { return (x + ALIGN - 1) & ~(ALIGN - 1); }
@@ -28,7 +30,7 @@ inline size_t align_up(size_t x) { return (x + ALIGN - 1) & ~(ALIGN - 1); }
 struct Layout {
     size_t w, z, coef, cnt, bits, rec, dxg, tlist, order, hdesc, flag, fflag, fpos, flist, tiles3, colinfo, hpos, hlist, hlen, hstart, tiles1, tiles2,
         seen, dk, deltak, gk, hk, part, hpart, counters, info, F, Fcopy, status, err_idx, err_what, bar,
-        objp, nheavy, prof, tl, dbg_dx, dbg_mark, rec2, rslot, ovf_cnt, total;
+        objp, nheavy, prof, tl, dbg_dx, dbg_mark, rec2, rslot, ovf_cnt, part_gh, total;
 };
 
 Layout make_layout(int64_t s, int64_t n, int64_t nnz)
@@ -88,6 +90,8 @@ Layout make_layout(int64_t s, int64_t n, int64_t nnz)
     L.rec2 = take(sizeof(Rec) * nnz);
     L.rslot = take(sizeof(uint32_t) * nnz);
     L.ovf_cnt = take(sizeof(int) * 16);
+    // dense kernel (only when every column is full): partial (g, h) per CTA per bundle column
+    L.part_gh = take(nnz == s * n ? sizeof(double) * 2 * (size_t)n * DENSE_GMAX : 0);
     L.total = off + ALIGN;  // slack for base alignment
     return L;
 }
@@ -124,7 +128,9 @@ struct pcdn_ctx {
     int G = 0;          // CTAs of the grid-mode step kernel (cooperative launch)
     int Gc = 0;         // CTAs of the cluster-mode step kernel (one cluster)
     int G_req = 0;
-    int mode_req = 0;   // 0 auto, 1 cluster, 2 grid, 3 cluster-resident
+    int mode_req = 0;   // 0 auto, 1 cluster, 2 grid, 3 cluster-resident, 4 dense
+    int Gd = 0;         // CTAs of the dense step kernel (0 = unavailable)
+    size_t dsmem = 0;
     int res_G = 0;      // CTAs of the cluster-resident kernel (power of two; 0 = unavailable)
     int res_lg = 0, res_Bs = 0, res_cap = 0, res_cap_req = 0;
     size_t res_smem = 0;
@@ -340,10 +346,12 @@ int launch_steps(pcdn_ctx *ctx, int64_t ntot, int64_t P, int64_t nsteps, int64_t
     a.rec2 = ctx->at<Rec>(L.rec2);
     a.rslot = ctx->at<uint32_t>(L.rslot);
     a.ovf_cnt = ctx->at<int>(L.ovf_cnt);
+    a.part_gh = ctx->at<double>(L.part_gh);
     CU(cudaMemsetAsync(a.bar, 0, sizeof(unsigned long long), ctx->stream));
     // cluster mode for steps small enough that 16 SMs keep up (hardware barrier, ~0.2 us);
     // grid mode (all SMs, software barrier) for large steps
     int mode = ctx->mode_req;
+    if (mode == 0 && ctx->Gd > 0) mode = 4;   // fully dense problem: row-block kernel
     if (mode == 0) {
         // cluster-resident when the samples fit the cluster's shared memory and the bundles are
         // small; else the HBM-state kernel as one cluster only while each of its warps has few
@@ -353,7 +361,12 @@ int launch_steps(pcdn_ctx *ctx, int64_t ntot, int64_t P, int64_t nsteps, int64_t
         else mode = (ctx->Gc >= 2 && est_nb <= 16384.0 && P <= 2 * NW * ctx->Gc) ? 1 : 2;
     }
     ctx->last_mode = mode;
-    if (mode == 3) {
+    if (mode == 4) {
+        if (ctx->Gd < 1) return set_err(ctx, PCDN_ERR_INVALID, "dense step kernel unavailable for this problem");
+        void *args[] = {&a};
+        CU(cudaLaunchCooperativeKernel((const void *)k_step_dense, dim3(ctx->Gd), dim3(NT), args, ctx->dsmem,
+                                       ctx->stream));
+    } else if (mode == 3) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(ctx->res_G);
         cfg.blockDim = dim3(NT);
@@ -477,6 +490,24 @@ int configure_launch(pcdn_ctx *ctx)
         }
         if (ctx->mode_req == 3 && ctx->res_G < 1)
             return set_err(ctx, PCDN_ERR_INVALID, "cluster-resident mode unavailable for s=%lld", (long long)ctx->s);
+    }
+    // dense row-block kernel: every column full, rows per CTA and bundle sizes within its smem
+    {
+        ctx->Gd = 0;
+        if (ctx->nnz == ctx->s * ctx->n) {
+            ctx->dsmem = sizeof(DenseSmem);
+            const void *kd = (const void *)k_step_dense;
+            CU(cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->dsmem));
+            int occd = 0;
+            CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occd, kd, NT, ctx->dsmem));
+            int gd = ctx->num_sms * occd;
+            if (ctx->mode_req == 4 && ctx->G_req > 0 && ctx->G_req < gd) gd = ctx->G_req;
+            if (gd > DENSE_GMAX) gd = DENSE_GMAX;
+            if (gd > GMAX) gd = GMAX;
+            if (gd >= 1 && (ctx->s + gd - 1) / gd <= D_RMAX) ctx->Gd = gd;
+        }
+        if (ctx->mode_req == 4 && ctx->Gd < 1)
+            return set_err(ctx, PCDN_ERR_INVALID, "dense mode needs every column full and <= %d rows per CTA", D_RMAX);
     }
     const bool want_cluster = ctx->mode_req == 1;
     ctx->G = (!want_cluster && ctx->G_req > 0 && ctx->G_req < maxg) ? ctx->G_req : maxg;
@@ -623,7 +654,7 @@ int pcdn_set_debug(pcdn_ctx *ctx, int on)
 int pcdn_set_launch(pcdn_ctx *ctx, int mode, int ctas, int heavy_len)
 {
     if (!ctx) return PCDN_ERR_INVALID;
-    if (mode < 0 || mode > 3 || ctas < 0 || heavy_len < 0 || (mode == 1 && ctas > 16) ||
+    if (mode < 0 || mode > 4 || ctas < 0 || heavy_len < 0 || (mode == 1 && ctas > 16) ||
         (mode == 3 && (ctas > 16 || (ctas & (ctas - 1)) != 0)))
         return set_err(ctx, PCDN_ERR_INVALID, "invalid launch knobs");
     ctx->mode_req = mode;

@@ -109,6 +109,7 @@ struct StepArgs {
     Rec *rec2;
     uint32_t *rslot;
     int *ovf_cnt;   // [16] overflow records received per CTA in the current step
+    double *part_gh;  // dense kernel: per-CTA partial (g, h) of every bundle column [G][P][2]
     // sync
     unsigned long long *bar;
     int *status;
@@ -149,11 +150,10 @@ __device__ __forceinline__ void grid_sync(unsigned long long *ctr, unsigned long
     target += gridDim.x;
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
+        __threadfence();          // release: the CTA's writes (ordered by the bar.sync above)
         atomicAdd(ctr, 1ULL);
-        while (ld_acquire(ctr) < target) {
+        while (ld_acquire(ctr) < target) {   // acquire: no trailing fence needed
         }
-        __threadfence();
     }
     __syncthreads();
 }
@@ -844,6 +844,29 @@ __device__ __forceinline__ double xreduce(double (&v)[W], int lane)
     return v[0];
 }
 
+// Totals of the G per-CTA partial rows part[c2][0..W) in a fixed order: warp w sums rows
+// c2 = w, w+NW, ... (lanes = slots), then warp 0 adds the NW warp sums in warp order.  red is a
+// [NW][32] shared scratch, tot the [32] shared result (valid after the __syncthreads inside).
+template <int W>
+__device__ __forceinline__ void grid_totals(const double *part, int G, double (*red)[32], double *tot, int lane,
+                                            int warp)
+{
+    double v = 0.0;
+    if (lane < W) {
+#pragma unroll 4
+        for (int c2 = warp; c2 < G; c2 += NW) v += ldcg(&part[(int64_t)c2 * NPART + lane]);
+    }
+    red[warp][lane] = v;
+    __syncthreads();
+    if (warp == 0 && lane < W) {
+        double t = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < NW; w2++) t += red[w2][lane];
+        tot[lane] = t;
+    }
+    __syncwarp();
+}
+
 struct WinState {
     int q0, nq, qacc, bad, win;
     unsigned tmask;   // cluster-resident kernel: owned samples (bit r) touched in this step
@@ -1019,18 +1042,9 @@ __device__ __forceinline__ void window(const StepArgs &a, StepSmem &sm, Sync &sy
         part[(int64_t)c * NPART + lane] = s;
     }
     sy.sync();
-    // every CTA reduces the G partials in the same fixed order (warp 0) and decides
+    // every CTA reduces the G partials in the same fixed order (all warps, then warp 0) and decides
+    grid_totals<W>(part, G, sm.red, sm.tot, lane, warp);
     if (warp == 0) {
-        double v[W];
-#pragma unroll
-        for (int q = 0; q < W; q++) v[q] = 0.0;
-        for (int c2 = lane; c2 < G; c2 += 32) {
-#pragma unroll
-            for (int q = 0; q < W; q++) v[q] += ldcg(&part[(int64_t)c2 * NPART + q]);
-        }
-        const double tot = xreduce<W>(v, lane);
-        if ((lane % SPL) == 0) sm.tot[lane / SPL] = tot;
-        __syncwarp();
         if (lane == 0) {
             const double Dl = sm.tot[LY::DELTA];
             int qa = -1, badl = 0;

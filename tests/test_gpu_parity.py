@@ -257,7 +257,7 @@ def test_solve_parity_launch_shapes(pk, launch):
 
 
 # ----------------------------------------------------------------------------- larger configs
-@pytest.mark.parametrize("cfg,mode", [(3, 1), (3, 2), (3, 3), (4, 1), (4, 2), (4, 3)])
+@pytest.mark.parametrize("cfg,mode", [(3, 1), (3, 2), (3, 3), (4, 1), (4, 2), (4, 3), (4, 4)])
 def test_step_parity_large_configs(pk, cfg, mode):
     """Configs 3 (Zipf text, heavy columns) and 4 (dense): sampled bundle steps at full size,
     in both launch modes."""
@@ -288,4 +288,30 @@ def test_solve_parity_config4_one_outer(pk):
     gs = s.solve(prob.P, seed=prob.seed, max_outer=1, trace=True)
     os_ = o.solve(prob.P, seed=prob.seed, max_outer=1)
     _compare_solve(gs, os_, s.w().cpu().numpy(), "cfg4")
+    s.close()
+
+
+# ----------------------------------------------------------------------------- dense row-block kernel
+@pytest.mark.parametrize("loss", [LOSS_LOGISTIC, LOSS_L2SVM])
+@pytest.mark.parametrize("ctas", [0, 1, 3, 7])
+def test_dense_kernel_tiny(pk, loss, ctas):
+    """Fully dense problems (every column full) through the row-block kernel (mode 4): one step
+    from injected states and short solves, against the oracle; CTA counts that leave some CTAs
+    without rows and bundles larger than a CTA's row block."""
+    prob = synth.tiny(31, 150, 30, density=1.0, loss=loss, c=2.0, P=5)
+    assert prob.nnz == prob.s * prob.n
+    rng = np.random.default_rng(31)
+    s = _solver(pk, prob, 4, ctas)
+    o = oracle.Oracle(prob)
+    ties = []
+    for rep in range(3):
+        w = _random_state(rng, prob.n, scale=0.5 * rep)
+        for B in _step_cases(prob, rng, sizes=[1, 5, 17, 30]):
+            s.set_w(w)
+            _compare_step(s.step(B), o.step(w, B), ties)
+    assert len(ties) <= 2, ties
+    s.reset()
+    gs = s.solve(7, seed=3, max_outer=5, trace=True)
+    os_ = o.solve(7, seed=3, max_outer=5)
+    _compare_solve(gs, os_, s.w().cpu().numpy(), f"dense ctas={ctas}")
     s.close()
