@@ -30,6 +30,7 @@ constexpr int NPART = 32;          // per-CTA partial slots (packed: Ls[nq], L1[
 constexpr int WREG = 4;            // bitmap words per thread kept in registers in phase C1
 constexpr int NE_MAX = 64;         // heavy entries handled per round inside one CTA
 constexpr int NREG = 8;            // rows with <= NREG records are folded by one thread
+constexpr int SHORT = 8;           // columns with <= SHORT nonzeros are reduced by one thread
 constexpr int NHW = 4;             // warps that fold rows with > NREG records
 constexpr int HB = 1024;           // per-warp sort buffer for such rows
 constexpr int TSM = 4096;          // touched samples of a row block kept in shared memory
@@ -766,39 +767,6 @@ __device__ double fold_warp(const StepArgs &a, int64_t off, int ni, int32_t *sk,
 // ------------------------------------------------------------------------------------
 constexpr int PF = 4;  // nonzeros per lane of a light column prefetched into registers
 
-// Immutable data of a warp's first light column of the NEXT step (order, col_ptr, row_idx,
-// val) plus w_j, loaded while the current step finishes: after the end-of-step barrier only
-// the cached per-sample factors still have to be gathered.  w_j is safe to load early: the
-// bundles of one launch are disjoint, so the current step never writes it.
-struct ColPref {
-    int64_t kk;  // position, -1 = none
-    int64_t p0, p1;
-    double wj;
-    int32_t j;
-    int32_t r[PF];
-    float x[PF];
-};
-
-__device__ __forceinline__ void prefetch_col(const StepArgs &a, ColPref &pf, int64_t kk, int64_t k1, int lane)
-{
-    pf.kk = -1;
-    if (kk >= k1) return;
-    pf.kk = kk;
-    pf.j = __ldg(&a.order[kk]);
-    pf.p0 = __ldg(&a.col_ptr[pf.j]);
-    pf.p1 = __ldg(&a.col_ptr[pf.j + 1]);
-    if (pf.p1 - pf.p0 > a.heavy_len) return;
-    pf.wj = ldcg(&a.w[pf.j]);
-#pragma unroll
-    for (int m = 0; m < PF; m++) {
-        const int64_t p = pf.p0 + lane + 32 * m;
-        if (p < pf.p1) {
-            pf.r[m] = __ldg(&a.row_idx[p]);
-            pf.x[m] = __ldg(&a.val[p]);
-        }
-    }
-}
-
 // The CTA's first bundle-share position (L1 term, Delta, w commit) and the thread's first
 // touched sample (loss change, commit), kept in registers from the line search to the commit.
 struct ShareReg {
@@ -1113,8 +1081,6 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
         }                                         \
     } while (0)
     const int64_t gw = (int64_t)c * NW + warp;
-    ColPref pf;
-    prefetch_col(a, pf, gw, min(a.P, a.ntot), lane);
     if (c == 0 && tid == 0) {
         sm.F = ldcg(a.F);
         for (int i = 0; i < 4; i++) sm.cnt[i] = 0;
@@ -1125,60 +1091,83 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
         const int64_t k1 = min(k0 + a.P, a.ntot);
         const int64_t Pt = k1 - k0;
 
-        // ---------------- phase A: light columns, one warp per column (a1, a2, a3) --------
-        {
-            for (int64_t kk = k0 + gw; kk < k1; kk += (int64_t)G * NW) {
-                const bool pre = kk == pf.kk;
-                const int32_t j = pre ? pf.j : __ldg(&a.order[kk]);
-                const int64_t p0 = pre ? pf.p0 : __ldg(&a.col_ptr[j]);
-                const int64_t p1 = pre ? pf.p1 : __ldg(&a.col_ptr[j + 1]);
-                if (p1 - p0 > a.heavy_len) continue;
+        // ---------------- phase A: light columns (a1, a2, a3) --------------------------------
+        // Positions in chunks of 32 per warp (one coalesced descriptor load): a short column
+        // (<= SHORT nonzeros) is reduced by its lane alone, in row order (no shuffles; the
+        // independent loads of all lanes' columns are in flight together); a medium one by the
+        // whole warp.  Heavy columns (> heavy_len) are split below (A').
+        // chunk width: 32 positions, fewer when the bundle would leave warps idle (small P)
+        const int cw = (int)min((int64_t)32, max((int64_t)1, (Pt + (int64_t)G * NW - 1) / ((int64_t)G * NW)));
+        for (int64_t ch = gw;; ch += (int64_t)G * NW) {
+            const int64_t kb = k0 + ch * cw;
+            if (kb >= k1) break;
+            const int64_t kk = kb + lane;
+            const int4 ci = (lane < cw && kk < k1) ? __ldg(&a.colinfo[kk]) : make_int4(0, -1, 0, 0);
+            const int len = ci.y;
+            if (len >= 0 && len <= SHORT) {
+                const int32_t j = ci.x;
+                const int64_t p0 = colinfo_p0(ci);
+                int32_t ri[SHORT];
+                float xv[SHORT];
+#pragma unroll
+                for (int e = 0; e < SHORT; e++) {
+                    ri[e] = 0;
+                    xv[e] = 0.f;
+                    if (e < len) {
+                        ri[e] = __ldg(&a.row_idx[p0 + e]);
+                        xv[e] = __ldg(&a.val[p0 + e]);
+                    }
+                }
+                const double wj = ldcg(&a.w[j]);
+                double2 cf[SHORT];
+#pragma unroll
+                for (int e = 0; e < SHORT; e++) cf[e] = e < len ? ldcg(&a.coef[ri[e]]) : make_double2(0.0, 0.0);
+                double g = 0.0, h = 0.0;
+#pragma unroll
+                for (int e = 0; e < SHORT; e++) {
+                    if (e < len) {
+                        const double x = (double)xv[e];
+                        g += x * cf[e].x;
+                        h += (x * x) * cf[e].y;
+                    }
+                }
+                const Dir r = finish_feature(a, g, h, wj);
+                a.dk[kk - k0] = r.d;
+                a.deltak[kk - k0] = r.delta;
+                if (a.g_out) {
+                    a.g_out[kk - k0] = r.g;
+                    a.h_out[kk - k0] = r.h;
+                }
+                if (a.d_out) a.d_out[kk - k0] = r.d;
+                if (r.d != 0.0 && len != a.s) {   // full columns are folded from CSC (dense_dx)
+#pragma unroll
+                    for (int e = 0; e < SHORT; e++)
+                        if (e < len) emit(a, ri[e], (int32_t)(kk - k0), r.d * (double)xv[e]);
+                }
+            }
+            unsigned med = __ballot_sync(0xffffffffu, len > SHORT && len <= a.heavy_len);
+            while (med) {
+                const int src = __ffs(med) - 1;
+                med &= med - 1;
+                const int32_t j = __shfl_sync(0xffffffffu, ci.x, src);
+                const int ml = __shfl_sync(0xffffffffu, len, src);
+                const int lo = __shfl_sync(0xffffffffu, ci.z, src), hi = __shfl_sync(0xffffffffu, ci.w, src);
+                const int64_t p0 = (int64_t)(((uint64_t)(uint32_t)hi << 32) | (uint64_t)(uint32_t)lo);
+                const int64_t p1 = p0 + ml;
+                const int64_t km = kb + src;
                 double gs, hs;
-                if (pre) {
-                    // prefetched column: only the cached factors are gathered here
-                    double g = 0.0, h = 0.0;
-#pragma unroll
-                    for (int m = 0; m < PF; m++) {
-                        if (p0 + lane + 32 * m < p1) {
-                            const double x = (double)pf.x[m];
-                            const double2 cf = ldcg(&a.coef[pf.r[m]]);
-                            g += x * cf.x;
-                            h += (x * x) * cf.y;
-                        }
-                    }
-                    for (int64_t p = p0 + lane + 32 * PF; p < p1; p += 32) {
-                        const int32_t i = __ldg(&a.row_idx[p]);
-                        const double x = (double)__ldg(&a.val[p]);
-                        const double2 cf = ldcg(&a.coef[i]);
-                        g += x * cf.x;
-                        h += (x * x) * cf.y;
-                    }
-                    gs = warp_sum(g);
-                    hs = warp_sum(h);
-                } else {
-                    col_gh(a, p0, p1, lane, gs, hs);
-                }
-                const double wj = pre ? pf.wj : ldcg(&a.w[j]);
-                const Dir r = finish_feature(a, gs, hs, wj);
+                col_gh(a, p0, p1, lane, gs, hs);
+                const Dir r = finish_feature(a, gs, hs, ldcg(&a.w[j]));
                 if (lane == 0) {
-                    a.dk[kk - k0] = r.d;
-                    a.deltak[kk - k0] = r.delta;
+                    a.dk[km - k0] = r.d;
+                    a.deltak[km - k0] = r.delta;
                     if (a.g_out) {
-                        a.g_out[kk - k0] = r.g;
-                        a.h_out[kk - k0] = r.h;
+                        a.g_out[km - k0] = r.g;
+                        a.h_out[km - k0] = r.h;
                     }
-                    if (a.d_out) a.d_out[kk - k0] = r.d;
+                    if (a.d_out) a.d_out[km - k0] = r.d;
                 }
-                if (r.d != 0.0 && p1 - p0 != a.s) {   // full columns are folded from CSC (dense_dx)
-                    if (pre) {
-#pragma unroll
-                        for (int m = 0; m < PF; m++)
-                            if (p0 + lane + 32 * m < p1) emit(a, pf.r[m], (int32_t)(kk - k0), r.d * (double)pf.x[m]);
-                        col_scatter(a, p0 + 32 * PF, p1, lane, (int32_t)(kk - k0), r.d);
-                    } else {
-                        col_scatter(a, p0, p1, lane, (int32_t)(kk - k0), r.d);
-                    }
-                }
+                if (r.d != 0.0 && ml != a.s) col_scatter(a, p0, p1, lane, (int32_t)(km - k0), r.d);
             }
         }
 
@@ -1505,8 +1494,6 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
         prev_q = qacc < 0 ? QW : qacc;
 
         // ---------------- commit (a5): this CTA's samples and bundle share; clear marks -----
-        // prefetch the next step's first light column of this warp (immutable data + w_j)
-        prefetch_col(a, pf, k1 + gw, min(k1 + a.P, a.ntot), lane);
         for (int64_t li = tid; li < nT; li += NT) {
             // the heavy-row fold may have produced dx for the register row: take dxg then
             const bool reg = li == tid && rr.has_dx;

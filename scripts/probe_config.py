@@ -22,6 +22,7 @@ ap.add_argument("--P", default="")
 ap.add_argument("--modes", default="0")
 ap.add_argument("--outer", type=int, default=1)
 ap.add_argument("--profile", action="store_true")
+ap.add_argument("--heavy", type=int, default=0, help="heavy_len launch knob (0 = keep)")
 args = ap.parse_args()
 t0 = time.time()
 prob = synth.config(args.cfg, loss=args.loss)
@@ -33,7 +34,7 @@ Ps = [int(x) for x in args.P.split(",") if x] or [prob.P]
 for P in Ps:
     for mode in [int(m) for m in args.modes.split(",")]:
         try:
-            s.set_launch(mode, 0, 0)
+            s.set_launch(mode, 0, args.heavy)
         except pk.PCDNError as e:
             print(json.dumps({"P": P, "mode": mode, "error": str(e)}), flush=True)
             continue
@@ -49,7 +50,7 @@ for P in Ps:
         steps = r["steps"]
         kms = r["t_step_kernel_ms"]
         gbs = r["alg_bytes"] / (kms / 1e3) / 1e9
-        out = {"cfg": args.cfg, "P": P, "mode_req": mode, "mode_used": used, "outer": r["outer_iters"],
+        out = {"cfg": args.cfg, "P": P, "mode_req": mode, "mode_used": used, "heavy_len": args.heavy, "outer": r["outer_iters"],
                "steps": steps, "step_us": 1e3 * kms / steps, "kernel_ms_per_outer": kms / max(1, r["outer_iters"]),
                "gpu_ms_per_outer": r["t_gpu_ms"] / max(1, r["outer_iters"]),
                "alg_bytes_per_step": r["alg_bytes"] / steps, "kernel_alg_GBs": gbs, "frac_measured_hbm": gbs / peak,
