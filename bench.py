@@ -307,13 +307,14 @@ def main():
 
     peak, peak_src = peaks()
     traffic = None
-    prof = load_json(os.path.join(ROOT, "profiles", "k_step_dram.json"), {})
-    if prof.get("workload") == f"cfg{args.config}" and prof.get("P") == prob.P:
-        traffic = prof.get("dram_bytes_per_launch")
+    prof = load_json(os.path.join(ROOT, "profiles", "k_step_dram.json"), {}).get(f"cfg{args.config}_P{prob.P}", {})
+    traffic = prof.get("dram_bytes_per_launch")
     per_launch_bytes = alg_bytes / max(1, step_launches)
     per_launch_ms = t_kernel / max(1, step_launches)
     achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
-    roof = {"bound": "hbm", "kernel": "pcdn::k_step (persistent, one launch per outer iteration)",
+    kname = {1: "k_step<ClusterSync>", 2: "k_step<GridSync>", 3: "k_step_res", 4: "k_step_dense"}.get(
+        pk.pcdn_phase_cycles(solver.ctx)[1], "k_step")
+    roof = {"bound": "hbm", "kernel": f"pcdn::{kname} (persistent, one launch per outer iteration)",
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "alg_bytes_per_launch": per_launch_bytes,
             "launch_ms": per_launch_ms, "peak_source": peak_src,
