@@ -237,3 +237,36 @@ class Oracle:
         rc = lib().ora_cdn(C.byref(self.pb), _p(w), _p(z), seed & 0xFFFFFFFFFFFFFFFF, int(max_outer),
                            _p(Ft) if trace else None, cap, C.byref(F))
         return dict(rc=rc, w=w, z=z, F=F.value, F_trace=Ft[:cap].copy())
+
+
+# ---------------------------------------------------------------------------------------------
+# Lemma 1(a) (proof, Eq. "ebtdef"): for a uniformly random
+# bundle B of P distinct features, lambda_bar(B) = max_{j in B} (X'X)_jj and, with lambda_k the
+# k-th smallest (X'X)_jj,
+#     f(P) = E[lambda_bar(B)] = (1 / C(n,P)) * sum_{k=P}^{n} lambda_k C(k-1, P-1)
+# (the maximum of a P-subset is lambda_k exactly when the other P-1 members are among the k-1
+# smaller ones).  Written out term by term in log-space (lgamma) so large n does not overflow.
+# ---------------------------------------------------------------------------------------------
+def column_sq_norms(prob) -> np.ndarray:
+    """lambda_j = (X'X)_jj = sum_i x_ij^2, fp64, from the CSC columns."""
+    out = np.zeros(int(prob.n))
+    for j in range(int(prob.n)):
+        a, b = int(prob.col_ptr[j]), int(prob.col_ptr[j + 1])
+        v = np.asarray(prob.val[a:b], dtype=np.float64)
+        out[j] = float(np.dot(v, v))
+    return out
+
+
+def expected_lambda_max(lam, P: int) -> float:
+    """f(P) of Lemma 1(a)."""
+    import math
+    lam = np.sort(np.asarray(lam, dtype=np.float64))   # lambda_1 <= ... <= lambda_n
+    n = lam.size
+    if not 1 <= P <= n:
+        raise ValueError("1 <= P <= n")
+    log_cnp = math.lgamma(n + 1) - math.lgamma(P + 1) - math.lgamma(n - P + 1)
+    tot = 0.0
+    for k in range(P, n + 1):   # 1-based k
+        log_c = math.lgamma(k) - math.lgamma(P) - math.lgamma(k - P + 1)
+        tot += lam[k - 1] * math.exp(log_c - log_cnp)
+    return tot
