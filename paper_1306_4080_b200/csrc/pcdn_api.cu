@@ -27,10 +27,16 @@ constexpr size_t ALIGN = 256;
 
 inline size_t align_up(size_t x) { return (x + ALIGN - 1) & ~(ALIGN - 1); }
 
+// per-outer-iteration lists (partition, column descriptors, heavy / full column lists); two sets
+// so that the lists of outer iteration k+1 can be built while the step kernel of k runs
+struct Lists {
+    size_t order, hdesc, flag, fflag, fpos, flist, tiles3, colinfo, hpos, hlist, hlen, hstart, tiles1, tiles2, nheavy;
+};
+
 struct Layout {
-    size_t w, z, coef, cnt, bits, rec, dxg, tlist, order, hdesc, flag, fflag, fpos, flist, tiles3, colinfo, hpos, hlist, hlen, hstart, tiles1, tiles2,
-        seen, dk, deltak, gk, hk, part, hpart, counters, info, F, Fcopy, status, err_idx, err_what, bar,
-        objp, nheavy, prof, tl, dbg_dx, dbg_mark, rec2, rslot, ovf_cnt, part_gh, total;
+    size_t w, z, coef, cnt, bits, rec, dxg, tlist, seen, dk, deltak, gk, hk, part, hpart, counters, info, F, Fcopy,
+        status, err_idx, err_what, bar, objp, prof, tl, dbg_dx, dbg_mark, rec2, rslot, ovf_cnt, part_gh, total;
+    Lists ls[2];
 };
 
 Layout make_layout(int64_t s, int64_t n, int64_t nnz)
@@ -52,20 +58,24 @@ Layout make_layout(int64_t s, int64_t n, int64_t nnz)
     L.rec = take(sizeof(Rec) * nnz);
     L.dxg = take(sizeof(double) * s);
     L.tlist = take(sizeof(int32_t) * nw * 32);
-    L.order = take(sizeof(int32_t) * n);
-    L.hdesc = take(sizeof(int4) * n);
-    L.flag = take(sizeof(int32_t) * n);
-    L.fflag = take(sizeof(int32_t) * n);
-    L.fpos = take(sizeof(int64_t) * (n + 1));
-    L.flist = take(sizeof(int32_t) * n);
-    L.tiles3 = take(sizeof(int64_t) * ntile);
-    L.colinfo = take(sizeof(int4) * n);
-    L.hpos = take(sizeof(int64_t) * (n + 1));
-    L.hlist = take(sizeof(int32_t) * n);
-    L.hlen = take(sizeof(int64_t) * n);
-    L.hstart = take(sizeof(int64_t) * (n + 1));
-    L.tiles1 = take(sizeof(int64_t) * ntile);
-    L.tiles2 = take(sizeof(int64_t) * ntile);
+    for (int b = 0; b < 2; b++) {
+        Lists &S = L.ls[b];
+        S.order = take(sizeof(int32_t) * n);
+        S.hdesc = take(sizeof(int4) * n);
+        S.flag = take(sizeof(int32_t) * n);
+        S.fflag = take(sizeof(int32_t) * n);
+        S.fpos = take(sizeof(int64_t) * (n + 1));
+        S.flist = take(sizeof(int32_t) * n);
+        S.tiles3 = take(sizeof(int64_t) * ntile);
+        S.colinfo = take(sizeof(int4) * n);
+        S.hpos = take(sizeof(int64_t) * (n + 1));
+        S.hlist = take(sizeof(int32_t) * n);
+        S.hlen = take(sizeof(int64_t) * n);
+        S.hstart = take(sizeof(int64_t) * (n + 1));
+        S.tiles1 = take(sizeof(int64_t) * ntile);
+        S.tiles2 = take(sizeof(int64_t) * ntile);
+        S.nheavy = take(sizeof(int64_t));
+    }
     L.seen = take(sizeof(uint32_t) * ((n + 31) / 32));
     L.dk = take(sizeof(double) * n);
     L.deltak = take(sizeof(double) * n);
@@ -82,7 +92,6 @@ Layout make_layout(int64_t s, int64_t n, int64_t nnz)
     L.err_what = take(sizeof(int));
     L.bar = take(sizeof(unsigned long long));
     L.objp = take(sizeof(double) * 2 * OBJ_NB);
-    L.nheavy = take(sizeof(int64_t));
     L.prof = take(sizeof(long long) * 16);
     L.tl = take(sizeof(long long) * TL_STEPS * NW * TL_PTS);
     L.dbg_dx = take(sizeof(double) * s);
@@ -139,6 +148,8 @@ struct pcdn_ctx {
     int num_sms = 0;
     size_t smem = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;      // builds the next outer iteration's lists during a step launch
+    cudaEvent_t ev_prep = nullptr;
     unsigned char *base = nullptr;
     Layout L{};
     HostMirror *hm = nullptr;
@@ -185,40 +196,52 @@ inline int grid1d(int64_t work, int nt = 256)
 // device-wide exclusive scan of in[0..n) (n bounded by *n_dev if non-null) into out[0..n]
 template <typename Tin>
 int scan(pcdn_ctx *ctx, const Tin *in, int64_t n_host, const int64_t *n_dev, int64_t *out, int64_t *tiles,
-         int64_t *total)
+         int64_t *total, cudaStream_t st)
 {
     const int64_t ntile = (n_host + SCAN_TILE - 1) / SCAN_TILE > 0 ? (n_host + SCAN_TILE - 1) / SCAN_TILE : 1;
-    k_scan_reduce<Tin, int64_t><<<(unsigned)ntile, SCAN_NT, 0, ctx->stream>>>(in, n_host, n_dev, tiles);
-    k_scan_tiles<int64_t><<<1, SCAN_NT, 0, ctx->stream>>>(tiles, ntile);
-    k_scan_apply<Tin, int64_t><<<(unsigned)ntile, SCAN_NT, 0, ctx->stream>>>(in, n_host, n_dev, tiles, out, total);
+    k_scan_reduce<Tin, int64_t><<<(unsigned)ntile, SCAN_NT, 0, st>>>(in, n_host, n_dev, tiles);
+    k_scan_tiles<int64_t><<<1, SCAN_NT, 0, st>>>(tiles, ntile);
+    k_scan_apply<Tin, int64_t><<<(unsigned)ntile, SCAN_NT, 0, st>>>(in, n_host, n_dev, tiles, out, total);
     ctx->launches += 3;
     CU(cudaGetLastError());
     return PCDN_OK;
 }
 
-// heavy-column lists for the positions held in ctx->order[0..ntot)
-int build_heavy(pcdn_ctx *ctx, int64_t ntot)
+// heavy-column and full-column lists for the positions held in list set `buf` (order[0..ntot))
+int build_heavy(pcdn_ctx *ctx, int64_t ntot, int buf, cudaStream_t st)
 {
-    const Layout &L = ctx->L;
-    int rc = scan<int32_t>(ctx, ctx->at<int32_t>(L.flag), ntot, nullptr, ctx->at<int64_t>(L.hpos),
-                           ctx->at<int64_t>(L.tiles1), ctx->at<int64_t>(L.nheavy));
+    const Lists &S = ctx->L.ls[buf];
+    int rc = scan<int32_t>(ctx, ctx->at<int32_t>(S.flag), ntot, nullptr, ctx->at<int64_t>(S.hpos),
+                           ctx->at<int64_t>(S.tiles1), ctx->at<int64_t>(S.nheavy), st);
     if (rc) return rc;
-    k_heavy_compact<<<grid1d(ntot), 256, 0, ctx->stream>>>(ctx->at<int64_t>(L.hpos), ntot, ctx->at<int32_t>(L.order),
-                                                           ctx->col_ptr, ctx->at<int32_t>(L.hlist),
-                                                           ctx->at<int64_t>(L.hlen), ctx->at<int4>(L.hdesc));
+    k_heavy_compact<<<grid1d(ntot), 256, 0, st>>>(ctx->at<int64_t>(S.hpos), ntot, ctx->at<int32_t>(S.order),
+                                                  ctx->col_ptr, ctx->at<int32_t>(S.hlist), ctx->at<int64_t>(S.hlen),
+                                                  ctx->at<int4>(S.hdesc));
     ctx->launches++;
     CU(cudaGetLastError());
-    rc = scan<int64_t>(ctx, ctx->at<int64_t>(L.hlen), ntot, ctx->at<int64_t>(L.nheavy), ctx->at<int64_t>(L.hstart),
-                       ctx->at<int64_t>(L.tiles2), nullptr);
+    rc = scan<int64_t>(ctx, ctx->at<int64_t>(S.hlen), ntot, ctx->at<int64_t>(S.nheavy), ctx->at<int64_t>(S.hstart),
+                       ctx->at<int64_t>(S.tiles2), nullptr, st);
     if (rc) return rc;
     // full columns (a nonzero in every row): their d'x contribution is folded straight from CSC
-    rc = scan<int32_t>(ctx, ctx->at<int32_t>(L.fflag), ntot, nullptr, ctx->at<int64_t>(L.fpos),
-                       ctx->at<int64_t>(L.tiles3), nullptr);
+    rc = scan<int32_t>(ctx, ctx->at<int32_t>(S.fflag), ntot, nullptr, ctx->at<int64_t>(S.fpos),
+                       ctx->at<int64_t>(S.tiles3), nullptr, st);
     if (rc) return rc;
-    k_full_compact<<<grid1d(ntot), 256, 0, ctx->stream>>>(ctx->at<int64_t>(L.fpos), ntot, ctx->at<int32_t>(L.flist));
+    k_full_compact<<<grid1d(ntot), 256, 0, st>>>(ctx->at<int64_t>(S.fpos), ntot, ctx->at<int32_t>(S.flist));
     ctx->launches++;
     CU(cudaGetLastError());
     return PCDN_OK;
+}
+
+// a0 for outer iteration k into list set `buf`: the partition pi_k and its lists
+int prep_outer(pcdn_ctx *ctx, uint64_t seed, int64_t k, int buf, cudaStream_t st)
+{
+    const Lists &S = ctx->L.ls[buf];
+    k_perm<<<grid1d(ctx->n), 256, 0, st>>>(seed, k, ctx->n, ctx->s, ctx->col_ptr, ctx->heavy_len,
+                                           ctx->at<int32_t>(S.order), ctx->at<int32_t>(S.flag),
+                                           ctx->at<int32_t>(S.fflag), ctx->at<int4>(S.colinfo));
+    ctx->launches++;
+    CU(cudaGetLastError());
+    return build_heavy(ctx, ctx->n, buf, st);
 }
 
 int objective_kernels(pcdn_ctx *ctx)
@@ -269,10 +292,13 @@ int reset_status(pcdn_ctx *ctx)
 }
 
 // Launch the persistent step kernel over `nsteps` bundles of the positions in ctx->order.
-int launch_steps(pcdn_ctx *ctx, int64_t ntot, int64_t P, int64_t nsteps, int64_t trace_off, double *g_out,
+int choose_mode(const pcdn_ctx *ctx, int64_t P);
+
+int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps, int64_t trace_off, double *g_out,
                  double *h_out, double *d_out)
 {
     const Layout &L = ctx->L;
+    const Lists &S = L.ls[buf];
     StepArgs a{};
     a.s = ctx->s;
     a.n = ctx->n;
@@ -298,14 +324,14 @@ int launch_steps(pcdn_ctx *ctx, int64_t ntot, int64_t P, int64_t nsteps, int64_t
     a.rec = ctx->at<Rec>(L.rec);
     a.dxg = ctx->at<double>(L.dxg);
     a.tlist = ctx->at<int32_t>(L.tlist);
-    a.order = ctx->at<int32_t>(L.order);
-    a.colinfo = ctx->at<int4>(L.colinfo);
-    a.hpos = ctx->at<int64_t>(L.hpos);
-    a.hlist = ctx->at<int32_t>(L.hlist);
-    a.hdesc = ctx->at<int4>(L.hdesc);
-    a.hstart = ctx->at<int64_t>(L.hstart);
-    a.fpos = ctx->at<int64_t>(L.fpos);
-    a.flist = ctx->at<int32_t>(L.flist);
+    a.order = ctx->at<int32_t>(S.order);
+    a.colinfo = ctx->at<int4>(S.colinfo);
+    a.hpos = ctx->at<int64_t>(S.hpos);
+    a.hlist = ctx->at<int32_t>(S.hlist);
+    a.hdesc = ctx->at<int4>(S.hdesc);
+    a.hstart = ctx->at<int64_t>(S.hstart);
+    a.fpos = ctx->at<int64_t>(S.fpos);
+    a.flist = ctx->at<int32_t>(S.flist);
     a.ntot = ntot;
     a.P = P;
     a.nsteps = nsteps;
@@ -350,16 +376,7 @@ int launch_steps(pcdn_ctx *ctx, int64_t ntot, int64_t P, int64_t nsteps, int64_t
     CU(cudaMemsetAsync(a.bar, 0, sizeof(unsigned long long), ctx->stream));
     // cluster mode for steps small enough that 16 SMs keep up (hardware barrier, ~0.2 us);
     // grid mode (all SMs, software barrier) for large steps
-    int mode = ctx->mode_req;
-    if (mode == 0 && ctx->Gd > 0) mode = 4;   // fully dense problem: row-block kernel
-    if (mode == 0) {
-        // cluster-resident when the samples fit the cluster's shared memory and the bundles are
-        // small; else the HBM-state kernel as one cluster only while each of its warps has few
-        // columns per step (they are processed one after another), otherwise over the whole grid
-        const double est_nb = (double)ctx->nnz * (double)P / (double)ctx->n;
-        if (ctx->res_G >= 2 && est_nb <= 65536.0) mode = 3;
-        else mode = (ctx->Gc >= 2 && est_nb <= 16384.0 && P <= 2 * NW * ctx->Gc) ? 1 : 2;
-    }
+    const int mode = choose_mode(ctx, P);
     ctx->last_mode = mode;
     if (mode == 4) {
         if (ctx->Gd < 1) return set_err(ctx, PCDN_ERR_INVALID, "dense step kernel unavailable for this problem");
@@ -401,6 +418,22 @@ int launch_steps(pcdn_ctx *ctx, int64_t ntot, int64_t P, int64_t nsteps, int64_t
     }
     ctx->launches++;
     return PCDN_OK;
+}
+
+// launch mode of the step kernel for bundles of size P (see pcdn_set_launch)
+int choose_mode(const pcdn_ctx *ctx, int64_t P)
+{
+    int mode = ctx->mode_req;
+    if (mode == 0 && ctx->Gd > 0) mode = 4;   // fully dense problem: row-block kernel
+    if (mode == 0) {
+        // cluster-resident when the samples fit the cluster's shared memory and the bundles are
+        // small; else the HBM-state kernel as one cluster only while each of its warps has few
+        // columns per step (they are processed one after another), otherwise over the whole grid
+        const double est_nb = (double)ctx->nnz * (double)P / (double)ctx->n;
+        if (ctx->res_G >= 2 && est_nb <= 65536.0) mode = 3;
+        else mode = (ctx->Gc >= 2 && est_nb <= 16384.0 && P <= 2 * NW * ctx->Gc) ? 1 : 2;
+    }
+    return mode;
 }
 
 int configure_launch(pcdn_ctx *ctx)
@@ -576,6 +609,12 @@ int pcdn_create(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_ptr, c
             e = cudaEventCreate(&ctx->ev[i]);
             if (e != cudaSuccess) return fail(set_err(ctx, PCDN_ERR_CUDA, "cudaEventCreate: %s", cudaGetErrorString(e)));
         }
+        if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&ctx->ev_prep, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();   // no overlap: lists are built on the context stream
+            ctx->side = nullptr;
+            ctx->ev_prep = nullptr;
+        }
     }
     int rc = configure_launch(ctx);
     if (rc) return fail(rc);
@@ -707,6 +746,11 @@ void pcdn_destroy(pcdn_ctx *ctx)
     if (ctx->stream || true) cudaStreamSynchronize(ctx->stream);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    if (ctx->side) {
+        cudaStreamSynchronize(ctx->side);
+        cudaStreamDestroy(ctx->side);
+    }
+    if (ctx->ev_prep) cudaEventDestroy(ctx->ev_prep);
     if (ctx->hm) cudaFreeHost(ctx->hm);
     delete ctx;
 }
@@ -787,13 +831,14 @@ int pcdn_bundle_step(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, pcdn_step_
     int rc;
     if ((rc = reset_status(ctx))) return rc;
     CU(cudaMemsetAsync(ctx->at<int64_t>(L.counters), 0, sizeof(int64_t) * 8, ctx->stream));
+    const Lists &S = L.ls[0];
     k_bundle_prep<<<grid1d(P), 256, 0, ctx->stream>>>(bundle, P, ctx->n, ctx->s, ctx->col_ptr, ctx->heavy_len,
-                                                      ctx->at<int32_t>(L.order), ctx->at<int32_t>(L.flag),
-                                                      ctx->at<int32_t>(L.fflag),
+                                                      ctx->at<int32_t>(S.order), ctx->at<int32_t>(S.flag),
+                                                      ctx->at<int32_t>(S.fflag),
                                                       ctx->at<uint32_t>(L.seen), ctx->at<int>(L.status),
                                                       ctx->at<long long>(L.err_idx),
                                                       (unsigned long long *)(ctx->at<int64_t>(L.counters) + 2),
-                                                      ctx->at<int4>(L.colinfo));
+                                                      ctx->at<int4>(S.colinfo));
     k_bundle_unseen<<<grid1d(P), 256, 0, ctx->stream>>>(bundle, P, ctx->n, ctx->at<uint32_t>(L.seen));
     ctx->launches += 2;
     CU(cudaGetLastError());
@@ -803,9 +848,9 @@ int pcdn_bundle_step(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, pcdn_step_
     CU(cudaStreamSynchronize(ctx->stream));
     if (ctx->hm->status)
         return set_err(ctx, PCDN_ERR_INVALID, "bundle entry %lld is out of range or repeated", (long long)ctx->hm->err_idx);
-    if ((rc = build_heavy(ctx, P))) return rc;
+    if ((rc = build_heavy(ctx, P, 0, ctx->stream))) return rc;
     if (ctx->debug) CU(cudaMemsetAsync(ctx->at<uint8_t>(L.dbg_mark), 0, ctx->s, ctx->stream));
-    if ((rc = launch_steps(ctx, P, P, 1, 0, g_out, h_out, d_out))) return rc;
+    if ((rc = launch_steps(ctx, 0, P, P, 1, 0, g_out, h_out, d_out))) return rc;
     if (info) {
         if ((rc = readback(ctx))) return rc;
         const double *v = ctx->hm->info;
@@ -864,19 +909,25 @@ int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_
     int32_t k = 0;
     double F = NAN, gap = NAN, t_step_ms = 0.0;
     CU(cudaEventRecord(ctx->ev[2], ctx->stream));
+    // the cluster-resident step kernel occupies one cluster of SMs: the next outer iteration's
+    // partition and lists are then built concurrently on the side stream (double-buffered sets)
+    const bool overlap = ctx->side != nullptr && choose_mode(ctx, P) == 3;
+    if (max_outer > 0 && (rc = prep_outer(ctx, seed, 0, 0, ctx->stream))) return rc;
     for (k = 0; k < max_outer; k++) {
-        // a0: partition pi_k and the per-step heavy-column lists
-        k_perm<<<grid1d(ctx->n), 256, 0, ctx->stream>>>(seed, k, ctx->n, ctx->s, ctx->col_ptr, ctx->heavy_len,
-                                                         ctx->at<int32_t>(L.order), ctx->at<int32_t>(L.flag),
-                                                         ctx->at<int32_t>(L.fflag),
-                                                         ctx->at<int4>(L.colinfo));
-        ctx->launches++;
-        CU(cudaGetLastError());
-        if ((rc = build_heavy(ctx, ctx->n))) return rc;
+        const int buf = k & 1;
+        // a0: partition pi_k and its lists (built ahead on the side stream when overlapping)
+        if (k > 0) {
+            if (overlap) CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_prep, 0));
+            else if ((rc = prep_outer(ctx, seed, k, buf, ctx->stream))) return rc;
+        }
         // a1..a5: all b bundle steps in one persistent launch
         CU(cudaEventRecord(ctx->ev[0], ctx->stream));
-        if ((rc = launch_steps(ctx, ctx->n, P, b, (int64_t)k * b, nullptr, nullptr, nullptr))) return rc;
+        if ((rc = launch_steps(ctx, buf, ctx->n, P, b, (int64_t)k * b, nullptr, nullptr, nullptr))) return rc;
         CU(cudaEventRecord(ctx->ev[1], ctx->stream));
+        if (overlap && k + 1 < max_outer) {
+            if ((rc = prep_outer(ctx, seed, k + 1, buf ^ 1, ctx->side))) return rc;
+            CU(cudaEventRecord(ctx->ev_prep, ctx->side));
+        }
         // a6: F from scratch (reading Z23), one readback per outer iteration
         if ((rc = objective_kernels(ctx))) return rc;
         if ((rc = readback(ctx))) return rc;
@@ -905,6 +956,9 @@ int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_
             }
         }
     }
+    // a list build for an outer iteration that was not run must finish before anything else uses
+    // the list sets on the context stream
+    if (overlap) CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_prep, 0));
     CU(cudaEventRecord(ctx->ev[3], ctx->stream));
     CU(cudaEventSynchronize(ctx->ev[3]));
     if (max_outer == 0) {
