@@ -366,7 +366,7 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
         a.res_off[3] = (int)RL.lq;
         a.res_off[4] = (int)RL.y;
         a.res_off[5] = (int)RL.recin;
-        a.res_off[6] = 0;
+        a.res_off[6] = (int)RL.tl;
         a.res_off[7] = (int)RL.total;
     }
     a.rec2 = ctx->at<Rec>(L.rec2);
@@ -396,7 +396,7 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        CU(cudaLaunchKernelEx(&cfg, k_step_res, a));
+        CU(cudaLaunchKernelEx(&cfg, ctx->loss == LOSS_LOGISTIC ? k_step_res<LOSS_LOGISTIC> : k_step_res<LOSS_L2SVM>, a));
     } else if (mode == 1) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(ctx->Gc);
@@ -480,7 +480,7 @@ int configure_launch(pcdn_ctx *ctx)
     {
         int optin = 0;
         CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        const void *kr = (const void *)k_step_res;
+        const void *kr = ctx->loss == LOSS_LOGISTIC ? (const void *)k_step_res<LOSS_LOGISTIC> : (const void *)k_step_res<LOSS_L2SVM>;
         CU(cudaFuncSetAttribute(kr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         ctx->res_G = 0;
         const int greq = ctx->mode_req == 3 ? ctx->G_req : 0;

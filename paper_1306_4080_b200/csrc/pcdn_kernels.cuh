@@ -669,6 +669,7 @@ __device__ __forceinline__ double fold_small(const StepArgs &a, int64_t off, int
     }
     double dx = 0.0;
     int last = -1;
+#pragma unroll 1
     for (int t = 0; t < ni; t++) {
         int best = 0x7fffffff;
         double bv = 0.0;

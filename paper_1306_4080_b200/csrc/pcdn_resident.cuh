@@ -47,6 +47,7 @@ constexpr int R_HB = 256;  // per-warp bitonic buffer for samples with many reco
 constexpr int R_CPW = 8;   // own bundle positions per warp whose column results stay in smem
 constexpr int R_WMAX = 16; // partial-row slots (WinLayout<QW>::W)
 constexpr int R_RP = 4;    // own light columns per warp staged a step ahead
+constexpr int R_TBW = 32 * NT / 32;   // touched-bitmap words (<= 32 owned samples per thread)
 
 struct __align__(16) RRec {  // a record: sample (then: next record of the sample's list), k, value
     int32_t li;
@@ -98,6 +99,8 @@ struct ResFixed {
     uint32_t recvcnt[16];        // records each producer CTA sent to this CTA (st.async, M0)
     int spilled;                 // this CTA wrote overflow records to HBM in the current step
     int nlong;                   // samples whose list is longer than NREG (queued in lq)
+    int ntl[2];                  // touched owned samples of the step, by step parity
+    uint32_t tb[R_TBW];          // owned samples that received a record in the current step
     int stage_n;                 // HBM staging used by long lists in the current step
     int dec_q[2], dec_bad[2];    // the decision of the window, by window parity
     double dec_alpha[2], dec_lhs[2], dec_rhs[2], dec_Delta[2], dec_nT[2];
@@ -111,7 +114,7 @@ struct ResFixed {
 // byte layout of the dynamic shared memory of one CTA (identical in every CTA of the cluster)
 struct ResLayout {
     int Bs, cap;
-    size_t zd, coef, head, lq, y, recin, total;
+    size_t zd, coef, head, lq, y, tl, recin, total;
 };
 
 __host__ __device__ inline size_t r_align16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -126,7 +129,8 @@ __host__ __device__ inline ResLayout res_layout(int Bs, int cap)
     L.coef = o; o = r_align16(o + sizeof(double2) * Bs);
     L.head = o; o = r_align16(o + sizeof(int32_t) * Bs);
     L.lq = o;   o = r_align16(o + sizeof(int32_t) * Bs);
-    L.y = o;    o = r_align16(o + Bs);
+    L.y = o;    o = r_align16(o + 2 * (size_t)Bs + 4);   // label bitmap of ALL samples (s <= 16 Bs)
+    L.tl = o;   o = r_align16(o + 2 * sizeof(uint16_t) * Bs);   // touched lists, by step parity
     L.recin = o; o = r_align16(o + sizeof(RRec) * cap);
     L.total = o;
     return L;
@@ -137,7 +141,8 @@ struct ResCtx {
     ResFixed *fx;
     double2 *zd, *coef;
     int32_t *head, *lq;
-    int8_t *y;
+    uint32_t *ybits;   // bit i = (y_i > 0), every sample of the problem (constant per launch)
+    uint16_t *tls;     // [2][Bs] touched owned samples (ascending li) of the step, by step parity
     RRec *recin;
     int lg, G, c, Bs, Bsc, cap, capP, per;
     int64_t my_ovf;
@@ -221,6 +226,9 @@ __device__ __forceinline__ void cluster_sync_all()
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ int res_ybit(const ResCtx &R, int32_t i) { return (R.ybits[i >> 5] >> (i & 31)) & 1u ? 1 : -1; }
+__device__ __forceinline__ int res_y(const ResCtx &R, int li) { return res_ybit(R, li * R.G + R.c); }
+
 // coef of sample i after the previous step: from the owner's (z_i, dx_i) and alpha_prev; a
 // sample the previous step did not touch has dx_i = 0 and its stored coef is used as is
 __device__ __forceinline__ double2 res_coef(const StepArgs &a, const ResCtx &R, int32_t i)
@@ -229,8 +237,9 @@ __device__ __forceinline__ double2 res_coef(const StepArgs &a, const ResCtx &R, 
     const int li = i >> R.lg;
     const double2 zd = *remote(&R.zd[li], owner);
     const double2 cf = *remote(&R.coef[li], owner);
+    const int yi = res_ybit(R, i);   // local bitmap: no dependent L2 load for a touched sample
     if (zd.y == 0.0) return cf;
-    return coef_of(a.loss, zd.x + R.alpha_prev * zd.y, (int)__ldg(&a.y[i]));
+    return coef_of(a.loss, zd.x + R.alpha_prev * zd.y, yi);
 }
 
 // Send the records (sample i, bundle position k, d_k x_ik) of the warp's valid lanes to their
@@ -437,7 +446,7 @@ __device__ __forceinline__ void res_lazy_commit(const StepArgs &a, const ResCtx 
         if (zd.y == 0.0) continue;
         const double zn = zd.x + R.alpha_prev * zd.y;
         R.zd[li] = make_double2(zn, 0.0);
-        R.coef[li] = coef_of(a.loss, zn, R.y[li]);
+        R.coef[li] = coef_of(a.loss, zn, res_y(R, li));
     }
 }
 
@@ -502,26 +511,18 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
     for (int q = 0; q < W; q++) acc[q] = 0.0;
     int ntouch = 0;
     unsigned longmask = 0;   // owned samples (bit r) whose list is longer than NREG
+    // the step's touched owned samples (ascending li; every owned sample when a full column moved):
+    // thread tid takes entries tid, tid + NT, ...  The previous step is already committed.
+    const uint16_t *tl = R.tls + (size_t)R.cb * R.Bs;
+    const int nT = fx.ntl[R.cb];
     if (ws.win == 0) {
         unsigned tm = 0;
-        for (int r = 0; r < R.per; r++) {
-            const int li = tid + r * NT;
-            if (li >= R.Bsc) break;
-            // lazy commit of the previous step (fused): z += alpha_prev dx_prev, coef
-            double2 zd = R.zd[li];
-            double2 cf;
-            bool cf_new = false;
-            if (zd.y != 0.0) {
-                zd.x = zd.x + R.alpha_prev * zd.y;
-                cf = coef_of(a.loss, zd.x, R.y[li]);
-                R.coef[li] = cf;
-                cf_new = true;
-            }
+        for (int r = 0;; r++) {
+            const int e = tid + r * NT;
+            if (e >= nT) break;
+            const int li = tl[e];
+            const double2 zd = R.zd[li];
             const int h = R.head[li];
-            if (h < 0 && !di.any) {
-                if (zd.y != 0.0) R.zd[li] = make_double2(zd.x, 0.0);
-                continue;
-            }
             tm |= 1u << r;
             ntouch++;
             // full columns first (bundle order), then the records (ascending k): a fixed order
@@ -541,13 +542,13 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
                 vv[0] = rc.v;
                 int ni = 1, p = rc.li;
 #pragma unroll
-                for (int e = 1; e < NREG; e++) {
-                    kk[e] = 0x7fffffff;
-                    vv[e] = 0.0;
+                for (int e2 = 1; e2 < NREG; e2++) {
+                    kk[e2] = 0x7fffffff;
+                    vv[e2] = 0.0;
                     if (p >= 0) {
                         rc = res_rec(a, R, p);
-                        kk[e] = rc.k;
-                        vv[e] = rc.v;
+                        kk[e2] = rc.k;
+                        vv[e2] = rc.v;
                         p = rc.li;
                         ni++;
                     }
@@ -561,14 +562,15 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
                 R.head[li] = -1;
                 dx = 0.0;
                 int last = -1;
-                for (int t = 0; t < ni; t++) {
+#pragma unroll 1
+                for (int t = 0; t < ni; t++) {   // not unrolled: a small hot instruction footprint
                     int best = 0x7fffffff;
                     double bv = 0.0;
 #pragma unroll
-                    for (int e = 0; e < NREG; e++) {
-                        const bool take = kk[e] > last && kk[e] < best;
-                        best = take ? kk[e] : best;
-                        bv = take ? vv[e] : bv;
+                    for (int e2 = 0; e2 < NREG; e2++) {
+                        const bool take = kk[e2] > last && kk[e2] < best;
+                        best = take ? kk[e2] : best;
+                        bv = take ? vv[e2] : bv;
                     }
                     last = best;
                     dx += bv;
@@ -581,8 +583,8 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
                 a.dbg_dx[i] = dx;
                 a.dbg_mark[i] = 1;
             }
-            const double cg = cf_new ? cf.x : R.coef[li].x;
-            const int yi = R.y[li];
+            const double cg = R.coef[li].x;
+            const int yi = res_y(R, li);
             double al = alpha0;
 #pragma unroll
             for (int q = 0; q < NQ; q++) {
@@ -592,13 +594,13 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
         }
         ws.tmask = tm;
     } else {
-        for (int r = 0; r < R.per; r++) {
+        for (int r = 0; r < 32; r++) {
             if (!((ws.tmask >> r) & 1u)) continue;
-            const int li = tid + r * NT;
+            const int li = tl[tid + r * NT];
             ntouch++;
             const double2 zd = R.zd[li];
             const double cg = R.coef[li].x;
-            const int yi = R.y[li];
+            const int yi = res_y(R, li);
             double al = alpha0;
 #pragma unroll
             for (int q = 0; q < NQ; q++) {
@@ -664,12 +666,12 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
         double acc2[W];
 #pragma unroll
         for (int q = 0; q < W; q++) acc2[q] = 0.0;
-        for (int r = 0; r < R.per; r++) {   // each owner thread, in its own fixed order
+        for (int r = 0; r < 32; r++) {   // each owner thread, in its own fixed order
             if (!((longmask >> r) & 1u)) continue;
-            const int li = tid + r * NT;
+            const int li = tl[tid + r * NT];
             const double2 zd = R.zd[li];
             const double cg = R.coef[li].x;
-            const int yi = R.y[li];
+            const int yi = res_y(R, li);
             double al = alpha0;
 #pragma unroll
             for (int q = 0; q < NQ; q++) {
@@ -765,8 +767,10 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
     pr.mark(fx, 5);
 }
 
+template <int LOSS>
 __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
 {
+    a.loss = LOSS;   // a compile-time loss: the other loss's code is dead (smaller instruction footprint)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, c = blockIdx.x;   // one cluster = the whole grid
@@ -778,7 +782,8 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         R.coef = reinterpret_cast<double2 *>(smem_raw + a.res_off[1]);
         R.head = reinterpret_cast<int32_t *>(smem_raw + a.res_off[2]);
         R.lq = reinterpret_cast<int32_t *>(smem_raw + a.res_off[3]);
-        R.y = reinterpret_cast<int8_t *>(smem_raw + a.res_off[4]);
+        R.ybits = reinterpret_cast<uint32_t *>(smem_raw + a.res_off[4]);
+        R.tls = reinterpret_cast<uint16_t *>(smem_raw + a.res_off[6]);
         R.recin = reinterpret_cast<RRec *>(smem_raw + a.res_off[5]);
         R.lg = a.res_lg;
         R.G = G;
@@ -807,13 +812,27 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         const int64_t i = (int64_t)li * G + c;
         R.zd[li] = make_double2(ldcg(&a.z[i]), 0.0);
         R.coef[li] = ldcg(&a.coef[i]);
-        R.y[li] = a.y[i];
         R.head[li] = -1;
         own += __ldg(&a.row_ptr[i + 1]) - __ldg(&a.row_ptr[i]);
+    }
+    // label bitmap: 8 words (256 samples) per warp and round, all loads in flight together
+    for (int64_t wb = (int64_t)warp * 256; wb < a.s; wb += 256 * NW) {
+        int8_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const int64_t i = wb + u * 32 + lane;
+            v[u] = i < a.s ? a.y[i] : (int8_t)0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const unsigned m = __ballot_sync(0xffffffffu, v[u] > 0);
+            if (lane == 0 && wb + u * 32 < a.s) R.ybits[(wb >> 5) + u] = m;
+        }
     }
     own = warp_sum(own);
     if (lane == 0) fx.scan_w[warp] = (unsigned long long)own;
     if (tid < 16) fx.pacc[tid] = 0;
+    for (int w = tid; w < R_TBW; w += NT) fx.tb[w] = 0u;
     if (tid < 16) {
         fx.sendcnt[tid] = 0;
         fx.recvcnt[tid] = 0;
@@ -824,6 +843,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         fx.nlong = 0;
         fx.stage_n = 0;
         fx.spilled = 0;
+        fx.ntl[0] = fx.ntl[1] = 0;
         fx.F = ldcg(a.F);
         for (int i = 0; i < 4; i++) fx.cnt[i] = 0;
     }
@@ -1105,6 +1125,21 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         RTL(R, 4);
         ph ^= 1u;
         PROF_MARK(1);
+        // lazy commit of the previous step to its touched owned samples (every producer has
+        // finished its gathers): z += alpha_prev dx, coef, dx = 0 -- while the records travel
+        {
+            const int pb = R.cb ^ 1;
+            const uint16_t *tlp = R.tls + (size_t)pb * R.Bs;
+            const int np = fx.ntl[pb];
+            for (int e = tid; e < np; e += NT) {
+                const int li = tlp[e];
+                const double2 zd = R.zd[li];
+                if (zd.y == 0.0) continue;
+                const double zn = zd.x + R.alpha_prev * zd.y;
+                R.zd[li] = make_double2(zn, 0.0);
+                R.coef[li] = coef_of(a.loss, zn, res_y(R, li));
+            }
+        }
 
         // ---------------- phase C1: lazy commit of the previous step, link the records --------
         RTL(R, 5);
@@ -1126,13 +1161,17 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
             for (int r = lane; r < np; r += 32) {
                 const int phys = warp * R.capP + r;
                 const int li = R.recin[phys].li;
-                R.recin[phys].li = atomicExch(&R.head[li], phys);
+                const int old = atomicExch(&R.head[li], phys);
+                R.recin[phys].li = old;
+                if (old < 0) atomicOr(&fx.tb[li >> 5], 1u << (li & 31));   // first record: touched
             }
         }
         for (int o = tid; o < n_ovf; o += NT) {
             int32_t *lip = reinterpret_cast<int32_t *>(&a.rec[R.my_ovf + o]);
             const int li = __ldcg(lip);
-            __stcg(lip, atomicExch(&R.head[li], R.cap + o));
+            const int old = atomicExch(&R.head[li], R.cap + o);
+            __stcg(lip, old);
+            if (old < 0) atomicOr(&fx.tb[li >> 5], 1u << (li & 31));
         }
         if (tid == 0 && n_ovf) {
             a.ovf_cnt[c] = 0;
@@ -1155,6 +1194,43 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
                 any |= d != 0.0;
             }
             di.any = __syncthreads_or(any) != 0;
+        }
+        RTL(R, 14);
+        // the step's touched owned samples, ascending (a fixed thread assignment for the fold and
+        // the line search): every owned sample when a full column moved, else the bitmap compacted
+        // by warp 0
+        {
+            uint16_t *tlc = R.tls + (size_t)R.cb * R.Bs;
+            const int nwords = (R.Bsc + 31) >> 5;
+            if (di.any) {
+                for (int e = tid; e < R.Bsc; e += NT) tlc[e] = (uint16_t)e;
+                for (int w = tid; w < nwords; w += NT) fx.tb[w] = 0u;
+                if (tid == 0) fx.ntl[R.cb] = R.Bsc;
+            } else if (warp == 0) {
+                const int wpl = (nwords + 31) >> 5;
+                const int w0 = lane * wpl, w1 = min(nwords, w0 + wpl);
+                int cnt = 0;
+                for (int w = w0; w < w1; w++) cnt += __popc(fx.tb[w]);
+                int incl = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += v;
+                }
+                int pos = incl - cnt;
+                for (int w = w0; w < w1; w++) {
+                    uint32_t m = fx.tb[w];
+                    fx.tb[w] = 0u;
+                    while (m) {
+                        const int b = __ffs(m) - 1;
+                        m &= m - 1;
+                        tlc[pos++] = (uint16_t)(w * 32 + b);
+                    }
+                }
+                if (lane == 31) fx.ntl[R.cb] = incl;
+            }
+            RTL(R, 15);
+            __syncthreads();
         }
         PROF_MARK(2);
         RTL(R, 7);

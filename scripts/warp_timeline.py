@@ -14,7 +14,7 @@ import paper_1306_4080_b200 as pk  # noqa: E402
 
 PTS = ["0 step start", "1 light cols done", "2 heavy done", "3 counts sent", "4 M0 done", "5 lazy commit",
        "6 M1 done", "7 linked", "8 fold+LS loops", "9 CTA reduce", "10 sent+staged", "11 M2 done",
-       "12 decided", "13 commit tail"]
+       "12 decided", "13 commit tail", "14 link+full cols", "15 compaction"]
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--P", type=int, default=None)
