@@ -139,6 +139,7 @@ struct pcdn_ctx {
     int G_req = 0;
     int mode_req = 0;   // 0 auto, 1 cluster, 2 grid, 3 cluster-resident, 4 dense
     int Gd = 0;         // CTAs of the dense step kernel (0 = unavailable)
+    int dense_tcap = 0; // floats per tile buffer of the dense step kernel
     size_t dsmem = 0;
     int res_G = 0;      // CTAs of the cluster-resident kernel (power of two; 0 = unavailable)
     int res_lg = 0, res_Bs = 0, res_cap = 0, res_cap_req = 0;
@@ -373,6 +374,7 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
     a.rslot = ctx->at<uint32_t>(L.rslot);
     a.ovf_cnt = ctx->at<int>(L.ovf_cnt);
     a.part_gh = ctx->at<double>(L.part_gh);
+    a.dense_tcap = ctx->dense_tcap;
     CU(cudaMemsetAsync(a.bar, 0, sizeof(unsigned long long), ctx->stream));
     // cluster mode for steps small enough that 16 SMs keep up (hardware barrier, ~0.2 us);
     // grid mode (all SMs, software barrier) for large steps
@@ -381,7 +383,9 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
     if (mode == 4) {
         if (ctx->Gd < 1) return set_err(ctx, PCDN_ERR_INVALID, "dense step kernel unavailable for this problem");
         void *args[] = {&a};
-        CU(cudaLaunchCooperativeKernel((const void *)k_step_dense, dim3(ctx->Gd), dim3(NT), args, ctx->dsmem,
+        const void *kd = ctx->loss == LOSS_LOGISTIC ? (const void *)k_step_dense<LOSS_LOGISTIC>
+                                                    : (const void *)k_step_dense<LOSS_L2SVM>;
+        CU(cudaLaunchCooperativeKernel(kd, dim3(ctx->Gd), dim3(NT), args, ctx->dsmem,
                                        ctx->stream));
     } else if (mode == 3) {
         cudaLaunchConfig_t cfg{};
@@ -528,8 +532,13 @@ int configure_launch(pcdn_ctx *ctx)
     {
         ctx->Gd = 0;
         if (ctx->nnz == ctx->s * ctx->n) {
-            ctx->dsmem = sizeof(DenseSmem);
-            const void *kd = (const void *)k_step_dense;
+            int optin = 0;
+            CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+            // the fixed part plus two tile buffers (the step's X_B rows, copied a step ahead)
+            ctx->dsmem = (size_t)optin;
+            ctx->dense_tcap = (int)((((size_t)optin - dense_fixed_bytes()) / (2 * sizeof(float))) & ~(size_t)31);
+            const void *kd = ctx->loss == LOSS_LOGISTIC ? (const void *)k_step_dense<LOSS_LOGISTIC>
+                                                        : (const void *)k_step_dense<LOSS_L2SVM>;
             CU(cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->dsmem));
             int occd = 0;
             CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occd, kd, NT, ctx->dsmem));
@@ -537,7 +546,7 @@ int configure_launch(pcdn_ctx *ctx)
             if (ctx->mode_req == 4 && ctx->G_req > 0 && ctx->G_req < gd) gd = ctx->G_req;
             if (gd > DENSE_GMAX) gd = DENSE_GMAX;
             if (gd > GMAX) gd = GMAX;
-            if (gd >= 1 && (ctx->s + gd - 1) / gd <= D_RMAX) ctx->Gd = gd;
+            if (gd >= 1 && (ctx->s + gd - 1) / gd + 3 <= D_RMAX) ctx->Gd = gd;   // + 3: 4-row aligned blocks
         }
         if (ctx->mode_req == 4 && ctx->Gd < 1)
             return set_err(ctx, PCDN_ERR_INVALID, "dense mode needs every column full and <= %d rows per CTA", D_RMAX);

@@ -111,6 +111,7 @@ struct StepArgs {
     uint32_t *rslot;
     int *ovf_cnt;   // [16] overflow records received per CTA in the current step
     double *part_gh;  // dense kernel: per-CTA partial (g, h) of every bundle column [G][P][2]
+    int dense_tcap;   // dense kernel: floats per shared-memory tile buffer (two buffers)
     // sync
     unsigned long long *bar;
     int *status;
@@ -169,6 +170,24 @@ struct GridSync {
     unsigned long long target;
     __device__ __forceinline__ explicit GridSync(unsigned long long *c) : ctr(c), target(0) {}
     __device__ __forceinline__ void sync() { grid_sync(ctr, target); }
+    // split barrier: arrive (the CTA's prior writes released), independent work, then wait
+    __device__ __forceinline__ void arrive()
+    {
+        target += gridDim.x;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(ctr, 1ULL);
+        }
+    }
+    __device__ __forceinline__ void wait()
+    {
+        if (threadIdx.x == 0) {
+            while (ld_acquire(ctr) < target) {
+            }
+        }
+        __syncthreads();
+    }
 };
 
 struct ClusterSync {
@@ -206,16 +225,9 @@ __device__ __forceinline__ double2 coef_of(int loss, double z, int yi)
     const double yd = (double)yi;
     if (loss == LOSS_LOGISTIC) {
         const double m = yd * z;
-        double sm, snm;
-        if (m >= 0) {
-            const double e = exp(-m);
-            sm = 1.0 / (1.0 + e);
-            snm = e / (1.0 + e);
-        } else {
-            const double e = exp(m);
-            sm = e / (1.0 + e);
-            snm = 1.0 / (1.0 + e);
-        }
+        const double e = exp(-fabs(m));   // one exp: exp(-m) for m >= 0, exp(m) below
+        const double q1 = 1.0 / (1.0 + e), q2 = e / (1.0 + e);
+        const double sm = m >= 0 ? q1 : q2, snm = m >= 0 ? q2 : q1;
         return make_double2(-snm * yd, sm * snm);
     }
     const double b = 1.0 - yd * z;
@@ -235,18 +247,18 @@ __device__ __forceinline__ double phi_of(int loss, double m)
 
 // Per-sample loss change at step alpha (reading Z7).  For the logistic loss sigma(-m) is taken
 // from the cached factor: G = -sigma(-m) y  =>  sigma(-m) = -G y (exact).
+// The logistic branch is out of line: its log1p / expm1 / softplus bodies are large, and one shared
+// copy keeps the step kernels' hot instruction footprint small (they are latency-bound loops).
+__device__ __noinline__ double lr_loss_change(double m, double u, double snm)
+{
+    if (fabs(u) <= 1.0) return log1p(expm1(-u) * snm);
+    return softplus(-(m + u)) - softplus(-m);
+}
+
 __device__ __forceinline__ double loss_change(int loss, double z, int yi, double cg, double dx, double alpha)
 {
     const double yd = (double)yi;
-    if (loss == LOSS_LOGISTIC) {
-        const double m = yd * z;
-        const double u = alpha * (yd * dx);
-        if (fabs(u) <= 1.0) {
-            const double snm = -cg * yd;
-            return log1p(expm1(-u) * snm);
-        }
-        return softplus(-(m + u)) - softplus(-m);
-    }
+    if (loss == LOSS_LOGISTIC) return lr_loss_change(yd * z, alpha * (yd * dx), -cg * yd);
     const double b1 = 1.0 - yd * (z + alpha * dx);
     const double b0 = 1.0 - yd * z;
     const double p1 = b1 > 0 ? b1 * b1 : 0.0;

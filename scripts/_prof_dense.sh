@@ -1,7 +1,7 @@
 timeout 300 python scripts/probe_config.py ${1:-4} --modes 4 --outer 1 --profile > gpurun_out/profd.jsonl 2>&1
 python -c "
 import json
-N=['G partial gh', 'bar1', 'D finish', 'bar2', 'X dx', 'LS compute', 'bar3', 'decide']
+N=['prefetch issue', 'B1', 'D finish', 'B2', 'X dx', 'LS+spec', 'G', '-', 'tile wait', 'decide prev']
 for l in open('gpurun_out/profd.jsonl'):
     d=json.loads(l)
     if 'phase_cycles' not in d: print(l.strip()[:200]); continue
