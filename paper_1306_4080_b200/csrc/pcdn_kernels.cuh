@@ -154,7 +154,9 @@ __device__ __forceinline__ void grid_sync(unsigned long long *ctr, unsigned long
     if (threadIdx.x == 0) {
         __threadfence();          // release: the CTA's writes (ordered by the bar.sync above)
         atomicAdd(ctr, 1ULL);
+        const long long t0 = clock64();
         while (ld_acquire(ctr) < target) {   // acquire: no trailing fence needed
+            if (clock64() - t0 > 8000000000LL) __trap();   // a broken protocol: fail, do not hang
         }
     }
     __syncthreads();
@@ -183,7 +185,9 @@ struct GridSync {
     __device__ __forceinline__ void wait()
     {
         if (threadIdx.x == 0) {
+            const long long t0 = clock64();
             while (ld_acquire(ctr) < target) {
+                if (clock64() - t0 > 8000000000LL) __trap();
             }
         }
         __syncthreads();
@@ -196,6 +200,14 @@ struct ClusterSync {
     __device__ __forceinline__ void sync()
     {
         asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
+    __device__ __forceinline__ void arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+    // the trailing CTA barrier orders the work done between arrive and wait (by some warps of this
+    // CTA) before everything after the wait, as GridSync::wait does
+    __device__ __forceinline__ void wait()
+    {
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        __syncthreads();
     }
 };
 
@@ -538,7 +550,16 @@ __global__ void k_heavy_compact(const int64_t *__restrict__ hpos, int64_t ntot, 
 // ------------------------------------------------------------------------------------
 // a1..a5: the persistent bundle-step kernel
 // ------------------------------------------------------------------------------------
+// The heavy-column work of one CTA in one step: entries [e_lo, e_hi) of the step, heavy nonzero
+// offsets relative to hb0, NH in total, this CTA's range [lo_c, hi_c) and the entries [ce0, ce1)
+// overlapping it.  Static per launch, so it is computed a step ahead by an otherwise idle warp.
+struct HeavyPlan {
+    int64_t e_lo, e_hi, hb0, NH, ce0, ce1;
+    int64_t f_lo, nf;   // the step's full columns: entries [f_lo, f_lo + nf) of flist
+};
+
 struct StepSmem {
+    HeavyPlan plan[2];   // heavy-column plan of this and the next step (by step parity)
     // heavy-column rounds
     int64_t hst[NE_MAX + 1];
     double hg[NE_MAX][NW];
@@ -626,13 +647,6 @@ __device__ __forceinline__ int64_t warp_first(int64_t lo, int64_t hi, int lane, 
     return m == 0 ? hi : min(hi, lo + (int64_t)(__ffs(m) - 1));
 }
 
-// The heavy-column work of one CTA in one step: entries [e_lo, e_hi) of the step, heavy nonzero
-// offsets relative to hb0, NH in total, this CTA's range [lo_c, hi_c) and the entries [ce0, ce1)
-// overlapping it.  Static per launch, so it is computed a step ahead by an otherwise idle warp.
-struct HeavyPlan {
-    int64_t e_lo, e_hi, hb0, NH, ce0, ce1;
-    int64_t f_lo, nf;   // the step's full columns: entries [f_lo, f_lo + nf) of flist
-};
 
 __device__ __forceinline__ void heavy_plan_warp(const StepArgs &a, int64_t k0, int64_t k1, int c, int G, int lane,
                                                 HeavyPlan *out)
@@ -1098,6 +1112,8 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
         sm.F = ldcg(a.F);
         for (int i = 0; i < 4; i++) sm.cnt[i] = 0;
     }
+    if (warp == 1 && a.nsteps > 0) heavy_plan_warp(a, 0, min(a.P, a.ntot), c, G, lane, &sm.plan[0]);
+    __syncthreads();
     for (int64_t t = 0; t < a.nsteps; t++) {
         if (prof) tprev = clock64();
         const int64_t k0 = t * a.P;
@@ -1186,27 +1202,17 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
 
         PROF_MARK(8);
         // ---------------- phase A': heavy columns, nnz-balanced over all warps -----------
-        const int64_t e_lo = __ldg(&a.hpos[k0]), e_hi = __ldg(&a.hpos[k1]);
+        // the plan (entry ranges from 32-ary warp searches) was computed a step ahead, inside the
+        // previous step's final barrier
+        const HeavyPlan hpl = sm.plan[t & 1];
+        const int64_t e_lo = hpl.e_lo, e_hi = hpl.e_hi;
         if (e_hi > e_lo) {
-            const int64_t hb0 = __ldg(&a.hstart[e_lo]);
-            const int64_t NH = __ldg(&a.hstart[e_hi]) - hb0;
+            const int64_t hb0 = hpl.hb0;
+            const int64_t NH = hpl.NH;
             const int64_t lo_c = (int64_t)c * NH / G, hi_c = (int64_t)(c + 1) * NH / G;
-            if (warp == 0) {
-                // first entry ending after lo_c, first entry starting at or after hi_c: 32-ary
-                // warp searches (one dependent load round per 32x narrowing)
-                const int64_t ce0 = warp_first(e_lo, e_hi, lane,
-                                               [&](int64_t e) { return __ldg(&a.hstart[e + 1]) - hb0 > lo_c; });
-                int64_t ce1 = warp_first(ce0, e_hi, lane, [&](int64_t e) { return __ldg(&a.hstart[e]) - hb0 >= hi_c; });
-                if (!(hi_c > lo_c)) ce1 = ce0;
-                if (lane == 0) {
-                    sm.ce0 = ce0;
-                    sm.ce1 = ce1;
-                    sm.cross_e[0] = sm.cross_e[1] = -1;
-                }
-            }
-            __syncthreads();
+            if (tid == 0) sm.cross_e[0] = sm.cross_e[1] = -1;   // ordered by the rounds' barriers / sy
             PROF_MARK(9);
-            const int64_t ce0 = sm.ce0, ce1 = sm.ce1;
+            const int64_t ce0 = hpl.ce0, ce1 = hpl.ce1;
             const int64_t a_w = lo_c + (int64_t)warp * (hi_c - lo_c) / NW;
             const int64_t b_w = lo_c + (int64_t)(warp + 1) * (hi_c - lo_c) / NW;
             for (int64_t rb = ce0; rb < ce1; rb += NE_MAX) {
@@ -1354,8 +1360,8 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
 
         // ---------------- the step's full columns (dense_dx) -----------------------------
         DenseInfo di;
-        di.f_lo = __ldg(&a.fpos[k0]);
-        di.nf = __ldg(&a.fpos[k1]) - di.f_lo;
+        di.f_lo = hpl.f_lo;
+        di.nf = hpl.nf;
         di.any = false;
         if (di.nf > 0) {
             int any = 0;
@@ -1558,7 +1564,10 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
             sm.cnt[2] += (int64_t)ws.nT_tot;
             sm.cnt[3] += Pt;
         }
-        sy.sync();
+        sy.arrive();
+        // the next step's heavy plan, while the barrier completes
+        if (warp == NW - 1 && k1 < a.ntot) heavy_plan_warp(a, k1, min(k1 + a.P, a.ntot), c, G, lane, &sm.plan[(t + 1) & 1]);
+        sy.wait();
         PROF_MARK(7);
         if (bad) break;
     }
