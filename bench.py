@@ -319,7 +319,15 @@ def main():
             "traffic": traffic, "alg_bytes_per_launch": per_launch_bytes,
             "launch_ms": per_launch_ms, "peak_source": peak_src,
             "share_of_step": t_kernel / t_ms if t_ms else None,
-            "frac_of_nominal_8TBs": achieved / NOMINAL_HBM_GBS}
+            "frac_of_nominal_8TBs": achieved / NOMINAL_HBM_GBS,
+            "alg_model": "SURVEY.md 8(d): 16 B per bundle nonzero + 16 B per touched sample + 28 B per position"}
+    if kname == "k_step_dense":
+        # a fully dense problem needs no row indices and keeps the per-sample state on chip: the bytes
+        # it must move are the fp32 values (4 B per bundle nonzero) plus the same per-sample/position
+        # terms -- the 8(d) model counts 12 B per nonzero this layout does not move
+        min_bytes = (alg_bytes - 12 * nnz) / max(1, step_launches)
+        roof["dense_min_bytes_per_launch"] = min_bytes
+        roof["dense_min_frac"] = min_bytes / (per_launch_ms / 1e3) / 1e9 / peak
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and fstar is not None:

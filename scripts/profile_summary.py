@@ -2,7 +2,7 @@
 launch shares from the ncu launch list, key counters of the `ncu --set full` capture of k_step,
 the hottest source lines, and the bench JSON line.  Reads gpurun_out/<tag>/ (run here, no GPU).
 
-usage: python scripts/profile_summary.py <tag> [<ncu-rep name>]"""
+usage: python scripts/profile_summary.py <tag> [<ncu-rep name> [<launch csv> <summary name> <bench json>]]"""
 import csv
 import json
 import os
@@ -14,13 +14,16 @@ from collections import defaultdict
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag = sys.argv[1]
 rep_name = sys.argv[2] if len(sys.argv) > 2 else "prof_kstep"
+launch_name = sys.argv[3] if len(sys.argv) > 3 else "launches.csv"
+summary_name = sys.argv[4] if len(sys.argv) > 4 else "summary.md"
+bench_name = sys.argv[5] if len(sys.argv) > 5 else "bench.json"
 src = os.path.join(ROOT, "gpurun_out", tag)
 dst = os.path.join(ROOT, "profiles", tag)
 os.makedirs(dst, exist_ok=True)
 out = []
 
 # 1. launch list -> per-kernel share
-lc = os.path.join(src, "launches.csv")
+lc = os.path.join(src, launch_name)
 if os.path.exists(lc):
     hdr, agg = None, defaultdict(lambda: [0, 0.0])
     for r in csv.reader(open(lc, errors="replace")):
@@ -42,7 +45,7 @@ if os.path.exists(lc):
     out.append("| kernel | launches | total us | mean us | share |\n|---|---|---|---|---|")
     for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
         out.append(f"| `{k}` | {n} | {t:.1f} | {t / n:.2f} | {100 * t / tot:.1f}% |")
-    shutil.copy(lc, os.path.join(dst, "launches.csv"))
+    shutil.copy(lc, os.path.join(dst, launch_name))
 
 # 2. full capture counters
 rep = os.path.join(src, rep_name + ".ncu-rep")
@@ -72,11 +75,11 @@ if os.path.exists(rep):
     out.append("\n## Hottest source lines (warp-stall samples)\n\n```\n" + hot + "```")
 
 # 3. bench line
-bj = os.path.join(src, "bench.json")
+bj = os.path.join(src, bench_name)
 if os.path.exists(bj):
     lines = [l for l in open(bj) if l.startswith("{")]
     if lines:
-        open(os.path.join(dst, "bench.json"), "w").write(lines[-1])
+        open(os.path.join(dst, bench_name), "w").write(lines[-1])
         b = json.loads(lines[-1])
         out.insert(0, f"# GPU pass {tag}\n\nbench: value {b['value']:.4g} {b['unit']}, ms_per_step {b['ms_per_step']:.3f}, "
                       f"roofline frac {b['roofline']['frac']:.4g} ({b['roofline']['achieved']:.2f} GB/s), "
@@ -85,5 +88,5 @@ for extra in ("pytest_gpu.log", "smi.txt"):
     p = os.path.join(src, extra)
     if os.path.exists(p):
         shutil.copy(p, os.path.join(dst, extra))
-open(os.path.join(dst, "summary.md"), "w").write("\n".join(out) + "\n")
+open(os.path.join(dst, summary_name), "w").write("\n".join(out) + "\n")
 print("\n".join(out))
