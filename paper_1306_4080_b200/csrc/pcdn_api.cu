@@ -145,7 +145,8 @@ struct pcdn_ctx {
     int res_lg = 0, res_Bs = 0, res_cap = 0, res_cap_req = 0;
     size_t res_smem = 0;
     int last_mode = 0;
-    int heavy_len = 128;
+    int heavy_len = 0;     // user override (pcdn_set_launch); 0 = per launch mode (heavy_for_mode)
+    int heavy_eff = 128;   // the value in force for the current solve / step (lists and kernels)
     int num_sms = 0;
     size_t smem = 0;
     cudaStream_t stream = nullptr;
@@ -237,7 +238,7 @@ int build_heavy(pcdn_ctx *ctx, int64_t ntot, int buf, cudaStream_t st)
 int prep_outer(pcdn_ctx *ctx, uint64_t seed, int64_t k, int buf, cudaStream_t st)
 {
     const Lists &S = ctx->L.ls[buf];
-    k_perm<<<grid1d(ctx->n), 256, 0, st>>>(seed, k, ctx->n, ctx->s, ctx->col_ptr, ctx->heavy_len,
+    k_perm<<<grid1d(ctx->n), 256, 0, st>>>(seed, k, ctx->n, ctx->s, ctx->col_ptr, ctx->heavy_eff,
                                            ctx->at<int32_t>(S.order), ctx->at<int32_t>(S.flag),
                                            ctx->at<int32_t>(S.fflag), ctx->at<int4>(S.colinfo));
     ctx->launches++;
@@ -294,6 +295,7 @@ int reset_status(pcdn_ctx *ctx)
 
 // Launch the persistent step kernel over `nsteps` bundles of the positions in ctx->order.
 int choose_mode(const pcdn_ctx *ctx, int64_t P);
+int heavy_for_mode(const pcdn_ctx *ctx, int mode);
 
 int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps, int64_t trace_off, double *g_out,
                  double *h_out, double *d_out)
@@ -315,7 +317,7 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
     a.nu = ctx->nu;
     a.loss = ctx->loss;
     a.qmax = ctx->qmax;
-    a.heavy_len = ctx->heavy_len;
+    a.heavy_len = ctx->heavy_eff;
     a.w = ctx->at<double>(L.w);
     a.z = ctx->at<double>(L.z);
     a.coef = ctx->at<double2>(L.coef);
@@ -425,6 +427,15 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
 }
 
 // launch mode of the step kernel for bundles of size P (see pcdn_set_launch)
+// Columns longer than this are split nnz-balanced over every warp of the launch (heavy lists).
+// The HBM-state kernels (modes 1, 2) reduce columns up to CTA_LEN nonzeros inside one CTA (no grid
+// exchange); the cluster-resident kernel splits everything above a warp's 128.
+int heavy_for_mode(const pcdn_ctx *ctx, int mode)
+{
+    if (ctx->heavy_len > 0) return ctx->heavy_len;
+    return (mode == 1 || mode == 2) ? CTA_LEN : MED_LEN;
+}
+
 int choose_mode(const pcdn_ctx *ctx, int64_t P)
 {
     int mode = ctx->mode_req;
@@ -824,7 +835,7 @@ int pcdn_objective(pcdn_ctx *ctx, int recompute_from_w, double *F_out)
 int pcdn_permutation(pcdn_ctx *ctx, uint64_t seed, int64_t k, int32_t *out)
 {
     if (!ctx || !out || k < 0) return PCDN_ERR_INVALID;
-    k_perm<<<grid1d(ctx->n), 256, 0, ctx->stream>>>(seed, k, ctx->n, ctx->s, ctx->col_ptr, ctx->heavy_len, out,
+    k_perm<<<grid1d(ctx->n), 256, 0, ctx->stream>>>(seed, k, ctx->n, ctx->s, ctx->col_ptr, ctx->heavy_eff, out,
                                                      nullptr, nullptr, nullptr);
     ctx->launches++;
     CU(cudaGetLastError());
@@ -841,7 +852,8 @@ int pcdn_bundle_step(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, pcdn_step_
     if ((rc = reset_status(ctx))) return rc;
     CU(cudaMemsetAsync(ctx->at<int64_t>(L.counters), 0, sizeof(int64_t) * 8, ctx->stream));
     const Lists &S = L.ls[0];
-    k_bundle_prep<<<grid1d(P), 256, 0, ctx->stream>>>(bundle, P, ctx->n, ctx->s, ctx->col_ptr, ctx->heavy_len,
+    ctx->heavy_eff = heavy_for_mode(ctx, choose_mode(ctx, P));
+    k_bundle_prep<<<grid1d(P), 256, 0, ctx->stream>>>(bundle, P, ctx->n, ctx->s, ctx->col_ptr, ctx->heavy_eff,
                                                       ctx->at<int32_t>(S.order), ctx->at<int32_t>(S.flag),
                                                       ctx->at<int32_t>(S.fflag),
                                                       ctx->at<uint32_t>(L.seen), ctx->at<int>(L.status),
@@ -920,7 +932,9 @@ int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_
     CU(cudaEventRecord(ctx->ev[2], ctx->stream));
     // the cluster-resident step kernel occupies one cluster of SMs: the next outer iteration's
     // partition and lists are then built concurrently on the side stream (double-buffered sets)
-    const bool overlap = ctx->side != nullptr && choose_mode(ctx, P) == 3;
+    const int smode = choose_mode(ctx, P);
+    ctx->heavy_eff = heavy_for_mode(ctx, smode);
+    const bool overlap = ctx->side != nullptr && smode == 3;
     if (max_outer > 0 && (rc = prep_outer(ctx, seed, 0, 0, ctx->stream))) return rc;
     for (k = 0; k < max_outer; k++) {
         const int buf = k & 1;

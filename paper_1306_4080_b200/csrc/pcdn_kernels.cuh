@@ -31,6 +31,9 @@ constexpr int WREG = 4;            // bitmap words per thread kept in registers 
 constexpr int NE_MAX = 64;         // heavy entries handled per round inside one CTA
 constexpr int NREG = 8;            // rows with <= NREG records are folded by one thread
 constexpr int SHORT = 8;           // columns with <= SHORT nonzeros are reduced by one thread
+constexpr int MED_LEN = 128;       // ... with <= MED_LEN by one warp
+constexpr int CTA_LEN = 2048;      // ... with <= CTA_LEN by one CTA in the HBM-state kernels (default)
+constexpr int MIDQ = 256;          // per-CTA queue of such columns in one step
 constexpr int NHW = 4;             // warps that fold rows with > NREG records
 constexpr int HB = 1024;           // per-warp sort buffer for such rows
 constexpr int TSM = 4096;          // touched samples of a row block kept in shared memory
@@ -560,6 +563,8 @@ struct HeavyPlan {
 
 struct StepSmem {
     HeavyPlan plan[2];   // heavy-column plan of this and the next step (by step parity)
+    int32_t midq[MIDQ];  // positions of this CTA's CTA-level columns in the step
+    int nmid;
     // heavy-column rounds
     int64_t hst[NE_MAX + 1];
     double hg[NE_MAX][NW];
@@ -614,11 +619,55 @@ __device__ __forceinline__ void col_gh(const StepArgs &a, int64_t p0, int64_t p1
     hs = warp_sum(h);
 }
 
+// N records of one thread at once: all slot atomics (and segment offsets) in flight together,
+// then the stores -- one emit() after another would serialise on each atomic's return.
+template <int N>
+__device__ __forceinline__ void emit_batch(const StepArgs &a, const int32_t (&ri)[N], const double (&v)[N], int nv,
+                                           int32_t k)
+{
+    int32_t slot[N];
+    int64_t off[N];
+#pragma unroll
+    for (int e = 0; e < N; e++) {
+        slot[e] = 0;
+        off[e] = 0;
+        if (e < nv) {
+            slot[e] = atomicAdd(&a.cnt[ri[e]], 1);
+            off[e] = __ldg(&a.row_ptr[ri[e]]);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < N; e++) {
+        if (e < nv) {
+            Rec r;
+            r.k = k;
+            r.pad = 0;
+            r.v = v[e];
+            __stcg(reinterpret_cast<double2 *>(&a.rec[off[e] + slot[e]]), *reinterpret_cast<double2 *>(&r));
+            if (slot[e] == 0) atomicOr(&a.bits[ri[e] >> 5], 1u << (ri[e] & 31));
+        }
+    }
+}
+
 __device__ __forceinline__ void col_scatter(const StepArgs &a, int64_t p0, int64_t p1, int lane, int32_t kpos, double d)
 {
-    for (int64_t p = p0 + lane; p < p1; p += 32) {
-        const int32_t i = __ldg(&a.row_idx[p]);
-        emit(a, i, kpos, d * (double)__ldg(&a.val[p]));
+    constexpr int B = 4;   // records per lane per batch
+    for (int64_t pb = p0 + lane; pb < p1; pb += 32 * B) {
+        int32_t ri[B];
+        double v[B];
+        int nv = 0;
+#pragma unroll
+        for (int e = 0; e < B; e++) {
+            const int64_t p = pb + 32 * e;
+            ri[e] = 0;
+            v[e] = 0.0;
+            if (p < p1) {
+                ri[e] = __ldg(&a.row_idx[p]);
+                v[e] = d * (double)__ldg(&a.val[p]);
+                nv = e + 1;
+            }
+        }
+        emit_batch<B>(a, ri, v, nv, kpos);
     }
 }
 
@@ -1113,6 +1162,7 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
         for (int i = 0; i < 4; i++) sm.cnt[i] = 0;
     }
     if (warp == 1 && a.nsteps > 0) heavy_plan_warp(a, 0, min(a.P, a.ntot), c, G, lane, &sm.plan[0]);
+    if (tid == 0) sm.nmid = 0;
     __syncthreads();
     for (int64_t t = 0; t < a.nsteps; t++) {
         if (prof) tprev = clock64();
@@ -1169,12 +1219,25 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
                 }
                 if (a.d_out) a.d_out[kk - k0] = r.d;
                 if (r.d != 0.0 && len != a.s) {   // full columns are folded from CSC (dense_dx)
+                    double v[SHORT];
 #pragma unroll
-                    for (int e = 0; e < SHORT; e++)
-                        if (e < len) emit(a, ri[e], (int32_t)(kk - k0), r.d * (double)xv[e]);
+                    for (int e = 0; e < SHORT; e++) v[e] = r.d * (double)xv[e];
+                    emit_batch<SHORT>(a, ri, v, len, (int32_t)(kk - k0));
                 }
             }
-            unsigned med = __ballot_sync(0xffffffffu, len > SHORT && len <= a.heavy_len);
+            const int med_len = min(a.heavy_len, MED_LEN);
+            unsigned med = __ballot_sync(0xffffffffu, len > SHORT && len <= med_len);
+            // longer columns up to heavy_len: one CTA each, after the light loop (queued here)
+            const unsigned mid = __ballot_sync(0xffffffffu, len > med_len && len <= a.heavy_len);
+            if (mid) {
+                int base = 0;
+                if (lane == 0) base = atomicAdd(&sm.nmid, __popc(mid));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                const int slot = base + __popc(mid & ((1u << lane) - 1u));
+                if (((mid >> lane) & 1u) && slot < MIDQ) sm.midq[slot] = (int32_t)kk;
+                // beyond the queue (very large bundles on few CTAs): reduced by this warp below
+                med |= __ballot_sync(0xffffffffu, ((mid >> lane) & 1u) && slot >= MIDQ);
+            }
             while (med) {
                 const int src = __ffs(med) - 1;
                 med &= med - 1;
@@ -1200,6 +1263,48 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
             }
         }
 
+        // ---------------- CTA-level columns (med_len < length <= heavy_len) --------------------
+        // each queued column is reduced by all warps of this CTA (nnz split evenly, warp partials
+        // added in warp order: a fixed order), then scattered by the same split; no grid exchange
+        __syncthreads();
+        {
+            const int nm = min(sm.nmid, MIDQ);
+            for (int q = 0; q < nm; q++) {
+                const int64_t km = sm.midq[q];
+                const int4 ci = __ldg(&a.colinfo[km]);
+                const int64_t p0 = colinfo_p0(ci);
+                const int64_t ml = ci.y;
+                const int64_t w0 = p0 + (int64_t)warp * ml / NW, w1 = p0 + (int64_t)(warp + 1) * ml / NW;
+                double gs, hs;
+                col_gh(a, w0, w1, lane, gs, hs, ml == a.s ? p0 : -1);
+                if (lane == 0) {
+                    sm.hg[0][warp] = gs;
+                    sm.hh[0][warp] = hs;
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    double g = 0.0, h = 0.0;
+                    for (int w2 = 0; w2 < NW; w2++) {
+                        g += sm.hg[0][w2];
+                        h += sm.hh[0][w2];
+                    }
+                    const Dir r = finish_feature(a, g, h, ldcg(&a.w[ci.x]));
+                    a.dk[km - k0] = r.d;
+                    a.deltak[km - k0] = r.delta;
+                    if (a.g_out) {
+                        a.g_out[km - k0] = r.g;
+                        a.h_out[km - k0] = r.h;
+                    }
+                    if (a.d_out) a.d_out[km - k0] = r.d;
+                    sm.hd[0] = r.d;
+                }
+                __syncthreads();
+                const double d = sm.hd[0];
+                if (d != 0.0 && ml != a.s) col_scatter(a, w0, w1, lane, (int32_t)(km - k0), d);
+                __syncthreads();   // hg / hd reused by the next column
+            }
+            if (tid == 0) sm.nmid = 0;   // ordered before the next step's queue by this step's barriers
+        }
         PROF_MARK(8);
         // ---------------- phase A': heavy columns, nnz-balanced over all warps -----------
         // the plan (entry ranges from 32-ary warp searches) was computed a step ahead, inside the

@@ -339,3 +339,29 @@ def test_dense_kernel_line_search_misses(pk, loss, shape, ctas):
     # kernel (modes 1, 2 and 4 alike), so its trace is held to 1e-7.
     _compare_solve(gs, os_, s.w().cpu().numpy(), f"dense misses {shape} ctas={ctas}", ftrace_rtol=1e-7)
     s.close()
+
+
+@pytest.mark.parametrize("loss", [LOSS_LOGISTIC, LOSS_L2SVM])
+@pytest.mark.parametrize("mode,ctas", [(1, 0), (1, 3), (2, 0), (2, 5)])
+def test_step_parity_cta_columns(pk, loss, mode, ctas):
+    """HBM-state kernels with their default split length: columns of 129..~300 nonzeros are
+    reduced by one CTA each (queued per CTA, no grid exchange), shorter ones by a warp or a lane,
+    a full column by the dense d'x pass.  Steps from injected states and a short solve."""
+    prob = synth.tiny(4242, 600, 48, density=0.4, loss=loss, c=2.0, P=9, full_cols=1, empty_cols=2)
+    lens = np.diff(prob.col_ptr)
+    assert (lens > 128).sum() >= 20 and (lens <= 128).sum() >= 2
+    rng = np.random.default_rng(4242)
+    s = _solver(pk, prob, mode, ctas)
+    o = oracle.Oracle(prob)
+    ties = []
+    for rep in range(2):
+        w = _random_state(rng, prob.n, scale=0.2 * (rep + 1))
+        for B in _step_cases(prob, rng, sizes=[1, 9, 33, 48]):
+            s.set_w(w)
+            _compare_step(s.step(B), o.step(w, B), ties)
+    assert len(ties) <= 2, ties
+    s.reset()
+    gs = s.solve(9, seed=5, max_outer=4, trace=True)
+    os_ = o.solve(9, seed=5, max_outer=4)
+    _compare_solve(gs, os_, s.w().cpu().numpy(), f"cta columns mode={mode}")
+    s.close()
