@@ -1618,31 +1618,90 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
         prev_q = qacc < 0 ? QW : qacc;
 
         // ---------------- commit (a5): this CTA's samples and bundle share; clear marks -----
-        for (int64_t li = tid; li < nT; li += NT) {
-            // the heavy-row fold may have produced dx for the register row: take dxg then
-            const bool reg = li == tid && rr.has_dx;
-            const int32_t i = li == tid ? rr.i : Tl[li];
-            const double dx = reg ? rr.dx : ldcg(&a.dxg[i]);
-            if (qacc >= 0) {
-                const double zn = (li == tid ? rr.zi : ldcg(&a.z[i])) + alpha_acc * dx;
-                a.z[i] = zn;
-                a.coef[i] = coef_of(a.loss, zn, li == tid ? rr.yi : (int)a.y[i]);
+        // CB samples of a thread per round: all their loads in flight together (large steps touch
+        // ~10^4 samples per row block); the per-sample arithmetic is unchanged
+        constexpr int CB = 4;
+        if (nT <= NT) {   // small steps: at most one sample per thread
+            if (tid < nT) {
+                const bool reg = rr.has_dx;
+                const int32_t i = rr.i;
+                const double dx = reg ? rr.dx : ldcg(&a.dxg[i]);
+                if (qacc >= 0) {
+                    const double zn = rr.zi + alpha_acc * dx;
+                    a.z[i] = zn;
+                    a.coef[i] = coef_of(a.loss, zn, rr.yi);
+                }
+                a.cnt[i] = 0;
+                if (a.debug) {
+                    a.dbg_dx[i] = dx;
+                    a.dbg_mark[i] = 1;
+                }
             }
-            a.cnt[i] = 0;
-            if (a.debug) {
-                a.dbg_dx[i] = dx;
-                a.dbg_mark[i] = 1;
+        } else
+        for (int64_t lb = tid; lb < nT; lb += (int64_t)NT * CB) {
+            int32_t ii[CB];
+            double dxv[CB], zv[CB];
+            int yv[CB];
+#pragma unroll
+            for (int e = 0; e < CB; e++) {
+                const int64_t li = lb + (int64_t)e * NT;
+                ii[e] = li < nT ? (li == tid ? rr.i : Tl[li]) : -1;
+            }
+#pragma unroll
+            for (int e = 0; e < CB; e++) {
+                const int64_t li = lb + (int64_t)e * NT;
+                dxv[e] = 0.0;
+                zv[e] = 0.0;
+                yv[e] = 1;
+                if (ii[e] >= 0) {
+                    // the heavy-row fold may have produced dx for the register row: take dxg then
+                    const bool reg = li == tid && rr.has_dx;
+                    dxv[e] = reg ? rr.dx : ldcg(&a.dxg[ii[e]]);
+                    if (qacc >= 0) {
+                        zv[e] = li == tid ? rr.zi : ldcg(&a.z[ii[e]]);
+                        yv[e] = li == tid ? rr.yi : (int)a.y[ii[e]];
+                    }
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < CB; e++) {
+                const int32_t i = ii[e];
+                if (i < 0) continue;
+                if (qacc >= 0) {
+                    const double zn = zv[e] + alpha_acc * dxv[e];
+                    a.z[i] = zn;
+                    a.coef[i] = coef_of(a.loss, zn, yv[e]);
+                }
+                a.cnt[i] = 0;
+                if (a.debug) {
+                    a.dbg_dx[i] = dxv[e];
+                    a.dbg_mark[i] = 1;
+                }
             }
         }
         for (int64_t wi = wb + tid; wi < we; wi += NT) a.bits[wi] = 0u;
         if (qacc >= 0) {
-            for (int64_t kk = pb0 + tid; kk < pb1; kk += NT) {
-                if (kk == sh.kk) {
-                    a.w[sh.j] = sh.wj + alpha_acc * sh.d;
-                } else {
-                    const int32_t j = __ldg(&a.order[kk]);
-                    a.w[j] = ldcg(&a.w[j]) + alpha_acc * ldcg(&a.dk[kk - k0]);
+            for (int64_t kb = pb0 + tid; kb < pb1; kb += (int64_t)NT * CB) {
+                int32_t jj[CB];
+                double wv[CB], dv[CB];
+#pragma unroll
+                for (int e = 0; e < CB; e++) {
+                    const int64_t kk = kb + (int64_t)e * NT;
+                    jj[e] = kk < pb1 ? (kk == sh.kk ? sh.j : __ldg(&a.order[kk])) : -1;
                 }
+#pragma unroll
+                for (int e = 0; e < CB; e++) {
+                    const int64_t kk = kb + (int64_t)e * NT;
+                    wv[e] = 0.0;
+                    dv[e] = 0.0;
+                    if (jj[e] >= 0) {
+                        wv[e] = kk == sh.kk ? sh.wj : ldcg(&a.w[jj[e]]);
+                        dv[e] = kk == sh.kk ? sh.d : ldcg(&a.dk[kk - k0]);
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < CB; e++)
+                    if (jj[e] >= 0) a.w[jj[e]] = wv[e] + alpha_acc * dv[e];
             }
         }
         PROF_MARK(6);
