@@ -158,8 +158,19 @@ int pcdn_set_debug(pcdn_ctx *ctx, int on);
  * 3 cluster-resident: one cluster of `ctas` CTAs (power of two <= 16; 0 = largest that fits)
  *   holding the per-sample state and the step's d'x records in distributed shared memory
  *   (DESIGN.md 7); PCDN_ERR_INVALID if the samples do not fit.
- * heavy_len: column length above which a column is split across warps/CTAs (0 = keep; 128 default). */
+ * 4 dense row-block kernel (every column full).
+ * heavy_len: column length above which a column is split nnz-balanced across the warps of the
+ * whole launch (0 = keep the current setting; default 0 = per mode: 2048 for modes 1-2, where
+ * columns of 129..2048 nonzeros are reduced by one CTA, 128 for mode 3). */
 int pcdn_set_launch(pcdn_ctx *ctx, int mode, int ctas, int heavy_len);
+
+/* HBM-state kernels (modes 1, 2): keep the per-sample state (z, coef, record counts, touched
+ * bitmap, d'x; one contiguous workspace window) L2-resident with a persisting access-policy window
+ * on the step-kernel launches (default on).  The first such launch sets the device's persisting-L2
+ * limit (cudaLimitPersistingL2CacheSize) to min(device maximum, window bytes) once; if the device
+ * refuses, the knob turns itself off.  Results are unchanged (a cache policy only).
+ * Returns PCDN_ERR_INVALID for a null context. */
+int pcdn_set_l2_persist(pcdn_ctx *ctx, int on);
 
 /* Testing knob of mode 3: cap the records a CTA keeps in shared memory per step (0 = as many as
  * fit); the rest spill to the CTA's HBM overflow region.  Results are unchanged. */

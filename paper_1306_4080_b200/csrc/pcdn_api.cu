@@ -4,6 +4,7 @@
 // of pcdn_kernels.cuh on the context stream; every step of the path runs on the device.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -55,9 +56,11 @@ Layout make_layout(int64_t s, int64_t n, int64_t nnz)
     L.coef = take(sizeof(double2) * s);
     L.cnt = take(sizeof(int32_t) * s);
     L.bits = take(sizeof(uint32_t) * nw);
-    L.rec = take(sizeof(Rec) * nnz);
     L.dxg = take(sizeof(double) * s);
     L.tlist = take(sizeof(int32_t) * nw * 32);
+    // [z, tlist end) is the per-sample state the HBM-state kernels touch at random: one contiguous
+    // window, kept L2-resident with a persisting access policy (launch_steps)
+    L.rec = take(sizeof(Rec) * nnz);
     for (int b = 0; b < 2; b++) {
         Lists &S = L.ls[b];
         S.order = take(sizeof(int32_t) * n);
@@ -147,6 +150,9 @@ struct pcdn_ctx {
     int last_mode = 0;
     int heavy_len = 0;     // user override (pcdn_set_launch); 0 = per launch mode (heavy_for_mode)
     int heavy_eff = 128;   // the value in force for the current solve / step (lists and kernels)
+    int l2_want = 1;       // pcdn_set_l2_persist
+    size_t l2_persist = 0; // bytes of L2 set aside for the per-sample state window (0 = off)
+    size_t l2_window = 0;  // max access-policy window size of the device
     int num_sms = 0;
     size_t smem = 0;
     cudaStream_t stream = nullptr;
@@ -403,24 +409,57 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
         cfg.attrs = at;
         cfg.numAttrs = 1;
         CU(cudaLaunchKernelEx(&cfg, ctx->loss == LOSS_LOGISTIC ? k_step_res<LOSS_LOGISTIC> : k_step_res<LOSS_L2SVM>, a));
-    } else if (mode == 1) {
+    } else {
+        // HBM-state kernels: the per-sample state (z, coef, cnt, bits, dxg, tlist) is gathered and
+        // scattered at random every step while CSC and records stream through L2; a persisting
+        // access-policy window keeps the state resident
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(ctx->Gc);
+        cfg.gridDim = dim3(mode == 1 ? ctx->Gc : ctx->G);
         cfg.blockDim = dim3(NT);
         cfg.dynamicSmemBytes = ctx->smem;
         cfg.stream = ctx->stream;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = ctx->Gc;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
+        cudaLaunchAttribute at[2];
+        int na = 0;
+        if (mode == 1) {
+            at[na].id = cudaLaunchAttributeClusterDimension;
+            at[na].val.clusterDim.x = ctx->Gc;
+            at[na].val.clusterDim.y = 1;
+            at[na].val.clusterDim.z = 1;
+            na++;
+        } else {
+            at[na].id = cudaLaunchAttributeCooperative;
+            at[na].val.cooperative = 1;
+            na++;
+        }
+        if (ctx->l2_want && ctx->l2_persist == 0) {
+            // first HBM-state launch: set aside L2 for the window (device limit, once)
+            int dev = 0, maxp = 0, maxw = 0;
+            CU(cudaGetDevice(&dev));
+            CU(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
+            CU(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+            const size_t want = std::min((size_t)maxp, L.rec - L.z);
+            if (want > 0 && maxw > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess) {
+                ctx->l2_persist = want;
+                ctx->l2_window = (size_t)maxw;
+            } else {
+                cudaGetLastError();
+                ctx->l2_want = 0;
+            }
+        }
+        if (ctx->l2_want && ctx->l2_persist > 0) {
+            const size_t wbytes = std::min(L.rec - L.z, ctx->l2_window);
+            at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+            at[na].val.accessPolicyWindow.base_ptr = (void *)(ctx->base + L.z);
+            at[na].val.accessPolicyWindow.num_bytes = wbytes;
+            at[na].val.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)ctx->l2_persist / (double)wbytes);
+            at[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            at[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            na++;
+        }
         cfg.attrs = at;
-        cfg.numAttrs = 1;
-        CU(cudaLaunchKernelEx(&cfg, k_step<ClusterSync>, a));
-    } else {
-        void *args[] = {&a};
-        CU(cudaLaunchCooperativeKernel((const void *)k_step<GridSync>, dim3(ctx->G), dim3(NT), args, ctx->smem,
-                                       ctx->stream));
+        cfg.numAttrs = na;
+        if (mode == 1) CU(cudaLaunchKernelEx(&cfg, k_step<ClusterSync>, a));
+        else CU(cudaLaunchKernelEx(&cfg, k_step<GridSync>, a));
     }
     ctx->launches++;
     return PCDN_OK;
@@ -720,6 +759,14 @@ int pcdn_set_launch(pcdn_ctx *ctx, int mode, int ctas, int heavy_len)
     ctx->G_req = ctas;
     if (heavy_len > 0) ctx->heavy_len = heavy_len;
     return configure_launch(ctx);
+}
+
+int pcdn_set_l2_persist(pcdn_ctx *ctx, int on)
+{
+    if (!ctx) return PCDN_ERR_INVALID;
+    ctx->l2_want = on ? 1 : 0;
+    if (on && ctx->l2_persist == 0) ctx->l2_want = 1;
+    return PCDN_OK;
 }
 
 int pcdn_set_resident_cap(pcdn_ctx *ctx, int cap)

@@ -23,11 +23,13 @@ ap.add_argument("--modes", default="0")
 ap.add_argument("--outer", type=int, default=1)
 ap.add_argument("--profile", action="store_true")
 ap.add_argument("--heavy", type=int, default=0, help="heavy_len launch knob (0 = keep)")
+ap.add_argument("--l2", type=int, default=1, help="persisting-L2 window of the HBM-state kernels (pcdn_set_l2_persist)")
 args = ap.parse_args()
 t0 = time.time()
 prob = synth.config(args.cfg, loss=args.loss)
 print(json.dumps({"generated_s": round(time.time() - t0, 1), "s": prob.s, "n": prob.n, "nnz": prob.nnz}), flush=True)
 s = pk.Solver(prob)
+pk.pcdn_set_l2_persist(s.ctx, args.l2)
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
 Ps = [int(x) for x in args.P.split(",") if x] or [prob.P]
