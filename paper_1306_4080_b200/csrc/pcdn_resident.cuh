@@ -1198,7 +1198,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         RTL(R, 14);
         // the step's touched owned samples, ascending (a fixed thread assignment for the fold and
         // the line search): every owned sample when a full column moved, else the bitmap compacted
-        // by warp 0
+        // by a CTA-wide scan
         {
             uint16_t *tlc = R.tls + (size_t)R.cb * R.Bs;
             const int nwords = (R.Bsc + 31) >> 5;
@@ -1206,28 +1206,29 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
                 for (int e = tid; e < R.Bsc; e += NT) tlc[e] = (uint16_t)e;
                 for (int w = tid; w < nwords; w += NT) fx.tb[w] = 0u;
                 if (tid == 0) fx.ntl[R.cb] = R.Bsc;
-            } else if (warp == 0) {
-                const int wpl = (nwords + 31) >> 5;
-                const int w0 = lane * wpl, w1 = min(nwords, w0 + wpl);
-                int cnt = 0;
-                for (int w = w0; w < w1; w++) cnt += __popc(fx.tb[w]);
+            } else {   // one bitmap word per thread (nwords <= R_TBW = NT): a CTA-wide scan
+                const uint32_t m0 = tid < nwords ? fx.tb[tid] : 0u;
+                const int cnt = __popc(m0);
                 int incl = cnt;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     const int v = __shfl_up_sync(0xffffffffu, incl, o);
                     if (lane >= o) incl += v;
                 }
-                int pos = incl - cnt;
-                for (int w = w0; w < w1; w++) {
-                    uint32_t m = fx.tb[w];
-                    fx.tb[w] = 0u;
-                    while (m) {
-                        const int b = __ffs(m) - 1;
-                        m &= m - 1;
-                        tlc[pos++] = (uint16_t)(w * 32 + b);
-                    }
+                if (lane == 31) fx.scan_w[warp] = (unsigned long long)incl;
+                __syncthreads();
+                const int sw = lane < NW ? (int)fx.scan_w[lane] : 0;
+                const int off = __reduce_add_sync(0xffffffffu, lane < warp ? sw : 0);
+                int pos = off + incl - cnt;
+                uint32_t m = m0;
+                while (m) {
+                    const int b = __ffs(m) - 1;
+                    m &= m - 1;
+                    tlc[pos++] = (uint16_t)(tid * 32 + b);
                 }
-                if (lane == 31) fx.ntl[R.cb] = incl;
+                if (tid < nwords) fx.tb[tid] = 0u;
+                const int tot = __reduce_add_sync(0xffffffffu, sw);
+                if (tid == 0) fx.ntl[R.cb] = tot;
             }
             RTL(R, 15);
             __syncthreads();
