@@ -35,7 +35,7 @@ class _Prob(C.Structure):
                 ("col_ptr", C.c_void_p), ("row_idx", C.c_void_p), ("val", C.c_void_p),
                 ("y", C.c_void_p), ("c", C.c_double), ("loss", C.c_int32), ("qmax", C.c_int32),
                 ("sigma", C.c_double), ("beta", C.c_double), ("gamma", C.c_double),
-                ("nu", C.c_double)]
+                ("nu", C.c_double), ("mu", C.c_double)]
 
 
 class _State(C.Structure):
@@ -82,7 +82,7 @@ def lib():
         L.ora_compute_z.restype = None
         L.ora_compute_z.argtypes = [C.POINTER(_Prob), C.c_void_p, C.c_void_p]
         L.ora_gh_all.restype = None
-        L.ora_gh_all.argtypes = [C.POINTER(_Prob), C.c_void_p, C.c_void_p, C.c_void_p]
+        L.ora_gh_all.argtypes = [C.POINTER(_Prob), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.ora_newton_dir.restype = C.c_double
         L.ora_newton_dir.argtypes = [C.c_double, C.c_double, C.c_double]
         L.ora_bundle_step.restype = C.c_int
@@ -143,7 +143,8 @@ def loss_change(loss: int, z: float, y: int, dx: float, alpha: float) -> float:
 class Oracle:
     """Oracle bound to one problem (any object with the synth.Problem fields)."""
 
-    def __init__(self, prob, sigma=0.01, beta=0.5, gamma=0.0, nu=1e-12, qmax=50):
+    def __init__(self, prob, sigma=0.01, beta=0.5, gamma=0.0, nu=1e-12, qmax=50, mu=0.0):
+        """mu: elastic-net weight of (mu/2)||w||^2 (reading Z25; 0 = the paper's problem)."""
         self.p = prob
         self.col_ptr = np.ascontiguousarray(prob.col_ptr, dtype=np.int64)
         self.row_idx = np.ascontiguousarray(prob.row_idx, dtype=np.int32)
@@ -151,7 +152,7 @@ class Oracle:
         self.y = np.ascontiguousarray(prob.y, dtype=np.int8)
         self.s, self.n = int(prob.s), int(prob.n)
         self.pb = _Prob(self.s, self.n, _p(self.col_ptr), _p(self.row_idx), _p(self.val), _p(self.y),
-                        float(prob.c), int(prob.loss), int(qmax), sigma, beta, gamma, nu)
+                        float(prob.c), int(prob.loss), int(qmax), sigma, beta, gamma, nu, float(mu))
 
     # --- plain evaluations ---
     def compute_z(self, w):
@@ -167,10 +168,11 @@ class Oracle:
         return lib().ora_objective(C.byref(self.pb), _p(z), _p(w))
 
     def gh(self, w):
+        w = np.ascontiguousarray(w, dtype=np.float64)
         z = self.compute_z(w)
         g = np.empty(self.n)
         h = np.empty(self.n)
-        lib().ora_gh_all(C.byref(self.pb), _p(z), _p(g), _p(h))
+        lib().ora_gh_all(C.byref(self.pb), _p(z), _p(w), _p(g), _p(h))
         return g, h
 
     def min_norm_subgrad(self, w):

@@ -21,6 +21,10 @@
  *   App.A.2 L2-SVM generalized Hessian, nu = 1e-12
  *   Eq.14 relative function value difference
  *   Alg.1 CDN (separately coded, for the P=1 reduction)
+ *   Elastic net (NEXT #4; "easily extended to ... elastic net"): the separable
+ *   term ||w||_1 + (mu/2)||w||_2^2, mu >= 0 (mu = 0: the paper's problem).  Reading Z25: the
+ *   smooth part becomes L(w) + (mu/2)||w||^2, so g_j, h_j gain mu w_j, mu (Eq.5 unchanged in form),
+ *   Delta (Eq.7) uses them, and the line search's L1 term gains (mu/2)((w_j+a d_j)^2 - w_j^2).
  * Readings where the paper is silent/ambiguous are DESIGN.md Z1..Z24 (cited inline).
  *
  * Parity status: every function here is pinned by tests/test_oracle_pins.py against
@@ -54,6 +58,7 @@ typedef struct {
     int32_t loss;             /* ORA_LOSS_* */
     int32_t qmax;             /* line-search cap (Z10) */
     double sigma, beta, gamma, nu;   /* Armijo constants, nu */
+    double mu;                /* elastic-net weight (reading Z25; 0 = the paper's problem) */
 } ora_prob;
 
 /* ------------------------------------------------------------------------------ */
@@ -163,10 +168,13 @@ void ora_GH(int loss, double z, int y, double *G, double *H)
 /* Eq.1 evaluated from scratch from (z = Xw, w) (a6, Z19, Z23). */
 double ora_objective(const ora_prob *pb, const double *z, const double *w)
 {
-    double loss = 0.0, l1 = 0.0;
+    double loss = 0.0, l1 = 0.0, l2 = 0.0;
     for (int64_t i = 0; i < pb->s; i++) loss += ora_phi(pb->loss, (double)pb->y[i] * z[i]);
-    for (int64_t j = 0; j < pb->n; j++) l1 += fabs(w[j]);
-    return pb->c * loss + l1;
+    for (int64_t j = 0; j < pb->n; j++) {
+        l1 += fabs(w[j]);
+        l2 += w[j] * w[j];
+    }
+    return pb->c * loss + l1 + 0.5 * pb->mu * l2;   /* Eq.1 (+ the elastic-net term, Z25) */
 }
 
 /* z = X w, column by column in ascending j (each z_i accumulates in ascending j). */
@@ -179,8 +187,9 @@ void ora_compute_z(const ora_prob *pb, const double *w, double *z)
 }
 
 /* g_j, h_j for one feature (Eq.13 / App.A.2), with the nu floor of reading Z4:
- * h <- max(h, nu) after the factor c, for both losses.  Also returns sum |terms|. */
-static void gh_one(const ora_prob *pb, const double *z, int64_t j,
+ * h <- max(h, nu) after the factor c (and the elastic-net terms mu w_j, mu of Z25), for both
+ * losses.  Also returns sum |terms|.  w may be NULL when mu == 0. */
+static void gh_one(const ora_prob *pb, const double *z, const double *w, int64_t j,
                    double *g, double *h, double *gabs, double *habs)
 {
     double gs = 0.0, hs = 0.0, ga = 0.0, ha = 0.0;
@@ -193,16 +202,17 @@ static void gh_one(const ora_prob *pb, const double *z, int64_t j,
         ga += fabs(x * G);
         ha += fabs((x * x) * H);
     }
-    *g = pb->c * gs;
-    *h = pb->c * hs;
+    const double wj = w ? w[j] : 0.0;
+    *g = pb->c * gs + pb->mu * wj;
+    *h = pb->c * hs + pb->mu;
     if (!(*h > pb->nu)) *h = pb->nu;
-    if (gabs) *gabs = pb->c * ga;
-    if (habs) *habs = pb->c * ha;
+    if (gabs) *gabs = pb->c * ga + fabs(pb->mu * wj);
+    if (habs) *habs = pb->c * ha + pb->mu;
 }
 
-void ora_gh_all(const ora_prob *pb, const double *z, double *g, double *h)
+void ora_gh_all(const ora_prob *pb, const double *z, const double *w, double *g, double *h)
 {
-    for (int64_t j = 0; j < pb->n; j++) gh_one(pb, z, j, &g[j], &h[j], NULL, NULL);
+    for (int64_t j = 0; j < pb->n; j++) gh_one(pb, z, w, j, &g[j], &h[j], NULL, NULL);
 }
 
 /* Eq.5; branches tested in printed order (reading Z17). */
@@ -287,7 +297,7 @@ int ora_bundle_step(const ora_prob *pb, ora_state *st, const int32_t *bundle, in
     for (int64_t kk = 0; kk < P; kk++) {
         int64_t j = bundle[kk];
         double ga, ha;
-        gh_one(pb, st->z, j, &g[kk], &h[kk], &ga, &ha);
+        gh_one(pb, st->z, st->w, j, &g[kk], &h[kk], &ga, &ha);
         double wj = st->w[j];
         d[kk] = ora_newton_dir(g[kk], h[kk], wj);
         double hw = h[kk] * wj;
@@ -344,7 +354,9 @@ int ora_bundle_step(const ora_prob *pb, ora_state *st, const int32_t *bundle, in
             double L1 = 0.0, Ls = 0.0, L1a = 0.0, Lsa = 0.0;
             for (int64_t kk = 0; kk < P; kk++) {
                 double wj = st->w[bundle[kk]];
-                double t = fabs(wj + alpha * d[kk]) - fabs(wj);
+                /* separable term change: |w+ad| - |w| + (mu/2)((w+ad)^2 - w^2), the latter as
+                 * mu a d (w + a d / 2) (reading Z25) */
+                double t = fabs(wj + alpha * d[kk]) - fabs(wj) + pb->mu * alpha * d[kk] * (wj + 0.5 * alpha * d[kk]);
                 L1 += t;
                 L1a += fabs(t);
             }
@@ -559,10 +571,10 @@ int ora_cdn(const ora_prob *pb, double *w, double *z, uint64_t seed, int32_t max
                     hl += 2.0 * x * x;
                 }
             }
-            gl *= pb->c;
-            hl *= pb->c;
-            if (!(hl > pb->nu)) hl = pb->nu;
             double wj = w[j], dj;
+            gl = gl * pb->c + pb->mu * wj;                     /* Z25 */
+            hl = hl * pb->c + pb->mu;
+            if (!(hl > pb->nu)) hl = pb->nu;
             if (gl + 1.0 <= hl * wj) dj = -(gl + 1.0) / hl;    /* Eq.5 */
             else if (gl - 1.0 >= hl * wj) dj = -(gl - 1.0) / hl;
             else dj = -wj;
@@ -577,7 +589,8 @@ int ora_cdn(const ora_prob *pb, double *w, double *z, uint64_t seed, int32_t max
                     double znew = z[i] + alpha * dj * (double)pb->val[p];
                     chg += ora_phi(pb->loss, yd * znew) - ora_phi(pb->loss, yd * z[i]);
                 }
-                double lhs = pb->c * chg + fabs(wj + alpha * dj) - fabs(wj);
+                double wn = wj + alpha * dj;
+                double lhs = pb->c * chg + fabs(wn) - fabs(wj) + 0.5 * pb->mu * (wn * wn - wj * wj);
                 if (lhs <= pb->sigma * alpha * Delta) {
                     ok = 1;
                     break;
@@ -610,7 +623,7 @@ double ora_min_norm_subgrad(const ora_prob *pb, const double *w, const double *z
             ora_GH(pb->loss, z[i], pb->y[i], &G, &H);
             gs += (double)pb->val[p] * G;
         }
-        double gj = pb->c * gs, v;
+        double gj = pb->c * gs + pb->mu * w[j], v;
         if (w[j] > 0) v = gj + 1.0;
         else if (w[j] < 0) v = gj - 1.0;
         else v = (gj > 1.0) ? gj - 1.0 : (gj < -1.0 ? gj + 1.0 : 0.0);

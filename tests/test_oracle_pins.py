@@ -536,3 +536,125 @@ def test_no_null_steps_before_convergence(oracle_mod, loss):
     fstar = o.solve(5, max_outer=600, seed=2)["F"]
     r = o.solve(5, eps=1e-9, fstar=fstar, max_outer=600, seed=2)
     assert r["rc"] == 0 and r["null_steps"] == 0
+
+
+# ------------------------------------------------------------------ elastic net (NEXT #4, Z25)
+# F(w) = c sum_i phi_i + ||w||_1 + (mu/2)||w||_2^2 (PCDN "can be easily
+# extended to ... elastic net").  Every expected value below comes from numpy / scipy / a closed
+# form written here, never from the oracle.
+MUS = [0.5, 3.0]
+
+
+def np_F_en(prob, w, mu, X=None):
+    return np_F(prob, w, X) + 0.5 * mu * float(np.dot(w, w))
+
+
+@pytest.mark.parametrize("loss", LOSSES)
+@pytest.mark.parametrize("mu", MUS)
+def test_elastic_objective_and_gradient(oracle_mod, loss, mu):
+    """F with the (mu/2)||w||^2 term against numpy; g_j = d(L + mu/2 ||w||^2)/dw_j by central
+    differences, h_j = the LR Hessian diagonal + mu (SVM: 2c sum x^2 over I(w) + mu)."""
+    rng = np.random.default_rng(71)
+    p = synth.tiny(71, 25, 9, density=0.5, loss=loss, c=1.3)
+    X = p.dense()
+    o = oracle_mod.Oracle(p, mu=mu)
+    for _ in range(4):
+        w = rng.normal(size=p.n) * 0.4
+        assert math.isclose(o.objective(w), np_F_en(p, w, mu, X), rel_tol=1e-12)
+        m = p.y * (X @ w)
+        if loss == LOSS_L2SVM and np.min(np.abs(1 - m)) < 1e-3:
+            continue
+        g, h = o.gh(w)
+        eps = 1e-6
+        sm = lambda v: np_loss(p, v, X) + 0.5 * mu * float(np.dot(v, v))
+        fd = np.array([(sm(w + eps * e) - sm(w - eps * e)) / (2 * eps) for e in np.eye(p.n)])
+        np.testing.assert_allclose(g, fd, rtol=1e-6, atol=1e-7)
+        if loss == LOSS_LOGISTIC:
+            s_ = 1.0 / (1.0 + np.exp(-m))
+            hd = p.c * ((X * X).T @ (s_ * (1 - s_))) + mu
+        else:
+            hd = p.c * ((X * X).T @ (2.0 * (1 - m > 0))) + mu
+        np.testing.assert_allclose(h, hd, rtol=1e-12)
+
+
+def test_elastic_one_dimensional_closed_forms(oracle_mod):
+    """s=1, x=1, y=+1.  SVM: F = c(1-w)^2 + |w| + mu w^2/2 is quadratic on (0, 1):
+    w* = (2c-1)/(2c+mu), reached in one Newton step.  LR: F'(w) = -c/(1+e^w) + 1 + mu w = 0 on
+    w > 0, solved here by scipy's brentq (independent of the oracle)."""
+    from scipy.optimize import brentq
+    for c, mu in ((1.0, 0.5), (3.0, 2.0), (10.0, 0.1)):
+        p = synth.from_dense([[1.0]], [1], c=c, loss=LOSS_L2SVM)
+        r = oracle_mod.Oracle(p, mu=mu).solve(1, max_outer=1)
+        ws = (2 * c - 1) / (2 * c + mu)
+        assert math.isclose(r["w"][0], ws, rel_tol=1e-14)
+        assert math.isclose(r["F"], c * (1 - ws) ** 2 + ws + 0.5 * mu * ws * ws, rel_tol=1e-14)
+    for c, mu in ((4.0, 0.5), (20.0, 3.0)):
+        p = synth.from_dense([[1.0]], [1], c=c, loss=LOSS_LOGISTIC)
+        r = oracle_mod.Oracle(p, mu=mu).solve(1, max_outer=200)
+        ws = brentq(lambda v: -c / (1 + math.exp(v)) + 1 + mu * v, 1e-12, 50.0, xtol=1e-15)
+        assert abs(r["w"][0] - ws) < 1e-10
+        assert math.isclose(r["F"], c * math.log1p(math.exp(-ws)) + ws + 0.5 * mu * ws * ws, rel_tol=1e-13)
+
+
+@pytest.mark.parametrize("loss", LOSSES)
+@pytest.mark.parametrize("mu", MUS)
+def test_elastic_line_search_incremental_vs_direct(oracle_mod, loss, mu):
+    """The line search's elastic-net term (Eq.12 from retained quantities + mu a d (w + a d/2))
+    against the direct F difference: same accepted q, LHS within rounding, and the accepted q
+    re-checked with numpy's F."""
+    rng = np.random.default_rng(91)
+    for seed in range(12):
+        Xc = rng.normal(size=(30, 2)) @ rng.normal(size=(2, 14)) + 0.05 * rng.normal(size=(30, 14))
+        p = synth.from_dense(Xc, np.where(rng.random(30) < 0.5, 1, -1), c=30.0, loss=loss)
+        X = p.dense()
+        o = oracle_mod.Oracle(p, mu=mu)
+        w = rng.normal(size=p.n) * 0.5
+        B = rng.choice(p.n, size=int(rng.integers(1, p.n + 1)), replace=False)
+        r0 = o.step(w, B, mode=0)
+        r1 = o.step(w, B, mode=1)
+        assert r0["q"] == r1["q"]
+        assert math.isclose(r0["lhs"], r1["lhs"], rel_tol=1e-8, abs_tol=1e-10 * (1 + r0["lhs_abs"]))
+        a = 0.5 ** r0["q"]
+        wn = w.copy()
+        wn[B] += a * r0["d"]
+        assert np_F_en(p, wn, mu, X) - np_F_en(p, w, mu, X) <= 0.01 * a * r0["Delta"] + 1e-10 * (1 + abs(r0["lhs"]))
+
+
+def _scipy_fstar_en(p, mu):
+    """L-BFGS-B on w = u - v, u, v >= 0 with the (mu/2)||u - v||^2 term."""
+    from scipy.optimize import minimize
+    X = p.dense()
+    n = p.n
+
+    def f(uv):
+        w = uv[:n] - uv[n:]
+        gl = np_grad(p, w, X) + mu * w
+        return np_loss(p, w, X) + np.sum(uv) + 0.5 * mu * float(np.dot(w, w)), np.concatenate([gl + 1.0, -gl + 1.0])
+
+    r = minimize(f, np.zeros(2 * n), jac=True, method="L-BFGS-B", bounds=[(0, None)] * (2 * n),
+                 options=dict(maxiter=50000, maxfun=100000, ftol=1e-16, gtol=1e-13))
+    return r.fun
+
+
+@pytest.mark.parametrize("loss", LOSSES)
+def test_elastic_global_convergence_and_cdn(oracle_mod, loss):
+    """With mu > 0: every P reaches the scipy optimum within 1e-6, F is monotone, the KKT
+    residual (with mu w_j in the gradient) -> 0, and P = 1 walks the separately coded CDN's
+    iterates (its line search uses the direct (mu/2)((w+ad)^2 - w^2))."""
+    mu = 1.5
+    p = synth.tiny(210, 40, 16, density=0.35, loss=loss, c=2.0)
+    o = oracle_mod.Oracle(p, mu=mu)
+    ref = _scipy_fstar_en(p, mu)
+    F0 = o.objective(np.zeros(p.n))
+    sg0, _ = o.min_norm_subgrad(np.zeros(p.n))
+    for P in (1, 5, 16):
+        r = o.solve(P, max_outer=300, seed=4)
+        assert abs(r["F"] - ref) <= 1e-6 * abs(ref), (P, r["F"], ref)
+        Ft = np.concatenate([[F0], r["F_trace"]])
+        assert np.all(np.diff(Ft) <= 1e-12 * F0)
+        sg, _ = o.min_norm_subgrad(r["w"])
+        assert sg <= 1e-4 * max(sg0, 1.0)
+    a = o.solve(1, max_outer=5, seed=2)
+    b = o.cdn(seed=2, max_outer=5, trace=True)
+    np.testing.assert_allclose(a["w"], b["w"], rtol=1e-9, atol=1e-11)
+    np.testing.assert_allclose(a["F_trace"], b["F_trace"], rtol=1e-11)
