@@ -176,6 +176,8 @@ def main():
                     help="run exactly this many outer iterations per solve (no Eq.14 stop test; for configs "
                          "without a committed F*)")
     ap.add_argument("--mode", type=int, default=0, help="step-kernel launch mode (pcdn_set_launch)")
+    ap.add_argument("--mu", type=float, default=0.0,
+                    help="elastic-net weight (pcdn_set_elastic; NEXT #4): needs --outer (no stored F*)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -185,9 +187,13 @@ def main():
     prob = synth.config(args.config, loss=args.loss)
     if args.P:
         prob.P = args.P
+    if args.mu > 0 and args.outer <= 0:
+        raise SystemExit("--mu needs --outer N (F* is stored for mu = 0 only)")
     fstar = fstar_for(args.config, prob.loss) if args.outer <= 0 else None
     lossname = "L1-logistic" if prob.loss == 0 else "L1-L2-loss-SVM"
     stop = f"Eq.14 gap {args.eps:g}" if args.outer <= 0 else f"{args.outer} outer iterations"
+    if args.mu > 0:
+        lossname += f" + elastic net mu={args.mu:g}"
     workload = (f"cfg{args.config}: {lossname} s={prob.s} x n={prob.n}, nnz={prob.nnz}, c={prob.c}, "
                 f"P={prob.P}, seed={prob.seed}, solve w0=0 -> {stop}")
     config = {"workload": workload, "config_index": args.config, "s": prob.s, "n": prob.n, "nnz": prob.nnz,
@@ -224,6 +230,8 @@ def main():
         solver = pk.Solver(prob, device=dev, stream=stream)
     if fstar is not None:
         pk.pcdn_set_reference(solver.ctx, fstar)
+    if args.mu > 0:
+        solver.set_elastic(args.mu)
     if args.mode:
         solver.set_launch(args.mode)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)

@@ -164,6 +164,14 @@ int pcdn_set_debug(pcdn_ctx *ctx, int on);
  * columns of 129..2048 nonzeros are reduced by one CTA, 128 for mode 3). */
 int pcdn_set_launch(pcdn_ctx *ctx, int mode, int ctas, int heavy_len);
 
+/* Elastic net ("easily extended to ... elastic net";
+ * reading Z25 of DESIGN.md): minimise  c sum_i phi_i + ||w||_1 + (mu/2)||w||_2^2.  mu >= 0 enters
+ * g_j (+ mu w_j), h_j (+ mu), the objective and the line search's separable term
+ * (+ mu a d_j (w_j + a d_j / 2)); mu = 0 (the default) is the paper's problem, bit for bit.
+ * Recomputes the maintained objective on the context's stream.  PCDN_ERR_INVALID for a null
+ * context or mu < 0 / not finite. */
+int pcdn_set_elastic(pcdn_ctx *ctx, double mu);
+
 /* HBM-state kernels (modes 1, 2): keep the per-sample state (z, coef, record counts, touched
  * bitmap, d'x; one contiguous workspace window) L2-resident with a persisting access-policy window
  * on the step-kernel launches (default on).  The first such launch sets the device's persisting-L2

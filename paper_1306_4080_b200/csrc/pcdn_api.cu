@@ -94,7 +94,7 @@ Layout make_layout(int64_t s, int64_t n, int64_t nnz)
     L.err_idx = take(sizeof(long long));
     L.err_what = take(sizeof(int));
     L.bar = take(sizeof(unsigned long long));
-    L.objp = take(sizeof(double) * 2 * OBJ_NB);
+    L.objp = take(sizeof(double) * 3 * OBJ_NB);
     L.prof = take(sizeof(long long) * 16);
     L.tl = take(sizeof(long long) * TL_STEPS * NW * TL_PTS);
     L.dbg_dx = take(sizeof(double) * s);
@@ -132,6 +132,7 @@ struct pcdn_ctx {
     double c = 1.0;
     int loss = 0;
     double sigma = 0.01, beta = 0.5, gamma = 0.0, nu = 1e-12;
+    double mu = 0.0;   // elastic-net weight (pcdn_set_elastic; reading Z25)
     int qmax = 50;
     double fstar = 0.0;
     bool has_fstar = false;
@@ -257,7 +258,7 @@ int objective_kernels(pcdn_ctx *ctx)
     const Layout &L = ctx->L;
     k_obj_partial<<<OBJ_NB, 256, 0, ctx->stream>>>(ctx->s, ctx->n, ctx->at<double>(L.z), ctx->y, ctx->at<double>(L.w),
                                                    ctx->loss, ctx->at<double>(L.objp));
-    k_obj_final<<<1, OBJ_NB, 0, ctx->stream>>>(ctx->at<double>(L.objp), ctx->c, ctx->at<double>(L.F),
+    k_obj_final<<<1, OBJ_NB, 0, ctx->stream>>>(ctx->at<double>(L.objp), ctx->c, ctx->mu, ctx->at<double>(L.F),
                                                ctx->at<double>(L.Fcopy));
     ctx->launches += 2;
     CU(cudaGetLastError());
@@ -321,6 +322,7 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
     a.beta = ctx->beta;
     a.gamma = ctx->gamma;
     a.nu = ctx->nu;
+    a.mu = ctx->mu;
     a.loss = ctx->loss;
     a.qmax = ctx->qmax;
     a.heavy_len = ctx->heavy_eff;
@@ -724,6 +726,14 @@ int pcdn_set_armijo(pcdn_ctx *ctx, double sigma, double beta, double gamma, int 
     return PCDN_OK;
 }
 
+int pcdn_set_elastic(pcdn_ctx *ctx, double mu)
+{
+    if (!ctx) return PCDN_ERR_INVALID;
+    if (!(mu >= 0) || !std::isfinite(mu)) return set_err(ctx, PCDN_ERR_INVALID, "elastic-net weight must be finite and >= 0");
+    ctx->mu = mu;
+    return objective_kernels(ctx);   // the maintained F now includes (mu/2)||w||^2
+}
+
 int pcdn_set_reference(pcdn_ctx *ctx, double f_star)
 {
     if (!ctx) return PCDN_ERR_INVALID;
@@ -870,7 +880,7 @@ int pcdn_objective(pcdn_ctx *ctx, int recompute_from_w, double *F_out)
     const Layout &L = ctx->L;
     k_obj_partial<<<OBJ_NB, 256, 0, ctx->stream>>>(ctx->s, ctx->n, ctx->at<double>(L.z), ctx->y, ctx->at<double>(L.w),
                                                    ctx->loss, ctx->at<double>(L.objp));
-    k_obj_final<<<1, OBJ_NB, 0, ctx->stream>>>(ctx->at<double>(L.objp), ctx->c, ctx->at<double>(L.Fcopy), nullptr);
+    k_obj_final<<<1, OBJ_NB, 0, ctx->stream>>>(ctx->at<double>(L.objp), ctx->c, ctx->mu, ctx->at<double>(L.Fcopy), nullptr);
     ctx->launches += 2;
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(&ctx->hm->Fcopy, ctx->at<double>(L.Fcopy), sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));

@@ -185,7 +185,7 @@ __device__ __forceinline__ void dense_ls_partial(const StepArgs &a, DenseFixed &
         for (int q = 0; q < nq; q++) {
 #pragma unroll
             for (int qq = 0; qq < QW; qq++)
-                if (qq == q) acc[QW + qq] += fabs(wj + al * d) - fabs(wj);
+                if (qq == q) acc[QW + qq] += fabs(wj + al * d) - fabs(wj) + a.mu * al * d * (wj + 0.5 * al * d);
             al *= a.beta;
         }
         acc[2 * QW] += dl;

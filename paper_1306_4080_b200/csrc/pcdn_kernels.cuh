@@ -67,6 +67,7 @@ struct StepArgs {
     const int64_t *__restrict__ row_ptr;  // CSR offsets: capacity of each sample's record segment
     const int8_t *__restrict__ y;
     double c, sigma, beta, gamma, nu;
+    double mu;   // elastic-net weight of (mu/2)||w||^2 (reading Z25; 0 = the paper's problem)
     int loss, qmax;
     int heavy_len;
     // state
@@ -297,8 +298,8 @@ struct Dir {
 __device__ __forceinline__ Dir finish_feature(const StepArgs &a, double gs, double hs, double wj)
 {
     Dir r;
-    r.g = a.c * gs;
-    r.h = a.c * hs;
+    r.g = a.c * gs + a.mu * wj;   // + the elastic-net gradient / curvature (Z25)
+    r.h = a.c * hs + a.mu;
     if (!(r.h > a.nu)) r.h = a.nu;
     r.d = newton_dir(r.g, r.h, wj);
     r.delta = r.g * r.d + a.gamma * r.h * r.d * r.d + fabs(wj + r.d) - fabs(wj);
@@ -1065,7 +1066,7 @@ __device__ __forceinline__ void window(const StepArgs &a, StepSmem &sm, Sync &sy
         double al = alpha0;
 #pragma unroll
         for (int q = 0; q < NQ; q++) {
-            acc[NQ + q] += fabs(wj + al * d) - fabs(wj);
+            acc[NQ + q] += fabs(wj + al * d) - fabs(wj) + a.mu * al * d * (wj + 0.5 * al * d);
             al *= a.beta;
         }
         acc[LY::DELTA] += reg ? sh.delta : ldcg(&a.deltak[kk - k0]);
@@ -1771,44 +1772,54 @@ __global__ void k_obj_partial(int64_t s, int64_t n, const double *__restrict__ z
     const int b = blockIdx.x;
     const int64_t zs0 = (int64_t)b * s / OBJ_NB, zs1 = (int64_t)(b + 1) * s / OBJ_NB;
     const int64_t ws0 = (int64_t)b * n / OBJ_NB, ws1 = (int64_t)(b + 1) * n / OBJ_NB;
-    double ls = 0.0, l1 = 0.0;
+    double ls = 0.0, l1 = 0.0, l2 = 0.0;
     for (int64_t i = zs0 + threadIdx.x; i < zs1; i += blockDim.x) ls += phi_of(loss, (double)y[i] * z[i]);
-    for (int64_t j = ws0 + threadIdx.x; j < ws1; j += blockDim.x) l1 += fabs(w[j]);
+    for (int64_t j = ws0 + threadIdx.x; j < ws1; j += blockDim.x) {
+        l1 += fabs(w[j]);
+        l2 += w[j] * w[j];
+    }
     ls = warp_sum(ls);
     l1 = warp_sum(l1);
-    __shared__ double sh[2][32];
+    l2 = warp_sum(l2);
+    __shared__ double sh[3][32];
     if ((threadIdx.x & 31) == 0) {
         sh[0][threadIdx.x >> 5] = ls;
         sh[1][threadIdx.x >> 5] = l1;
+        sh[2][threadIdx.x >> 5] = l2;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double a0 = 0.0, a1 = 0.0;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
         for (int w2 = 0; w2 < (int)(blockDim.x >> 5); w2++) {
             a0 += sh[0][w2];
             a1 += sh[1][w2];
+            a2 += sh[2][w2];
         }
-        partial[2 * b] = a0;
-        partial[2 * b + 1] = a1;
+        partial[3 * b] = a0;
+        partial[3 * b + 1] = a1;
+        partial[3 * b + 2] = a2;
     }
 }
 
-__global__ void k_obj_final(const double *__restrict__ partial, double c, double *F, double *F_copy)
+// F = c sum phi + ||w||_1 + (mu/2)||w||^2 (Eq.1 + the elastic-net term of Z25)
+__global__ void k_obj_final(const double *__restrict__ partial, double c, double mu, double *F, double *F_copy)
 {
-    __shared__ double sh[2][OBJ_NB];
+    __shared__ double sh[3][OBJ_NB];
     const int t = threadIdx.x;
-    sh[0][t] = partial[2 * t];
-    sh[1][t] = partial[2 * t + 1];
+    sh[0][t] = partial[3 * t];
+    sh[1][t] = partial[3 * t + 1];
+    sh[2][t] = partial[3 * t + 2];
     __syncthreads();
     for (int o = OBJ_NB / 2; o > 0; o >>= 1) {
         if (t < o) {
             sh[0][t] += sh[0][t + o];
             sh[1][t] += sh[1][t + o];
+            sh[2][t] += sh[2][t + o];
         }
         __syncthreads();
     }
     if (t == 0) {
-        const double Fv = c * sh[0][0] + sh[1][0];
+        const double Fv = c * sh[0][0] + sh[1][0] + 0.5 * mu * sh[2][0];
         *F = Fv;
         if (F_copy) *F_copy = Fv;
     }

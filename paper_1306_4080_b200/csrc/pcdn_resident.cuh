@@ -627,7 +627,7 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
         double al = alpha0;
 #pragma unroll
         for (int q = 0; q < NQ; q++) {
-            acc[NQ + q] += fabs(wj + al * d) - fabs(wj);
+            acc[NQ + q] += fabs(wj + al * d) - fabs(wj) + a.mu * al * d * (wj + 0.5 * al * d);
             al *= a.beta;
         }
         acc[LY::DELTA] += dl;

@@ -365,3 +365,45 @@ def test_step_parity_cta_columns(pk, loss, mode, ctas):
     os_ = o.solve(9, seed=5, max_outer=4)
     _compare_solve(gs, os_, s.w().cpu().numpy(), f"cta columns mode={mode}")
     s.close()
+
+
+# ----------------------------------------------------------------------------- elastic net
+@pytest.mark.parametrize("loss", [LOSS_LOGISTIC, LOSS_L2SVM])
+@pytest.mark.parametrize("mu", [0.5, 3.0])
+@pytest.mark.parametrize("launch", [(0, 0, 0), (1, 4, 0), (2, 0, 0), (2, 3, 2), (3, 0, 0), (3, 16, 1)])
+def test_elastic_net_parity(pk, loss, mu, launch):
+    """Elastic net (NEXT #4, reading Z25): c sum phi + ||w||_1 + (mu/2)||w||^2 through every
+    step kernel (cluster and grid HBM-state, forced heavy split, cluster-resident): steps from
+    injected states and a short solve, against the oracle with the same mu."""
+    rng = np.random.default_rng(int(mu * 10) + loss)
+    ties = []
+    for case in (0, 2, 4):
+        kw = dict(TINY[case])
+        prob = synth.tiny(loss=loss, c=3.0, P=5, **kw)
+        s = _solver(pk, prob, *launch)
+        s.set_elastic(mu)
+        o = oracle.Oracle(prob, mu=mu)
+        for rep in range(2):
+            w = _random_state(rng, prob.n, scale=0.4 * (rep + 1))
+            for B in _step_cases(prob, rng, nb=3):
+                s.set_w(w)
+                _compare_step(s.step(B), o.step(w, B), ties)
+        s.reset()
+        gs = s.solve(5, seed=7, max_outer=5, trace=True)
+        os_ = o.solve(5, seed=7, max_outer=5)
+        _compare_solve(gs, os_, s.w().cpu().numpy(), f"elastic mu={mu} launch={launch} case={case}")
+        s.close()
+    assert len(ties) <= 2, ties
+
+
+@pytest.mark.parametrize("loss", [LOSS_LOGISTIC, LOSS_L2SVM])
+def test_elastic_net_dense_kernel(pk, loss):
+    """The dense row-block kernel (mode 4) with mu > 0, including its speculative commit."""
+    prob = synth.tiny(31, 40, 200, density=1.0, loss=loss, c=10.0, P=50)
+    s = _solver(pk, prob, 4, 3)
+    s.set_elastic(2.0)
+    o = oracle.Oracle(prob, mu=2.0)
+    gs = s.solve(50, seed=3, max_outer=4, trace=True)
+    os_ = o.solve(50, seed=3, max_outer=4)
+    _compare_solve(gs, os_, s.w().cpu().numpy(), "elastic dense", ftrace_rtol=1e-7)
+    s.close()
