@@ -407,3 +407,48 @@ def test_elastic_net_dense_kernel(pk, loss):
     os_ = o.solve(50, seed=3, max_outer=4)
     _compare_solve(gs, os_, s.w().cpu().numpy(), "elastic dense", ftrace_rtol=1e-7)
     s.close()
+
+
+# ----------------------------------------------------------------------------- one-call host API
+@pytest.mark.parametrize("cfg,loss", [(1, LOSS_LOGISTIC), (1, LOSS_L2SVM), (2, LOSS_L2SVM)])
+def test_train_host_matches_oracle(pk, cfg, loss):
+    """pcdn_train_host (host arrays in, w out; the API bench.py's e2e number goes through):
+    same stop, outer count and q-level trajectory as the oracle's solve to the Eq.14 gap."""
+    prob = synth.config(cfg, loss=loss)
+    o = oracle.Oracle(prob)
+    fstar = o.solve(prob.P, seed=prob.seed, max_outer=60)["F"]
+    os_ = o.solve(prob.P, eps=1e-3, fstar=fstar, seed=prob.seed, max_outer=60)
+    arrs = [np.ascontiguousarray(getattr(prob, k), dtype=dt) for k, dt in
+            (("col_ptr", np.int64), ("row_idx", np.int32), ("val", np.float32), ("row_ptr", np.int64),
+             ("col_idx", np.int32), ("csr_val", np.float32), ("y", np.int8))]
+    st, inf, w = pk.pcdn_train_host(*arrs, prob.c, prob.loss, prob.P, 1e-3, fstar, prob.seed, 60)
+    assert st == pk.PCDN_OK
+    assert inf.outer_iters == os_["outer"] and inf.steps == os_["steps"]
+    assert abs(inf.F - os_["F"]) <= 1e-6 * abs(os_["F"])
+    assert np.max(np.abs(w - os_["w"])) <= 1e-5
+    # invalid inputs come back as PCDN_ERR_INVALID, not as a crash
+    with pytest.raises(pk.PCDNError) as ei:
+        pk.pcdn_train_host(*arrs, prob.c, prob.loss, 0, 1e-3, fstar, prob.seed, 60)
+    assert ei.value.status == pk.PCDN_ERR_INVALID
+    with pytest.raises(pk.PCDNError) as ei:
+        pk.pcdn_train_host(*arrs, prob.c, prob.loss, prob.P, 1e-3, -1.0, prob.seed, 60)
+    assert ei.value.status == pk.PCDN_ERR_INVALID
+
+
+def test_knob_validation(pk):
+    """Out-of-range knobs return PCDN_ERR_INVALID and leave the context usable."""
+    prob = synth.tiny(12, 30, 10, density=0.4)
+    s = _solver(pk, prob)
+    for call in (lambda: s.set_elastic(-1.0), lambda: s.set_elastic(float("nan")),
+                 lambda: s.set_launch(7), lambda: s.set_launch(3, 3), lambda: s.set_launch(1, 17),
+                 lambda: pk.pcdn_set_armijo(s.ctx, 1.5, 0.5, 0.0, 50),
+                 lambda: pk.pcdn_set_armijo(s.ctx, 0.01, 0.5, 0.0, 1000),
+                 lambda: pk.pcdn_set_reference(s.ctx, -2.0),
+                 lambda: s.step(np.zeros(0, dtype=np.int32))):
+        with pytest.raises(pk.PCDNError) as ei:
+            call()
+        assert ei.value.status == pk.PCDN_ERR_INVALID
+    o = oracle.Oracle(prob)
+    r = s.solve(4, seed=1, max_outer=3, trace=True)   # still usable
+    _compare_solve(r, o.solve(4, seed=1, max_outer=3), s.w().cpu().numpy(), "after invalid knobs")
+    s.close()
