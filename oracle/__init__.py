@@ -17,7 +17,7 @@ _SRC = os.path.join(_HERE, "pcdn_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 OK, ERR_INVALID, BUDGET, ERR_NUMERIC = 0, 1, 2, 3
-LOSS_LOGISTIC, LOSS_L2SVM = 0, 1
+LOSS_LOGISTIC, LOSS_L2SVM, LOSS_SQUARED = 0, 1, 2
 
 
 def build(force: bool = False) -> str:
@@ -35,7 +35,7 @@ class _Prob(C.Structure):
                 ("col_ptr", C.c_void_p), ("row_idx", C.c_void_p), ("val", C.c_void_p),
                 ("y", C.c_void_p), ("c", C.c_double), ("loss", C.c_int32), ("qmax", C.c_int32),
                 ("sigma", C.c_double), ("beta", C.c_double), ("gamma", C.c_double),
-                ("nu", C.c_double), ("mu", C.c_double)]
+                ("nu", C.c_double), ("mu", C.c_double), ("t", C.c_void_p)]
 
 
 class _State(C.Structure):
@@ -151,8 +151,13 @@ class Oracle:
         self.val = np.ascontiguousarray(prob.val, dtype=np.float32)
         self.y = np.ascontiguousarray(prob.y, dtype=np.int8)
         self.s, self.n = int(prob.s), int(prob.n)
+        tt = getattr(prob, "t", None)
+        if int(prob.loss) == LOSS_SQUARED and tt is None:
+            raise ValueError("the squared loss needs real targets prob.t")
+        self.t = None if tt is None else np.ascontiguousarray(tt, dtype=np.float64)
         self.pb = _Prob(self.s, self.n, _p(self.col_ptr), _p(self.row_idx), _p(self.val), _p(self.y),
-                        float(prob.c), int(prob.loss), int(qmax), sigma, beta, gamma, nu, float(mu))
+                        float(prob.c), int(prob.loss), int(qmax), sigma, beta, gamma, nu, float(mu),
+                        _p(self.t))
 
     # --- plain evaluations ---
     def compute_z(self, w):

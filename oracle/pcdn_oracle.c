@@ -21,6 +21,9 @@
  *   App.A.2 L2-SVM generalized Hessian, nu = 1e-12
  *   Eq.14 relative function value difference
  *   Alg.1 CDN (separately coded, for the P=1 reduction)
+ *   Lasso (NEXT #4; "easily extended to ... Lasso"): the squared loss
+ *   phi = (t_i - w'x_i)^2 with real targets t (reading Z26): G = 2(z - t), H = 2, the line-search
+ *   summand (t - z - a dx)^2 - (t - z)^2 = a dx (a dx + 2(z - t)).
  *   Elastic net (NEXT #4; "easily extended to ... elastic net"): the separable
  *   term ||w||_1 + (mu/2)||w||_2^2, mu >= 0 (mu = 0: the paper's problem).  Reading Z25: the
  *   smooth part becomes L(w) + (mu/2)||w||^2, so g_j, h_j gain mu w_j, mu (Eq.5 unchanged in form),
@@ -47,6 +50,7 @@
 
 #define ORA_LOSS_LOGISTIC 0
 #define ORA_LOSS_L2SVM 1
+#define ORA_LOSS_SQUARED 2   /* Lasso / elastic-net regression (reading Z26) */
 
 typedef struct {
     int64_t s, n;
@@ -59,6 +63,7 @@ typedef struct {
     int32_t qmax;             /* line-search cap (Z10) */
     double sigma, beta, gamma, nu;   /* Armijo constants, nu */
     double mu;                /* elastic-net weight (reading Z25; 0 = the paper's problem) */
+    const double *t;          /* s real targets of the squared loss (Z26); NULL otherwise */
 } ora_prob;
 
 /* ------------------------------------------------------------------------------ */
@@ -165,11 +170,31 @@ void ora_GH(int loss, double z, int y, double *G, double *H)
     }
 }
 
+/* Per-sample forms with the sample's target available (the squared loss needs t_i, Z26). */
+static double phi_i(const ora_prob *pb, int64_t i, double z)
+{
+    if (pb->loss == ORA_LOSS_SQUARED) {
+        double r = pb->t[i] - z;
+        return r * r;
+    }
+    return ora_phi(pb->loss, (double)pb->y[i] * z);
+}
+
+static void GH_i(const ora_prob *pb, int64_t i, double z, double *G, double *H)
+{
+    if (pb->loss == ORA_LOSS_SQUARED) {   /* d/dz (t - z)^2 = 2(z - t), d2/dz2 = 2 */
+        *G = 2.0 * (z - pb->t[i]);
+        *H = 2.0;
+        return;
+    }
+    ora_GH(pb->loss, z, pb->y[i], G, H);
+}
+
 /* Eq.1 evaluated from scratch from (z = Xw, w) (a6, Z19, Z23). */
 double ora_objective(const ora_prob *pb, const double *z, const double *w)
 {
     double loss = 0.0, l1 = 0.0, l2 = 0.0;
-    for (int64_t i = 0; i < pb->s; i++) loss += ora_phi(pb->loss, (double)pb->y[i] * z[i]);
+    for (int64_t i = 0; i < pb->s; i++) loss += phi_i(pb, i, z[i]);
     for (int64_t j = 0; j < pb->n; j++) {
         l1 += fabs(w[j]);
         l2 += w[j] * w[j];
@@ -196,7 +221,7 @@ static void gh_one(const ora_prob *pb, const double *z, const double *w, int64_t
     for (int64_t p = pb->col_ptr[j]; p < pb->col_ptr[j + 1]; p++) {
         int64_t i = pb->row_idx[p];
         double x = (double)pb->val[p], G, H;
-        ora_GH(pb->loss, z[i], pb->y[i], &G, &H);
+        GH_i(pb, i, z[i], &G, &H);
         gs += x * G;
         hs += (x * x) * H;
         ga += fabs(x * G);
@@ -362,7 +387,9 @@ int ora_bundle_step(const ora_prob *pb, ora_state *st, const int32_t *bundle, in
             }
             for (int64_t a = 0; a < nl; a++) {
                 int32_t i = st->list[a];
-                double t = loss_change(pb->loss, st->z[i], pb->y[i], st->dx[i], alpha);
+                double t = pb->loss == ORA_LOSS_SQUARED
+                               ? alpha * st->dx[i] * (alpha * st->dx[i] + 2.0 * (st->z[i] - pb->t[i]))   /* Z26 */
+                               : loss_change(pb->loss, st->z[i], pb->y[i], st->dx[i], alpha);
                 Ls += t;
                 Lsa += fabs(t);
             }
@@ -562,7 +589,10 @@ int ora_cdn(const ora_prob *pb, double *w, double *z, uint64_t seed, int32_t max
             for (int64_t p = pb->col_ptr[j]; p < pb->col_ptr[j + 1]; p++) {
                 int64_t i = pb->row_idx[p];
                 double x = (double)pb->val[p], yd = (double)pb->y[i];
-                if (pb->loss == ORA_LOSS_LOGISTIC) {
+                if (pb->loss == ORA_LOSS_SQUARED) {            /* d/dw_j sum (t - x'w)^2 */
+                    gl += -2.0 * (pb->t[i] - z[i]) * x;
+                    hl += 2.0 * x * x;
+                } else if (pb->loss == ORA_LOSS_LOGISTIC) {
                     double ta = tau(yd * z[i]);
                     gl += (ta - 1.0) * yd * x;                 /* Eq.13 */
                     hl += ta * (1.0 - ta) * x * x;
@@ -587,7 +617,9 @@ int ora_cdn(const ora_prob *pb, double *w, double *z, uint64_t seed, int32_t max
                     int64_t i = pb->row_idx[p];
                     double yd = (double)pb->y[i];
                     double znew = z[i] + alpha * dj * (double)pb->val[p];
-                    chg += ora_phi(pb->loss, yd * znew) - ora_phi(pb->loss, yd * z[i]);
+                    chg += pb->loss == ORA_LOSS_SQUARED
+                               ? (pb->t[i] - znew) * (pb->t[i] - znew) - (pb->t[i] - z[i]) * (pb->t[i] - z[i])
+                               : ora_phi(pb->loss, yd * znew) - ora_phi(pb->loss, yd * z[i]);
                 }
                 double wn = wj + alpha * dj;
                 double lhs = pb->c * chg + fabs(wn) - fabs(wj) + 0.5 * pb->mu * (wn * wn - wj * wj);
@@ -620,7 +652,7 @@ double ora_min_norm_subgrad(const ora_prob *pb, const double *w, const double *z
         for (int64_t p = pb->col_ptr[j]; p < pb->col_ptr[j + 1]; p++) {
             int64_t i = pb->row_idx[p];
             double G, H;
-            ora_GH(pb->loss, z[i], pb->y[i], &G, &H);
+            GH_i(pb, i, z[i], &G, &H);
             gs += (double)pb->val[p] * G;
         }
         double gj = pb->c * gs + pb->mu * w[j], v;

@@ -16,4 +16,6 @@ from .generate import (  # noqa: F401
     csr_to_csc,
     LOSS_LOGISTIC,
     LOSS_L2SVM,
+    LOSS_SQUARED,
+    regression,
 )

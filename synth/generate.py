@@ -18,6 +18,7 @@ import numpy as np
 
 LOSS_LOGISTIC = 0  # Eq. 2
 LOSS_L2SVM = 1     # Eq. 3
+LOSS_SQUARED = 2   # Lasso / elastic-net regression (reading Z26)
 
 GEN_VERSION = 1
 
@@ -41,6 +42,7 @@ class Problem:
     P: int
     seed: int
     meta: dict = field(default_factory=dict)
+    t: np.ndarray | None = None   # float64[s] real targets of the squared loss (else None)
 
     @property
     def nnz(self) -> int:
@@ -63,8 +65,25 @@ class Problem:
     def with_loss(self, loss: int) -> "Problem":
         p = Problem(**{k: getattr(self, k) for k in self.__dataclass_fields__})
         p.loss = loss
-        p.name = self.name + ("-lr" if loss == LOSS_LOGISTIC else "-svm")
+        p.name = self.name + {LOSS_LOGISTIC: "-lr", LOSS_L2SVM: "-svm"}.get(loss, "-sq")
         return p
+
+
+def regression(prob: "Problem", noise: float = 0.1, support: int = 500, seed: int | None = None) -> "Problem":
+    """The same design matrix with real targets t = X w* + N(0, noise^2) for a planted w* with
+    `support` N(0,1) nonzeros (uniform without replacement), loss = LOSS_SQUARED.  Data
+    generation only (a matrix-vector product), no PCDN arithmetic."""
+    rng = np.random.default_rng((prob.seed if seed is None else seed) + 7919)
+    k = min(int(support), prob.n)
+    wstar = np.zeros(prob.n)
+    wstar[rng.choice(prob.n, size=k, replace=False)] = rng.normal(size=k)
+    rows = np.repeat(np.arange(prob.s), np.diff(prob.row_ptr))
+    t = np.bincount(rows, weights=prob.csr_val.astype(np.float64) * wstar[prob.col_idx], minlength=prob.s)
+    if noise > 0:
+        t = t + rng.normal(0.0, noise, size=prob.s)
+    p = prob.with_loss(LOSS_SQUARED)
+    p.t = t
+    return p
 
 
 # ----------------------------------------------------------------------------------

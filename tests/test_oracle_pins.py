@@ -658,3 +658,98 @@ def test_elastic_global_convergence_and_cdn(oracle_mod, loss):
     b = o.cdn(seed=2, max_outer=5, trace=True)
     np.testing.assert_allclose(a["w"], b["w"], rtol=1e-9, atol=1e-11)
     np.testing.assert_allclose(a["F_trace"], b["F_trace"], rtol=1e-11)
+
+
+# ------------------------------------------------------------------ Lasso (NEXT #4, Z26)
+# F(w) = c sum_i (t_i - x_i'w)^2 + ||w||_1 (+ (mu/2)||w||^2): "PCDN ... can be
+# easily extended to other problems such as Lasso and elastic net".  References: numpy, closed
+# forms, and scikit-learn's coordinate-descent Lasso / ElasticNet (an independent solver).
+from synth import LOSS_SQUARED  # noqa: E402
+
+
+def _reg(seed, s, n, density, c, noise=0.1, support=4):
+    p = synth.tiny(seed, s, n, density=density, c=c)
+    return synth.regression(p, noise=noise, support=support)
+
+
+def np_F_sq(p, w, mu=0.0, X=None):
+    X = p.dense() if X is None else X
+    r = p.t - X @ w
+    return p.c * float(np.dot(r, r)) + np.sum(np.abs(w)) + 0.5 * mu * float(np.dot(w, w))
+
+
+def test_squared_objective_gh(oracle_mod):
+    """F, g_j by central differences, h_j = 2c sum_i x_ij^2 (+ mu), against numpy."""
+    rng = np.random.default_rng(81)
+    for mu in (0.0, 1.0):
+        p = _reg(81, 25, 9, 0.5, 1.3)
+        X = p.dense()
+        o = oracle_mod.Oracle(p, mu=mu)
+        for _ in range(4):
+            w = rng.normal(size=p.n) * 0.4
+            assert math.isclose(o.objective(w), np_F_sq(p, w, mu, X), rel_tol=1e-12)
+            g, h = o.gh(w)
+            sm = lambda v: p.c * float(np.dot(p.t - X @ v, p.t - X @ v)) + 0.5 * mu * float(np.dot(v, v))
+            eps = 1e-6
+            fd = np.array([(sm(w + eps * e) - sm(w - eps * e)) / (2 * eps) for e in np.eye(p.n)])
+            np.testing.assert_allclose(g, fd, rtol=1e-6, atol=1e-7)
+            np.testing.assert_allclose(h, 2 * p.c * np.sum(X * X, axis=0) + mu, rtol=1e-13)
+
+
+def test_squared_one_dimensional_closed_form(oracle_mod):
+    """s=1, x=1: F = c(t - w)^2 + |w| has w* = soft(t, 1/(2c)) = sign(t) max(|t| - 1/(2c), 0),
+    reached in one Newton step (a quadratic)."""
+    for t, c in ((2.0, 1.0), (-3.0, 0.5), (0.2, 1.0), (5.0, 10.0)):
+        p = synth.from_dense([[1.0]], [1], c=c)
+        p = synth.regression(p, noise=0.0, support=1)
+        p.t = np.array([t])
+        r = oracle_mod.Oracle(p).solve(1, max_outer=1)
+        ws = math.copysign(max(abs(t) - 1 / (2 * c), 0.0), t)
+        assert abs(r["w"][0] - ws) <= 1e-15 * max(1.0, abs(ws))
+        assert math.isclose(r["F"], c * (t - ws) ** 2 + abs(ws), rel_tol=1e-14)
+
+
+@pytest.mark.parametrize("mu", [0.0, 0.8])
+def test_squared_matches_sklearn(oracle_mod, mu):
+    """The oracle's optimum equals scikit-learn's (an independent coordinate-descent solver):
+    Lasso(alpha) minimises (1/2s)||t - Xw||^2 + alpha ||w||_1, i.e. our F with c = 1/(2 s alpha);
+    ElasticNet(alpha, l1_ratio=rho) gives c = 1/(2 s alpha rho), mu = (1 - rho)/rho.  Every P
+    reaches it (global convergence); P = 1 walks the separately coded CDN."""
+    from sklearn.linear_model import ElasticNet, Lasso
+    p = _reg(91, 60, 20, 0.4, 1.0, noise=0.2, support=6)
+    X = p.dense()
+    s_ = p.s
+    if mu == 0.0:
+        alpha = 0.02
+        p.c = 1.0 / (2 * s_ * alpha)
+        m = Lasso(alpha=alpha, fit_intercept=False, tol=1e-14, max_iter=1000000).fit(X, p.t)
+    else:
+        rho = 1.0 / (1.0 + mu)
+        alpha = 0.02 / rho
+        p.c = 1.0 / (2 * s_ * alpha * rho)
+        m = ElasticNet(alpha=alpha, l1_ratio=rho, fit_intercept=False, tol=1e-14, max_iter=1000000).fit(X, p.t)
+    ref = np_F_sq(p, m.coef_, mu, X)
+    o = oracle_mod.Oracle(p, mu=mu)
+    for P in (1, 5, 20):
+        r = o.solve(P, max_outer=600, seed=2)
+        assert abs(r["F"] - ref) <= 1e-7 * abs(ref), (P, r["F"], ref)
+        np.testing.assert_allclose(r["w"], m.coef_, atol=1e-5)
+    a = o.solve(1, max_outer=4, seed=6)
+    b = o.cdn(seed=6, max_outer=4, trace=True)
+    np.testing.assert_allclose(a["w"], b["w"], rtol=1e-9, atol=1e-11)
+    np.testing.assert_allclose(a["F_trace"], b["F_trace"], rtol=1e-11)
+
+
+def test_squared_line_search_incremental_vs_direct(oracle_mod):
+    """a dx (a dx + 2(z - t)) summed over T (the Z26 summand) against the direct F difference."""
+    rng = np.random.default_rng(93)
+    for seed in range(10):
+        Xc = rng.normal(size=(30, 2)) @ rng.normal(size=(2, 14)) + 0.05 * rng.normal(size=(30, 14))
+        p = synth.regression(synth.from_dense(Xc, np.ones(30), c=5.0), noise=0.3, support=4, seed=seed)
+        o = oracle_mod.Oracle(p)
+        w = rng.normal(size=p.n) * 0.5
+        B = rng.choice(p.n, size=int(rng.integers(1, p.n + 1)), replace=False)
+        r0 = o.step(w, B, mode=0)
+        r1 = o.step(w, B, mode=1)
+        assert r0["q"] == r1["q"]
+        assert math.isclose(r0["lhs"], r1["lhs"], rel_tol=1e-8, abs_tol=1e-10 * (1 + r0["lhs_abs"]))
