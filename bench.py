@@ -184,13 +184,16 @@ def main():
 
     import synth
     ws, rank, local = dist_setup()
-    prob = synth.config(args.config, loss=args.loss)
+    if args.loss == 2:   # Lasso / elastic-net regression on the config's design matrix (Z26)
+        prob = synth.regression(synth.config(args.config), noise=0.1, support=min(500, synth.config(args.config).n))
+    else:
+        prob = synth.config(args.config, loss=args.loss)
     if args.P:
         prob.P = args.P
-    if args.mu > 0 and args.outer <= 0:
-        raise SystemExit("--mu needs --outer N (F* is stored for mu = 0 only)")
+    if (args.mu > 0 or args.loss == 2) and args.outer <= 0:
+        raise SystemExit("--mu / --loss 2 need --outer N (F* is stored for the paper's two losses, mu = 0)")
     fstar = fstar_for(args.config, prob.loss) if args.outer <= 0 else None
-    lossname = "L1-logistic" if prob.loss == 0 else "L1-L2-loss-SVM"
+    lossname = {0: "L1-logistic", 1: "L1-L2-loss-SVM", 2: "Lasso (squared loss, planted targets)"}[prob.loss]
     stop = f"Eq.14 gap {args.eps:g}" if args.outer <= 0 else f"{args.outer} outer iterations"
     if args.mu > 0:
         lossname += f" + elastic net mu={args.mu:g}"

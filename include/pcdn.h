@@ -42,6 +42,8 @@ extern "C" {
 
 #define PCDN_LOSS_LOGISTIC 0 /* Eq.2 */
 #define PCDN_LOSS_L2SVM 1    /* Eq.3, generalized Hessian App. A.2        */
+#define PCDN_LOSS_SQUARED 2  /* (t_i - w'x_i)^2 with real targets: Lasso / elastic net
+                                (reading Z26); pcdn_set_targets */
 
 typedef struct pcdn_ctx pcdn_ctx;
 
@@ -163,6 +165,15 @@ int pcdn_set_debug(pcdn_ctx *ctx, int on);
  * whole launch (0 = keep the current setting; default 0 = per mode: 2048 for modes 1-2, where
  * columns of 129..2048 nonzeros are reduced by one CTA, 128 for mode 3). */
 int pcdn_set_launch(pcdn_ctx *ctx, int mode, int ctas, int heavy_len);
+
+/* Squared loss (PCDN_LOSS_SQUARED, reading Z26): borrow the real targets t (DEVICE fp64[s], kept
+ * alive and unmodified by the caller) -- F = c sum_i (t_i - w'x_i)^2 + ||w||_1 (+ elastic net).
+ * Required before any state-dependent call on a squared-loss context (those return
+ * PCDN_ERR_INVALID until then; pcdn_create accepts y = NULL for this loss and ignores y).
+ * Validates that every target is finite, then resets the state (w = 0, z, factors, F).
+ * PCDN_ERR_INVALID: null context/pointer, another loss, or a non-finite target.
+ * pcdn_train_host does not take targets and rejects this loss. */
+int pcdn_set_targets(pcdn_ctx *ctx, const double *t);
 
 /* Elastic net ("easily extended to ... elastic net";
  * reading Z25 of DESIGN.md): minimise  c sum_i phi_i + ||w||_1 + (mu/2)||w||_2^2.  mu >= 0 enters

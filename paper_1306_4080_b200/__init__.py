@@ -12,14 +12,14 @@ import ctypes as C
 import numpy as np
 
 from ._abi import (  # noqa: F401
-    PCDN_BUDGET, PCDN_ERR_CUDA, PCDN_ERR_INVALID, PCDN_ERR_NOMEM, PCDN_ERR_NUMERIC, PCDN_LOSS_L2SVM,
+    PCDN_BUDGET, PCDN_ERR_CUDA, PCDN_ERR_INVALID, PCDN_ERR_NOMEM, PCDN_ERR_NUMERIC, PCDN_LOSS_L2SVM, PCDN_LOSS_SQUARED,
     PCDN_LOSS_LOGISTIC, PCDN_OK, PCDNError, check, lib, pcdn_solve_info, pcdn_step_info,
 )
 
 __all__ = [
     "pcdn_workspace_bytes", "pcdn_create", "pcdn_set_armijo", "pcdn_set_reference", "pcdn_bundle_step",
     "pcdn_last_touched", "pcdn_solve", "pcdn_objective", "pcdn_get_w", "pcdn_set_w", "pcdn_get_z",
-    "pcdn_reset", "pcdn_permutation", "pcdn_set_trace", "pcdn_set_debug", "pcdn_set_launch", "pcdn_set_resident_cap", "pcdn_set_l2_persist", "pcdn_set_elastic", "pcdn_set_profile", "pcdn_phase_cycles", "pcdn_warp_timeline",
+    "pcdn_reset", "pcdn_permutation", "pcdn_set_trace", "pcdn_set_debug", "pcdn_set_launch", "pcdn_set_resident_cap", "pcdn_set_l2_persist", "pcdn_set_elastic", "pcdn_set_targets", "pcdn_set_profile", "pcdn_phase_cycles", "pcdn_warp_timeline",
     "pcdn_last_error", "pcdn_destroy", "pcdn_train_host", "pcdn_version", "Solver", "PCDNError",
 ]
 
@@ -133,6 +133,10 @@ def pcdn_set_launch(ctx, mode=0, ctas=0, heavy_len=0):
     return check(ctx, lib().pcdn_set_launch(ctx, int(mode), int(ctas), int(heavy_len)))
 
 
+def pcdn_set_targets(ctx, t):
+    return check(ctx, lib().pcdn_set_targets(ctx, _ptr(t)))
+
+
 def pcdn_set_elastic(ctx, mu):
     return check(ctx, lib().pcdn_set_elastic(ctx, float(mu)))
 
@@ -215,6 +219,10 @@ class Solver:
         self.ctx = pcdn_create(self.s, self.n, self.nnz, self.col_ptr, self.row_idx, self.val, self.row_ptr,
                                self.col_idx, self.csr_val, self.y, self.c, self.loss, self.workspace, self.stream)
         pcdn_set_armijo(self.ctx, sigma, beta, gamma, q_max)
+        self.t = None
+        if self.loss == PCDN_LOSS_SQUARED:   # Lasso / elastic-net regression: real targets
+            self.t = T(prob.t, np.float64)
+            pcdn_set_targets(self.ctx, self.t)
 
     # state
     def w(self):

@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libpcdn.so")
 
 PCDN_OK, PCDN_ERR_INVALID, PCDN_BUDGET, PCDN_ERR_NUMERIC, PCDN_ERR_CUDA, PCDN_ERR_NOMEM = 0, 1, 2, 3, 4, 5
-PCDN_LOSS_LOGISTIC, PCDN_LOSS_L2SVM = 0, 1
+PCDN_LOSS_LOGISTIC, PCDN_LOSS_L2SVM, PCDN_LOSS_SQUARED = 0, 1, 2
 STATUS_NAMES = {0: "PCDN_OK", 1: "PCDN_ERR_INVALID", 2: "PCDN_BUDGET", 3: "PCDN_ERR_NUMERIC",
                 4: "PCDN_ERR_CUDA", 5: "PCDN_ERR_NOMEM"}
 
@@ -65,6 +65,7 @@ SIGNATURES = {
     "pcdn_set_resident_cap": (C.c_int, [P, C.c_int]),
     "pcdn_set_l2_persist": (C.c_int, [P, C.c_int]),
     "pcdn_set_elastic": (C.c_int, [P, C.c_double]),
+    "pcdn_set_targets": (C.c_int, [P, C.c_void_p]),
     "pcdn_set_profile": (C.c_int, [P, C.c_int]),
     "pcdn_phase_cycles": (C.c_int, [P, P, C.POINTER(C.c_int32)]),
     "pcdn_warp_timeline": (C.c_int, [P, P]),

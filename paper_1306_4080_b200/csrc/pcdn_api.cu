@@ -35,7 +35,7 @@ struct Lists {
 };
 
 struct Layout {
-    size_t w, z, coef, cnt, bits, rec, dxg, tlist, seen, dk, deltak, gk, hk, part, hpart, counters, info, F, Fcopy,
+    size_t ydummy, w, z, coef, cnt, bits, rec, dxg, tlist, seen, dk, deltak, gk, hk, part, hpart, counters, info, F, Fcopy,
         status, err_idx, err_what, bar, objp, prof, tl, dbg_dx, dbg_mark, rec2, rslot, ovf_cnt, part_gh, total;
     Lists ls[2];
 };
@@ -51,6 +51,7 @@ Layout make_layout(int64_t s, int64_t n, int64_t nnz)
     };
     const int64_t nw = (s + 31) / 32;
     const int64_t ntile = (n + 1 + SCAN_TILE - 1) / SCAN_TILE + 1;
+    L.ydummy = take(s);   // zero labels for the squared loss (which ignores them)
     L.w = take(sizeof(double) * n);
     L.z = take(sizeof(double) * s);
     L.coef = take(sizeof(double2) * s);
@@ -129,6 +130,7 @@ struct pcdn_ctx {
     const int32_t *col_idx = nullptr;
     const float *csr_val = nullptr;
     const int8_t *y = nullptr;
+    const double *t = nullptr;   // squared-loss targets (pcdn_set_targets; borrowed device fp64[s])
     double c = 1.0;
     int loss = 0;
     double sigma = 0.01, beta = 0.5, gamma = 0.0, nu = 1e-12;
@@ -253,11 +255,19 @@ int prep_outer(pcdn_ctx *ctx, uint64_t seed, int64_t k, int buf, cudaStream_t st
     return build_heavy(ctx, ctx->n, buf, st);
 }
 
+// the squared loss has no state before its targets are given (pcdn_set_targets)
+#define PCDN_NEED_TARGETS(ctx)                                                                             \
+    do {                                                                                                   \
+        if ((ctx)->loss == PCDN_LOSS_SQUARED && !(ctx)->t)                                                 \
+            return set_err((ctx), PCDN_ERR_INVALID, "squared loss: call pcdn_set_targets first");        \
+    } while (0)
+
 int objective_kernels(pcdn_ctx *ctx)
 {
+    PCDN_NEED_TARGETS(ctx);
     const Layout &L = ctx->L;
     k_obj_partial<<<OBJ_NB, 256, 0, ctx->stream>>>(ctx->s, ctx->n, ctx->at<double>(L.z), ctx->y, ctx->at<double>(L.w),
-                                                   ctx->loss, ctx->at<double>(L.objp));
+                                                   ctx->loss, ctx->at<double>(L.objp), ctx->t);
     k_obj_final<<<1, OBJ_NB, 0, ctx->stream>>>(ctx->at<double>(L.objp), ctx->c, ctx->mu, ctx->at<double>(L.F),
                                                ctx->at<double>(L.Fcopy));
     ctx->launches += 2;
@@ -267,10 +277,11 @@ int objective_kernels(pcdn_ctx *ctx)
 
 int refresh_z(pcdn_ctx *ctx, int zero)
 {
+    PCDN_NEED_TARGETS(ctx);
     const Layout &L = ctx->L;
     k_set_z<<<grid1d(ctx->s), 256, 0, ctx->stream>>>(ctx->s, ctx->row_ptr, ctx->col_idx, ctx->csr_val, ctx->y,
                                                      ctx->at<double>(L.w), ctx->loss, ctx->at<double>(L.z),
-                                                     ctx->at<double2>(L.coef), zero);
+                                                     ctx->at<double2>(L.coef), zero, ctx->t);
     ctx->launches++;
     CU(cudaGetLastError());
     return PCDN_OK;
@@ -304,9 +315,17 @@ int reset_status(pcdn_ctx *ctx)
 int choose_mode(const pcdn_ctx *ctx, int64_t P);
 int heavy_for_mode(const pcdn_ctx *ctx, int mode);
 
+const void *dense_kernel(int loss)
+{
+    return loss == LOSS_LOGISTIC ? (const void *)k_step_dense<LOSS_LOGISTIC>
+           : loss == LOSS_L2SVM  ? (const void *)k_step_dense<LOSS_L2SVM>
+                                 : (const void *)k_step_dense<LOSS_SQ>;
+}
+
 int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps, int64_t trace_off, double *g_out,
                  double *h_out, double *d_out)
 {
+    PCDN_NEED_TARGETS(ctx);
     const Layout &L = ctx->L;
     const Lists &S = L.ls[buf];
     StepArgs a{};
@@ -317,6 +336,7 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
     a.val = ctx->val;
     a.row_ptr = ctx->row_ptr;
     a.y = ctx->y;
+    a.t = ctx->t;
     a.c = ctx->c;
     a.sigma = ctx->sigma;
     a.beta = ctx->beta;
@@ -393,8 +413,7 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
     if (mode == 4) {
         if (ctx->Gd < 1) return set_err(ctx, PCDN_ERR_INVALID, "dense step kernel unavailable for this problem");
         void *args[] = {&a};
-        const void *kd = ctx->loss == LOSS_LOGISTIC ? (const void *)k_step_dense<LOSS_LOGISTIC>
-                                                    : (const void *)k_step_dense<LOSS_L2SVM>;
+        const void *kd = dense_kernel(ctx->loss);
         CU(cudaLaunchCooperativeKernel(kd, dim3(ctx->Gd), dim3(NT), args, ctx->dsmem,
                                        ctx->stream));
     } else if (mode == 3) {
@@ -410,7 +429,8 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        CU(cudaLaunchKernelEx(&cfg, ctx->loss == LOSS_LOGISTIC ? k_step_res<LOSS_LOGISTIC> : k_step_res<LOSS_L2SVM>, a));
+        CU(cudaLaunchKernelEx(&cfg, ctx->loss == LOSS_LOGISTIC ? k_step_res<LOSS_LOGISTIC>
+                                    : ctx->loss == LOSS_L2SVM ? k_step_res<LOSS_L2SVM> : k_step_res<LOSS_SQ>, a));
     } else {
         // HBM-state kernels: the per-sample state (z, coef, cnt, bits, dxg, tlist) is gathered and
         // scattered at random every step while CSC and records stream through L2; a persisting
@@ -536,7 +556,8 @@ int configure_launch(pcdn_ctx *ctx)
     {
         int optin = 0;
         CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        const void *kr = ctx->loss == LOSS_LOGISTIC ? (const void *)k_step_res<LOSS_LOGISTIC> : (const void *)k_step_res<LOSS_L2SVM>;
+        const void *kr = ctx->loss == LOSS_LOGISTIC ? (const void *)k_step_res<LOSS_LOGISTIC>
+                         : ctx->loss == LOSS_L2SVM ? (const void *)k_step_res<LOSS_L2SVM> : (const void *)k_step_res<LOSS_SQ>;
         CU(cudaFuncSetAttribute(kr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         ctx->res_G = 0;
         const int greq = ctx->mode_req == 3 ? ctx->G_req : 0;
@@ -589,8 +610,7 @@ int configure_launch(pcdn_ctx *ctx)
             // the fixed part plus two tile buffers (the step's X_B rows, copied a step ahead)
             ctx->dsmem = (size_t)optin;
             ctx->dense_tcap = (int)((((size_t)optin - dense_fixed_bytes()) / (2 * sizeof(float))) & ~(size_t)31);
-            const void *kd = ctx->loss == LOSS_LOGISTIC ? (const void *)k_step_dense<LOSS_LOGISTIC>
-                                                        : (const void *)k_step_dense<LOSS_L2SVM>;
+            const void *kd = dense_kernel(ctx->loss);
             CU(cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->dsmem));
             int occd = 0;
             CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occd, kd, NT, ctx->dsmem));
@@ -641,9 +661,10 @@ int pcdn_create(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_ptr, c
         return fail(set_err(ctx, PCDN_ERR_INVALID, "invalid sizes s=%lld n=%lld nnz=%lld", (long long)s,
                             (long long)n, (long long)nnz));
     if (!(c > 0) || !std::isfinite(c)) return fail(set_err(ctx, PCDN_ERR_INVALID, "c must be finite and > 0"));
-    if (loss != PCDN_LOSS_LOGISTIC && loss != PCDN_LOSS_L2SVM)
+    if (loss != PCDN_LOSS_LOGISTIC && loss != PCDN_LOSS_L2SVM && loss != PCDN_LOSS_SQUARED)
         return fail(set_err(ctx, PCDN_ERR_INVALID, "unknown loss %d", loss));
-    if (!csc_col_ptr || !csr_row_ptr || !y || (nnz > 0 && (!csc_row_idx || !csc_val || !csr_col_idx || !csr_val)))
+    if (!csc_col_ptr || !csr_row_ptr || (!y && loss != PCDN_LOSS_SQUARED) ||
+        (nnz > 0 && (!csc_row_idx || !csc_val || !csr_col_idx || !csr_val)))
         return fail(set_err(ctx, PCDN_ERR_INVALID, "null input pointer"));
     ctx->L = make_layout(s, n, nnz);
     if (!workspace || workspace_bytes < ctx->L.total)
@@ -658,7 +679,8 @@ int pcdn_create(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_ptr, c
     ctx->row_ptr = csr_row_ptr;
     ctx->col_idx = csr_col_idx;
     ctx->csr_val = csr_val;
-    ctx->y = y;
+    // the squared loss ignores labels: a zeroed workspace array stands in when none is given
+    ctx->y = (loss == PCDN_LOSS_SQUARED && !y) ? ctx->at<int8_t>(ctx->L.ydummy) : y;
     ctx->c = c;
     ctx->loss = loss;
     ctx->stream = (cudaStream_t)cuda_stream;
@@ -687,7 +709,8 @@ int pcdn_create(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_ptr, c
     if ((rc = reset_status(ctx))) return fail(rc);
     const Layout &L = ctx->L;
     k_validate<<<grid1d(s > n ? s : n), 256, 0, ctx->stream>>>(s, n, nnz, csc_col_ptr, csc_row_idx, csc_val,
-                                                               csr_row_ptr, csr_col_idx, csr_val, y,
+                                                               csr_row_ptr, csr_col_idx, csr_val,
+                                                               loss == PCDN_LOSS_SQUARED ? nullptr : y,
                                                                ctx->at<int>(L.status), ctx->at<long long>(L.err_idx),
                                                                ctx->at<int>(L.err_what));
     k_validate_transpose<<<grid1d(s), 256, 0, ctx->stream>>>(s, csc_col_ptr, csc_row_idx, csc_val, csr_row_ptr,
@@ -709,7 +732,8 @@ int pcdn_create(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_ptr, c
         return fail(set_err(ctx, PCDN_ERR_INVALID, "invalid input: %s at index %lld", what[wv],
                             (long long)ctx->hm->err_idx));
     }
-    if ((rc = pcdn_reset(ctx))) return fail(rc);
+    // the squared loss gets its state (z, coef, F) once its targets arrive (pcdn_set_targets)
+    if (loss != PCDN_LOSS_SQUARED && (rc = pcdn_reset(ctx))) return fail(rc);
     *out = ctx;
     return PCDN_OK;
 }
@@ -724,6 +748,24 @@ int pcdn_set_armijo(pcdn_ctx *ctx, double sigma, double beta, double gamma, int 
     ctx->gamma = gamma;
     ctx->qmax = q_max;
     return PCDN_OK;
+}
+
+int pcdn_set_targets(pcdn_ctx *ctx, const double *t)
+{
+    if (!ctx) return PCDN_ERR_INVALID;
+    if (ctx->loss != PCDN_LOSS_SQUARED) return set_err(ctx, PCDN_ERR_INVALID, "targets belong to the squared loss");
+    if (!t) return set_err(ctx, PCDN_ERR_INVALID, "null targets");
+    int rc;
+    if ((rc = reset_status(ctx))) return rc;
+    k_check_finite<<<grid1d(ctx->s), 256, 0, ctx->stream>>>(t, ctx->s, ctx->at<int>(ctx->L.status),
+                                                            ctx->at<long long>(ctx->L.err_idx));
+    ctx->launches++;
+    CU(cudaGetLastError());
+    if ((rc = readback(ctx))) return rc;
+    if (ctx->hm->status)
+        return set_err(ctx, PCDN_ERR_INVALID, "non-finite target at index %lld", (long long)ctx->hm->err_idx);
+    ctx->t = t;
+    return pcdn_reset(ctx);   // w = 0, z, coef = (2(z - t), 2), F
 }
 
 int pcdn_set_elastic(pcdn_ctx *ctx, double mu)
@@ -878,8 +920,9 @@ int pcdn_objective(pcdn_ctx *ctx, int recompute_from_w, double *F_out)
         if ((rc = refresh_z(ctx, 0))) return rc;
     }
     const Layout &L = ctx->L;
+    PCDN_NEED_TARGETS(ctx);
     k_obj_partial<<<OBJ_NB, 256, 0, ctx->stream>>>(ctx->s, ctx->n, ctx->at<double>(L.z), ctx->y, ctx->at<double>(L.w),
-                                                   ctx->loss, ctx->at<double>(L.objp));
+                                                   ctx->loss, ctx->at<double>(L.objp), ctx->t);
     k_obj_final<<<1, OBJ_NB, 0, ctx->stream>>>(ctx->at<double>(L.objp), ctx->c, ctx->mu, ctx->at<double>(L.Fcopy), nullptr);
     ctx->launches += 2;
     CU(cudaGetLastError());
@@ -1076,6 +1119,7 @@ int pcdn_train_host(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_pt
                     const float *csr_val, const int8_t *y, double c, int loss, int64_t P, double eps, double f_star,
                     uint64_t seed, int32_t max_outer, void *cuda_stream, double *w_out, pcdn_solve_info *info)
 {
+    if (loss == PCDN_LOSS_SQUARED) return PCDN_ERR_INVALID;   // needs targets: use pcdn_create + pcdn_set_targets
     pcdn_ctx *ctx = nullptr;  // for CU() error text only
     if (s < 1 || n < 1 || nnz < 0 || !csc_col_ptr || !csr_row_ptr || !y || !w_out) return PCDN_ERR_INVALID;
     if (eps > 0 && !(f_star > 0)) return PCDN_ERR_INVALID;

@@ -166,7 +166,7 @@ __device__ __forceinline__ void dense_ls_partial(const StepArgs &a, DenseFixed &
         // the speculative coef for the next step's G phase, by the threads after the pairs
         if (spec) {
             for (int r = tid - ((R * nq) % NT); r < R; r += NT)
-                if (r >= 0) spec[r] = coef_of(LOSS, __fma_rn(alpha_s, sm.dx[r], sm.z[r]), sm.y[r]);
+                if (r >= 0) spec[r] = coef_next(LOSS, coefc[r], __fma_rn(alpha_s, sm.dx[r], sm.z[r]), alpha_s * sm.dx[r], sm.y[r]);
         }
     }
     for (int m = tid; m < nown; m += NT) {
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
             for (int r = tid; r < R; r += NT) {
                 const double zn = __fma_rn(alpha_acc, sm.dx[r], sm.z[r]);   // the same rounding as the speculation
                 sm.z[r] = zn;
-                if (!hit) sm.coef[cc ^ 1][r] = coef_of(LOSS, zn, sm.y[r]);
+                if (!hit) sm.coef[cc ^ 1][r] = coef_next(LOSS, sm.coef[cc][r], zn, alpha_acc * sm.dx[r], sm.y[r]);
             }
             cc ^= 1;
             if (a.debug) {

@@ -45,6 +45,7 @@ constexpr int SCAN_NT = 256;
 
 constexpr int LOSS_LOGISTIC = 0;
 constexpr int LOSS_L2SVM = 1;
+constexpr int LOSS_SQ = 2;         // squared loss (t_i - w'x_i)^2, Lasso / elastic net (reading Z26)
 
 struct __align__(16) Rec {   // one contribution d_k x_ik to sample i, k = bundle position
     int32_t k;
@@ -68,6 +69,7 @@ struct StepArgs {
     const int8_t *__restrict__ y;
     double c, sigma, beta, gamma, nu;
     double mu;   // elastic-net weight of (mu/2)||w||^2 (reading Z25; 0 = the paper's problem)
+    const double *t;   // real targets of the squared loss (reading Z26), else unused
     int loss, qmax;
     int heavy_len;
     // state
@@ -251,6 +253,15 @@ __device__ __forceinline__ double2 coef_of(int loss, double z, int yi)
     return make_double2(0.0, 0.0);
 }
 
+// The per-sample factors after a step alpha*dx from (z, cf_old): the squared loss's G = 2(z - t) is
+// linear in z, so it is carried forward by adding 2 alpha dx (no target needed; Z26); the other
+// losses re-evaluate at the new z.
+__device__ __forceinline__ double2 coef_next(int loss, double2 cf_old, double z_new, double adx, int yi)
+{
+    if (loss == LOSS_SQ) return make_double2(cf_old.x + 2.0 * adx, 2.0);
+    return coef_of(loss, z_new, yi);
+}
+
 __device__ __forceinline__ double softplus(double t) { return (t > 0 ? t : 0.0) + log1p(exp(-fabs(t))); }
 
 // phi(m), Eq.2 / Eq.3 (overflow-safe, reading Z19)
@@ -275,6 +286,10 @@ __device__ __forceinline__ double loss_change(int loss, double z, int yi, double
 {
     const double yd = (double)yi;
     if (loss == LOSS_LOGISTIC) return lr_loss_change(yd * z, alpha * (yd * dx), -cg * yd);
+    if (loss == LOSS_SQ) {   // (t - z - a)^2 - (t - z)^2 = a (a + 2(z - t)) = a (a + G), a = alpha dx (Z26)
+        const double u = alpha * dx;
+        return u * (u + cg);
+    }
     const double b1 = 1.0 - yd * (z + alpha * dx);
     const double b0 = 1.0 - yd * z;
     const double p1 = b1 > 0 ? b1 * b1 : 0.0;
@@ -1630,7 +1645,8 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
                 if (qacc >= 0) {
                     const double zn = rr.zi + alpha_acc * dx;
                     a.z[i] = zn;
-                    a.coef[i] = coef_of(a.loss, zn, rr.yi);
+                    const double2 cfo = a.loss == LOSS_SQ ? ldcg(&a.coef[i]) : make_double2(0.0, 0.0);
+                    a.coef[i] = coef_next(a.loss, cfo, zn, alpha_acc * dx, rr.yi);
                 }
                 a.cnt[i] = 0;
                 if (a.debug) {
@@ -1671,7 +1687,8 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
                 if (qacc >= 0) {
                     const double zn = zv[e] + alpha_acc * dxv[e];
                     a.z[i] = zn;
-                    a.coef[i] = coef_of(a.loss, zn, yv[e]);
+                    const double2 cfo = a.loss == LOSS_SQ ? ldcg(&a.coef[i]) : make_double2(0.0, 0.0);
+                    a.coef[i] = coef_next(a.loss, cfo, zn, alpha_acc * dxv[e], yv[e]);
                 }
                 a.cnt[i] = 0;
                 if (a.debug) {
@@ -1753,27 +1770,34 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
 // z_i = sum_j w_j x_ij over row i in ascending column order, then the cached factors.
 __global__ void k_set_z(int64_t s, const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col_idx,
                         const float *__restrict__ csr_val, const int8_t *__restrict__ y, const double *__restrict__ w,
-                        int loss, double *z, double2 *coef, int zero)
+                        int loss, double *z, double2 *coef, int zero, const double *__restrict__ t)
 {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
         double zi = 0.0;
         if (!zero)
             for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; p++) zi += w[col_idx[p]] * (double)csr_val[p];
         z[i] = zi;
-        coef[i] = coef_of(loss, zi, y[i]);
+        coef[i] = loss == LOSS_SQ ? make_double2(2.0 * (zi - t[i]), 2.0) : coef_of(loss, zi, y[i]);
     }
 }
 
 // F = c sum_i phi(y_i z_i) + sum_j |w_j|, fixed two-level order: tile b of each array
 constexpr int OBJ_NB = 256;
 __global__ void k_obj_partial(int64_t s, int64_t n, const double *__restrict__ z, const int8_t *__restrict__ y,
-                              const double *__restrict__ w, int loss, double *partial)
+                              const double *__restrict__ w, int loss, double *partial, const double *__restrict__ t)
 {
     const int b = blockIdx.x;
     const int64_t zs0 = (int64_t)b * s / OBJ_NB, zs1 = (int64_t)(b + 1) * s / OBJ_NB;
     const int64_t ws0 = (int64_t)b * n / OBJ_NB, ws1 = (int64_t)(b + 1) * n / OBJ_NB;
     double ls = 0.0, l1 = 0.0, l2 = 0.0;
-    for (int64_t i = zs0 + threadIdx.x; i < zs1; i += blockDim.x) ls += phi_of(loss, (double)y[i] * z[i]);
+    for (int64_t i = zs0 + threadIdx.x; i < zs1; i += blockDim.x) {
+        if (loss == LOSS_SQ) {
+            const double r = t[i] - z[i];
+            ls += r * r;
+        } else {
+            ls += phi_of(loss, (double)y[i] * z[i]);
+        }
+    }
     for (int64_t j = ws0 + threadIdx.x; j < ws1; j += blockDim.x) {
         l1 += fabs(w[j]);
         l2 += w[j] * w[j];
@@ -1825,6 +1849,16 @@ __global__ void k_obj_final(const double *__restrict__ partial, double c, double
     }
 }
 
+// status 1 + first index of a non-finite value (squared-loss targets)
+__global__ void k_check_finite(const double *__restrict__ t, int64_t s, int *status, long long *err_idx)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x)
+        if (!isfinite(t[i])) {
+            atomicMax(status, 1);
+            atomicMin(err_idx, (long long)i);
+        }
+}
+
 // Input validation: code 1 + first offending index.
 __global__ void k_validate(int64_t s, int64_t n, int64_t nnz, const int64_t *__restrict__ col_ptr,
                            const int32_t *__restrict__ row_idx, const float *__restrict__ val,
@@ -1867,7 +1901,7 @@ __global__ void k_validate(int64_t s, int64_t n, int64_t nnz, const int64_t *__r
             if (p > a0 && cidx <= col_idx[p - 1]) fail(11, p);
             if (!isfinite(csr_val[p])) fail(12, p);
         }
-        if (y[i] != 1 && y[i] != -1) fail(13, i);
+        if (y && y[i] != 1 && y[i] != -1) fail(13, i);   // labels unused by the squared loss
     }
 }
 

@@ -239,7 +239,7 @@ __device__ __forceinline__ double2 res_coef(const StepArgs &a, const ResCtx &R, 
     const double2 cf = *remote(&R.coef[li], owner);
     const int yi = res_ybit(R, i);   // local bitmap: no dependent L2 load for a touched sample
     if (zd.y == 0.0) return cf;
-    return coef_of(a.loss, zd.x + R.alpha_prev * zd.y, yi);
+    return coef_next(a.loss, cf, zd.x + R.alpha_prev * zd.y, R.alpha_prev * zd.y, yi);
 }
 
 // Send the records (sample i, bundle position k, d_k x_ik) of the warp's valid lanes to their
@@ -446,7 +446,7 @@ __device__ __forceinline__ void res_lazy_commit(const StepArgs &a, const ResCtx 
         if (zd.y == 0.0) continue;
         const double zn = zd.x + R.alpha_prev * zd.y;
         R.zd[li] = make_double2(zn, 0.0);
-        R.coef[li] = coef_of(a.loss, zn, res_y(R, li));
+        R.coef[li] = coef_next(a.loss, R.coef[li], zn, R.alpha_prev * zd.y, res_y(R, li));
     }
 }
 
@@ -1137,7 +1137,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
                 if (zd.y == 0.0) continue;
                 const double zn = zd.x + R.alpha_prev * zd.y;
                 R.zd[li] = make_double2(zn, 0.0);
-                R.coef[li] = coef_of(a.loss, zn, res_y(R, li));
+                R.coef[li] = coef_next(a.loss, R.coef[li], zn, R.alpha_prev * zd.y, res_y(R, li));
             }
         }
 

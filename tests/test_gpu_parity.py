@@ -452,3 +452,64 @@ def test_knob_validation(pk):
     r = s.solve(4, seed=1, max_outer=3, trace=True)   # still usable
     _compare_solve(r, o.solve(4, seed=1, max_outer=3), s.w().cpu().numpy(), "after invalid knobs")
     s.close()
+
+
+# ----------------------------------------------------------------------------- Lasso (squared loss)
+@pytest.mark.parametrize("mu", [0.0, 1.0])
+@pytest.mark.parametrize("launch", [(0, 0, 0), (1, 4, 0), (2, 0, 0), (2, 3, 2), (3, 0, 0), (3, 16, 1)])
+def test_lasso_parity(pk, mu, launch):
+    """Lasso / elastic-net regression (NEXT #4, reading Z26): F = c sum (t_i - w'x_i)^2 + ||w||_1
+    (+ mu/2 ||w||^2) through every step kernel: steps from injected states and a short solve
+    against the oracle (whose G = 2(z - t) is re-evaluated, while the kernels carry G forward)."""
+    rng = np.random.default_rng(17 + int(mu))
+    ties = []
+    for case in (0, 2, 4):
+        kw = dict(TINY[case])
+        prob = synth.regression(synth.tiny(c=0.7, P=5, **kw), noise=0.2, support=4)
+        s = _solver(pk, prob, *launch)
+        if mu:
+            s.set_elastic(mu)
+        o = oracle.Oracle(prob, mu=mu)
+        for rep in range(2):
+            w = _random_state(rng, prob.n, scale=0.4 * (rep + 1))
+            for B in _step_cases(prob, rng, nb=3):
+                s.set_w(w)
+                _compare_step(s.step(B), o.step(w, B), ties)
+        s.reset()
+        gs = s.solve(5, seed=9, max_outer=5, trace=True)
+        os_ = o.solve(5, seed=9, max_outer=5)
+        _compare_solve(gs, os_, s.w().cpu().numpy(), f"lasso mu={mu} launch={launch} case={case}")
+        s.close()
+    assert len(ties) <= 2, ties
+
+
+def test_lasso_dense_kernel_and_targets_api(pk):
+    """The dense kernel on a regression problem; a squared-loss context refuses state-dependent
+    calls until its targets arrive, and refuses non-finite targets."""
+    prob = synth.regression(synth.tiny(31, 40, 200, density=1.0, c=2.0, P=50), noise=0.3, support=10)
+    s = _solver(pk, prob, 4, 3)
+    o = oracle.Oracle(prob)
+    gs = s.solve(50, seed=3, max_outer=4, trace=True)
+    os_ = o.solve(50, seed=3, max_outer=4)
+    _compare_solve(gs, os_, s.w().cpu().numpy(), "lasso dense", ftrace_rtol=1e-7)
+    bad = s.torch.full((prob.s,), float("nan"), dtype=s.torch.float64, device=s.device)
+    with pytest.raises(pk.PCDNError) as ei:
+        pk.pcdn_set_targets(s.ctx, bad)
+    assert ei.value.status == pk.PCDN_ERR_INVALID
+    s.close()
+    # a context created for the squared loss without targets: state-dependent calls are invalid
+    import torch
+    dev = torch.device("cuda")
+    T = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(dev)  # noqa: E731
+    arrs = [T(prob.col_ptr, np.int64), T(prob.row_idx, np.int32), T(prob.val, np.float32),
+            T(prob.row_ptr, np.int64), T(prob.col_idx, np.int32), T(prob.csr_val, np.float32)]
+    ws = torch.empty(pk.pcdn_workspace_bytes(prob.s, prob.n, prob.nnz), dtype=torch.uint8, device=dev)
+    ctx = pk.pcdn_create(prob.s, prob.n, prob.nnz, *arrs, None, prob.c, pk.PCDN_LOSS_SQUARED, ws,
+                         torch.cuda.current_stream(dev))
+    with pytest.raises(pk.PCDNError) as ei:
+        pk.pcdn_reset(ctx)
+    assert ei.value.status == pk.PCDN_ERR_INVALID
+    t = T(prob.t, np.float64)
+    pk.pcdn_set_targets(ctx, t)
+    assert math.isclose(pk.pcdn_objective(ctx, 0), o.objective(np.zeros(prob.n)), rel_tol=1e-12)
+    pk.pcdn_destroy(ctx)
