@@ -87,7 +87,8 @@ size_t pcdn_workspace_bytes(int64_t s, int64_t n, int64_t nnz);
  *   csc_row_idx[nnz] (int32, strictly increasing inside each column, < s),
  *   csc_val[nnz] (fp32, finite) -- column x^j of X;
  *   csr_row_ptr[s+1], csr_col_idx[nnz], csr_val[nnz] -- the same nonzeros by row;
- *   y[s] (int8 in {-1,+1}); c > 0 (Eq.1); loss = PCDN_LOSS_*.
+ *   y[s] (int8 in {-1,+1}; ignored, and may be NULL, for PCDN_LOSS_SQUARED, whose
+ *   real targets come from pcdn_set_targets); c > 0 (Eq.1); loss = PCDN_LOSS_*.
  *   workspace: device buffer of >= pcdn_workspace_bytes(s,n,nnz) bytes, 256-byte aligned.
  *   cuda_stream: cudaStream_t (NULL = legacy default stream).
  * Validates every invariant above on the device (PCDN_ERR_INVALID names the first offending
