@@ -180,6 +180,15 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t a, int rank)
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
     return r;
 }
+// 16-byte load from another CTA's shared memory by a shared::cluster address (mapa), without
+// generic-address translation
+__device__ __forceinline__ double2 ld_dsmem_f64x2(uint32_t raddr)
+{
+    double2 v;
+    asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(raddr) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ void st_async_u32(uint32_t raddr, uint32_t v, uint32_t rbar)
 {
     RCHK(raddr, 4, 4);
@@ -235,8 +244,8 @@ __device__ __forceinline__ double2 res_coef(const StepArgs &a, const ResCtx &R, 
 {
     const int owner = i & (R.G - 1);
     const int li = i >> R.lg;
-    const double2 zd = *remote(&R.zd[li], owner);
-    const double2 cf = *remote(&R.coef[li], owner);
+    const double2 zd = ld_dsmem_f64x2(mapa_u32(s_addr(&R.zd[li]), owner));
+    const double2 cf = ld_dsmem_f64x2(mapa_u32(s_addr(&R.coef[li]), owner));
     const int yi = res_ybit(R, i);   // local bitmap: no dependent L2 load for a touched sample
     if (zd.y == 0.0) return cf;
     return coef_next(a.loss, cf, zd.x + R.alpha_prev * zd.y, R.alpha_prev * zd.y, yi);
