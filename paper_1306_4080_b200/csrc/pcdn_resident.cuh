@@ -500,6 +500,15 @@ __device__ __forceinline__ void res_stage_cols(const StepArgs &a, ResFixed &fx, 
     __syncwarp();
 }
 
+// The owner state of the next step's first staged column, gathered while the current step's
+// decision is taken (valid from the M2 arrival of window 0 to the next step's M0: no owner writes
+// its samples in between)
+struct Pref {
+    double2 zd, cf;
+    int y;
+    bool ok;
+};
+
 // One Armijo window over candidates q0 .. q0+NQ-1 (Eq.6 with Eq.12 from retained quantities):
 // per-sample loss changes over this CTA's touched samples (window 0 also folds d'x_i), the L1
 // term and Delta over the CTA's own bundle positions, a fixed-order CTA partial row, sent to
@@ -508,7 +517,7 @@ __device__ __forceinline__ void res_stage_cols(const StepArgs &a, ResFixed &fx, 
 template <int NQ>
 __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, WinState &ws, int64_t k0, int64_t k1,
                                           int tid, int lane, int warp, ResProf &pr, int wcount, const DenseInfo &di,
-                                          int64_t kn0, int64_t kn1)
+                                          int64_t kn0, int64_t kn1, Pref &pf)
 {
     using LY = WinLayout<NQ>;
     constexpr int W = LY::W;
@@ -720,6 +729,19 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
     if (ws.win == 0) RTL(R, 10);
     mbar_wait(mb2, (uint32_t)((wcount >> 1) & 1));
     if (ws.win == 0) RTL(R, 11);
+    // every fold of this step is done (all partial rows arrived): gather the owner state of the
+    // next step's first staged column now, overlapped with the decision below
+    if (ws.win == 0 && kn0 < kn1) {
+        const int len = fx.stg_ci[warp][0].y;
+        pf.ok = len >= 0 && len <= a.heavy_len;
+        if (pf.ok && lane < len) {
+            const int32_t i = fx.stg_r[warp][0][lane];
+            const int owner = i & (R.G - 1), li = i >> R.lg;
+            pf.zd = ld_dsmem_f64x2(mapa_u32(s_addr(&R.zd[li]), owner));
+            pf.cf = ld_dsmem_f64x2(mapa_u32(s_addr(&R.coef[li]), owner));
+            pf.y = res_ybit(R, i);
+        }
+    }
     pr.mark(fx, 4);
     // warp 0: the G partial rows (local now), fixed-order tree, decision; broadcast in the CTA
     // (every CTA computes the identical decision)
@@ -883,6 +905,8 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
     const bool prof = pr.on;
 #define PROF_MARK(i) pr.mark(fx, i)
     int prev_q = 0;
+    Pref pf;
+    pf.ok = false;
     int wcount = 0;            // windows so far in this launch (M2 phase parity)
     uint32_t ph = 0;           // bit 0: M0 parity, bit 1: M1 parity
     res_stage_cols(a, fx, 0, min(a.P, a.ntot), gw, GN, warp, lane);
@@ -917,7 +941,14 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
                     if (stg) {
                         if (lane < len) {
                             const double x = (double)fx.stg_x[warp][m][lane];
-                            const double2 cf = res_coef(a, R, fx.stg_r[warp][m][lane]);
+                            double2 cf;
+                            if (m == 0 && pf.ok) {   // gathered during the previous step's decision
+                                cf = pf.zd.y == 0.0 ? pf.cf
+                                                    : coef_next(a.loss, pf.cf, pf.zd.x + R.alpha_prev * pf.zd.y,
+                                                                R.alpha_prev * pf.zd.y, pf.y);
+                            } else {
+                                cf = res_coef(a, R, fx.stg_r[warp][m][lane]);
+                            }
                             g += x * cf.x;
                             h += (x * x) * cf.y;
                         }
@@ -968,6 +999,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
             }
         }
 
+        pf.ok = false;   // consumed (re-gathered by this step's first window for the next step)
         RTL(R, 1);
         PROF_MARK(8);
         // ---------------- phase A': heavy columns, nnz-balanced over all warps -----------
@@ -1253,8 +1285,8 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         ws.bad = 0;
         ws.win = 0;
         while (true) {
-            if (ws.nq <= 2) res_window<2>(a, R, ws, k0, k1, tid, lane, warp, pr, wcount, di, k1, kn1);
-            else res_window<QW>(a, R, ws, k0, k1, tid, lane, warp, pr, wcount, di, k1, kn1);
+            if (ws.nq <= 2) res_window<2>(a, R, ws, k0, k1, tid, lane, warp, pr, wcount, di, k1, kn1, pf);
+            else res_window<QW>(a, R, ws, k0, k1, tid, lane, warp, pr, wcount, di, k1, kn1, pf);
             wcount++;
             if (ws.qacc >= 0 || ws.bad) break;
             ws.q0 += ws.nq;
