@@ -730,18 +730,22 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
     mbar_wait(mb2, (uint32_t)((wcount >> 1) & 1));
     if (ws.win == 0) RTL(R, 11);
     // every fold of this step is done (all partial rows arrived): gather the owner state of the
-    // next step's first staged column now, overlapped with the decision below
-    if (ws.win == 0 && kn0 < kn1) {
-        const int len = fx.stg_ci[warp][0].y;
-        pf.ok = len >= 0 && len <= a.heavy_len;
-        if (pf.ok && lane < len) {
-            const int32_t i = fx.stg_r[warp][0][lane];
-            const int owner = i & (R.G - 1), li = i >> R.lg;
-            pf.zd = ld_dsmem_f64x2(mapa_u32(s_addr(&R.zd[li]), owner));
-            pf.cf = ld_dsmem_f64x2(mapa_u32(s_addr(&R.coef[li]), owner));
-            pf.y = res_ybit(R, i);
+    // next step's first staged column now, overlapped with the decision below (warp 0, which takes
+    // the decision, gathers after it: its shared-memory reads must not queue behind remote loads)
+    auto prefetch = [&]() {
+        if (ws.win == 0 && kn0 < kn1) {
+            const int len = fx.stg_ci[warp][0].y;
+            pf.ok = len >= 0 && len <= a.heavy_len;
+            if (pf.ok && lane < len) {
+                const int32_t i = fx.stg_r[warp][0][lane];
+                const int owner = i & (R.G - 1), li = i >> R.lg;
+                pf.zd = ld_dsmem_f64x2(mapa_u32(s_addr(&R.zd[li]), owner));
+                pf.cf = ld_dsmem_f64x2(mapa_u32(s_addr(&R.coef[li]), owner));
+                pf.y = res_ybit(R, i);
+            }
         }
-    }
+    };
+    if (warp != 0) prefetch();
     pr.mark(fx, 4);
     // warp 0: the G partial rows (local now), fixed-order tree, decision; broadcast in the CTA
     // (every CTA computes the identical decision)
@@ -784,6 +788,7 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
             fx.dec_Delta[buf] = Dl;
             fx.dec_nT[buf] = nTt;
         }
+        prefetch();
     }
     __syncthreads();   // dec_*[buf] is rewritten two windows later, after two more syncs
     ws.qacc = fx.dec_q[buf];
