@@ -29,7 +29,7 @@ constexpr int QW = 6;              // Armijo candidates of a wide line-search wi
 constexpr int NPART = 32;          // per-CTA partial slots (packed: Ls[nq], L1[nq], Delta, |T|)
 constexpr int WREG = 4;            // bitmap words per thread kept in registers in phase C1
 constexpr int NE_MAX = 64;         // heavy entries handled per round inside one CTA
-constexpr int NREG = 8;            // rows with <= NREG records are folded by one thread
+constexpr int NREG = 4;            // rows with <= NREG records are folded by one thread
 constexpr int SHORT = 8;           // columns with <= SHORT nonzeros are reduced by one thread
 constexpr int MED_LEN = 128;       // ... with <= MED_LEN by one warp
 constexpr int CTA_LEN = 2048;      // ... with <= CTA_LEN by one CTA in the HBM-state kernels (default)
@@ -773,6 +773,9 @@ __device__ __forceinline__ double fold_small(const StepArgs &a, int64_t off, int
         last = best;
         dx += bv;
     }
+    // every record of a sample has its own bundle position: a repeat would have been dropped above
+    // (and summed by the warp fold), so it is an internal error, never a silent fix
+    if (last == 0x7fffffff) atomicMax(a.status, 6);
     return dx;
 }
 
@@ -1199,7 +1202,8 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
             const int64_t kk = kb + lane;
             const int4 ci = (lane < cw && kk < k1) ? __ldg(&a.colinfo[kk]) : make_int4(0, -1, 0, 0);
             const int len = ci.y;
-            if (len >= 0 && len <= SHORT) {
+            // (a column longer than heavy_len belongs to the heavy path alone, however short)
+            if (len >= 0 && len <= SHORT && len <= a.heavy_len) {
                 const int32_t j = ci.x;
                 const int64_t p0 = colinfo_p0(ci);
                 int32_t ri[SHORT];

@@ -593,6 +593,7 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
                     last = best;
                     dx += bv;
                 }
+                if (last == 0x7fffffff) atomicMax(a.status, 6);   // a repeated position: internal error
             }
             dx = dxd + dx;
             R.zd[li] = make_double2(zd.x, dx);
