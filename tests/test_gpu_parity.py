@@ -513,3 +513,24 @@ def test_lasso_dense_kernel_and_targets_api(pk):
     pk.pcdn_set_targets(ctx, t)
     assert math.isclose(pk.pcdn_objective(ctx, 0), o.objective(np.zeros(prob.n)), rel_tol=1e-12)
     pk.pcdn_destroy(ctx)
+
+
+@pytest.mark.parametrize("launch", [(1, 4, 2), (2, 3, 2), (2, 0, 1), (1, 1, 3)])
+def test_short_columns_with_small_split_length(pk, launch):
+    """Regression: with a split length below the lane path's 8 nonzeros, a short column must be
+    reduced once (by the heavy path), not also by its lane -- duplicates went unnoticed where the
+    register fold drops repeated positions and corrupted d'x where a warp folds a long list (a
+    dense row).  Columns of 3-8 nonzeros, one dense row, whole-problem bundles."""
+    for loss in (LOSS_LOGISTIC, LOSS_L2SVM):
+        prob = synth.tiny(606, 30, 40, density=0.15, loss=loss, c=2.0, dense_rows=1, P=40)
+        s = _solver(pk, prob, *launch)
+        o = oracle.Oracle(prob)
+        rng = np.random.default_rng(606)
+        ties = []
+        for rep in range(3):
+            w = _random_state(rng, prob.n, scale=0.3 * rep)
+            for B in (np.arange(prob.n, dtype=np.int32), rng.permutation(prob.n)[:25].astype(np.int32)):
+                s.set_w(w)
+                _compare_step(s.step(B), o.step(w, B), ties)
+        assert len(ties) <= 1, ties
+        s.close()
