@@ -95,6 +95,9 @@ def lib():
         L.ora_cdn.restype = C.c_int
         L.ora_cdn.argtypes = [C.POINTER(_Prob), C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32,
                               C.c_void_p, C.c_int64, C.POINTER(C.c_double)]
+        L.ora_scdn.restype = C.c_int
+        L.ora_scdn.argtypes = [C.POINTER(_Prob), C.c_void_p, C.c_void_p, C.c_int64, C.c_uint64, C.c_int32,
+                               C.c_void_p, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_double)]
         L.ora_min_norm_subgrad.restype = C.c_double
         L.ora_min_norm_subgrad.argtypes = [C.POINTER(_Prob), C.c_void_p, C.c_void_p, C.c_void_p]
         L.ora_loss_change.restype = C.c_double
@@ -234,6 +237,18 @@ class Oracle:
         return dict(rc=rc, w=w, z=z, F=info.F, gap=info.gap, outer=int(info.outer_iters),
                     steps=int(info.steps), nnz=int(info.nnz_processed), touched=int(info.touched_total), null_steps=int(info.null_steps),
                     q_trace=qt[:ns].copy(), F_trace=Ft[:ns].copy(), outer_F=oF[:int(info.outer_iters)].copy())
+
+    def scdn(self, Pbar, seed=0, max_outer=10, w0=None):
+        """Alg.2 (Shotgun CDN), synchronous reading Z27: the F trace has one entry per iteration."""
+        w = np.zeros(self.n) if w0 is None else np.array(w0, dtype=np.float64, copy=True)
+        z = np.zeros(self.s)
+        cap = max_outer * (-(-self.n // int(Pbar)))
+        Ft = np.zeros(max(cap, 1))
+        steps = C.c_int64()
+        F = C.c_double()
+        rc = lib().ora_scdn(C.byref(self.pb), _p(w), _p(z), int(Pbar), seed & 0xFFFFFFFFFFFFFFFF, int(max_outer),
+                            _p(Ft), cap, C.byref(steps), C.byref(F))
+        return dict(rc=rc, w=w, z=z, F=F.value, steps=int(steps.value), F_trace=Ft[:int(steps.value)].copy())
 
     def cdn(self, seed=0, max_outer=10, w0=None, trace=False):
         w = np.zeros(self.n) if w0 is None else np.array(w0, dtype=np.float64, copy=True)

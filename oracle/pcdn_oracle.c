@@ -21,6 +21,7 @@
  *   App.A.2 L2-SVM generalized Hessian, nu = 1e-12
  *   Eq.14 relative function value difference
  *   Alg.1 CDN (separately coded, for the P=1 reduction)
+ *   Alg.2 SCDN (Shotgun CDN, NEXT #3; synchronous reading Z27)
  *   Lasso (NEXT #4; "easily extended to ... Lasso"): the squared loss
  *   phi = (t_i - w'x_i)^2 with real targets t (reading Z26): G = 2(z - t), H = 2, the line-search
  *   summand (t - z - a dx)^2 - (t - z)^2 = a dx (a dx + 2(z - t)).
@@ -639,6 +640,76 @@ int ora_cdn(const ora_prob *pb, double *w, double *z, uint64_t seed, int32_t max
     }
     if (F_out) *F_out = ora_objective(pb, z, w);
     free(perm);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------------ */
+/* SCDN, Alg.2, synchronous reading Z27: each iteration takes the */
+/* next P-bar features of the partition stream pi_k (the same bundles PCDN visits);   */
+/* every feature computes d_j (Eq.5) and its own 1-D Armijo step alpha_j (Eq.6 with   */
+/* d = d_j e_j, direct phi differences over its column) at the iteration's start      */
+/* state, then ALL updates w_j += alpha_j d_j are applied together (the deterministic */
+/* limit of Shotgun's concurrent updates).  No P-dimensional line search: F may rise  */
+/* when correlated features move together.  P-bar = 1 is CDN.          */
+/* ------------------------------------------------------------------------------ */
+int ora_scdn(const ora_prob *pb, double *w, double *z, int64_t Pbar, uint64_t seed, int32_t max_outer,
+             double *F_trace, int64_t trace_cap, int64_t *steps_out, double *F_out)
+{
+    const int64_t n = pb->n;
+    if (Pbar < 1 || Pbar > n) return ORA_ERR_INVALID;
+    int32_t *perm = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+    double *step = (double *)malloc(sizeof(double) * (size_t)Pbar);
+    ora_compute_z(pb, w, z);
+    int64_t steps = 0;
+    int rc = ORA_OK;
+    for (int32_t k = 0; k < max_outer && rc == ORA_OK; k++) {
+        ora_permutation(seed, k, n, perm);
+        for (int64_t t0 = 0; t0 < n; t0 += Pbar) {
+            const int64_t Pt = (n - t0) < Pbar ? (n - t0) : Pbar;
+            for (int64_t kk = 0; kk < Pt; kk++) {          /* "in parallel": all from the same state */
+                const int64_t j = perm[t0 + kk];
+                double g, h;
+                gh_one(pb, z, w, j, &g, &h, NULL, NULL);
+                const double wj = w[j];
+                const double dj = ora_newton_dir(g, h, wj);
+                const double Delta = g * dj + pb->gamma * h * dj * dj + fabs(wj + dj) - fabs(wj);
+                double alpha = 1.0, take = 0.0;
+                for (int32_t q = 0; q <= pb->qmax; q++) {
+                    double chg = 0.0;
+                    for (int64_t p = pb->col_ptr[j]; p < pb->col_ptr[j + 1]; p++) {
+                        const int64_t i = pb->row_idx[p];
+                        const double znew = z[i] + alpha * dj * (double)pb->val[p];
+                        chg += phi_i(pb, i, znew) - phi_i(pb, i, z[i]);
+                    }
+                    const double wn = wj + alpha * dj;
+                    const double lhs = pb->c * chg + fabs(wn) - fabs(wj) + 0.5 * pb->mu * (wn * wn - wj * wj);
+                    if (lhs <= pb->sigma * alpha * Delta) {
+                        take = alpha;
+                        break;
+                    }
+                    alpha *= pb->beta;
+                }
+                step[kk] = take * dj;                       /* null step (Z10): 0 */
+            }
+            for (int64_t kk = 0; kk < Pt; kk++) {          /* apply all updates together */
+                const int64_t j = perm[t0 + kk];
+                if (step[kk] == 0.0) continue;
+                w[j] += step[kk];
+                for (int64_t p = pb->col_ptr[j]; p < pb->col_ptr[j + 1]; p++)
+                    z[pb->row_idx[p]] += step[kk] * (double)pb->val[p];
+            }
+            if (F_trace && steps < trace_cap) F_trace[steps] = ora_objective(pb, z, w);
+            steps++;
+            if (!isfinite(ora_objective(pb, z, w))) {
+                rc = ORA_ERR_NUMERIC;
+                break;
+            }
+        }
+    }
+    if (steps_out) *steps_out = steps;
+    if (F_out) *F_out = ora_objective(pb, z, w);
+    free(perm);
+    free(step);
     return rc;
 }
 

@@ -753,3 +753,53 @@ def test_squared_line_search_incremental_vs_direct(oracle_mod):
         r1 = o.step(w, B, mode=1)
         assert r0["q"] == r1["q"]
         assert math.isclose(r0["lhs"], r1["lhs"], rel_tol=1e-8, abs_tol=1e-10 * (1 + r0["lhs_abs"]))
+
+
+# ------------------------------------------------------------------ SCDN (NEXT #3, Z27)
+@pytest.mark.parametrize("loss", LOSSES)
+def test_scdn_pbar1_is_cdn(oracle_mod, loss):
+    """Alg.2 with P-bar = 1 updates one coordinate at a time with its own 1-D Armijo step: it IS
+    the separately coded CDN (Alg.1), iterate for iterate."""
+    for seed in range(3):
+        p = synth.tiny(300 + seed, 30, 12, density=0.3, loss=loss, c=3.0)
+        o = oracle_mod.Oracle(p)
+        a = o.scdn(1, seed=seed, max_outer=5)
+        b = o.cdn(seed=seed, max_outer=5, trace=True)
+        np.testing.assert_allclose(a["w"], b["w"], rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(a["F_trace"], b["F_trace"], rtol=1e-12)
+
+
+@pytest.mark.parametrize("loss", LOSSES)
+def test_scdn_can_increase_F_where_pcdn_cannot(oracle_mod, loss):
+    """with correlated features SCDN's parallel updates (no joint line search) can
+    increase F; PCDN on the same bundles is monotone (Lemma 1(c) + the P-dim Armijo rule).  Each
+    SCDN update alone passes its own Armijo test (checked with numpy)."""
+    rng = np.random.default_rng(7)
+    Xc = rng.normal(size=(40, 1)) @ np.ones((1, 16)) + 0.02 * rng.normal(size=(40, 16))   # near-duplicate columns
+    p = synth.from_dense(Xc, np.where(rng.random(40) < 0.5, 1, -1), c=10.0, loss=loss)
+    o = oracle_mod.Oracle(p)
+    F0 = o.objective(np.zeros(p.n))
+    sc = o.scdn(16, seed=1, max_outer=3)
+    Fs = np.concatenate([[F0], sc["F_trace"]])
+    assert np.any(np.diff(Fs) > 1e-9 * F0)          # SCDN rises somewhere
+    pc = o.solve(16, seed=1, max_outer=3)
+    Fp = np.concatenate([[F0], pc["F_trace"]])
+    assert np.all(np.diff(Fp) <= 1e-12 * F0)         # PCDN never does
+    # and the one-dimensional steps of the first SCDN iteration each pass Armijo alone
+    X = p.dense()
+    w = np.zeros(p.n)
+    g, h = o.gh(w)
+    for j in range(p.n):
+        d = oracle_mod.newton_dir(g[j], h[j], 0.0)
+        delta = g[j] * d + abs(d)
+        if d == 0.0:
+            continue
+        ok = False
+        for q in range(51):
+            a = 0.5 ** q
+            e = np.zeros(p.n)
+            e[j] = a * d
+            if np_F(p, e, X) - np_F(p, w, X) <= 0.01 * a * delta + 1e-12:
+                ok = True
+                break
+        assert ok
