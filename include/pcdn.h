@@ -167,6 +167,15 @@ int pcdn_set_debug(pcdn_ctx *ctx, int on);
  * columns of 129..2048 nonzeros are reduced by one CTA, 128 for mode 3). */
 int pcdn_set_launch(pcdn_ctx *ctx, int mode, int ctas, int heavy_len);
 
+/* SCDN baseline (Alg.2 Shotgun CDN; reading Z27): with
+ * on != 0, pcdn_bundle_step / pcdn_solve run SCDN instead of PCDN -- each feature of a bundle (of
+ * size P-bar = P) takes its own 1-D Armijo step from the bundle's start state and all updates are
+ * applied together, with no P-dimensional line search (the accepted q is reported as 0).  The
+ * paper's setting is P-bar = 8.  Runs on the cluster-resident kernel only: a
+ * solve/step returns PCDN_ERR_INVALID in another launch mode, or when a bundle column is longer
+ * than the warp split length (pcdn_set_launch's heavy_len).  PCDN_ERR_INVALID: null context. */
+int pcdn_set_scdn(pcdn_ctx *ctx, int on);
+
 /* Squared loss (PCDN_LOSS_SQUARED, reading Z26): borrow the real targets t (DEVICE fp64[s], kept
  * alive and unmodified by the caller) -- F = c sum_i (t_i - w'x_i)^2 + ||w||_1 (+ elastic net).
  * Required before any state-dependent call on a squared-loss context (those return

@@ -19,7 +19,7 @@ from ._abi import (  # noqa: F401
 __all__ = [
     "pcdn_workspace_bytes", "pcdn_create", "pcdn_set_armijo", "pcdn_set_reference", "pcdn_bundle_step",
     "pcdn_last_touched", "pcdn_solve", "pcdn_objective", "pcdn_get_w", "pcdn_set_w", "pcdn_get_z",
-    "pcdn_reset", "pcdn_permutation", "pcdn_set_trace", "pcdn_set_debug", "pcdn_set_launch", "pcdn_set_resident_cap", "pcdn_set_l2_persist", "pcdn_set_elastic", "pcdn_set_targets", "pcdn_set_profile", "pcdn_phase_cycles", "pcdn_warp_timeline",
+    "pcdn_reset", "pcdn_permutation", "pcdn_set_trace", "pcdn_set_debug", "pcdn_set_launch", "pcdn_set_resident_cap", "pcdn_set_l2_persist", "pcdn_set_elastic", "pcdn_set_targets", "pcdn_set_scdn", "pcdn_set_profile", "pcdn_phase_cycles", "pcdn_warp_timeline",
     "pcdn_last_error", "pcdn_destroy", "pcdn_train_host", "pcdn_version", "Solver", "PCDNError",
 ]
 
@@ -131,6 +131,10 @@ def pcdn_set_debug(ctx, on):
 
 def pcdn_set_launch(ctx, mode=0, ctas=0, heavy_len=0):
     return check(ctx, lib().pcdn_set_launch(ctx, int(mode), int(ctas), int(heavy_len)))
+
+
+def pcdn_set_scdn(ctx, on):
+    return check(ctx, lib().pcdn_set_scdn(ctx, int(bool(on))))
 
 
 def pcdn_set_targets(ctx, t):
@@ -290,6 +294,10 @@ class Solver:
             res["q_trace"] = qt[:ns].cpu().numpy()
             res["F_trace"] = Ft[:ns].cpu().numpy()
         return res
+
+    def set_scdn(self, on=True):
+        """Run SCDN (Alg.2, synchronous reading Z27) instead of PCDN (pcdn_set_scdn)."""
+        pcdn_set_scdn(self.ctx, on)
 
     def set_elastic(self, mu):
         """Elastic-net weight: minimise c sum phi + ||w||_1 + (mu/2)||w||^2 (pcdn_set_elastic)."""

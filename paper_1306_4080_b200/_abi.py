@@ -66,6 +66,7 @@ SIGNATURES = {
     "pcdn_set_l2_persist": (C.c_int, [P, C.c_int]),
     "pcdn_set_elastic": (C.c_int, [P, C.c_double]),
     "pcdn_set_targets": (C.c_int, [P, C.c_void_p]),
+    "pcdn_set_scdn": (C.c_int, [P, C.c_int]),
     "pcdn_set_profile": (C.c_int, [P, C.c_int]),
     "pcdn_phase_cycles": (C.c_int, [P, P, C.POINTER(C.c_int32)]),
     "pcdn_warp_timeline": (C.c_int, [P, P]),

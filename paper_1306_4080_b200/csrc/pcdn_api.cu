@@ -135,6 +135,7 @@ struct pcdn_ctx {
     int loss = 0;
     double sigma = 0.01, beta = 0.5, gamma = 0.0, nu = 1e-12;
     double mu = 0.0;   // elastic-net weight (pcdn_set_elastic; reading Z25)
+    int scdn = 0;      // pcdn_set_scdn (Alg.2, reading Z27)
     int qmax = 50;
     double fstar = 0.0;
     bool has_fstar = false;
@@ -255,6 +256,8 @@ int prep_outer(pcdn_ctx *ctx, uint64_t seed, int64_t k, int buf, cudaStream_t st
     return build_heavy(ctx, ctx->n, buf, st);
 }
 
+#define SCDN_HEAVY_MSG "SCDN: a bundle column is longer than the warp split length; raise it with pcdn_set_launch(ctx, 3, 0, L)"
+
 // the squared loss has no state before its targets are given (pcdn_set_targets)
 #define PCDN_NEED_TARGETS(ctx)                                                                             \
     do {                                                                                                   \
@@ -337,6 +340,7 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
     a.row_ptr = ctx->row_ptr;
     a.y = ctx->y;
     a.t = ctx->t;
+    a.scdn = ctx->scdn;
     a.c = ctx->c;
     a.sigma = ctx->sigma;
     a.beta = ctx->beta;
@@ -410,6 +414,8 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
     // grid mode (all SMs, software barrier) for large steps
     const int mode = choose_mode(ctx, P);
     ctx->last_mode = mode;
+    if (ctx->scdn && mode != 3)
+        return set_err(ctx, PCDN_ERR_INVALID, "SCDN runs on the cluster-resident kernel (mode 3; samples must fit)");
     if (mode == 4) {
         if (ctx->Gd < 1) return set_err(ctx, PCDN_ERR_INVALID, "dense step kernel unavailable for this problem");
         void *args[] = {&a};
@@ -768,6 +774,13 @@ int pcdn_set_targets(pcdn_ctx *ctx, const double *t)
     return pcdn_reset(ctx);   // w = 0, z, coef = (2(z - t), 2), F
 }
 
+int pcdn_set_scdn(pcdn_ctx *ctx, int on)
+{
+    if (!ctx) return PCDN_ERR_INVALID;
+    ctx->scdn = on ? 1 : 0;
+    return PCDN_OK;
+}
+
 int pcdn_set_elastic(pcdn_ctx *ctx, double mu)
 {
     if (!ctx) return PCDN_ERR_INVALID;
@@ -985,6 +998,7 @@ int pcdn_bundle_step(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, pcdn_step_
         info->bundle_nnz = ctx->hm->counters[2];
         info->n_touched = (int64_t)v[7];
         if (ctx->hm->status == 3) return set_err(ctx, PCDN_ERR_NUMERIC, "non-finite line-search quantities");
+        if (ctx->hm->status == 7) return set_err(ctx, PCDN_ERR_INVALID, SCDN_HEAVY_MSG);
         if (ctx->hm->status) return set_err(ctx, PCDN_ERR_CUDA, "internal consistency check failed (%d)", ctx->hm->status);
     }
     return PCDN_OK;
@@ -1061,6 +1075,12 @@ int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_
         if (ctx->hm->status == 3 || !std::isfinite(F)) {
             status = PCDN_ERR_NUMERIC;
             set_err(ctx, PCDN_ERR_NUMERIC, "non-finite objective in outer iteration %d", k);
+            k++;
+            break;
+        }
+        if (ctx->hm->status == 7) {
+            status = PCDN_ERR_INVALID;
+            set_err(ctx, PCDN_ERR_INVALID, SCDN_HEAVY_MSG);
             k++;
             break;
         }

@@ -70,6 +70,7 @@ struct StepArgs {
     double c, sigma, beta, gamma, nu;
     double mu;   // elastic-net weight of (mu/2)||w||^2 (reading Z25; 0 = the paper's problem)
     const double *t;   // real targets of the squared loss (reading Z26), else unused
+    int scdn;          // 1: SCDN (Alg.2, reading Z27) -- per-feature 1-D steps, no P-dim line search
     int loss, qmax;
     int heavy_len;
     // state

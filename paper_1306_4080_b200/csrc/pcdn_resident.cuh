@@ -251,6 +251,41 @@ __device__ __forceinline__ double2 res_coef(const StepArgs &a, const ResCtx &R, 
     return coef_next(a.loss, cf, zd.x + R.alpha_prev * zd.y, R.alpha_prev * zd.y, yi);
 }
 
+// SCDN (Alg.2; synchronous reading Z27): feature j's own 1-D Armijo step
+// (Eq.6 with d = d_j e_j) from the step's start state, by the warp that owns the column.  Per
+// candidate alpha = beta^q: the column's loss change (the owner state re-gathered per chunk of 32
+// nonzeros, the previous step applied on the fly), warp-summed in a fixed order, plus the
+// separable terms.  Returns alpha_j (0: no candidate passes, a null update).
+__device__ double res_scdn_alpha(const StepArgs &a, const ResCtx &R, int64_t p0, int64_t p1, const int32_t *srow,
+                                 const float *sx, double d, double wj, double delta, int lane)
+{
+    double alpha = 1.0;
+    for (int q = 0; q <= a.qmax; q++) {
+        double chg = 0.0;
+        for (int64_t pb = p0; pb < p1; pb += 32) {
+            const int64_t p = pb + lane;
+            if (p < p1) {
+                const bool st = srow && pb == p0;
+                const int32_t i = st ? srow[lane] : __ldg(&a.row_idx[p]);
+                const double x = (double)(st ? sx[lane] : __ldg(&a.val[p]));
+                const int owner = i & (R.G - 1), li = i >> R.lg;
+                const double2 zd = ld_dsmem_f64x2(mapa_u32(s_addr(&R.zd[li]), owner));
+                const double2 cf = ld_dsmem_f64x2(mapa_u32(s_addr(&R.coef[li]), owner));
+                const int yi = res_ybit(R, i);
+                const double zc = zd.x + R.alpha_prev * zd.y;
+                const double2 cc = zd.y == 0.0 ? cf : coef_next(a.loss, cf, zc, R.alpha_prev * zd.y, yi);
+                chg += loss_change(a.loss, zc, yi, cc.x, d * x, alpha);
+            }
+        }
+        chg = warp_sum(chg);
+        const double wn = wj + alpha * d;
+        const double lhs = a.c * chg + fabs(wn) - fabs(wj) + a.mu * alpha * d * (wj + 0.5 * alpha * d);
+        if (lhs <= a.sigma * alpha * delta) return alpha;
+        alpha *= a.beta;
+    }
+    return 0.0;
+}
+
 // Send the records (sample i, bundle position k, d_k x_ik) of the warp's valid lanes to their
 // owners.  Every producer CTA p has a fixed region [p*capP, (p+1)*capP) of each owner's record
 // buffer; the slot comes from a LOCAL shared-memory counter per owner (one atomic per group of
@@ -769,9 +804,9 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
             if (qa < 0 && !badl) {
                 const double lhs = L1 + a.c * Ls;
                 const double rhs = a.sigma * al * Dl;
-                if (!isfinite(lhs) || !isfinite(Dl)) {
+                if (!isfinite(lhs) || (!a.scdn && !isfinite(Dl))) {
                     badl = 1;
-                } else if (lhs <= rhs) {
+                } else if (a.scdn || lhs <= rhs) {   // SCDN takes the combined step as it is (Z27)
                     qa = ws.q0 + q;
                     alpha_a = al;
                     la = lhs;
@@ -972,7 +1007,10 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
                     hs = warp_sum(h);
                 }
                 const double wj = stg ? fx.stg_w[warp][m] : ldcg(&a.w[j]);
-                const Dir r = finish_feature(a, gs, hs, wj);
+                Dir r = finish_feature(a, gs, hs, wj);
+                if (a.scdn && r.d != 0.0)   // SCDN: the feature's own 1-D step replaces d_j (Z27)
+                    r.d *= res_scdn_alpha(a, R, p0, p1, stg ? fx.stg_r[warp][m] : nullptr,
+                                          stg ? fx.stg_x[warp][m] : nullptr, r.d, wj, r.delta, lane);
                 if (lane == 0) {
                     if (m >= R_CPW || a.d_out || len == a.s) {
                         a.dk[kk - k0] = r.d;
@@ -1011,6 +1049,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         // ---------------- phase A': heavy columns, nnz-balanced over all warps -----------
         const HeavyPlan hpl = fx.plan[t & 1];   // computed a step ahead (see the count exchange)
         const int64_t e_lo = hpl.e_lo, e_hi = hpl.e_hi;
+        if (a.scdn && e_hi > e_lo && tid == 0) atomicMax(a.status, 7);   // SCDN needs warp-owned columns
         if (e_hi > e_lo) {
             const int64_t hb0 = hpl.hb0, NH = hpl.NH;
             const int64_t lo_c = (int64_t)c * NH / G, hi_c = (int64_t)(c + 1) * NH / G;

@@ -534,3 +534,50 @@ def test_short_columns_with_small_split_length(pk, launch):
                 _compare_step(s.step(B), o.step(w, B), ties)
         assert len(ties) <= 1, ties
         s.close()
+
+
+# ----------------------------------------------------------------------------- SCDN baseline
+@pytest.mark.parametrize("loss", [LOSS_LOGISTIC, LOSS_L2SVM])
+@pytest.mark.parametrize("Pbar", [1, 8, 16])
+def test_scdn_parity(pk, loss, Pbar):
+    """SCDN (Alg.2, NEXT #3, synchronous reading Z27) on the cluster-resident kernel: the F
+    trace per iteration and the final w against the oracle's SCDN; P-bar = 1 is CDN."""
+    for case in (0, 1, 3):
+        kw = dict(TINY[case])
+        prob = synth.tiny(loss=loss, c=3.0, P=Pbar, **kw)
+        Pb = min(Pbar, prob.n)
+        s = _solver(pk, prob, 3, 0, 100000)   # every column within one warp's reach
+        s.set_scdn(True)
+        o = oracle.Oracle(prob)
+        gs = s.solve(Pb, seed=11, max_outer=4, trace=True)
+        os_ = o.scdn(Pb, seed=11, max_outer=4)
+        assert gs["steps"] == os_["steps"]
+        assert np.all(gs["q_trace"] == 0)
+        _close(gs["F_trace"], os_["F_trace"], np.abs(os_["F_trace"]) * 1e-3, f"scdn F trace case {case}")
+        assert abs(gs["F"] - os_["F"]) <= 1e-6 * abs(os_["F"])
+        assert np.max(np.abs(s.w().cpu().numpy() - os_["w"])) <= 1e-5
+        s.close()
+
+
+def test_scdn_rises_where_pcdn_does_not(pk):
+    """PAPER.md:126 on the GPU: near-duplicate columns, P-bar = n: SCDN's F rises at some
+    iteration, PCDN's never does (both through the C-ABI)."""
+    rng = np.random.default_rng(7)
+    Xc = rng.normal(size=(40, 1)) @ np.ones((1, 16)) + 0.02 * rng.normal(size=(40, 16))
+    prob = synth.from_dense(Xc, np.where(rng.random(40) < 0.5, 1, -1), c=10.0, loss=LOSS_LOGISTIC, P=16)
+    s = _solver(pk, prob, 3, 0, 100000)
+    F0 = s.objective()
+    s.set_scdn(True)
+    sc = s.solve(16, seed=1, max_outer=3, trace=True)
+    assert np.any(np.diff(np.concatenate([[F0], sc["F_trace"]])) > 1e-9 * F0)
+    s.set_scdn(False)
+    s.reset()
+    pc = s.solve(16, seed=1, max_outer=3, trace=True)
+    assert np.all(np.diff(np.concatenate([[F0], pc["F_trace"]])) <= 1e-12 * F0)
+    # SCDN is refused where its per-feature line search cannot run
+    s.set_scdn(True)
+    s.set_launch(2)
+    with pytest.raises(pk.PCDNError) as ei:
+        s.solve(16, seed=1, max_outer=1)
+    assert ei.value.status == pk.PCDN_ERR_INVALID
+    s.close()
