@@ -167,6 +167,35 @@ int pcdn_set_debug(pcdn_ctx *ctx, int on);
  * columns of 129..2048 nonzeros are reduced by one CTA, 128 for mode 3). */
 int pcdn_set_launch(pcdn_ctx *ctx, int mode, int ctas, int heavy_len);
 
+/* Sample-sharded step: data larger than one GPU.  Each rank
+ * creates a context over ITS rows (their CSC/CSR, labels / targets); w and the partition stream
+ * are replicated.  One PCDN bundle step (Alg.3 l.6-10 with Alg.4) is then, on every rank, for the
+ * same device bundle[P] (distinct feature indices; not validated here):
+ *   pcdn_shard_gh          -> gh_out (DEVICE fp64[2P]): sum_i x_ij G_i, sum_i x_ij^2 H_i over the
+ *                             local samples (Eq.13 / App. A.2 factors, before the factor c);
+ *   caller: sum gh over the ranks (in rank order, for bit-identical results on every rank);
+ *   pcdn_shard_direction   d_j (Eq.5), the Delta terms (Eq.7) from the GLOBAL sums, and the d'x
+ *                             records of the local samples;
+ *   pcdn_shard_line_search -> out (DEVICE fp64[13]) for candidates alpha = beta^(q0+q), q < 6:
+ *                             out[q] = local sum_i phi change (Eq.12 summand, before c);
+ *                             out[6+q] = the bundle's separable-term change, out[12] = Delta --
+ *                             both only if with_l1 (exactly one rank), else 0.  first = 1 for the
+ *                             step's first window (folds d'x_i), 0 for later windows;
+ *   caller: sum out over the ranks; accept the first q with out[6+q] + c out[q] <= sigma alpha
+ *           out[12] (Eq.6); none in the window -> the next window (q0 += 6, first = 0);
+ *   pcdn_shard_commit      w_B += alpha d_B (every rank), z and the factors of the local touched
+ *                             samples (alpha = 0: a null step, records cleared).  Synchronizes.
+ *   pcdn_shard_loss        -> loss_out (host): c sum_i phi_i over the local samples (the caller
+ *                             adds ||w||_1 (+ mu/2 ||w||^2) once: Eq.1 at an outer boundary).
+ * The kernels never wait on another rank (the caller's collectives sit between the calls).
+ * Returns PCDN_ERR_INVALID for null pointers, P outside [1, n], q0 < 0, alpha < 0 / not finite. */
+int pcdn_shard_gh(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, double *gh_out);
+int pcdn_shard_direction(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, const double *gh);
+int pcdn_shard_line_search(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, int q0, int first, int with_l1,
+                           double *out);
+int pcdn_shard_commit(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, double alpha);
+int pcdn_shard_loss(pcdn_ctx *ctx, double *loss_out);
+
 /* SCDN baseline (Alg.2 Shotgun CDN; reading Z27): with
  * on != 0, pcdn_bundle_step / pcdn_solve run SCDN instead of PCDN -- each feature of a bundle (of
  * size P-bar = P) takes its own 1-D Armijo step from the bundle's start state and all updates are

@@ -318,3 +318,10 @@ class Solver:
             self.close()
         except Exception:
             pass
+
+
+# sample-sharded step (NEXT #2): C-ABI wrappers and the rank-level driver
+from .sharded import (  # noqa: E402,F401
+    ShardedSolver, pcdn_shard_commit, pcdn_shard_direction, pcdn_shard_gh, pcdn_shard_line_search, pcdn_shard_loss,
+    rank_order_sum,
+)

@@ -67,6 +67,11 @@ SIGNATURES = {
     "pcdn_set_elastic": (C.c_int, [P, C.c_double]),
     "pcdn_set_targets": (C.c_int, [P, C.c_void_p]),
     "pcdn_set_scdn": (C.c_int, [P, C.c_int]),
+    "pcdn_shard_gh": (C.c_int, [P, C.c_void_p, C.c_int64, C.c_void_p]),
+    "pcdn_shard_direction": (C.c_int, [P, C.c_void_p, C.c_int64, C.c_void_p]),
+    "pcdn_shard_line_search": (C.c_int, [P, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p]),
+    "pcdn_shard_commit": (C.c_int, [P, C.c_void_p, C.c_int64, C.c_double]),
+    "pcdn_shard_loss": (C.c_int, [P, C.POINTER(C.c_double)]),
     "pcdn_set_profile": (C.c_int, [P, C.c_int]),
     "pcdn_phase_cycles": (C.c_int, [P, P, C.POINTER(C.c_int32)]),
     "pcdn_warp_timeline": (C.c_int, [P, P]),

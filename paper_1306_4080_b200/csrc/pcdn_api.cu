@@ -17,6 +17,7 @@
 #include "pcdn_kernels.cuh"
 #include "pcdn_resident.cuh"
 #include "pcdn_dense.cuh"
+#include "pcdn_shard.cuh"
 
 using namespace pcdn;
 
@@ -1132,6 +1133,122 @@ int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_
     }
     (void)gap;
     return status;
+}
+
+// ---------------------------------------------------------------------------------------
+// Sample-sharded step (pcdn_shard.cuh): host-driven phases
+// ---------------------------------------------------------------------------------------
+static StepArgs shard_args(pcdn_ctx *ctx, int64_t P)
+{
+    const Layout &L = ctx->L;
+    StepArgs a{};
+    a.s = ctx->s;
+    a.n = ctx->n;
+    a.col_ptr = ctx->col_ptr;
+    a.row_idx = ctx->row_idx;
+    a.val = ctx->val;
+    a.row_ptr = ctx->row_ptr;
+    a.y = ctx->y;
+    a.t = ctx->t;
+    a.c = ctx->c;
+    a.sigma = ctx->sigma;
+    a.beta = ctx->beta;
+    a.gamma = ctx->gamma;
+    a.nu = ctx->nu;
+    a.mu = ctx->mu;
+    a.loss = ctx->loss;
+    a.qmax = ctx->qmax;
+    a.w = ctx->at<double>(L.w);
+    a.z = ctx->at<double>(L.z);
+    a.coef = ctx->at<double2>(L.coef);
+    a.cnt = ctx->at<int32_t>(L.cnt);
+    a.bits = ctx->at<uint32_t>(L.bits);
+    a.rec = ctx->at<Rec>(L.rec);
+    a.dxg = ctx->at<double>(L.dxg);
+    a.dk = ctx->at<double>(L.dk);
+    a.deltak = ctx->at<double>(L.deltak);
+    a.part = ctx->at<double>(L.part);
+    a.P = P;
+    a.status = ctx->at<int>(L.status);
+    return a;
+}
+
+static int shard_blocks(int64_t work, int per)
+{
+    int64_t b = (work + per - 1) / per;
+    if (b < 1) b = 1;
+    if (b > 2 * GMAX * NPART / SH_W) b = 2 * GMAX * NPART / SH_W;   // partial rows fit the part buffer
+    return (int)b;
+}
+
+int pcdn_shard_gh(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, double *gh_out)
+{
+    if (!ctx || !bundle || !gh_out || P < 1 || P > ctx->n) return PCDN_ERR_INVALID;
+    PCDN_NEED_TARGETS(ctx);
+    int rc;
+    if ((rc = reset_status(ctx))) return rc;
+    k_sh_gh<<<shard_blocks(P * 32, SH_NT), SH_NT, 0, ctx->stream>>>(shard_args(ctx, P), bundle, P, gh_out);
+    ctx->launches++;
+    CU(cudaGetLastError());
+    return PCDN_OK;
+}
+
+int pcdn_shard_direction(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, const double *gh)
+{
+    if (!ctx || !bundle || !gh || P < 1 || P > ctx->n) return PCDN_ERR_INVALID;
+    PCDN_NEED_TARGETS(ctx);
+    k_sh_dir<<<shard_blocks(P * 32, SH_NT), SH_NT, 0, ctx->stream>>>(shard_args(ctx, P), bundle, P, gh);
+    ctx->launches++;
+    CU(cudaGetLastError());
+    return PCDN_OK;
+}
+
+int pcdn_shard_line_search(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, int q0, int first, int with_l1,
+                           double *out)
+{
+    if (!ctx || !bundle || !out || P < 1 || P > ctx->n || q0 < 0) return PCDN_ERR_INVALID;
+    PCDN_NEED_TARGETS(ctx);
+    const StepArgs a = shard_args(ctx, P);
+    // short lists by threads, long ones by warps; their partial rows side by side, summed in order
+    const int nbl = std::min(shard_blocks(ctx->s * 32, SH_LNT), 4 * ctx->num_sms);
+    const int nb = std::min(shard_blocks(ctx->s, SH_NT), 2 * GMAX * NPART / SH_W - nbl);
+    k_sh_ls<<<nb, SH_NT, 0, ctx->stream>>>(a, q0, first, a.part);
+    k_sh_ls_long<<<nbl, SH_LNT, 0, ctx->stream>>>(a, q0, first, a.part + (size_t)nb * SH_W);
+    k_sh_ls_final<<<1, SH_NT, 0, ctx->stream>>>(a, bundle, P, q0, nb + nbl, a.part, with_l1, out);
+    ctx->launches += 3;
+    CU(cudaGetLastError());
+    return PCDN_OK;
+}
+
+int pcdn_shard_commit(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, double alpha)
+{
+    if (!ctx || !bundle || P < 1 || P > ctx->n || !(alpha >= 0) || !std::isfinite(alpha)) return PCDN_ERR_INVALID;
+    PCDN_NEED_TARGETS(ctx);
+    k_sh_commit<<<shard_blocks(ctx->s, SH_NT), SH_NT, 0, ctx->stream>>>(shard_args(ctx, P), bundle, P, alpha);
+    ctx->launches++;
+    CU(cudaGetLastError());
+    int rc;
+    if ((rc = readback(ctx))) return rc;
+    if (ctx->hm->status) return set_err(ctx, PCDN_ERR_CUDA, "internal consistency check failed (%d)", ctx->hm->status);
+    return PCDN_OK;
+}
+
+int pcdn_shard_loss(pcdn_ctx *ctx, double *loss_out)
+{
+    if (!ctx || !loss_out) return PCDN_ERR_INVALID;
+    PCDN_NEED_TARGETS(ctx);
+    // c * sum_i phi_i of the local samples (Eq.1 without the separable terms): F with w's terms
+    // removed -- evaluate F(z, w = 0 view) by the objective kernels on the copy slot
+    const Layout &L = ctx->L;
+    k_obj_partial<<<OBJ_NB, 256, 0, ctx->stream>>>(ctx->s, 0, ctx->at<double>(L.z), ctx->y, ctx->at<double>(L.w),
+                                                   ctx->loss, ctx->at<double>(L.objp), ctx->t);
+    k_obj_final<<<1, OBJ_NB, 0, ctx->stream>>>(ctx->at<double>(L.objp), ctx->c, 0.0, ctx->at<double>(L.Fcopy), nullptr);
+    ctx->launches += 2;
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(&ctx->hm->Fcopy, ctx->at<double>(L.Fcopy), sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    *loss_out = ctx->hm->Fcopy;
+    return PCDN_OK;
 }
 
 int pcdn_train_host(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_ptr, const int32_t *csc_row_idx,

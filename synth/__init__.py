@@ -18,4 +18,5 @@ from .generate import (  # noqa: F401
     LOSS_L2SVM,
     LOSS_SQUARED,
     regression,
+    shard_rows,
 )

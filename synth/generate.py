@@ -69,6 +69,24 @@ class Problem:
         return p
 
 
+def shard_rows(prob: "Problem", rank: int, world: int) -> "Problem":
+    """Rows [floor(rank s / world), floor((rank+1) s / world)) of `prob` as a Problem of their own
+    (CSR slice, CSC rebuilt from it, labels / targets sliced); n and every parameter unchanged.
+    Data layout only: the sample-sharded step gives each rank one of these."""
+    r0, r1 = rank * prob.s // world, (rank + 1) * prob.s // world
+    a, b = int(prob.row_ptr[r0]), int(prob.row_ptr[r1])
+    row_ptr = (prob.row_ptr[r0:r1 + 1] - a).astype(np.int64)
+    col_idx = prob.col_idx[a:b].copy()
+    csr_val = prob.csr_val[a:b].copy()
+    col_ptr, row_idx, val = csr_to_csc(r1 - r0, prob.n, row_ptr, col_idx, csr_val)
+    p = Problem(name=f"{prob.name}-shard{rank}of{world}", s=r1 - r0, n=prob.n, col_ptr=col_ptr, row_idx=row_idx,
+                val=val, row_ptr=row_ptr, col_idx=col_idx, csr_val=csr_val, y=prob.y[r0:r1].copy(), c=prob.c,
+                loss=prob.loss, P=prob.P, seed=prob.seed, meta=dict(prob.meta, rows=(r0, r1)))
+    if prob.t is not None:
+        p.t = prob.t[r0:r1].copy()
+    return p
+
+
 def regression(prob: "Problem", noise: float = 0.1, support: int = 500, seed: int | None = None) -> "Problem":
     """The same design matrix with real targets t = X w* + N(0, noise^2) for a planted w* with
     `support` N(0,1) nonzeros (uniform without replacement), loss = LOSS_SQUARED.  Data

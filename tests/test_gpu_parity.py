@@ -581,3 +581,79 @@ def test_scdn_rises_where_pcdn_does_not(pk):
         s.solve(16, seed=1, max_outer=1)
     assert ei.value.status == pk.PCDN_ERR_INVALID
     s.close()
+
+
+# ----------------------------------------------------------------------------- sample-sharded step
+def _sharded_case(loss, kind):
+    if kind == "lasso":
+        return synth.regression(synth.tiny(5, 150, 30, density=0.1, full_cols=2, dense_rows=1, c=0.7), noise=0.2,
+                                support=5)
+    return synth.tiny(5, 150, 30, density=0.1, loss=loss, c=3.0, full_cols=2, dense_rows=1)
+
+
+@pytest.mark.parametrize("loss,kind,mu", [(LOSS_LOGISTIC, "", 0.0), (LOSS_L2SVM, "", 0.0),
+                                          (LOSS_LOGISTIC, "", 1.0), (LOSS_L2SVM, "lasso", 0.5)])
+def test_sharded_world1_matches_oracle(pk, loss, kind, mu):
+    """The sample-sharded step (NEXT #2) with one rank: the four C-ABI phases and the host
+    decision reproduce the oracle's solve step for step (q trace, maintained F, final w)."""
+    prob = _sharded_case(loss, kind)
+    ss = pk.ShardedSolver(prob)
+    if mu:
+        ss.set_elastic(mu)
+    o = oracle.Oracle(prob, mu=mu)
+    r = ss.solve(7, seed=4, max_outer=5, trace=True)
+    os_ = o.solve(7, seed=4, max_outer=5)
+    assert np.array_equal(r["q_trace"], os_["q_trace"])
+    assert r["steps"] == os_["steps"]
+    _close(r["F_trace"], os_["F_trace"], np.abs(os_["F_trace"]) * 1e-3, "sharded F trace")
+    assert abs(r["F"] - os_["F"]) <= 1e-9 * abs(os_["F"])
+    assert np.max(np.abs(ss.w().cpu().numpy() - os_["w"])) <= 1e-9
+    ss.close()
+
+
+def _sharded_worker(rank, world, port, loss, kind, q):
+    import os as _os
+    import torch
+    import torch.distributed as dist
+    import paper_1306_4080_b200 as pk_
+    _os.environ["MASTER_ADDR"] = "127.0.0.1"
+    _os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        shard = synth.shard_rows(_sharded_case(loss, kind), rank, world)
+        ss = pk_.ShardedSolver(shard, group=dist.group.WORLD)
+        r = ss.solve(7, seed=4, max_outer=5, trace=True)
+        q.put((rank, r["q_trace"], r["F_trace"], r["F"], ss.w().cpu().numpy()))
+        ss.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("loss,kind", [(LOSS_LOGISTIC, ""), (LOSS_L2SVM, ""), (LOSS_L2SVM, "lasso")])
+def test_sharded_two_ranks_match_oracle(pk, loss, kind):
+    """Two ranks (two processes; host-side gloo collectives between the phases, so no kernel ever
+    waits on another rank -- one GPU serves both) each own half the rows: both ranks take the
+    identical decisions and reach the oracle's trajectory."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, loss, kind, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    res = sorted([q.get(timeout=300) for _ in range(2)], key=lambda t: t[0])
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    prob = _sharded_case(loss, kind)
+    os_ = oracle.Oracle(prob).solve(7, seed=4, max_outer=5)
+    for rank, qt, Ft, F, w in res:
+        assert np.array_equal(qt, os_["q_trace"]), rank
+        _close(Ft, os_["F_trace"], np.abs(os_["F_trace"]) * 1e-3, f"rank {rank} F trace")
+        assert abs(F - os_["F"]) <= 1e-9 * abs(os_["F"])
+        assert np.max(np.abs(w - os_["w"])) <= 1e-9
+    assert np.array_equal(res[0][4], res[1][4])   # replicated w: bit-identical on both ranks

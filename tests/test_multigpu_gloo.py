@@ -56,3 +56,37 @@ def test_aggregate_single_process():
     import bench
     t, tot = bench.aggregate_over_ranks(3.0, {"nnz": 5}, None)
     assert t == 3.0 and tot == {"nnz": 5.0}
+
+
+def _sum_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    from paper_1306_4080_b200.sharded import rank_order_sum
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(100 + rank)
+        t = torch.randn(64, dtype=torch.float64, generator=g) * 10 ** torch.randint(-8, 8, (64,), generator=g)
+        s = rank_order_sum(t, dist.group.WORLD)
+        q.put((rank, t.numpy(), s.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_rank_order_sum():
+    """The sample-sharded step's cross-rank sums (gloo, world 2): every rank gets the identical
+    bits, equal to the parts added in rank order (so every rank takes the same decision)."""
+    import numpy as np
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_sum_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)], key=lambda t: t[0])
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = res[0][1] + res[1][1]
+    assert np.array_equal(res[0][2], want) and np.array_equal(res[1][2], want)
