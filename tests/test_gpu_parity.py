@@ -657,3 +657,45 @@ def test_sharded_two_ranks_match_oracle(pk, loss, kind):
         assert abs(F - os_["F"]) <= 1e-9 * abs(os_["F"])
         assert np.max(np.abs(w - os_["w"])) <= 1e-9
     assert np.array_equal(res[0][4], res[1][4])   # replicated w: bit-identical on both ranks
+
+
+# ----------------------------------------------------------------------------- degenerate shapes
+@pytest.mark.parametrize("launch", [(0, 0, 0), (1, 1, 0), (2, 0, 0), (3, 0, 0), (4, 0, 0)])
+def test_one_dimensional_closed_forms_gpu(pk, launch):
+    """s = 1, x = 1, y = +1 through every step kernel: SVM w* = 1 - 1/(2c) in one Newton step,
+    LR w* = ln(c - 1) (the closed forms of tests/test_oracle_pins.py), Lasso w* = t - 1/(2c)."""
+    for c in (1.0, 3.0):
+        p = synth.from_dense([[1.0]], [1], c=c, loss=LOSS_L2SVM, P=1)
+        s = _solver(pk, p, *launch)
+        r = s.solve(1, seed=0, max_outer=1)
+        assert math.isclose(s.w().cpu().numpy()[0], 1 - 1 / (2 * c), rel_tol=1e-15)
+        assert math.isclose(r["F"], 1 - 1 / (4 * c), rel_tol=1e-15)
+        s.close()
+    p = synth.from_dense([[1.0]], [1], c=4.0, loss=LOSS_LOGISTIC, P=1)
+    s = _solver(pk, p, *launch)
+    s.solve(1, seed=0, max_outer=80)
+    assert abs(s.w().cpu().numpy()[0] - math.log(3.0)) < 1e-10
+    s.close()
+    p = synth.regression(synth.from_dense([[1.0]], [1], c=2.0, P=1), noise=0.0, support=1)
+    p.t = np.array([1.5])
+    s = _solver(pk, p, *launch)
+    s.solve(1, seed=0, max_outer=1)
+    assert math.isclose(s.w().cpu().numpy()[0], 1.5 - 1 / 4.0, rel_tol=1e-15)
+    s.close()
+
+
+@pytest.mark.parametrize("shape", [(1, 7), (50, 1), (3, 3), (33, 64)])
+@pytest.mark.parametrize("launch", [(0, 0, 0), (1, 4, 0), (2, 3, 1), (3, 2, 0)])
+def test_tiny_shapes_parity(pk, shape, launch):
+    """One sample, one feature, and shapes around warp / CTA boundaries: full solves (P = 1, a
+    middle P, P = n) against the oracle in each launch mode."""
+    s_, n_ = shape
+    for loss in (LOSS_LOGISTIC, LOSS_L2SVM):
+        prob = synth.tiny(900 + s_ + n_, s_, n_, density=0.6, loss=loss, c=2.0)
+        o = oracle.Oracle(prob)
+        for P in sorted({1, max(1, n_ // 2), n_}):
+            s = _solver(pk, prob, *launch)
+            gs = s.solve(P, seed=2, max_outer=4, trace=True)
+            os_ = o.solve(P, seed=2, max_outer=4)
+            _compare_solve(gs, os_, s.w().cpu().numpy(), f"shape {shape} P={P} launch {launch}")
+            s.close()
