@@ -436,8 +436,8 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        CU(cudaLaunchKernelEx(&cfg, ctx->loss == LOSS_LOGISTIC ? k_step_res<LOSS_LOGISTIC>
-                                    : ctx->loss == LOSS_L2SVM ? k_step_res<LOSS_L2SVM> : k_step_res<LOSS_SQ>, a));
+        void *kargs[] = {&a};
+        CU(cudaLaunchKernelExC(&cfg, res_kernel(ctx->loss, ctx->scdn != 0), kargs));
     } else {
         // HBM-state kernels: the per-sample state (z, coef, cnt, bits, dxg, tlist) is gathered and
         // scattered at random every step while CSC and records stream through L2; a persisting
@@ -563,9 +563,10 @@ int configure_launch(pcdn_ctx *ctx)
     {
         int optin = 0;
         CU(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        const void *kr = ctx->loss == LOSS_LOGISTIC ? (const void *)k_step_res<LOSS_LOGISTIC>
-                         : ctx->loss == LOSS_L2SVM ? (const void *)k_step_res<LOSS_L2SVM> : (const void *)k_step_res<LOSS_SQ>;
+        const void *kr = res_kernel(ctx->loss, false);
+        const void *krs = res_kernel(ctx->loss, true);   // the SCDN instantiation: same layout
         CU(cudaFuncSetAttribute(kr, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        CU(cudaFuncSetAttribute(krs, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         ctx->res_G = 0;
         const int greq = ctx->mode_req == 3 ? ctx->G_req : 0;
         for (int lg = 4; lg >= 0; lg--) {
@@ -581,6 +582,7 @@ int configure_launch(pcdn_ctx *ctx)
             if (cap < (ctx->res_cap_req > 0 ? 1 : 256)) continue;
             const size_t sm = res_layout((int)Bs, cap).total;
             CU(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            CU(cudaFuncSetAttribute(krs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             cudaLaunchConfig_t cfg{};
             cfg.gridDim = dim3(G);
             cfg.blockDim = dim3(NT);

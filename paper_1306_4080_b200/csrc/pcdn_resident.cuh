@@ -839,10 +839,11 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
     pr.mark(fx, 5);
 }
 
-template <int LOSS>
+template <int LOSS, bool SCDN>
 __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
 {
     a.loss = LOSS;   // a compile-time loss: the other loss's code is dead (smaller instruction footprint)
+    a.scdn = SCDN;   // likewise the SCDN baseline's per-feature line search
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, c = blockIdx.x;   // one cluster = the whole grid
@@ -1201,6 +1202,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
             st_async_u32(mapa_u32(s_addr(&fx.recvcnt[c]), tid), (uint32_t)fx.sendcnt[tid], mapa_u32(mb0, tid));
             fx.sendcnt[tid] = 0;
         }
+        __syncwarp();   // warp 0 (tid < G <= 16) has read fx.spilled before tid 0 resets it below
         if (tid == 0) mbar_arrive_tx(mb0, (uint32_t)(4 * G));
         // while the counts travel: the next step's heavy plan (one warp) and every warp's next
         // own light columns (descriptor, w_j, first 32 nonzeros) into shared memory
@@ -1237,7 +1239,8 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
             const int tot_in = __reduce_add_sync(0xffffffffu, nin);
             if (tid == 0) mbar_arrive_tx(mb1, (uint32_t)(16 * tot_in));
         }
-        __syncthreads();   // heads reset by the lazy commit
+        // (no CTA barrier here: the lazy commit touches zd/coef, the links below touch head/recin;
+        // the fold reads zd only after the compaction barrier)
         if (tid == 0) fx.spilled = 0;
         mbar_wait(mb1, (ph >> 1) & 1u);
         RTL(R, 6);
@@ -1410,6 +1413,18 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
         for (int i = 0; i < 16; i++) a.prof[i] += fx.pacc[i];
 #undef PROF_MARK
     cluster_sync_all();   // no CTA exits while another may still read its shared memory
+}
+
+// the instantiation for a context's loss and solver
+inline const void *res_kernel(int loss, bool scdn)
+{
+    if (scdn)
+        return loss == LOSS_LOGISTIC ? (const void *)k_step_res<LOSS_LOGISTIC, true>
+               : loss == LOSS_L2SVM  ? (const void *)k_step_res<LOSS_L2SVM, true>
+                                     : (const void *)k_step_res<LOSS_SQ, true>;
+    return loss == LOSS_LOGISTIC ? (const void *)k_step_res<LOSS_LOGISTIC, false>
+           : loss == LOSS_L2SVM  ? (const void *)k_step_res<LOSS_L2SVM, false>
+                                 : (const void *)k_step_res<LOSS_SQ, false>;
 }
 
 }  // namespace pcdn
