@@ -786,21 +786,24 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
     // warp 0: the G partial rows (local now), fixed-order tree, decision; broadcast in the CTA
     // (every CTA computes the identical decision)
     if (warp == 0) {
-        double tot;
-        {
-            double v[W];
+        // lane l < W sums slot l over the G rows in row order (independent loads, one add chain:
+        // shorter than a shuffle tree's dependent levels)
+        double tot = 0.0;
+        if (lane < W) {
+            double v[16];
 #pragma unroll
-            for (int q = 0; q < W; q++) v[q] = lane < R.G ? fx.part_in[buf][lane][q] : 0.0;
-            tot = xreduce<W>(v, lane);   // lane l holds slot l / SPL
+            for (int r = 0; r < 16; r++) v[r] = r < R.G ? fx.part_in[buf][r][lane] : 0.0;
+#pragma unroll
+            for (int r = 0; r < 16; r++) tot += v[r];
         }
-        const double Dl = __shfl_sync(0xffffffffu, tot, LY::DELTA * SPL);
-        const double nTt = __shfl_sync(0xffffffffu, tot, LY::NTOUCH * SPL);
+        const double Dl = __shfl_sync(0xffffffffu, tot, LY::DELTA);
+        const double nTt = __shfl_sync(0xffffffffu, tot, LY::NTOUCH);
         int qa = -1, badl = 0;
         double al = alpha0, la = 0.0, ra = 0.0, alpha_a = 0.0;
 #pragma unroll
         for (int q = 0; q < NQ; q++) {
-            const double Ls = __shfl_sync(0xffffffffu, tot, q * SPL);
-            const double L1 = __shfl_sync(0xffffffffu, tot, (NQ + q) * SPL);
+            const double Ls = __shfl_sync(0xffffffffu, tot, q);
+            const double L1 = __shfl_sync(0xffffffffu, tot, NQ + q);
             if (qa < 0 && !badl) {
                 const double lhs = L1 + a.c * Ls;
                 const double rhs = a.sigma * al * Dl;
@@ -834,8 +837,8 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
     ws.rhs = fx.dec_rhs[buf];
     ws.Delta = fx.dec_Delta[buf];
     ws.nT_tot = fx.dec_nT[buf];
-    ws.win++;
     if (ws.win == 0) RTL(R, 12);
+    ws.win++;
     pr.mark(fx, 5);
 }
 
