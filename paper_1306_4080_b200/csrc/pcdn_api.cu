@@ -519,8 +519,34 @@ int choose_mode(const pcdn_ctx *ctx, int64_t P)
     return mode;
 }
 
+// Load every kernel of the library once per process.  Under CUDA's default lazy module loading
+// each kernel is loaded at its first use, and the one-call host API (which creates a context per
+// call) was measured to pay ~8 ms per call more than with eager loading (scripts/_create_time.py).
+static void preload_kernels()
+{
+    static bool done = false;
+    if (done) return;
+    done = true;
+    const void *fns[] = {
+        (const void *)k_perm, (const void *)k_full_compact, (const void *)k_bundle_prep, (const void *)k_bundle_unseen,
+        (const void *)k_scan_reduce<int32_t, int64_t>, (const void *)k_scan_reduce<int64_t, int64_t>,
+        (const void *)k_scan_apply<int32_t, int64_t>, (const void *)k_scan_apply<int64_t, int64_t>,
+        (const void *)k_scan_tiles<int64_t>, (const void *)k_heavy_compact, (const void *)k_step<GridSync>,
+        (const void *)k_step<ClusterSync>, res_kernel(LOSS_LOGISTIC, false), res_kernel(LOSS_L2SVM, false),
+        res_kernel(LOSS_SQ, false), res_kernel(LOSS_LOGISTIC, true), res_kernel(LOSS_L2SVM, true),
+        res_kernel(LOSS_SQ, true), dense_kernel(LOSS_LOGISTIC), dense_kernel(LOSS_L2SVM), dense_kernel(LOSS_SQ),
+        (const void *)k_set_z, (const void *)k_obj_partial, (const void *)k_obj_final, (const void *)k_validate,
+        (const void *)k_validate_transpose, (const void *)k_check_finite, (const void *)k_sh_gh, (const void *)k_sh_dir,
+        (const void *)k_sh_ls, (const void *)k_sh_ls_long, (const void *)k_sh_ls_final, (const void *)k_sh_commit};
+    for (const void *f : fns) {
+        cudaFuncAttributes fa;
+        if (cudaFuncGetAttributes(&fa, f) != cudaSuccess) cudaGetLastError();
+    }
+}
+
 int configure_launch(pcdn_ctx *ctx)
 {
+    preload_kernels();
     int dev = 0;
     CU(cudaGetDevice(&dev));
     CU(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1263,6 +1289,18 @@ int pcdn_train_host(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_pt
     if (s < 1 || n < 1 || nnz < 0 || !csc_col_ptr || !csr_row_ptr || !y || !w_out) return PCDN_ERR_INVALID;
     if (eps > 0 && !(f_star > 0)) return PCDN_ERR_INVALID;
     cudaStream_t st = (cudaStream_t)cuda_stream;
+    {
+        // keep the stream-ordered allocations of repeated calls in the device's pool instead of
+        // returning them to the driver at every synchronisation (once per process)
+        static bool pool_set = false;
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (!pool_set && cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            if (cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr) != cudaSuccess) cudaGetLastError();
+            pool_set = true;
+        }
+    }
     const size_t ws = pcdn_workspace_bytes(s, n, nnz);
     const size_t sz[] = {sizeof(int64_t) * (n + 1), sizeof(int32_t) * nnz, sizeof(float) * nnz,
                          sizeof(int64_t) * (s + 1), sizeof(int32_t) * nnz, sizeof(float) * nnz, (size_t)s, ws,
