@@ -224,9 +224,12 @@ int pcdn_set_elastic(pcdn_ctx *ctx, double mu);
 
 /* HBM-state kernels (modes 1, 2): keep the per-sample state (z, coef, record counts, touched
  * bitmap, d'x; one contiguous workspace window) L2-resident with a persisting access-policy window
- * on the step-kernel launches (default on).  The first such launch sets the device's persisting-L2
- * limit (cudaLimitPersistingL2CacheSize) to min(device maximum, window bytes) once; if the device
- * refuses, the knob turns itself off.  Results are unchanged (a cache policy only).
+ * on the step-kernel launches of SMALL steps (estimated bundle nonzeros <= 65536; default OFF).
+ * The first such launch sets the device's persisting-L2 limit (cudaLimitPersistingL2CacheSize) to
+ * min(device maximum, window bytes) -- a device-wide carve-out that then also shrinks the L2
+ * available to large steps and to other work (config 5: -4% step time at P = 4096, but +50% at
+ * P = 10^5..10^6 once the carve-out exists), hence opt-in; if the device refuses, the knob turns
+ * itself off.  Results are unchanged (a cache policy only).
  * Returns PCDN_ERR_INVALID for a null context. */
 int pcdn_set_l2_persist(pcdn_ctx *ctx, int on);
 

@@ -155,7 +155,7 @@ struct pcdn_ctx {
     int last_mode = 0;
     int heavy_len = 0;     // user override (pcdn_set_launch); 0 = per launch mode (heavy_for_mode)
     int heavy_eff = 128;   // the value in force for the current solve / step (lists and kernels)
-    int l2_want = 1;       // pcdn_set_l2_persist
+    int l2_want = 0;       // pcdn_set_l2_persist (off by default: a device-wide carve-out)
     size_t l2_persist = 0; // bytes of L2 set aside for the per-sample state window (0 = off)
     size_t l2_window = 0;  // max access-policy window size of the device
     int num_sms = 0;
@@ -460,7 +460,10 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
             at[na].val.cooperative = 1;
             na++;
         }
-        if (ctx->l2_want && ctx->l2_persist == 0) {
+        // only for small steps: a large step streams records and CSC through L2, and the carve-out
+        // then costs more than it saves (cfg5: -4% step time at P = 4096, +26% at P = 10^6)
+        const bool small_step = (double)ctx->nnz * (double)P / (double)ctx->n <= 65536.0;
+        if (ctx->l2_want && small_step && ctx->l2_persist == 0) {
             // first HBM-state launch: set aside L2 for the window (device limit, once)
             int dev = 0, maxp = 0, maxw = 0;
             CU(cudaGetDevice(&dev));
@@ -475,7 +478,7 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
                 ctx->l2_want = 0;
             }
         }
-        if (ctx->l2_want && ctx->l2_persist > 0) {
+        if (ctx->l2_want && small_step && ctx->l2_persist > 0) {
             const size_t wbytes = std::min(L.rec - L.z, ctx->l2_window);
             at[na].id = cudaLaunchAttributeAccessPolicyWindow;
             at[na].val.accessPolicyWindow.base_ptr = (void *)(ctx->base + L.z);

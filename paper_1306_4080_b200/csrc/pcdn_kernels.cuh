@@ -29,7 +29,7 @@ constexpr int QW = 6;              // Armijo candidates of a wide line-search wi
 constexpr int NPART = 32;          // per-CTA partial slots (packed: Ls[nq], L1[nq], Delta, |T|)
 constexpr int WREG = 4;            // bitmap words per thread kept in registers in phase C1
 constexpr int NE_MAX = 64;         // heavy entries handled per round inside one CTA
-constexpr int NREG = 4;            // rows with <= NREG records are folded by one thread
+constexpr int NREG = 8;            // rows with <= NREG records are folded by one thread
 constexpr int SHORT = 8;           // columns with <= SHORT nonzeros are reduced by one thread
 constexpr int MED_LEN = 128;       // ... with <= MED_LEN by one warp
 constexpr int CTA_LEN = 2048;      // ... with <= CTA_LEN by one CTA in the HBM-state kernels (default)

@@ -47,6 +47,7 @@ constexpr int R_HB = 256;  // per-warp bitonic buffer for samples with many reco
 constexpr int R_CPW = 8;   // own bundle positions per warp whose column results stay in smem
 constexpr int R_WMAX = 16; // partial-row slots (WinLayout<QW>::W)
 constexpr int R_RP = 4;    // own light columns per warp staged a step ahead
+constexpr int R_NREG = 4;  // records of a sample folded in one thread's registers (more: a warp)
 constexpr int R_TBW = 32 * NT / 32;   // touched-bitmap words (<= 32 owned samples per thread)
 
 struct __align__(16) RRec {  // a record: sample (then: next record of the sample's list), k, value
@@ -98,7 +99,7 @@ struct ResFixed {
     int sendcnt[16];             // records this CTA sent to each owner in the current step
     uint32_t recvcnt[16];        // records each producer CTA sent to this CTA (st.async, M0)
     int spilled;                 // this CTA wrote overflow records to HBM in the current step
-    int nlong;                   // samples whose list is longer than NREG (queued in lq)
+    int nlong;                   // samples whose list is longer than R_NREG (queued in lq)
     int ntl[2];                  // touched owned samples of the step, by step parity
     uint32_t tb[R_TBW];          // owned samples that received a record in the current step
     int stage_n;                 // HBM staging used by long lists in the current step
@@ -356,7 +357,7 @@ __device__ __forceinline__ RRec res_rec(const StepArgs &a, const ResCtx &R, int 
     return *reinterpret_cast<const RRec *>(&raw);
 }
 
-// Fold of one long list (> NREG records) by a warp.  Lane 0 walks the list into HBM staging
+// Fold of one long list (> R_NREG records) by a warp.  Lane 0 walks the list into HBM staging
 // (the CTA's rec2 region); <= R_HB records are bitonic-sorted by k in shared memory and summed
 // by lane-contiguous partials combined in a fixed tree; longer lists by repeated warp-wide
 // minimum extraction.  The k of one sample's records are distinct (one record per column).
@@ -563,7 +564,7 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
 #pragma unroll
     for (int q = 0; q < W; q++) acc[q] = 0.0;
     int ntouch = 0;
-    unsigned longmask = 0;   // owned samples (bit r) whose list is longer than NREG
+    unsigned longmask = 0;   // owned samples (bit r) whose list is longer than R_NREG
     // the step's touched owned samples (ascending li; every owned sample when a full column moved):
     // thread tid takes entries tid, tid + NT, ...  The previous step is already committed.
     const uint16_t *tl = R.tls + (size_t)R.cb * R.Bs;
@@ -588,14 +589,14 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
                 dx = rc.v;
                 R.head[li] = -1;
             } else {
-                // up to NREG records: gather, then add in ascending k (selection in registers)
-                int kk[NREG];
-                double vv[NREG];
+                // up to R_NREG records: gather, then add in ascending k (selection in registers)
+                int kk[R_NREG];
+                double vv[R_NREG];
                 kk[0] = rc.k;
                 vv[0] = rc.v;
                 int ni = 1, p = rc.li;
 #pragma unroll
-                for (int e2 = 1; e2 < NREG; e2++) {
+                for (int e2 = 1; e2 < R_NREG; e2++) {
                     kk[e2] = 0x7fffffff;
                     vv[e2] = 0.0;
                     if (p >= 0) {
@@ -620,7 +621,7 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
                     int best = 0x7fffffff;
                     double bv = 0.0;
 #pragma unroll
-                    for (int e2 = 0; e2 < NREG; e2++) {
+                    for (int e2 = 0; e2 < R_NREG; e2++) {
                         const bool take = kk[e2] > last && kk[e2] < best;
                         best = take ? kk[e2] : best;
                         bv = take ? vv[e2] : bv;
@@ -697,7 +698,7 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
     __syncthreads();
     if (ws.win == 0) RTL(R, 9);
     if (ws.win == 0 && fx.nlong > 0) {
-        // rare: samples with more than NREG records in this step.  Warps fold their lists, the
+        // rare: samples with more than R_NREG records in this step.  Warps fold their lists, the
         // owning threads add their loss changes, and the per-warp rows get a second fixed-order
         // contribution (the structure depends only on the data, so results stay deterministic).
         const int nl = fx.nlong;
