@@ -699,3 +699,18 @@ def test_tiny_shapes_parity(pk, shape, launch):
             os_ = o.solve(P, seed=2, max_outer=4)
             _compare_solve(gs, os_, s.w().cpu().numpy(), f"shape {shape} P={P} launch {launch}")
             s.close()
+
+
+def test_l2_persist_window_changes_nothing(pk):
+    """pcdn_set_l2_persist (an L2 access policy on the HBM-state kernels' launches) is a cache
+    policy only: w, the q trace and the F trace are bit-identical with and without it."""
+    prob = synth.config(1)
+    out = []
+    for on in (0, 1):
+        s = _solver(pk, prob, 2)
+        pk.pcdn_set_l2_persist(s.ctx, on)
+        r = s.solve(prob.P, seed=prob.seed, max_outer=2, trace=True)
+        out.append((s.w().cpu().numpy(), r["q_trace"], r["F_trace"]))
+        s.close()
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(a, b)
