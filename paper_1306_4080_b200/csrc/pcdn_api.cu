@@ -8,6 +8,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
+#include <cstddef>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -35,9 +36,23 @@ struct Lists {
     size_t order, hdesc, flag, fflag, fpos, flist, tiles3, colinfo, hpos, hlist, hlen, hstart, tiles1, tiles2, nheavy;
 };
 
+struct HostMirror {  // the readback block: device copy in the workspace, pinned host copy
+    double F;
+    double Fcopy;
+    long long err_idx;
+    int status;
+    int err_what;
+    int stop;   // set on the device at an outer boundary that ends the solve: later step launches exit
+    unsigned ticket;   // k_obj's last-block ticket (zero between launches)
+    int64_t counters[8];
+    double info[8];
+};
+
+static_assert(sizeof(HostMirror) % 8 == 0, "k_obj copies the read-back block in 8-byte words");
+
 struct Layout {
     size_t ydummy, w, z, coef, cnt, bits, rec, dxg, tlist, seen, dk, deltak, gk, hk, part, hpart, counters, info, F, Fcopy,
-        status, err_idx, err_what, bar, objp, prof, tl, dbg_dx, dbg_mark, rec2, rslot, ovf_cnt, part_gh, total;
+        status, err_idx, err_what, stop, ticket, mirror, bar, objp, prof, tl, dbg_dx, dbg_mark, rec2, rslot, ovf_cnt, part_gh, total;
     Lists ls[2];
 };
 
@@ -88,13 +103,17 @@ Layout make_layout(int64_t s, int64_t n, int64_t nnz)
     L.hk = take(sizeof(double) * 8);
     L.part = take(sizeof(double) * 2 * GMAX * NPART);
     L.hpart = take(sizeof(HPart) * GMAX * 2);
-    L.counters = take(sizeof(int64_t) * 8);
-    L.info = take(sizeof(double) * 8);
-    L.F = take(sizeof(double));
-    L.Fcopy = take(sizeof(double));
-    L.status = take(sizeof(int));
-    L.err_idx = take(sizeof(long long));
-    L.err_what = take(sizeof(int));
+    // the readback scalars: one block laid out as HostMirror, copied to the host in one piece
+    L.mirror = take(sizeof(HostMirror));
+    L.F = L.mirror + offsetof(HostMirror, F);
+    L.Fcopy = L.mirror + offsetof(HostMirror, Fcopy);
+    L.status = L.mirror + offsetof(HostMirror, status);
+    L.err_what = L.mirror + offsetof(HostMirror, err_what);
+    L.err_idx = L.mirror + offsetof(HostMirror, err_idx);
+    L.stop = L.mirror + offsetof(HostMirror, stop);
+    L.ticket = L.mirror + offsetof(HostMirror, ticket);
+    L.counters = L.mirror + offsetof(HostMirror, counters);
+    L.info = L.mirror + offsetof(HostMirror, info);
     L.bar = take(sizeof(unsigned long long));
     L.objp = take(sizeof(double) * 3 * OBJ_NB);
     L.prof = take(sizeof(long long) * 16);
@@ -109,16 +128,6 @@ Layout make_layout(int64_t s, int64_t n, int64_t nnz)
     L.total = off + ALIGN;  // slack for base alignment
     return L;
 }
-
-struct HostMirror {  // pinned readback block
-    double F;
-    double Fcopy;
-    int status;
-    int err_what;
-    long long err_idx;
-    int64_t counters[8];
-    double info[8];
-};
 
 }  // namespace
 
@@ -165,11 +174,14 @@ struct pcdn_ctx {
     cudaEvent_t ev_prep = nullptr;
     unsigned char *base = nullptr;
     Layout L{};
-    HostMirror *hm = nullptr;
+    HostMirror *hm = nullptr;   // [3]: hm[0] for single calls, hm[1..2] the solve's readback ring
+    HostMirror *hm_dev = nullptr;   // device address of the mapped pinned hm
+    bool solving = false;       // inside pcdn_solve: step launches honour the device stop flag
+    bool bar_clean = false;     // the grid barrier was re-armed on the device (k_obj): no memset
     int32_t *q_trace = nullptr;
     double *F_trace = nullptr;
     int64_t trace_cap = 0;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[10] = {};   // 0-3 single calls / solve span, 4-7 step spans (ring of 2), 8-9 readbacks
     int64_t launches = 0;
     char err[512] = {0};
 
@@ -246,7 +258,8 @@ int build_heavy(pcdn_ctx *ctx, int64_t ntot, int buf, cudaStream_t st)
 }
 
 // a0 for outer iteration k into list set `buf`: the partition pi_k and its lists
-int prep_outer(pcdn_ctx *ctx, uint64_t seed, int64_t k, int buf, cudaStream_t st)
+// (lists = false: the permutation and column descriptors only -- all the dense kernel reads)
+int prep_outer(pcdn_ctx *ctx, uint64_t seed, int64_t k, int buf, cudaStream_t st, bool lists = true)
 {
     const Lists &S = ctx->L.ls[buf];
     k_perm<<<grid1d(ctx->n), 256, 0, st>>>(seed, k, ctx->n, ctx->s, ctx->col_ptr, ctx->heavy_eff,
@@ -254,7 +267,7 @@ int prep_outer(pcdn_ctx *ctx, uint64_t seed, int64_t k, int buf, cudaStream_t st
                                            ctx->at<int32_t>(S.fflag), ctx->at<int4>(S.colinfo));
     ctx->launches++;
     CU(cudaGetLastError());
-    return build_heavy(ctx, ctx->n, buf, st);
+    return lists ? build_heavy(ctx, ctx->n, buf, st) : PCDN_OK;
 }
 
 #define SCDN_HEAVY_MSG "SCDN: a bundle column is longer than the warp split length; raise it with pcdn_set_launch(ctx, 3, 0, L)"
@@ -266,14 +279,17 @@ int prep_outer(pcdn_ctx *ctx, uint64_t seed, int64_t k, int buf, cudaStream_t st
             return set_err((ctx), PCDN_ERR_INVALID, "squared loss: call pcdn_set_targets first");        \
     } while (0)
 
-int objective_kernels(pcdn_ctx *ctx)
+// (stop_eps >= 0: also the solve's device-side stop test -- Eq.14 gap <= stop_eps when
+// stop_eps > 0, a non-finite F, or a raised status -- into the stop flag)
+int objective_kernels(pcdn_ctx *ctx, double stop_eps = -1.0)
 {
     PCDN_NEED_TARGETS(ctx);
     const Layout &L = ctx->L;
     k_obj_partial<<<OBJ_NB, 256, 0, ctx->stream>>>(ctx->s, ctx->n, ctx->at<double>(L.z), ctx->y, ctx->at<double>(L.w),
                                                    ctx->loss, ctx->at<double>(L.objp), ctx->t);
     k_obj_final<<<1, OBJ_NB, 0, ctx->stream>>>(ctx->at<double>(L.objp), ctx->c, ctx->mu, ctx->at<double>(L.F),
-                                               ctx->at<double>(L.Fcopy));
+                                               ctx->at<double>(L.Fcopy), stop_eps, ctx->fstar,
+                                               ctx->at<int>(L.status), stop_eps >= 0 ? ctx->at<int>(L.stop) : nullptr);
     ctx->launches += 2;
     CU(cudaGetLastError());
     return PCDN_OK;
@@ -293,15 +309,8 @@ int refresh_z(pcdn_ctx *ctx, int zero)
 
 int readback(pcdn_ctx *ctx)
 {
-    const Layout &L = ctx->L;
-    CU(cudaMemcpyAsync(&ctx->hm->F, ctx->at<double>(L.F), sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaMemcpyAsync(&ctx->hm->status, ctx->at<int>(L.status), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaMemcpyAsync(&ctx->hm->err_idx, ctx->at<long long>(L.err_idx), sizeof(long long), cudaMemcpyDeviceToHost,
+    CU(cudaMemcpyAsync(ctx->hm, ctx->at<HostMirror>(ctx->L.mirror), sizeof(HostMirror), cudaMemcpyDeviceToHost,
                        ctx->stream));
-    CU(cudaMemcpyAsync(&ctx->hm->err_what, ctx->at<int>(L.err_what), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaMemcpyAsync(ctx->hm->counters, ctx->at<int64_t>(L.counters), sizeof(int64_t) * 8, cudaMemcpyDeviceToHost,
-                       ctx->stream));
-    CU(cudaMemcpyAsync(ctx->hm->info, ctx->at<double>(L.info), sizeof(double) * 8, cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     return PCDN_OK;
 }
@@ -309,9 +318,9 @@ int readback(pcdn_ctx *ctx)
 int reset_status(pcdn_ctx *ctx)
 {
     const Layout &L = ctx->L;
-    CU(cudaMemsetAsync(ctx->at<int>(L.status), 0, sizeof(int), ctx->stream));
+    // status, err_what, stop (contiguous in the mirror block) and err_idx
+    CU(cudaMemsetAsync(ctx->at<int>(L.status), 0, 4 * sizeof(int), ctx->stream));
     CU(cudaMemsetAsync(ctx->at<long long>(L.err_idx), 0x7f, sizeof(long long), ctx->stream));
-    CU(cudaMemsetAsync(ctx->at<int>(L.err_what), 0, sizeof(int), ctx->stream));
     return PCDN_OK;
 }
 
@@ -368,6 +377,7 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
     a.hstart = ctx->at<int64_t>(S.hstart);
     a.fpos = ctx->at<int64_t>(S.fpos);
     a.flist = ctx->at<int32_t>(S.flist);
+    a.stop = ctx->solving ? ctx->at<int>(L.stop) : nullptr;
     a.ntot = ntot;
     a.P = P;
     a.nsteps = nsteps;
@@ -410,7 +420,8 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
     a.ovf_cnt = ctx->at<int>(L.ovf_cnt);
     a.part_gh = ctx->at<double>(L.part_gh);
     a.dense_tcap = ctx->dense_tcap;
-    CU(cudaMemsetAsync(a.bar, 0, sizeof(unsigned long long), ctx->stream));
+    if (!ctx->bar_clean) CU(cudaMemsetAsync(a.bar, 0, sizeof(unsigned long long), ctx->stream));
+    ctx->bar_clean = false;
     // cluster mode for steps small enough that 16 SMs keep up (hardware barrier, ~0.2 us);
     // grid mode (all SMs, software barrier) for large steps
     const int mode = choose_mode(ctx, P);
@@ -538,7 +549,7 @@ static void preload_kernels()
         (const void *)k_step<ClusterSync>, res_kernel(LOSS_LOGISTIC, false), res_kernel(LOSS_L2SVM, false),
         res_kernel(LOSS_SQ, false), res_kernel(LOSS_LOGISTIC, true), res_kernel(LOSS_L2SVM, true),
         res_kernel(LOSS_SQ, true), dense_kernel(LOSS_LOGISTIC), dense_kernel(LOSS_L2SVM), dense_kernel(LOSS_SQ),
-        (const void *)k_set_z, (const void *)k_obj_partial, (const void *)k_obj_final, (const void *)k_validate,
+        (const void *)k_set_z, (const void *)k_obj_partial, (const void *)k_obj_final, (const void *)k_obj, (const void *)k_validate,
         (const void *)k_validate_transpose, (const void *)k_check_finite, (const void *)k_sh_gh, (const void *)k_sh_dir,
         (const void *)k_sh_ls, (const void *)k_sh_ls_long, (const void *)k_sh_ls_final, (const void *)k_sh_commit};
     for (const void *f : fns) {
@@ -724,9 +735,12 @@ int pcdn_create(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_ptr, c
     ctx->stream = (cudaStream_t)cuda_stream;
     ctx->base = reinterpret_cast<unsigned char *>(align_up(reinterpret_cast<uintptr_t>(workspace)));
     {
-        cudaError_t e = cudaMallocHost(&ctx->hm, sizeof(HostMirror));
-        if (e != cudaSuccess) return fail(set_err(ctx, PCDN_ERR_CUDA, "cudaMallocHost: %s", cudaGetErrorString(e)));
-        for (int i = 0; i < 4; i++) {
+        cudaError_t e = cudaHostAlloc(&ctx->hm, 3 * sizeof(HostMirror), cudaHostAllocMapped | cudaHostAllocPortable);
+        if (e != cudaSuccess) return fail(set_err(ctx, PCDN_ERR_CUDA, "cudaHostAlloc: %s", cudaGetErrorString(e)));
+        e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&ctx->hm_dev), ctx->hm, 0);
+        if (e != cudaSuccess)
+            return fail(set_err(ctx, PCDN_ERR_CUDA, "cudaHostGetDevicePointer: %s", cudaGetErrorString(e)));
+        for (int i = 0; i < 10; i++) {
             e = cudaEventCreate(&ctx->ev[i]);
             if (e != cudaSuccess) return fail(set_err(ctx, PCDN_ERR_CUDA, "cudaEventCreate: %s", cudaGetErrorString(e)));
         }
@@ -968,7 +982,8 @@ int pcdn_objective(pcdn_ctx *ctx, int recompute_from_w, double *F_out)
     PCDN_NEED_TARGETS(ctx);
     k_obj_partial<<<OBJ_NB, 256, 0, ctx->stream>>>(ctx->s, ctx->n, ctx->at<double>(L.z), ctx->y, ctx->at<double>(L.w),
                                                    ctx->loss, ctx->at<double>(L.objp), ctx->t);
-    k_obj_final<<<1, OBJ_NB, 0, ctx->stream>>>(ctx->at<double>(L.objp), ctx->c, ctx->mu, ctx->at<double>(L.Fcopy), nullptr);
+    k_obj_final<<<1, OBJ_NB, 0, ctx->stream>>>(ctx->at<double>(L.objp), ctx->c, ctx->mu, ctx->at<double>(L.Fcopy), nullptr, -1.0, 0.0,
+                                               nullptr, nullptr);
     ctx->launches += 2;
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(&ctx->hm->Fcopy, ctx->at<double>(L.Fcopy), sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1080,50 +1095,112 @@ int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_
     // partition and lists are then built concurrently on the side stream (double-buffered sets)
     const int smode = choose_mode(ctx, P);
     ctx->heavy_eff = heavy_for_mode(ctx, smode);
+    // the dense kernel needs only the permutation: k_obj computes it (no launch of its own)
     const bool overlap = ctx->side != nullptr && smode == 3;
-    if (max_outer > 0 && (rc = prep_outer(ctx, seed, 0, 0, ctx->stream))) return rc;
+    const bool lists = smode != 4;
+    // Outer iteration kk, queued without waiting: partition pi_kk's lists were built during the
+    // previous one; the step launch; the next partition into the other list set (on the side
+    // stream beside the one-cluster kernel, after the step that last read that set; else behind
+    // the step launch); F from scratch with the device-side stop test; the readback into ring slot
+    // kk & 1.  The host queues iteration k+1 before it waits for iteration k's readback, so the
+    // GPU never idles on the host's stop decision; when iteration k ends the solve, iteration
+    // k+1's step launch finds the stop flag and exits without touching the state.
+    HostMirror *const ring = ctx->hm + 1;
+    auto enqueue_outer = [&](int32_t kk) -> int {
+        const int buf = kk & 1, r = kk & 1;
+        if (kk > 0 && overlap) CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_prep, 0));
+        CU(cudaEventRecord(ctx->ev[4 + 2 * r], ctx->stream));
+        ctx->bar_clean = kk > 0;   // re-armed by the previous outer iteration's k_obj
+        int rc2 = launch_steps(ctx, buf, ctx->n, P, b, (int64_t)kk * b, nullptr, nullptr, nullptr);
+        if (rc2) return rc2;
+        CU(cudaEventRecord(ctx->ev[5 + 2 * r], ctx->stream));
+        if (kk + 1 < max_outer && lists) {
+            if (overlap && kk > 0) CU(cudaStreamWaitEvent(ctx->side, ctx->ev[5 + 2 * (r ^ 1)], 0));
+            if ((rc2 = prep_outer(ctx, seed, kk + 1, buf ^ 1, overlap ? ctx->side : ctx->stream, lists))) return rc2;
+            if (overlap) CU(cudaEventRecord(ctx->ev_prep, ctx->side));
+        }
+        // a6: F from scratch (reading Z23) and the Eq.14 test in one launch, which also writes the
+        // read-back block into ring slot r (mapped pinned memory)
+        {
+            const Layout &L = ctx->L;
+            ObjBoundary o{};
+            o.c = ctx->c;
+            o.mu = ctx->mu;
+            o.eps = eps > 0 ? eps : 0.0;
+            o.fstar = ctx->fstar;
+            o.F = ctx->at<double>(L.F);
+            o.status = ctx->at<int>(L.status);
+            o.stop = ctx->at<int>(L.stop);
+            o.ticket = ctx->at<unsigned>(L.ticket);
+            o.bar = ctx->at<unsigned long long>(L.bar);
+            o.mirror = ctx->at<unsigned long long>(L.mirror);
+            o.mirror_host = reinterpret_cast<unsigned long long *>(ctx->hm_dev + 1 + r);
+            o.mirror_words = (int)(sizeof(HostMirror) / 8);
+            if (!lists && kk + 1 < max_outer) {
+                const Lists &S = L.ls[buf ^ 1];
+                o.perm = 1;
+                o.seed = seed;
+                o.k_next = kk + 1;
+                o.n = ctx->n;
+                o.s = ctx->s;
+                o.col_ptr = ctx->col_ptr;
+                o.heavy_len = ctx->heavy_eff;
+                o.order = ctx->at<int32_t>(S.order);
+                o.flag = ctx->at<int32_t>(S.flag);
+                o.fflag = ctx->at<int32_t>(S.fflag);
+                o.colinfo = ctx->at<int4>(S.colinfo);
+            }
+            k_obj<<<OBJ_NB, OBJ_NB, 0, ctx->stream>>>(ctx->s, ctx->n, ctx->at<double>(L.z), ctx->y,
+                                                      ctx->at<double>(L.w), ctx->loss, ctx->at<double>(L.objp), ctx->t, o);
+            ctx->launches++;
+            CU(cudaGetLastError());
+        }
+        CU(cudaEventRecord(ctx->ev[8 + r], ctx->stream));
+        return PCDN_OK;
+    };
+    struct SolvingScope {
+        pcdn_ctx *c;
+        ~SolvingScope() { c->solving = false; }
+    } scope{ctx};
+    ctx->solving = true;
+    int32_t last = -1;   // last outer iteration queued
+    if (max_outer > 0) {
+        if ((rc = prep_outer(ctx, seed, 0, 0, ctx->stream, lists))) return rc;
+        if ((rc = enqueue_outer(0))) return rc;
+        last = 0;
+    }
     for (k = 0; k < max_outer; k++) {
-        const int buf = k & 1;
-        // a0: partition pi_k and its lists (built ahead on the side stream when overlapping)
-        if (k > 0) {
-            if (overlap) CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_prep, 0));
-            else if ((rc = prep_outer(ctx, seed, k, buf, ctx->stream))) return rc;
+        if (k + 1 < max_outer) {
+            if ((rc = enqueue_outer(k + 1))) return rc;
+            last = k + 1;
         }
-        // a1..a5: all b bundle steps in one persistent launch
-        CU(cudaEventRecord(ctx->ev[0], ctx->stream));
-        if ((rc = launch_steps(ctx, buf, ctx->n, P, b, (int64_t)k * b, nullptr, nullptr, nullptr))) return rc;
-        CU(cudaEventRecord(ctx->ev[1], ctx->stream));
-        if (overlap && k + 1 < max_outer) {
-            if ((rc = prep_outer(ctx, seed, k + 1, buf ^ 1, ctx->side))) return rc;
-            CU(cudaEventRecord(ctx->ev_prep, ctx->side));
-        }
-        // a6: F from scratch (reading Z23), one readback per outer iteration
-        if ((rc = objective_kernels(ctx))) return rc;
-        if ((rc = readback(ctx))) return rc;
+        const int r = k & 1;
+        CU(cudaEventSynchronize(ctx->ev[8 + r]));
+        const HostMirror &m = ring[r];
         float ms = 0.f;
-        CU(cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]));
+        CU(cudaEventElapsedTime(&ms, ctx->ev[4 + 2 * r], ctx->ev[5 + 2 * r]));
         t_step_ms += ms;
-        F = ctx->hm->F;
-        if (ctx->hm->status == 3 || !std::isfinite(F)) {
+        F = m.F;
+        if (m.status == 3 || !std::isfinite(F)) {
             status = PCDN_ERR_NUMERIC;
             set_err(ctx, PCDN_ERR_NUMERIC, "non-finite objective in outer iteration %d", k);
             k++;
             break;
         }
-        if (ctx->hm->status == 7) {
+        if (m.status == 7) {
             status = PCDN_ERR_INVALID;
             set_err(ctx, PCDN_ERR_INVALID, SCDN_HEAVY_MSG);
             k++;
             break;
         }
-        if (ctx->hm->status) {
+        if (m.status) {
             status = PCDN_ERR_CUDA;
-            set_err(ctx, PCDN_ERR_CUDA, "internal consistency check failed (%d)", ctx->hm->status);
+            set_err(ctx, PCDN_ERR_CUDA, "internal consistency check failed (%d)", m.status);
             k++;
             break;
         }
         if (eps > 0) {
-            gap = (F - ctx->fstar) / ctx->fstar;  // Eq.14
+            gap = (F - ctx->fstar) / ctx->fstar;  // Eq.14 (the same test as k_obj_final's)
             if (gap <= eps) {
                 status = PCDN_OK;
                 k++;
@@ -1139,6 +1216,8 @@ int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_
     if (max_outer == 0) {
         if ((rc = readback(ctx))) return rc;
         F = ctx->hm->F;
+    } else {
+        ctx->hm[0] = ring[last & 1];   // counters after every queued launch (a stopped one adds nothing)
     }
     if (info) {
         float ms = 0.f;
@@ -1273,7 +1352,8 @@ int pcdn_shard_loss(pcdn_ctx *ctx, double *loss_out)
     const Layout &L = ctx->L;
     k_obj_partial<<<OBJ_NB, 256, 0, ctx->stream>>>(ctx->s, 0, ctx->at<double>(L.z), ctx->y, ctx->at<double>(L.w),
                                                    ctx->loss, ctx->at<double>(L.objp), ctx->t);
-    k_obj_final<<<1, OBJ_NB, 0, ctx->stream>>>(ctx->at<double>(L.objp), ctx->c, 0.0, ctx->at<double>(L.Fcopy), nullptr);
+    k_obj_final<<<1, OBJ_NB, 0, ctx->stream>>>(ctx->at<double>(L.objp), ctx->c, 0.0, ctx->at<double>(L.Fcopy), nullptr, -1.0, 0.0,
+                                               nullptr, nullptr);
     ctx->launches += 2;
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(&ctx->hm->Fcopy, ctx->at<double>(L.Fcopy), sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));

@@ -246,6 +246,7 @@ __device__ __forceinline__ void dense_decide(const StepArgs &a, DenseFixed &sm, 
 template <int LOSS>
 __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
 {
+    if (a.stop && ldcg(a.stop)) return;   // the solve already ended (queued ahead; grid-uniform)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     DenseFixed &sm = *reinterpret_cast<DenseFixed *>(smem_raw);
     float *tiles = reinterpret_cast<float *>(smem_raw + dense_fixed_bytes());

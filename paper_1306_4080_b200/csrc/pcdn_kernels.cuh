@@ -73,6 +73,7 @@ struct StepArgs {
     int scdn;          // 1: SCDN (Alg.2, reading Z27) -- per-feature 1-D steps, no P-dim line search
     int loss, qmax;
     int heavy_len;
+    const int *stop;   // nullable: set by an earlier outer boundary's stop test -> the launch exits at once
     // state
     double *w;
     double *z;
@@ -390,8 +391,9 @@ __device__ __forceinline__ int64_t colinfo_p0(const int4 &ci)
 
 // order[t] = pi_k(t); flag[t] = column length > heavy_len; fflag[t] = column is full (holds a
 // nonzero in every row: its entry for row i sits at col_ptr[j] + i); colinfo[t] (nullable)
-__global__ void k_perm(uint64_t seed, int64_t k, int64_t n, int64_t s, const int64_t *__restrict__ col_ptr,
-                       int heavy_len, int32_t *order, int32_t *flag, int32_t *fflag, int4 *colinfo)
+__device__ __forceinline__ void perm_positions(uint64_t seed, int64_t k, int64_t n, int64_t s,
+                                               const int64_t *__restrict__ col_ptr, int heavy_len, int32_t *order,
+                                               int32_t *flag, int32_t *fflag, int4 *colinfo)
 {
     const FeistelKeys f = feistel_keys(seed, k, n);
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
@@ -404,6 +406,12 @@ __global__ void k_perm(uint64_t seed, int64_t k, int64_t n, int64_t s, const int
             if (colinfo) colinfo[t] = make_colinfo((int32_t)j, p0, len);
         }
     }
+}
+
+__global__ void k_perm(uint64_t seed, int64_t k, int64_t n, int64_t s, const int64_t *__restrict__ col_ptr,
+                       int heavy_len, int32_t *order, int32_t *flag, int32_t *fflag, int4 *colinfo)
+{
+    perm_positions(seed, k, n, s, col_ptr, heavy_len, order, flag, fflag, colinfo);
 }
 
 // full-column compaction: flist[e] = position of the e-th full column (fpos = exclusive scan)
@@ -1153,6 +1161,7 @@ __device__ __forceinline__ void window(const StepArgs &a, StepSmem &sm, Sync &sy
 template <class Sync>
 __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
 {
+    if (a.stop && ldcg(a.stop)) return;   // the solve already ended (queued ahead; grid-uniform)
     Sync sy(a.bar);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     StepSmem &sm = *reinterpret_cast<StepSmem *>(smem_raw);
@@ -1788,8 +1797,9 @@ __global__ void k_set_z(int64_t s, const int64_t *__restrict__ row_ptr, const in
 
 // F = c sum_i phi(y_i z_i) + sum_j |w_j|, fixed two-level order: tile b of each array
 constexpr int OBJ_NB = 256;
-__global__ void k_obj_partial(int64_t s, int64_t n, const double *__restrict__ z, const int8_t *__restrict__ y,
-                              const double *__restrict__ w, int loss, double *partial, const double *__restrict__ t)
+__device__ __forceinline__ void obj_block_partial(int64_t s, int64_t n, const double *__restrict__ z,
+                                                  const int8_t *__restrict__ y, const double *__restrict__ w, int loss,
+                                                  double *partial, const double *__restrict__ t)
 {
     const int b = blockIdx.x;
     const int64_t zs0 = (int64_t)b * s / OBJ_NB, zs1 = (int64_t)(b + 1) * s / OBJ_NB;
@@ -1830,14 +1840,24 @@ __global__ void k_obj_partial(int64_t s, int64_t n, const double *__restrict__ z
     }
 }
 
+__global__ void k_obj_partial(int64_t s, int64_t n, const double *__restrict__ z, const int8_t *__restrict__ y,
+                              const double *__restrict__ w, int loss, double *partial, const double *__restrict__ t)
+{
+    obj_block_partial(s, n, z, y, w, loss, partial, t);
+}
+
 // F = c sum phi + ||w||_1 + (mu/2)||w||^2 (Eq.1 + the elastic-net term of Z25)
-__global__ void k_obj_final(const double *__restrict__ partial, double c, double mu, double *F, double *F_copy)
+// stop (nullable): the solve's device-side stop test at this outer boundary -- the Eq.14 gap
+// (F - F*)/F* <= eps (eps > 0), a non-finite F, or a raised status -- so that step launches the
+// host queued ahead exit at once (the host takes the same decision from the read-back F)
+__device__ __forceinline__ void obj_final_body(const double *partial, double c, double mu, double *F,
+                                               double *F_copy, double eps, double fstar, const int *status, int *stop)
 {
     __shared__ double sh[3][OBJ_NB];
     const int t = threadIdx.x;
-    sh[0][t] = partial[3 * t];
-    sh[1][t] = partial[3 * t + 1];
-    sh[2][t] = partial[3 * t + 2];
+    sh[0][t] = __ldcg(&partial[3 * t]);
+    sh[1][t] = __ldcg(&partial[3 * t + 1]);
+    sh[2][t] = __ldcg(&partial[3 * t + 2]);
     __syncthreads();
     for (int o = OBJ_NB / 2; o > 0; o >>= 1) {
         if (t < o) {
@@ -1851,7 +1871,65 @@ __global__ void k_obj_final(const double *__restrict__ partial, double c, double
         const double Fv = c * sh[0][0] + sh[1][0] + 0.5 * mu * sh[2][0];
         *F = Fv;
         if (F_copy) *F_copy = Fv;
+        if (stop && (!isfinite(Fv) || ldcg(status) != 0 || (eps > 0 && (Fv - fstar) / fstar <= eps))) *stop = 1;
     }
+}
+
+__global__ void k_obj_final(const double *__restrict__ partial, double c, double mu, double *F, double *F_copy,
+                            double eps, double fstar, const int *status, int *stop)
+{
+    obj_final_body(partial, c, mu, F, F_copy, eps, fstar, status, stop);
+}
+
+// The solve's outer boundary in one launch (OBJ_NB blocks of OBJ_NB threads): the block partials,
+// then the last block to finish (ticket) sums them in the fixed order of k_obj_final, takes the
+// stop test, re-arms the step kernels' grid barrier and the ticket, and copies the read-back block
+// (F, status, counters, ...) straight into mapped pinned host memory -- no copy-engine work between
+// two step launches.
+struct ObjBoundary {
+    double c, mu, eps, fstar;
+    double *F;
+    const int *status;
+    int *stop;
+    unsigned *ticket;
+    unsigned long long *bar;
+    const unsigned long long *mirror;   // device block (8-byte words)
+    unsigned long long *mirror_host;    // mapped pinned host block
+    int mirror_words;
+    // optional: the next outer iteration's partition (k_perm's output) when nothing else of the
+    // list build is needed (the dense kernel)
+    int perm;
+    uint64_t seed;
+    int64_t k_next, n, s;
+    const int64_t *col_ptr;
+    int heavy_len;
+    int32_t *order, *flag, *fflag;
+    int4 *colinfo;
+};
+__global__ void __launch_bounds__(OBJ_NB) k_obj(int64_t s, int64_t n, const double *__restrict__ z,
+                                                const int8_t *__restrict__ y, const double *__restrict__ w, int loss,
+                                                double *partial, const double *__restrict__ t, ObjBoundary o)
+{
+    if (o.perm) perm_positions(o.seed, o.k_next, o.n, o.s, o.col_ptr, o.heavy_len, o.order, o.flag, o.fflag, o.colinfo);
+    obj_block_partial(s, n, z, y, w, loss, partial, t);
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(o.ticket, 1u) == (unsigned)(OBJ_NB - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    obj_final_body(partial, o.c, o.mu, o.F, nullptr, o.eps, o.fstar, o.status, o.stop);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *o.ticket = 0u;
+        *o.bar = 0ull;
+    }
+    __threadfence();
+    __syncthreads();
+    for (int e = threadIdx.x; e < o.mirror_words; e += blockDim.x) o.mirror_host[e] = __ldcg(&o.mirror[e]);
+    __threadfence_system();
 }
 
 // status 1 + first index of a non-finite value (squared-loss targets)

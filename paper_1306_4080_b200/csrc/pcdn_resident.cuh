@@ -846,6 +846,7 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
 template <int LOSS, bool SCDN>
 __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
 {
+    if (a.stop && ldcg(a.stop)) return;   // the solve already ended (queued ahead; grid-uniform)
     a.loss = LOSS;   // a compile-time loss: the other loss's code is dead (smaller instruction footprint)
     a.scdn = SCDN;   // likewise the SCDN baseline's per-feature line search
     extern __shared__ __align__(16) unsigned char smem_raw[];
