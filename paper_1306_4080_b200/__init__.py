@@ -126,7 +126,7 @@ def pcdn_set_trace(ctx, q_trace, F_trace, capacity):
 
 
 def pcdn_set_debug(ctx, on):
-    return check(ctx, lib().pcdn_set_debug(ctx, 1 if on else 0))
+    return check(ctx, lib().pcdn_set_debug(ctx, int(on)))
 
 
 def pcdn_set_launch(ctx, mode=0, ctas=0, heavy_len=0):

@@ -34,6 +34,7 @@ inline size_t align_up(size_t x) { return (x + ALIGN - 1) & ~(ALIGN - 1); }
 // so that the lists of outer iteration k+1 can be built while the step kernel of k runs
 struct Lists {
     size_t order, hdesc, flag, fflag, fpos, flist, tiles3, colinfo, hpos, hlist, hlen, hstart, tiles1, tiles2, nheavy;
+    size_t lb, ticket;   // k_prep_lists: tile states (zeroed at create) and its ticket pair
 };
 
 struct HostMirror {  // the readback block: device copy in the workspace, pinned host copy
@@ -95,6 +96,8 @@ Layout make_layout(int64_t s, int64_t n, int64_t nnz)
         S.tiles1 = take(sizeof(int64_t) * ntile);
         S.tiles2 = take(sizeof(int64_t) * ntile);
         S.nheavy = take(sizeof(int64_t));
+        S.lb = take(sizeof(LbTile) * (size_t)((n + PL_TILE - 1) / PL_TILE + 1));
+        S.ticket = take(sizeof(unsigned) * 2);
     }
     L.seen = take(sizeof(uint32_t) * ((n + 31) / 32));
     L.dk = take(sizeof(double) * n);
@@ -178,6 +181,8 @@ struct pcdn_ctx {
     HostMirror *hm_dev = nullptr;   // device address of the mapped pinned hm
     bool solving = false;       // inside pcdn_solve: step launches honour the device stop flag
     bool bar_clean = false;     // the grid barrier was re-armed on the device (k_obj): no memset
+    unsigned prep_epoch = 0;    // k_prep_lists launches (tile-state epoch)
+    bool split_prep = false;    // test knob: build the lists with k_perm + scans + compactions
     int32_t *q_trace = nullptr;
     double *F_trace = nullptr;
     int64_t trace_cap = 0;
@@ -257,11 +262,33 @@ int build_heavy(pcdn_ctx *ctx, int64_t ntot, int buf, cudaStream_t st)
     return PCDN_OK;
 }
 
-// a0 for outer iteration k into list set `buf`: the partition pi_k and its lists
+// a0 for outer iteration k into list set `buf`: the partition pi_k and its lists, one launch
 // (lists = false: the permutation and column descriptors only -- all the dense kernel reads)
 int prep_outer(pcdn_ctx *ctx, uint64_t seed, int64_t k, int buf, cudaStream_t st, bool lists = true)
 {
     const Lists &S = ctx->L.ls[buf];
+    if (lists && !ctx->split_prep) {
+        PrepLists o{};
+        o.order = ctx->at<int32_t>(S.order);
+        o.colinfo = ctx->at<int4>(S.colinfo);
+        o.hpos = ctx->at<int64_t>(S.hpos);
+        o.hstart = ctx->at<int64_t>(S.hstart);
+        o.fpos = ctx->at<int64_t>(S.fpos);
+        o.nheavy = ctx->at<int64_t>(S.nheavy);
+        o.hlist = ctx->at<int32_t>(S.hlist);
+        o.flist = ctx->at<int32_t>(S.flist);
+        o.hdesc = ctx->at<int4>(S.hdesc);
+        o.lb = ctx->at<LbTile>(S.lb);
+        o.ticket = ctx->at<unsigned>(S.ticket);
+        const int64_t ntiles = (ctx->n + PL_TILE - 1) / PL_TILE;
+        ctx->prep_epoch = (ctx->prep_epoch + 1) & 0x3fffffffu;
+        if (ctx->prep_epoch == 0) ctx->prep_epoch = 1;   // 0 is the zeroed workspace's state
+        k_prep_lists<<<(unsigned)ntiles, PL_NT, 0, st>>>(seed, k, ctx->n, ctx->s, ctx->col_ptr, ctx->heavy_eff,
+                                                         ctx->prep_epoch, o);
+        ctx->launches++;
+        CU(cudaGetLastError());
+        return PCDN_OK;
+    }
     k_perm<<<grid1d(ctx->n), 256, 0, st>>>(seed, k, ctx->n, ctx->s, ctx->col_ptr, ctx->heavy_eff,
                                            ctx->at<int32_t>(S.order), ctx->at<int32_t>(S.flag),
                                            ctx->at<int32_t>(S.fflag), ctx->at<int4>(S.colinfo));
@@ -549,7 +576,7 @@ static void preload_kernels()
         (const void *)k_step<ClusterSync>, res_kernel(LOSS_LOGISTIC, false), res_kernel(LOSS_L2SVM, false),
         res_kernel(LOSS_SQ, false), res_kernel(LOSS_LOGISTIC, true), res_kernel(LOSS_L2SVM, true),
         res_kernel(LOSS_SQ, true), dense_kernel(LOSS_LOGISTIC), dense_kernel(LOSS_L2SVM), dense_kernel(LOSS_SQ),
-        (const void *)k_set_z, (const void *)k_obj_partial, (const void *)k_obj_final, (const void *)k_obj, (const void *)k_validate,
+        (const void *)k_set_z, (const void *)k_obj_partial, (const void *)k_obj_final, (const void *)k_obj, (const void *)k_prep_lists, (const void *)k_validate,
         (const void *)k_validate_transpose, (const void *)k_check_finite, (const void *)k_sh_gh, (const void *)k_sh_dir,
         (const void *)k_sh_ls, (const void *)k_sh_ls_long, (const void *)k_sh_ls_final, (const void *)k_sh_commit};
     for (const void *f : fns) {
@@ -856,7 +883,8 @@ int pcdn_set_trace(pcdn_ctx *ctx, int32_t *q_trace, double *F_trace, int64_t cap
 int pcdn_set_debug(pcdn_ctx *ctx, int on)
 {
     if (!ctx) return PCDN_ERR_INVALID;
-    ctx->debug = on ? 1 : 0;
+    ctx->debug = (on & 1) ? 1 : 0;
+    ctx->split_prep = (on & 2) != 0;
     return PCDN_OK;
 }
 

@@ -575,6 +575,171 @@ __global__ void k_heavy_compact(const int64_t *__restrict__ hpos, int64_t ntot, 
     }
 }
 
+// a0 in one launch: the permutation pi_k of a whole outer iteration and the lists the step kernels
+// read -- column descriptors, heavy-column lists (hpos, hlist, hdesc, hstart) and full-column
+// lists (fpos, flist) -- with the three position-order prefix sums taken by a single-pass scan
+// (tiles claimed in order from a ticket; decoupled look-back over the tiles' published aggregate /
+// inclusive sums; integer sums, so exact).  The output equals k_perm + build_heavy's twelve
+// launches.  Tile states carry the launch's epoch, so they need no clearing between launches; the
+// last tile to finish re-arms the ticket.
+constexpr int PL_NT = 256, PL_PER = 2, PL_TILE = PL_NT * PL_PER;
+struct alignas(64) LbTile {
+    long long agg[3];   // (heavy count, heavy nnz, full count) of the tile
+    long long inc[3];   // the same, inclusive of every earlier tile
+    unsigned flag;      // epoch << 2 | 1 (agg valid) or | 2 (inc valid)
+};
+struct PrepLists {
+    int32_t *order;
+    int4 *colinfo;
+    int64_t *hpos, *hstart, *fpos, *nheavy;
+    int32_t *hlist, *flist;
+    int4 *hdesc;
+    LbTile *lb;
+    unsigned *ticket;   // [0] next tile, [1] tiles done
+};
+__global__ void __launch_bounds__(PL_NT) k_prep_lists(uint64_t seed, int64_t k, int64_t n, int64_t s,
+                                                      const int64_t *__restrict__ col_ptr, int heavy_len,
+                                                      unsigned epoch, PrepLists o)
+{
+    __shared__ unsigned s_tile;
+    __shared__ long long s_w[3][PL_NT / 32];
+    __shared__ long long s_pre[3];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned ntiles = (unsigned)((n + PL_TILE - 1) / PL_TILE);
+    if (tid == 0) s_tile = atomicAdd(&o.ticket[0], 1u);
+    __syncthreads();
+    const unsigned tile = s_tile;
+    const FeistelKeys f = feistel_keys(seed, k, n);
+    // this thread's PL_PER consecutive positions
+    int32_t jv[PL_PER];
+    int64_t p0v[PL_PER], lenv[PL_PER];
+    long long v[3] = {0, 0, 0};
+    const int64_t tb = (int64_t)tile * PL_TILE + (int64_t)tid * PL_PER;
+#pragma unroll
+    for (int e = 0; e < PL_PER; e++) {
+        const int64_t t = tb + e;
+        jv[e] = 0;
+        p0v[e] = 0;
+        lenv[e] = -1;
+        if (t < n) {
+            const int32_t j = (int32_t)feistel_perm(f, n, t);
+            const int64_t p0 = __ldg(&col_ptr[j]), len = __ldg(&col_ptr[j + 1]) - p0;
+            jv[e] = j;
+            p0v[e] = p0;
+            lenv[e] = len;
+            o.order[t] = j;
+            o.colinfo[t] = make_colinfo(j, p0, len);
+            if (len > heavy_len) {
+                v[0] += 1;
+                v[1] += len;
+            }
+            if (len == s) v[2] += 1;
+        }
+    }
+    // block exclusive scan of v (warp shuffles, then the warp totals)
+    long long inc[3] = {v[0], v[1], v[2]};
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+            const long long u = __shfl_up_sync(0xffffffffu, inc[q], d);
+            if (lane >= d) inc[q] += u;
+        }
+    }
+    if (lane == 31)
+        for (int q = 0; q < 3; q++) s_w[q][warp] = inc[q];
+    __syncthreads();
+    long long wpre[3] = {0, 0, 0}, tot[3] = {0, 0, 0};
+    for (int w2 = 0; w2 < PL_NT / 32; w2++)
+        for (int q = 0; q < 3; q++) {
+            if (w2 < warp) wpre[q] += s_w[q][w2];
+            tot[q] += s_w[q][w2];
+        }
+    // publish the aggregate, look back (warp 0, 32 tiles at a time), publish the inclusive sum
+    if (warp == 0) {
+        LbTile &me = o.lb[tile];
+        if (lane == 0) {
+            for (int q = 0; q < 3; q++) me.agg[q] = tot[q];
+            if (tile == 0)
+                for (int q = 0; q < 3; q++) me.inc[q] = tot[q];
+            __threadfence();
+            *(volatile unsigned *)&me.flag = (epoch << 2) | (tile == 0 ? 2u : 1u);
+        }
+        long long pre[3] = {0, 0, 0};
+        long long base = (long long)tile - 1;
+        while (base >= 0) {
+            const long long i = base - lane;
+            unsigned st = 2u;   // before tile 0: an inclusive sum of zero
+            long long val[3] = {0, 0, 0};
+            if (i >= 0) {
+                const volatile unsigned *fp = &o.lb[i].flag;
+                unsigned fl;
+                do {
+                    fl = *fp;
+                } while ((fl >> 2) != epoch || (fl & 3u) == 0u);
+                st = fl & 3u;
+                __threadfence();
+                const long long *src = st == 2u ? o.lb[i].inc : o.lb[i].agg;
+                for (int q = 0; q < 3; q++) val[q] = __ldcg(&src[q]);
+            }
+            const unsigned pm = __ballot_sync(0xffffffffu, st == 2u);
+            const int lp = pm ? __ffs(pm) - 1 : 32;   // the nearest tile with an inclusive sum
+            for (int q = 0; q < 3; q++) {
+                long long x = lane <= lp ? val[q] : 0;
+                for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
+                pre[q] += x;
+            }
+            if (pm) break;
+            base -= 32;
+        }
+        if (lane == 0) {
+            if (tile != 0) {
+                for (int q = 0; q < 3; q++) me.inc[q] = pre[q] + tot[q];
+                __threadfence();
+                *(volatile unsigned *)&me.flag = (epoch << 2) | 2u;
+            }
+            for (int q = 0; q < 3; q++) s_pre[q] = pre[q];
+        }
+    }
+    __syncthreads();
+    long long run[3];
+    for (int q = 0; q < 3; q++) run[q] = s_pre[q] + wpre[q] + inc[q] - v[q];   // exclusive, at tb
+#pragma unroll
+    for (int e = 0; e < PL_PER; e++) {
+        const int64_t t = tb + e;
+        if (t >= n) break;
+        o.hpos[t] = run[0];
+        o.fpos[t] = run[2];
+        const int64_t len = lenv[e];
+        if (len > heavy_len) {
+            const int64_t cs = p0v[e];
+            o.hlist[run[0]] = (int32_t)t;
+            o.hdesc[run[0]] = make_int4((int)t, jv[e], (int)(uint32_t)(cs & 0xffffffffLL), (int)(cs >> 32));
+            o.hstart[run[0]] = run[1];
+            run[0] += 1;
+            run[1] += len;
+        }
+        if (len == s) {
+            o.flist[run[2]] = (int32_t)t;
+            run[2] += 1;
+        }
+        if (t == n - 1) {   // the totals
+            o.hpos[n] = run[0];
+            o.fpos[n] = run[2];
+            o.hstart[run[0]] = run[1];
+            *o.nheavy = run[0];
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(&o.ticket[1], 1u) == ntiles - 1) {   // every tile claimed and finished
+            o.ticket[0] = 0u;
+            o.ticket[1] = 0u;
+        }
+    }
+}
+
 // ------------------------------------------------------------------------------------
 // a1..a5: the persistent bundle-step kernel
 // ------------------------------------------------------------------------------------

@@ -714,3 +714,33 @@ def test_l2_persist_window_changes_nothing(pk):
         s.close()
     for a, b in zip(out[0], out[1]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("case", ["tiny", "cfg1", "cfg3", "n1", "n513"])
+@pytest.mark.parametrize("launch", [(2, 0, 0), (3, 0, 0), (3, 4, 0, 2), (1, 16, 3)])
+def test_single_pass_lists_match_split_build(pk, case, launch):
+    """The single-pass list build (k_prep_lists: permutation + three look-back prefix sums +
+    compactions in one launch) against the reference sequence of launches (k_perm, device-wide
+    scans, k_heavy_compact, k_full_compact; pcdn_set_debug bit 2): solves over several outer
+    iterations (fresh tile epochs, the ticket re-armed each time) are bit-identical.  Cases cover
+    heavy and full columns, n below / just above one tile, one feature, and many tiles (cfg3,
+    n = 10^6: 1954 tiles)."""
+    if case == "tiny":
+        prob = synth.tiny(777, 90, 40, density=0.3, loss=LOSS_LOGISTIC, c=4.0, dense_rows=3, full_cols=2, P=6)
+    elif case == "n1":
+        prob = synth.from_dense(np.array([[1.0], [0.5], [-2.0]], dtype=np.float32), [1, -1, 1], c=2.0, P=1)
+    elif case == "n513":
+        prob = synth.tiny(5, 64, 513, density=0.2, loss=LOSS_L2SVM, c=2.0, full_cols=3, P=37)
+    else:
+        prob = synth.config(int(case[3:]))
+    if case == "cfg3" and (launch[0] == 1 or len(launch) == 4):
+        pytest.skip("cfg3 needs the full 16-CTA cluster (resident) or the grid: covered by the other launches")
+    out = []
+    for dbg in (0, 2):
+        s = _solver(pk, prob, *launch)
+        pk.pcdn_set_debug(s.ctx, dbg)
+        r = s.solve(prob.P, seed=5, max_outer=3, trace=True)
+        out.append((s.w().cpu().numpy(), r["q_trace"], r["F_trace"], r["steps"]))
+        s.close()
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
