@@ -576,7 +576,7 @@ static void preload_kernels()
         (const void *)k_step<ClusterSync>, res_kernel(LOSS_LOGISTIC, false), res_kernel(LOSS_L2SVM, false),
         res_kernel(LOSS_SQ, false), res_kernel(LOSS_LOGISTIC, true), res_kernel(LOSS_L2SVM, true),
         res_kernel(LOSS_SQ, true), dense_kernel(LOSS_LOGISTIC), dense_kernel(LOSS_L2SVM), dense_kernel(LOSS_SQ),
-        (const void *)k_set_z, (const void *)k_obj_partial, (const void *)k_obj_final, (const void *)k_obj, (const void *)k_prep_lists, (const void *)k_validate,
+        (const void *)k_set_z, (const void *)k_obj_partial, (const void *)k_obj_final, (const void *)k_obj, (const void *)k_prep_lists, (const void *)k_solve_init, (const void *)k_validate,
         (const void *)k_validate_transpose, (const void *)k_check_finite, (const void *)k_sh_gh, (const void *)k_sh_dir,
         (const void *)k_sh_ls, (const void *)k_sh_ls_long, (const void *)k_sh_ls_final, (const void *)k_sh_commit};
     for (const void *f : fns) {
@@ -1112,8 +1112,11 @@ int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_
     const Layout &L = ctx->L;
     const int64_t launches0 = ctx->launches;
     int rc;
-    if ((rc = reset_status(ctx))) return rc;
-    CU(cudaMemsetAsync(ctx->at<int64_t>(L.counters), 0, sizeof(int64_t) * 8, ctx->stream));
+    // status / error / stop / ticket / counters and the grid barrier, in one launch
+    k_solve_init<<<1, 32, 0, ctx->stream>>>(ctx->at<int>(L.status), ctx->at<long long>(L.err_idx),
+                                            ctx->at<int64_t>(L.counters), ctx->at<unsigned long long>(L.bar));
+    ctx->launches++;
+    CU(cudaGetLastError());
     const int64_t b = (ctx->n + P - 1) / P;
     int status = PCDN_BUDGET;
     int32_t k = 0;
@@ -1138,7 +1141,7 @@ int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_
         const int buf = kk & 1, r = kk & 1;
         if (kk > 0 && overlap) CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_prep, 0));
         CU(cudaEventRecord(ctx->ev[4 + 2 * r], ctx->stream));
-        ctx->bar_clean = kk > 0;   // re-armed by the previous outer iteration's k_obj
+        ctx->bar_clean = true;   // re-armed by k_solve_init / the previous outer iteration's k_obj
         int rc2 = launch_steps(ctx, buf, ctx->n, P, b, (int64_t)kk * b, nullptr, nullptr, nullptr);
         if (rc2) return rc2;
         CU(cudaEventRecord(ctx->ev[5 + 2 * r], ctx->stream));
@@ -1191,16 +1194,13 @@ int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_
         ~SolvingScope() { c->solving = false; }
     } scope{ctx};
     ctx->solving = true;
-    int32_t last = -1;   // last outer iteration queued
     if (max_outer > 0) {
         if ((rc = prep_outer(ctx, seed, 0, 0, ctx->stream, lists))) return rc;
         if ((rc = enqueue_outer(0))) return rc;
-        last = 0;
     }
     for (k = 0; k < max_outer; k++) {
         if (k + 1 < max_outer) {
             if ((rc = enqueue_outer(k + 1))) return rc;
-            last = k + 1;
         }
         const int r = k & 1;
         CU(cudaEventSynchronize(ctx->ev[8 + r]));
@@ -1245,7 +1245,7 @@ int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_
         if ((rc = readback(ctx))) return rc;
         F = ctx->hm->F;
     } else {
-        ctx->hm[0] = ring[last & 1];   // counters after every queued launch (a stopped one adds nothing)
+        ctx->hm[0] = ring[(k - 1) & 1];   // the last outer iteration taken (a queued one after it was a no-op)
     }
     if (info) {
         float ms = 0.f;

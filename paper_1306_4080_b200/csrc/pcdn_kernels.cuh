@@ -2046,6 +2046,19 @@ __global__ void k_obj_final(const double *__restrict__ partial, double c, double
     obj_final_body(partial, c, mu, F, F_copy, eps, fstar, status, stop);
 }
 
+// The solve's starting state of the read-back block (status, err_what, stop and ticket are
+// consecutive ints; err_idx starts at the largest value for atomicMin) and the grid barrier
+__global__ void k_solve_init(int *status4, long long *err_idx, int64_t *counters, unsigned long long *bar)
+{
+    const int t = threadIdx.x;
+    if (t < 4) status4[t] = 0;
+    if (t < 8) counters[t] = 0;
+    if (t == 0) {
+        *err_idx = 0x7f7f7f7f7f7f7f7fLL;
+        *bar = 0ull;
+    }
+}
+
 // The solve's outer boundary in one launch (OBJ_NB blocks of OBJ_NB threads): the block partials,
 // then the last block to finish (ticket) sums them in the fixed order of k_obj_final, takes the
 // stop test, re-arms the step kernels' grid barrier and the ticket, and copies the read-back block
@@ -2075,6 +2088,7 @@ __global__ void __launch_bounds__(OBJ_NB) k_obj(int64_t s, int64_t n, const doub
                                                 const int8_t *__restrict__ y, const double *__restrict__ w, int loss,
                                                 double *partial, const double *__restrict__ t, ObjBoundary o)
 {
+    if (ldcg(o.stop)) return;   // queued after the outer iteration that ended the solve (grid-uniform)
     if (o.perm) perm_positions(o.seed, o.k_next, o.n, o.s, o.col_ptr, o.heavy_len, o.order, o.flag, o.fflag, o.colinfo);
     obj_block_partial(s, n, z, y, w, loss, partial, t);
     __shared__ bool last;
