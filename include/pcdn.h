@@ -245,10 +245,11 @@ int pcdn_set_resident_cap(pcdn_ctx *ctx, int cap);
  * 5 barrier + decision, 6 commit, 7 end-of-step barrier).  pcdn_set_profile(ctx, 1) zeroes the
  * counters; pcdn_phase_cycles copies the 16 counters to out (host) and the launch mode used by
  * the last step launch (1 cluster, 2 grid) to *mode (host, nullable).  Synchronizes. */
-int pcdn_set_profile(pcdn_ctx *ctx, int on);   /* on: 0 off, 1 phase counters, 2 + warp timeline */
+int pcdn_set_profile(pcdn_ctx *ctx, int on);   /* on: 0 off, 1 phase counters, 2 warp timeline */
 int pcdn_phase_cycles(pcdn_ctx *ctx, int64_t *out, int32_t *mode);
 
-/* Profiling mode 2 (pcdn_set_profile(ctx, 2)) also records, for CTA 0 of the cluster-resident
+/* Profiling mode 2 (pcdn_set_profile(ctx, 2)) records instead (the phase counters stay off, so
+ * that thread 0 of CTA 0 runs unmarked), for CTA 0 of the cluster-resident
  * step kernel, clock64() of every warp at 16 points of each of the first 16 steps of a launch.
  * out (host) gets int64[16 steps][16 warps][16 points] (0 = point not reached).  Synchronizes. */
 int pcdn_warp_timeline(pcdn_ctx *ctx, int64_t *out);

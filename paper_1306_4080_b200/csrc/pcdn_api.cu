@@ -422,7 +422,7 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
     a.counters = ctx->at<int64_t>(L.counters);
     a.info = ctx->at<double>(L.info);
     a.debug = ctx->debug;
-    a.prof = ctx->profile ? ctx->at<long long>(L.prof) : nullptr;
+    a.prof = ctx->profile == 1 ? ctx->at<long long>(L.prof) : nullptr;   // (the timeline mode runs unmarked)
     a.tl = ctx->profile == 2 ? ctx->at<long long>(L.tl) : nullptr;
     a.dbg_dx = ctx->at<double>(L.dbg_dx);
     a.dbg_mark = ctx->at<uint8_t>(L.dbg_mark);

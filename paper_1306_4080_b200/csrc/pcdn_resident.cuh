@@ -536,6 +536,35 @@ __device__ __forceinline__ void res_stage_cols(const StepArgs &a, ResFixed &fx, 
     __syncwarp();
 }
 
+// L2 prefetch of everything res_stage_cols will load for the next step [kb, ke) of this CTA (the
+// descriptors, the row / value lines and w_j of the NW x R_RP staged columns), issued by one warp
+// during the fold, where the upper warps idle when the step touches fewer samples than threads:
+// the staging after the partial-row send then hits L2 instead of HBM.
+__device__ __forceinline__ void prefetch_l2(const void *p)
+{
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+__device__ __forceinline__ void res_l2_prefetch_next(const StepArgs &a, int64_t kb, int64_t ke, int c, int G, int lane)
+{
+    const int64_t GN = (int64_t)G * NW;
+#pragma unroll
+    for (int e = 0; e < (NW * R_RP + 31) / 32; e++) {
+        const int idx = lane + 32 * e, w = idx % NW, m = idx / NW;
+        const int64_t kk = kb + (int64_t)c * NW + w + (int64_t)m * GN;
+        if (m < R_RP && kk < ke) {
+            const int4 ci = __ldg(&a.colinfo[kk]);
+            if (ci.y > 0 && ci.y <= a.heavy_len) {
+                const int64_t p0 = colinfo_p0(ci), p1 = p0 + ci.y - 1;
+                prefetch_l2(&a.row_idx[p0]);
+                prefetch_l2(&a.row_idx[p1]);
+                prefetch_l2(&a.val[p0]);
+                prefetch_l2(&a.val[p1]);
+                prefetch_l2(&a.w[ci.x]);
+            }
+        }
+    }
+}
+
 // The owner state of the next step's first staged column, gathered while the current step's
 // decision is taken (valid from the M2 arrival of window 0 to the next step's M0: no owner writes
 // its samples in between)
@@ -690,6 +719,7 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
     acc[LY::NTOUCH] = (double)ntouch;
     pr.mark(fx, 3);
     if (ws.win == 0) RTL(R, 8);
+    if (ws.win == 0 && kn0 < kn1 && warp == NW - 1) res_l2_prefetch_next(a, kn0, kn1, R.c, R.G, lane);
     constexpr int SPL = 32 / W;
     {
         const double tot = xreduce<W>(acc, lane);

@@ -28,9 +28,11 @@ for _ in range(2):
 s.reset()
 torch.cuda.synchronize()
 from torch.profiler import profile, ProfilerActivity  # noqa: E402
-with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-    r = s.solve(prob.P, seed=prob.seed, max_outer=args.outer, eps=0.0)
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    pk.pcdn_reset(s.ctx)   # as bench.py's timed solve: from w = 0
+    st_, inf_ = pk.pcdn_solve(s.ctx, prob.P, 0.0, prob.seed, args.outer)
     torch.cuda.synchronize()
+r = inf_.as_dict()
 ev = []
 for e in prof.events():
     if e.device_type == torch.autograd.DeviceType.CUDA or "cuda" in str(e.device_type).lower():

@@ -38,10 +38,11 @@ nxt = []
 for st in range(2, 15):
     nxt.append(tl[st + 1, :, 0][tl[st + 1, :, 0] > 0].min() - tl[st, :, 0][tl[st, :, 0] > 0].min())
 print(f"cfg{args.config} P={P}: step period {np.mean(nxt):.0f} cycles ({np.mean(nxt) / 1965:.2f} us at 1965 MHz)")
-print(f"{'point':22s} {'min':>8s} {'median':>8s} {'max':>8s}   (cycles since step start, mean over steps)")
+print(f"{'point':22s} {'min':>8s} {'median':>8s} {'max':>8s} {'warp0':>8s} {'warp15':>8s}   (cycles since step start, mean over steps)")
 for p, name in enumerate(PTS):
     v = rel[:, :, p]
-    print(f"{name:22s} {np.nanmean(np.nanmin(v, 1)):8.0f} {np.nanmean(np.nanmedian(v, 1)):8.0f} {np.nanmean(np.nanmax(v, 1)):8.0f}")
+    print(f"{name:22s} {np.nanmean(np.nanmin(v, 1)):8.0f} {np.nanmean(np.nanmedian(v, 1)):8.0f} {np.nanmean(np.nanmax(v, 1)):8.0f}"
+          f" {np.nanmean(v[:, 0]):8.0f} {np.nanmean(v[:, -1]):8.0f}")
 d78 = np.nanmedian(rel[:, :, 8] - rel[:, :, 7], 0)
 d01 = np.nanmedian(rel[:, :, 1] - rel[:, :, 0], 0)
 print("per-warp median cycles, fold+LS pass (7->8):", " ".join(f"{v:.0f}" for v in d78))
