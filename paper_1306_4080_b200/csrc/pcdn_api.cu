@@ -81,14 +81,14 @@ Layout make_layout(int64_t s, int64_t n, int64_t nnz)
     L.rec = take(sizeof(Rec) * nnz);
     for (int b = 0; b < 2; b++) {
         Lists &S = L.ls[b];
-        S.order = take(sizeof(int32_t) * n);
+        S.order = take(sizeof(int32_t) * n * (b == 0 ? 2 : 1));   // set 0: two partitions (dense solve)
         S.hdesc = take(sizeof(int4) * n);
         S.flag = take(sizeof(int32_t) * n);
         S.fflag = take(sizeof(int32_t) * n);
         S.fpos = take(sizeof(int64_t) * (n + 1));
         S.flist = take(sizeof(int32_t) * n);
         S.tiles3 = take(sizeof(int64_t) * ntile);
-        S.colinfo = take(sizeof(int4) * n);
+        S.colinfo = take(sizeof(int4) * n * (b == 0 ? 2 : 1));
         S.hpos = take(sizeof(int64_t) * (n + 1));
         S.hlist = take(sizeof(int32_t) * n);
         S.hlen = take(sizeof(int64_t) * n);
@@ -183,6 +183,10 @@ struct pcdn_ctx {
     bool bar_clean = false;     // the grid barrier was re-armed on the device (k_obj): no memset
     unsigned prep_epoch = 0;    // k_prep_lists launches (tile-state epoch)
     bool split_prep = false;    // test knob: build the lists with k_perm + scans + compactions
+    bool dense_per_outer = false;   // test knob: the dense solve as one launch per outer iteration
+    int dense_outers = 0;       // > 0: the dense launch runs up to this many outer iterations
+    uint64_t cur_seed = 0;
+    double cur_eps = 0.0;
     int32_t *q_trace = nullptr;
     double *F_trace = nullptr;
     int64_t trace_cap = 0;
@@ -447,6 +451,15 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
     a.ovf_cnt = ctx->at<int>(L.ovf_cnt);
     a.part_gh = ctx->at<double>(L.part_gh);
     a.dense_tcap = ctx->dense_tcap;
+    a.n_outer = ctx->dense_outers;
+    a.outer0 = 0;
+    a.seed = ctx->cur_seed;
+    a.eps_stop = ctx->cur_eps;
+    a.fstar = ctx->fstar;
+    a.objp = ctx->at<double>(L.objp);
+    a.pflag = ctx->at<int32_t>(L.ls[1].flag);
+    a.pfflag = ctx->at<int32_t>(L.ls[1].fflag);
+    a.outers_done = ctx->at<int64_t>(L.counters) + 5;
     if (!ctx->bar_clean) CU(cudaMemsetAsync(a.bar, 0, sizeof(unsigned long long), ctx->stream));
     ctx->bar_clean = false;
     // cluster mode for steps small enough that 16 SMs keep up (hardware barrier, ~0.2 us);
@@ -885,6 +898,7 @@ int pcdn_set_debug(pcdn_ctx *ctx, int on)
     if (!ctx) return PCDN_ERR_INVALID;
     ctx->debug = (on & 1) ? 1 : 0;
     ctx->split_prep = (on & 2) != 0;
+    ctx->dense_per_outer = (on & 4) != 0;
     return PCDN_OK;
 }
 
@@ -1194,11 +1208,42 @@ int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_
         ~SolvingScope() { c->solving = false; }
     } scope{ctx};
     ctx->solving = true;
-    if (max_outer > 0) {
+    // the dense kernel runs the whole solve in one launch: its outer boundaries (a6: F from
+    // scratch, the Eq.14 test, the next partition) happen inside it, with no host round trip
+    const bool fused = smode == 4 && !ctx->dense_per_outer && max_outer > 0;
+    if (fused) {
+        struct DenseScope {
+            pcdn_ctx *c;
+            ~DenseScope() { c->dense_outers = 0; }
+        } dscope{ctx};
+        if ((rc = prep_outer(ctx, seed, 0, 0, ctx->stream, false))) return rc;
+        ctx->dense_outers = max_outer;
+        ctx->cur_seed = seed;
+        ctx->cur_eps = eps > 0 ? eps : 0.0;
+        ctx->bar_clean = true;   // k_solve_init
+        CU(cudaEventRecord(ctx->ev[4], ctx->stream));
+        if ((rc = launch_steps(ctx, 0, ctx->n, P, b, 0, nullptr, nullptr, nullptr))) return rc;
+        CU(cudaEventRecord(ctx->ev[5], ctx->stream));
+        if ((rc = readback(ctx))) return rc;
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, ctx->ev[4], ctx->ev[5]));
+        t_step_ms = ms;
+        F = ctx->hm->F;
+        k = (int32_t)ctx->hm->counters[5];
+        if (ctx->hm->status == 3 || !std::isfinite(F)) {
+            status = PCDN_ERR_NUMERIC;
+            set_err(ctx, PCDN_ERR_NUMERIC, "non-finite objective in outer iteration %d", k - 1);
+        } else if (ctx->hm->status) {
+            status = PCDN_ERR_CUDA;
+            set_err(ctx, PCDN_ERR_CUDA, "internal consistency check failed (%d)", ctx->hm->status);
+        } else if (eps > 0 && (F - ctx->fstar) / ctx->fstar <= eps) {
+            status = PCDN_OK;
+        }
+    } else if (max_outer > 0) {
         if ((rc = prep_outer(ctx, seed, 0, 0, ctx->stream, lists))) return rc;
         if ((rc = enqueue_outer(0))) return rc;
     }
-    for (k = 0; k < max_outer; k++) {
+    for (k = fused ? k : 0; !fused && k < max_outer; k++) {
         if (k + 1 < max_outer) {
             if ((rc = enqueue_outer(k + 1))) return rc;
         }
@@ -1244,7 +1289,7 @@ int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_
     if (max_outer == 0) {
         if ((rc = readback(ctx))) return rc;
         F = ctx->hm->F;
-    } else {
+    } else if (!fused) {
         ctx->hm[0] = ring[(k - 1) & 1];   // the last outer iteration taken (a queued one after it was a no-op)
     }
     if (info) {

@@ -25,6 +25,9 @@
 //   the committed z and the G phase is redone (one extra barrier): the arithmetic of every accepted
 //   step is exactly that of the sequential algorithm.
 // Every sample is touched when some d_j != 0 (reading Z8): T = all rows.
+// With a.n_outer > 1 the launch runs the whole solve: at each outer boundary every CTA recomputes F
+// from (z, w) with k_obj's arithmetic, takes the Eq.14 stop test, and the grid writes the next
+// partition (so order / colinfo are read through L2, never the non-coherent path).
 #pragma once
 #include "pcdn_kernels.cuh"
 #include "pcdn_resident.cuh"   // mbarrier primitives
@@ -78,7 +81,7 @@ __device__ __forceinline__ void dense_prefetch(const StepArgs &a, float *tile, u
         for (int pos = tid; pos < Pt; pos += NT) {
             if (pos < pa || pos >= pb) continue;
             // the first descriptor of each thread was loaded early (p0_first): no dependent load here
-            const int64_t cp = (pos == tid ? p0_first : colinfo_p0(__ldg(&a.colinfo[k0 + pos]))) + r0;
+            const int64_t cp = (pos == tid ? p0_first : colinfo_p0(__ldcg(&a.colinfo[k0 + pos]))) + r0;
             bulk_g2s(tile + (int64_t)pos * Rs, a.val + cp, (uint32_t)R * 4u, mbar);
         }
     }
@@ -106,7 +109,7 @@ __device__ __forceinline__ void dense_gphase(const StepArgs &a, const float *til
                 }
             }
         } else {
-            const float *xp = a.val + colinfo_p0(__ldg(&a.colinfo[k0 + pos])) + r0;
+            const float *xp = a.val + colinfo_p0(__ldcg(&a.colinfo[k0 + pos])) + r0;
             const int head = min(R, (int)((4 - (((uintptr_t)xp >> 2) & 3)) & 3));
             int r = 0;
             for (; r < head; r++) {
@@ -177,7 +180,7 @@ __device__ __forceinline__ void dense_ls_partial(const StepArgs &a, DenseFixed &
             dl = sm.odl[m];
         } else {   // beyond the staged slots: from HBM
             const int pos = c + G * m;
-            wj = ldcg(&a.w[__ldg(&a.order[k0 + pos])]);
+            wj = ldcg(&a.w[__ldcg(&a.order[k0 + pos])]);
             d = ldcg(&a.dk[pos]);
             dl = ldcg(&a.deltak[pos]);
         }
@@ -243,6 +246,55 @@ __device__ __forceinline__ void dense_decide(const StepArgs &a, DenseFixed &sm, 
     __syncthreads();
 }
 
+// The outer boundary of a whole-solve launch (a6): F from scratch over (z, w) -- k_obj's blocks and
+// tree, bit for bit -- the Eq.14 stop test, and the next outer iteration's partition into the other
+// half of order / colinfo.
+template <int LOSS>
+__device__ __forceinline__ bool dense_boundary(const StepArgs &a, DenseFixed &sm, GridSync &sy, int64_t r0, int R, int G,
+                                               int c, int tid, int oi)
+{
+    for (int r = tid; r < R; r += NT) a.z[r0 + r] = sm.z[r];
+    sy.sync();   // z of every row and the w commits of the last step
+    const bool more = oi + 1 < a.n_outer;
+    if (more) {
+        const int64_t kn = (int64_t)((oi + 1) & 1) * a.n;
+        perm_positions(a.seed, a.outer0 + oi + 1, a.n, a.s, a.col_ptr, a.heavy_len,
+                       const_cast<int32_t *>(a.order) + kn, a.pflag, a.pfflag, const_cast<int4 *>(a.colinfo) + kn);
+    }
+    const int h = tid / OBJ_NB, gt = tid % OBJ_NB;
+    double(*wsum)[3] = reinterpret_cast<double(*)[3]>(&sm.red[0][0] + h * 3 * (OBJ_NB / 32));
+    for (int rb = 0; rb < OBJ_NB; rb += 2 * G) {
+        const int b = rb + 2 * c + h;
+        obj_group_partial(b, gt, gt >> 5, a.s, a.n, a.z, a.y, a.w, LOSS, a.t, wsum, a.objp, b < OBJ_NB);
+    }
+    sy.sync();   // the partials (and the next partition)
+    double *sh = sm.dcol;   // [3][OBJ_NB]: k_obj_final's tree, in every CTA
+    if (tid < OBJ_NB) {
+        sh[tid] = __ldcg(&a.objp[3 * tid]);
+        sh[OBJ_NB + tid] = __ldcg(&a.objp[3 * tid + 1]);
+        sh[2 * OBJ_NB + tid] = __ldcg(&a.objp[3 * tid + 2]);
+    }
+    __syncthreads();
+    for (int o = OBJ_NB / 2; o > 0; o >>= 1) {
+        if (tid < o) {
+            sh[tid] += sh[tid + o];
+            sh[OBJ_NB + tid] += sh[OBJ_NB + tid + o];
+            sh[2 * OBJ_NB + tid] += sh[2 * OBJ_NB + tid + o];
+        }
+        __syncthreads();
+    }
+    const double Fv = a.c * sh[0] + sh[OBJ_NB] + 0.5 * a.mu * sh[2 * OBJ_NB];
+    const bool stop = !more || !isfinite(Fv) || (a.eps_stop > 0 && (Fv - a.fstar) / a.fstar <= a.eps_stop);
+    if (tid == 0) sm.F = Fv;
+    if (c == 0 && tid == 0) {
+        *a.F = Fv;
+        *a.outers_done = oi + 1;
+        if (!isfinite(Fv)) atomicMax(a.status, 3);
+    }
+    __syncthreads();   // sh (dcol) is reused by the next step
+    return stop;
+}
+
 template <int LOSS>
 __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
 {
@@ -288,13 +340,6 @@ __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
     __syncthreads();
     bool inflight = false;   // a tile copy was issued and not yet waited for (for step inflight_t)
     int64_t inflight_t = 0;
-    if (use_tile && a.nsteps > 0) {
-        const int P0 = (int)min(a.P, a.ntot);
-        dense_prefetch(a, tiles, s_addr(&tmb[0]), 0, P0, r0, R, Rs, tid, tid < P0 ? colinfo_p0(__ldg(&a.colinfo[tid])) : 0,
-                       0, P0);
-        inflight = true;
-        inflight_t = 0;
-    }
     long long tprev = 0;
     const bool prof = a.prof != nullptr && c == 0 && tid == 0;
 #define DPROF(i)                                 \
@@ -309,7 +354,8 @@ __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
     // the step waiting for its decision (published by the next barrier)
     bool pend = false, pend_any = false, bad = false;
     int pend_q0 = 0, pend_nq = 0, pend_nown = 0;
-    int64_t pend_k0 = 0, pend_t = 0;
+    int64_t pend_k0 = 0, pend_t = 0;   // pend_t: step index within the launch
+    bool pend_last = false;            // the pending step is its outer iteration's last
     int pend_Pt = 0;
     double alpha_s = 1.0;
 
@@ -363,7 +409,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
                     a.w[sm.oj[m]] = sm.ow[m] + alpha_acc * sm.od[m];
                 } else {
                     const int pos = c + G * m;
-                    const int32_t j = __ldg(&a.order[pend_k0 + pos]);
+                    const int32_t j = __ldcg(&a.order[pend_k0 + pos]);
                     a.w[j] = ldcg(&a.w[j]) + alpha_acc * ldcg(&a.dk[pos]);
                 }
             }
@@ -372,7 +418,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
             double F = sm.F;
             if (qacc >= 0) F = F + lhs_acc;
             sm.F = F;
-            if (bad || pend_t == a.nsteps - 1) {
+            if (bad || pend_last) {
                 *a.F = F;
                 if (bad) atomicMax(a.status, 3);
                 a.info[0] = (double)qacc;
@@ -398,18 +444,32 @@ __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
         return !hit;
     };
 
+    // outer iterations of this launch (one unless a.n_outer > 1: then positions of outer oi sit at
+    // [kb, kb + ntot) of order / colinfo, and steps are numbered T = T0 + t across the launch for
+    // the tile buffers' mbarrier phases and the traces)
+    for (int oi = 0;; oi++) {
+    const int64_t kb = (int64_t)(oi & 1) * a.n;
+    const int64_t T0 = (int64_t)oi * a.nsteps;
+    if (use_tile && a.nsteps > 0) {
+        const int P0 = (int)min(a.P, a.ntot);
+        dense_prefetch(a, tiles + (size_t)(T0 & 1) * (size_t)a.dense_tcap, s_addr(&tmb[T0 & 1]), kb, P0, r0, R, Rs, tid,
+                       tid < P0 ? colinfo_p0(__ldcg(&a.colinfo[kb + tid])) : 0, 0, P0);
+        inflight = true;
+        inflight_t = T0;
+    }
     for (int64_t t = 0; t < a.nsteps; t++) {
         if (prof) tprev = clock64();
-        const int64_t k0 = t * a.P;
-        const int64_t k1 = min(k0 + a.P, a.ntot);
+        const int64_t T = T0 + t;
+        const int64_t k0 = kb + t * a.P;
+        const int64_t k1 = min(k0 + a.P, kb + a.ntot);
         const int Pt = (int)(k1 - k0);
         float *tile = nullptr;
         // the next step's first tile descriptor of this thread, loaded now (used after the G phase)
-        const int64_t kn1 = min(k1 + a.P, a.ntot);
-        const int64_t p0n = (use_tile && k1 + tid < kn1) ? colinfo_p0(__ldg(&a.colinfo[k1 + tid])) : 0;
+        const int64_t kn1 = min(k1 + a.P, kb + a.ntot);
+        const int64_t p0n = (use_tile && k1 + tid < kn1) ? colinfo_p0(__ldcg(&a.colinfo[k1 + tid])) : 0;
         if (use_tile) {
-            tile = tiles + (size_t)(t & 1) * (size_t)a.dense_tcap;
-            mbar_wait(s_addr(&tmb[t & 1]), (uint32_t)((t >> 1) & 1));   // this step's tile (issued a step ahead)
+            tile = tiles + (size_t)(T & 1) * (size_t)a.dense_tcap;
+            mbar_wait(s_addr(&tmb[T & 1]), (uint32_t)((T >> 1) & 1));   // this step's tile (issued a step ahead)
             inflight = false;
         }
         DPROF(8);
@@ -421,10 +481,10 @@ __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
         // the next step's tile, issued while the barrier completes (in the background of this
         // step's remaining phases)
         if (use_tile && t + 1 < a.nsteps) {
-            dense_prefetch(a, tiles + (size_t)((t + 1) & 1) * (size_t)a.dense_tcap, s_addr(&tmb[(t + 1) & 1]), k1,
+            dense_prefetch(a, tiles + (size_t)((T + 1) & 1) * (size_t)a.dense_tcap, s_addr(&tmb[(T + 1) & 1]), k1,
                            (int)(kn1 - k1), r0, R, Rs, tid, p0n, 0, (int)(kn1 - k1));
             inflight = true;
-            inflight_t = t + 1;
+            inflight_t = T + 1;
         }
         DPROF(0);
         sy.wait();
@@ -471,7 +531,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
             g = warp_sum(g);
             h = warp_sum(h);
             if (lane == 0) {
-                const int32_t j = __ldg(&a.order[k0 + pos]);
+                const int32_t j = __ldcg(&a.order[k0 + pos]);
                 const double wj = ldcg(&a.w[j]);
                 const Dir r = finish_feature(a, g, h, wj);
                 a.dk[pos] = r.d;
@@ -513,7 +573,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
                         for (int pos = 0; pos < Pt; pos++) {
                             const double d = pos < D_PMAX ? sm.dcol[pos] : ldcg(&a.dk[pos]);
                             const double xv = tile ? (double)tile[(int64_t)pos * Rs + r]
-                                                   : (double)__ldg(&a.val[colinfo_p0(__ldg(&a.colinfo[k0 + pos])) + r0 + r]);
+                                                   : (double)__ldg(&a.val[colinfo_p0(__ldcg(&a.colinfo[k0 + pos])) + r0 + r]);
                             if (d != 0.0) x += d * xv;
                         }
                         sm.dx[r] = x;
@@ -531,7 +591,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
                         for (int pos = e0; pos < e1; pos++) {
                             const double d = pos < D_PMAX ? sm.dcol[pos] : ldcg(&a.dk[pos]);
                             const double xv = tile ? (double)tile[(int64_t)pos * Rs + r]
-                                                   : (double)__ldg(&a.val[colinfo_p0(__ldg(&a.colinfo[k0 + pos])) + r0 + r]);
+                                                   : (double)__ldg(&a.val[colinfo_p0(__ldcg(&a.colinfo[k0 + pos])) + r0 + r]);
                             x += d * xv;
                         }
                     }
@@ -566,15 +626,21 @@ __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
         pend_nq = nq;
         pend_nown = nown;
         pend_k0 = k0;
-        pend_t = t;
+        pend_t = T;
+        pend_last = t == a.nsteps - 1;
         pend_Pt = Pt;
         __syncthreads();   // speculative coef complete before the next G phase reads it
         DPROF(5);
     }
-    if (pend && !bad) {   // the last step of the launch: publish and decide it
+    if (pend && !bad) {   // the last step of the outer iteration: publish and decide it
         sy.sync();
         resolve();
     }
+    if (a.n_outer <= 0 || bad) break;   // one outer iteration per launch (the host takes a6)
+    // ---------------- outer boundary (a6) inside the launch ------------------------------------
+    if (dense_boundary<LOSS>(a, sm, sy, r0, R, G, c, tid, oi)) break;
+    prev_q = 0;   // as a fresh launch
+    }   // outer iterations
     if (inflight)   // nothing may still be landing in shared memory at exit (an early break)
         mbar_wait(s_addr(&tmb[inflight_t & 1]), (uint32_t)((inflight_t >> 1) & 1));
     // ---------------- epilogue: own rows back to HBM ----------------------------------------

@@ -120,6 +120,16 @@ struct StepArgs {
     int *ovf_cnt;   // [16] overflow records received per CTA in the current step
     double *part_gh;  // dense kernel: per-CTA partial (g, h) of every bundle column [G][P][2]
     int dense_tcap;   // dense kernel: floats per shared-memory tile buffer (two buffers)
+    // dense kernel, whole solve in one launch (n_outer > 1): outer iteration oi uses positions
+    // [oi&1]*n of order/colinfo (2n each); at every outer boundary the kernel recomputes F from
+    // (z, w) exactly as k_obj, takes the Eq.14 stop test and builds the next partition itself
+    int n_outer;
+    int64_t outer0;   // outer iteration index of the launch's first (the partition stream's k)
+    uint64_t seed;
+    double eps_stop, fstar;
+    double *objp;                 // [3 * OBJ_NB] objective partials
+    int32_t *pflag, *pfflag;      // scratch for perm_positions
+    int64_t *outers_done;
     // sync
     unsigned long long *bar;
     int *status;
@@ -2003,6 +2013,54 @@ __device__ __forceinline__ void obj_block_partial(int64_t s, int64_t n, const do
         partial[3 * b + 1] = a1;
         partial[3 * b + 2] = a2;
     }
+}
+
+// obj_block_partial's arithmetic for block b by a group of OBJ_NB consecutive threads (gt = thread
+// in the group, gw = warp in the group, wsum = the group's OBJ_NB/32 x 3 scratch): the same per-thread
+// strides, warp sums and warp order, so the partials equal k_obj's bit for bit
+__device__ __forceinline__ void obj_group_partial(int b, int gt, int gw, int64_t s, int64_t n,
+                                                  const double *__restrict__ z, const int8_t *__restrict__ y,
+                                                  const double *__restrict__ w, int loss, const double *__restrict__ t,
+                                                  double (*wsum)[3], double *partial, bool write)
+{
+    // (write == false: a group without a block this round; it only joins the barriers)
+    const int64_t zs0 = write ? (int64_t)b * s / OBJ_NB : 0, zs1 = write ? (int64_t)(b + 1) * s / OBJ_NB : 0;
+    const int64_t ws0 = write ? (int64_t)b * n / OBJ_NB : 0, ws1 = write ? (int64_t)(b + 1) * n / OBJ_NB : 0;
+    double ls = 0.0, l1 = 0.0, l2 = 0.0;
+    for (int64_t i = zs0 + gt; i < zs1; i += OBJ_NB) {
+        if (loss == LOSS_SQ) {
+            const double r = t[i] - __ldcg(&z[i]);
+            ls += r * r;
+        } else {
+            ls += phi_of(loss, (double)y[i] * __ldcg(&z[i]));
+        }
+    }
+    for (int64_t j = ws0 + gt; j < ws1; j += OBJ_NB) {
+        const double wj = __ldcg(&w[j]);
+        l1 += fabs(wj);
+        l2 += wj * wj;
+    }
+    ls = warp_sum(ls);
+    l1 = warp_sum(l1);
+    l2 = warp_sum(l2);
+    if ((gt & 31) == 0) {
+        wsum[gw][0] = ls;
+        wsum[gw][1] = l1;
+        wsum[gw][2] = l2;
+    }
+    __syncthreads();
+    if (gt == 0 && write) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        for (int w2 = 0; w2 < OBJ_NB / 32; w2++) {
+            a0 += wsum[w2][0];
+            a1 += wsum[w2][1];
+            a2 += wsum[w2][2];
+        }
+        partial[3 * b] = a0;
+        partial[3 * b + 1] = a1;
+        partial[3 * b + 2] = a2;
+    }
+    __syncthreads();
 }
 
 __global__ void k_obj_partial(int64_t s, int64_t n, const double *__restrict__ z, const int8_t *__restrict__ y,

@@ -744,3 +744,29 @@ def test_single_pass_lists_match_split_build(pk, case, launch):
         s.close()
     for a, b in zip(out[0], out[1]):
         assert np.array_equal(np.asarray(a), np.asarray(b))
+
+
+@pytest.mark.parametrize("loss", [LOSS_LOGISTIC, LOSS_L2SVM])
+@pytest.mark.parametrize("to_gap", [False, True])
+def test_dense_whole_solve_launch_matches_per_outer(pk, loss, to_gap):
+    """The dense kernel runs a whole solve in one launch (outer boundaries, F from scratch, the
+    Eq.14 test and the next partition inside it).  Against one launch per outer iteration
+    (pcdn_set_debug bit 4, the boundary in k_obj): w, the q and F traces, the outer count and F
+    are bit-identical; to a gap the stop lands on the same outer iteration."""
+    prob = synth.tiny(31, 150, 30, density=1.0, loss=loss, c=2.0, P=5)
+    fstar = None
+    if to_gap:
+        fstar = oracle.Oracle(prob).solve(prob.P, seed=3, max_outer=200)["F"]
+    out = []
+    for dbg in (0, 4):
+        s = _solver(pk, prob)
+        pk.pcdn_set_debug(s.ctx, dbg)
+        if to_gap:
+            r = s.solve(prob.P, eps=1e-4, seed=3, max_outer=60, fstar=fstar, trace=True)
+        else:
+            r = s.solve(prob.P, seed=3, max_outer=7, trace=True)
+        out.append((s.w().cpu().numpy(), r["q_trace"], r["F_trace"], r["outer_iters"], r["F"], r["steps"], r["rc"]))
+        s.close()
+    assert out[0][3] == out[1][3] and (to_gap or out[0][3] == 7)
+    for a, b in zip(out[0], out[1]):
+        assert np.array_equal(np.asarray(a), np.asarray(b))
