@@ -325,7 +325,9 @@ def main():
     achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
     kname = {1: "k_step<ClusterSync>", 2: "k_step<GridSync>", 3: "k_step_res", 4: "k_step_dense"}.get(
         pk.pcdn_phase_cycles(solver.ctx)[1], "k_step")
-    roof = {"bound": "hbm", "kernel": f"pcdn::{kname} (persistent, one launch per outer iteration)",
+    launch_desc = ("persistent, one launch per solve: figures per outer iteration" if kname == "k_step_dense"
+                   else "persistent, one launch per outer iteration")
+    roof = {"bound": "hbm", "kernel": f"pcdn::{kname} ({launch_desc})",
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "alg_bytes_per_launch": per_launch_bytes,
             "launch_ms": per_launch_ms, "peak_source": peak_src,

@@ -21,5 +21,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --config 4 $ARGS > $OUT/ncu_launch4.log 2>&1; echo "ncu launches cfg4 rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step_res -s 20 -c 1 \
     -o $OUT/prof_kstep python bench.py $ARGS > $OUT/ncu_full.log 2>&1; echo "ncu full rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step_dense -s 5 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step_dense -s 2 -c 1 \
     -o $OUT/prof_dense python bench.py --config 4 $ARGS > $OUT/ncu_dense.log 2>&1; echo "ncu dense rc=$?"
