@@ -770,3 +770,28 @@ def test_dense_whole_solve_launch_matches_per_outer(pk, loss, to_gap):
     assert out[0][3] == out[1][3] and (to_gap or out[0][3] == 7)
     for a, b in zip(out[0], out[1]):
         assert np.array_equal(np.asarray(a), np.asarray(b))
+
+
+@pytest.mark.parametrize("cfg_mode", [(1, 3), (1, 2), (None, 4)])
+def test_stop_flag_state_between_calls(pk, cfg_mode):
+    """A solve that stops at the Eq.14 gap leaves the device stop flag raised (the outer iteration
+    queued after it exited at once); the calls after it must not see it: a bundle step still
+    moves the state exactly as the oracle's, and the next solve runs all its outer iterations."""
+    cfg, mode = cfg_mode
+    prob = synth.config(cfg) if cfg else synth.tiny(31, 150, 30, density=1.0, c=2.0, P=5)
+    o = oracle.Oracle(prob)
+    fstar = o.solve(prob.P, seed=4, max_outer=300)["F"]
+    s = _solver(pk, prob, mode)
+    r = s.solve(prob.P, eps=1e-2, seed=4, max_outer=100, fstar=fstar)
+    ro = o.solve(prob.P, eps=1e-2, fstar=fstar, seed=4, max_outer=100)
+    assert r["rc"] == ro["rc"] == 0 and r["outer_iters"] == ro["outer"] < 100
+    assert r["steps"] == ro["steps"]
+    w = s.w().cpu().numpy()
+    B = np.arange(min(prob.n, prob.P), dtype=np.int32)
+    ties = []
+    _compare_step(s.step(B), o.step(w, B), ties)
+    assert len(ties) <= 2, ties
+    s.reset()
+    r2 = s.solve(prob.P, seed=4, max_outer=3)
+    assert r2["outer_iters"] == 3 and r2["rc"] == pk.PCDN_BUDGET
+    s.close()
