@@ -258,8 +258,10 @@ __device__ __forceinline__ bool dense_boundary(const StepArgs &a, DenseFixed &sm
     const bool more = oi + 1 < a.n_outer;
     if (more) {
         const int64_t kn = (int64_t)((oi + 1) & 1) * a.n;
+        // from the last CTA down: the objective blocks below start at CTA 0, so the two run side by side
         perm_positions(a.seed, a.outer0 + oi + 1, a.n, a.s, a.col_ptr, a.heavy_len,
-                       const_cast<int32_t *>(a.order) + kn, a.pflag, a.pfflag, const_cast<int4 *>(a.colinfo) + kn);
+                       const_cast<int32_t *>(a.order) + kn, a.pflag, a.pfflag, const_cast<int4 *>(a.colinfo) + kn,
+                       (int64_t)(G - 1 - c) * NT + tid, (int64_t)G * NT);
     }
     const int h = tid / OBJ_NB, gt = tid % OBJ_NB;
     double(*wsum)[3] = reinterpret_cast<double(*)[3]>(&sm.red[0][0] + h * 3 * (OBJ_NB / 32));

@@ -401,12 +401,18 @@ __device__ __forceinline__ int64_t colinfo_p0(const int4 &ci)
 
 // order[t] = pi_k(t); flag[t] = column length > heavy_len; fflag[t] = column is full (holds a
 // nonzero in every row: its entry for row i sits at col_ptr[j] + i); colinfo[t] (nullable)
+// (t0, stride: this thread's first position and the stride; by default the grid-stride order)
 __device__ __forceinline__ void perm_positions(uint64_t seed, int64_t k, int64_t n, int64_t s,
                                                const int64_t *__restrict__ col_ptr, int heavy_len, int32_t *order,
-                                               int32_t *flag, int32_t *fflag, int4 *colinfo)
+                                               int32_t *flag, int32_t *fflag, int4 *colinfo, int64_t t0 = -1,
+                                               int64_t stride = 0)
 {
     const FeistelKeys f = feistel_keys(seed, k, n);
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    if (t0 < 0) {
+        t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+        stride = (int64_t)gridDim.x * blockDim.x;
+    }
+    for (int64_t t = t0; t < n; t += stride) {
         const int64_t j = feistel_perm(f, n, t);
         order[t] = (int32_t)j;
         if (flag) {
