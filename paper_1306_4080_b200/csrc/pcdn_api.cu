@@ -310,18 +310,22 @@ int prep_outer(pcdn_ctx *ctx, uint64_t seed, int64_t k, int buf, cudaStream_t st
             return set_err((ctx), PCDN_ERR_INVALID, "squared loss: call pcdn_set_targets first");        \
     } while (0)
 
-// (stop_eps >= 0: also the solve's device-side stop test -- Eq.14 gap <= stop_eps when
-// stop_eps > 0, a non-finite F, or a raised status -- into the stop flag)
-int objective_kernels(pcdn_ctx *ctx, double stop_eps = -1.0)
+// F from scratch into F and Fcopy (one k_obj launch; no stop test, no read-back copy)
+int objective_kernels(pcdn_ctx *ctx)
 {
     PCDN_NEED_TARGETS(ctx);
     const Layout &L = ctx->L;
-    k_obj_partial<<<OBJ_NB, 256, 0, ctx->stream>>>(ctx->s, ctx->n, ctx->at<double>(L.z), ctx->y, ctx->at<double>(L.w),
-                                                   ctx->loss, ctx->at<double>(L.objp), ctx->t);
-    k_obj_final<<<1, OBJ_NB, 0, ctx->stream>>>(ctx->at<double>(L.objp), ctx->c, ctx->mu, ctx->at<double>(L.F),
-                                               ctx->at<double>(L.Fcopy), stop_eps, ctx->fstar,
-                                               ctx->at<int>(L.status), stop_eps >= 0 ? ctx->at<int>(L.stop) : nullptr);
-    ctx->launches += 2;
+    ObjBoundary o{};
+    o.c = ctx->c;
+    o.mu = ctx->mu;
+    o.F = ctx->at<double>(L.F);
+    o.F_copy = ctx->at<double>(L.Fcopy);
+    o.status = ctx->at<int>(L.status);
+    o.ticket = ctx->at<unsigned>(L.ticket);
+    o.bar = ctx->at<unsigned long long>(L.bar);
+    k_obj<<<OBJ_NB, OBJ_NB, 0, ctx->stream>>>(ctx->s, ctx->n, ctx->at<double>(L.z), ctx->y, ctx->at<double>(L.w),
+                                              ctx->loss, ctx->at<double>(L.objp), ctx->t, o);
+    ctx->launches++;
     CU(cudaGetLastError());
     return PCDN_OK;
 }
@@ -963,7 +967,7 @@ const char *pcdn_last_error(const pcdn_ctx *ctx) { return ctx ? ctx->err : "null
 void pcdn_destroy(pcdn_ctx *ctx)
 {
     if (!ctx) return;
-    if (ctx->stream || true) cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
     if (ctx->side) {

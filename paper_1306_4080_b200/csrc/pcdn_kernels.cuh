@@ -2131,12 +2131,13 @@ __global__ void k_solve_init(int *status4, long long *err_idx, int64_t *counters
 struct ObjBoundary {
     double c, mu, eps, fstar;
     double *F;
+    double *F_copy;                     // nullable
     const int *status;
     int *stop;
     unsigned *ticket;
     unsigned long long *bar;
     const unsigned long long *mirror;   // device block (8-byte words)
-    unsigned long long *mirror_host;    // mapped pinned host block
+    unsigned long long *mirror_host;    // mapped pinned host block (nullable: no copy)
     int mirror_words;
     // optional: the next outer iteration's partition (k_perm's output) when nothing else of the
     // list build is needed (the dense kernel)
@@ -2152,7 +2153,7 @@ __global__ void __launch_bounds__(OBJ_NB) k_obj(int64_t s, int64_t n, const doub
                                                 const int8_t *__restrict__ y, const double *__restrict__ w, int loss,
                                                 double *partial, const double *__restrict__ t, ObjBoundary o)
 {
-    if (ldcg(o.stop)) return;   // queued after the outer iteration that ended the solve (grid-uniform)
+    if (o.stop && ldcg(o.stop)) return;   // queued after the outer iteration that ended the solve (grid-uniform)
     if (o.perm) perm_positions(o.seed, o.k_next, o.n, o.s, o.col_ptr, o.heavy_len, o.order, o.flag, o.fflag, o.colinfo);
     obj_block_partial(s, n, z, y, w, loss, partial, t);
     __shared__ bool last;
@@ -2163,16 +2164,18 @@ __global__ void __launch_bounds__(OBJ_NB) k_obj(int64_t s, int64_t n, const doub
     __syncthreads();
     if (!last) return;
     __threadfence();
-    obj_final_body(partial, o.c, o.mu, o.F, nullptr, o.eps, o.fstar, o.status, o.stop);
+    obj_final_body(partial, o.c, o.mu, o.F, o.F_copy, o.eps, o.fstar, o.status, o.stop);
     __syncthreads();
     if (threadIdx.x == 0) {
         *o.ticket = 0u;
         *o.bar = 0ull;
     }
-    __threadfence();
-    __syncthreads();
-    for (int e = threadIdx.x; e < o.mirror_words; e += blockDim.x) o.mirror_host[e] = __ldcg(&o.mirror[e]);
-    __threadfence_system();
+    if (o.mirror_host) {
+        __threadfence();
+        __syncthreads();
+        for (int e = threadIdx.x; e < o.mirror_words; e += blockDim.x) o.mirror_host[e] = __ldcg(&o.mirror[e]);
+        __threadfence_system();
+    }
 }
 
 // status 1 + first index of a non-finite value (squared-loss targets)
