@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstddef>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -577,6 +578,30 @@ int choose_mode(const pcdn_ctx *ctx, int64_t P)
     return mode;
 }
 
+// The side stream that builds the next outer iteration's lists beside the cluster-resident kernel:
+// one per device for the whole process (creating a stream per context cost ~0.2-0.8 ms in the
+// one-call host API); contexts order their own work on it with events.
+static cudaStream_t shared_side_stream()
+{
+    static std::mutex mu;
+    static cudaStream_t streams[64] = {};
+    static bool tried[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    std::lock_guard<std::mutex> lock(mu);
+    if (!tried[dev]) {
+        tried[dev] = true;
+        if (cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess) {
+            cudaGetLastError();
+            streams[dev] = nullptr;
+        }
+    }
+    return streams[dev];
+}
+
 // Load every kernel of the library once per process.  Under CUDA's default lazy module loading
 // each kernel is loaded at its first use, and the one-call host API (which creates a context per
 // call) was measured to pay ~8 ms per call more than with eager loading (scripts/_create_time.py).
@@ -788,8 +813,8 @@ int pcdn_create(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_ptr, c
             e = cudaEventCreate(&ctx->ev[i]);
             if (e != cudaSuccess) return fail(set_err(ctx, PCDN_ERR_CUDA, "cudaEventCreate: %s", cudaGetErrorString(e)));
         }
-        if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess ||
-            cudaEventCreateWithFlags(&ctx->ev_prep, cudaEventDisableTiming) != cudaSuccess) {
+        ctx->side = shared_side_stream();
+        if (!ctx->side || cudaEventCreateWithFlags(&ctx->ev_prep, cudaEventDisableTiming) != cudaSuccess) {
             cudaGetLastError();   // no overlap: lists are built on the context stream
             ctx->side = nullptr;
             ctx->ev_prep = nullptr;
@@ -970,11 +995,11 @@ void pcdn_destroy(pcdn_ctx *ctx)
     cudaStreamSynchronize(ctx->stream);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
-    if (ctx->side) {
-        cudaStreamSynchronize(ctx->side);
-        cudaStreamDestroy(ctx->side);
+    // the side stream is shared by the process's contexts: wait for this context's work on it only
+    if (ctx->ev_prep) {
+        cudaEventSynchronize(ctx->ev_prep);
+        cudaEventDestroy(ctx->ev_prep);
     }
-    if (ctx->ev_prep) cudaEventDestroy(ctx->ev_prep);
     if (ctx->hm) cudaFreeHost(ctx->hm);
     delete ctx;
 }
