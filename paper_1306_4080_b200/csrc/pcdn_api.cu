@@ -834,7 +834,7 @@ int pcdn_create(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_ptr, c
                                                                loss == PCDN_LOSS_SQUARED ? nullptr : y,
                                                                ctx->at<int>(L.status), ctx->at<long long>(L.err_idx),
                                                                ctx->at<int>(L.err_what));
-    k_validate_transpose<<<grid1d(s), 256, 0, ctx->stream>>>(s, csc_col_ptr, csc_row_idx, csc_val, csr_row_ptr,
+    k_validate_transpose<<<grid1d(s * 32), 256, 0, ctx->stream>>>(s, csc_col_ptr, csc_row_idx, csc_val, csr_row_ptr,
                                                              csr_col_idx, csr_val, ctx->at<int>(L.status),
                                                              ctx->at<long long>(L.err_idx), ctx->at<int>(L.err_what));
     {

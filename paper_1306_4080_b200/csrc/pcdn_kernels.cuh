@@ -2240,8 +2240,12 @@ __global__ void k_validate_transpose(int64_t s, const int64_t *__restrict__ col_
                                      const int32_t *__restrict__ col_idx, const float *__restrict__ csr_val,
                                      int *status, long long *err_idx, int *err_what)
 {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s; i += (int64_t)gridDim.x * blockDim.x) {
-        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; p++) {
+    // one warp per row, lanes over its nonzeros: the binary searches of a row run side by side
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = gw; i < s; i += nw) {
+        for (int64_t p = row_ptr[i] + lane; p < row_ptr[i + 1]; p += 32) {
             const int32_t j = col_idx[p];
             int64_t lo = col_ptr[j], hi = col_ptr[j + 1];
             while (lo < hi) {

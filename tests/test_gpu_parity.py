@@ -795,3 +795,25 @@ def test_stop_flag_state_between_calls(pk, cfg_mode):
     r2 = s.solve(prob.P, seed=4, max_outer=3)
     assert r2["outer_iters"] == 3 and r2["rc"] == pk.PCDN_BUDGET
     s.close()
+
+
+@pytest.mark.parametrize("corrupt", ["value", "column", "none"])
+def test_csr_csc_consistency_check(pk, corrupt):
+    """pcdn_create checks that the CSR arrays describe the same matrix as the CSC ones (one warp
+    per row, a binary search per nonzero): a changed value or a moved column index is refused
+    with PCDN_ERR_INVALID; the unchanged matrix is accepted."""
+    prob = synth.tiny(41, 300, 70, density=0.2, c=2.0, P=7)
+    p = int(prob.row_ptr[137]) + 1   # a nonzero in the middle of row 137
+    if corrupt == "value":
+        prob.csr_val = prob.csr_val.copy()
+        prob.csr_val[p] += 1.0
+    elif corrupt == "column":
+        prob.col_idx = prob.col_idx.copy()
+        row = set(prob.col_idx[prob.row_ptr[137]:prob.row_ptr[138]].tolist())
+        prob.col_idx[p] = next(j for j in range(prob.n) if j not in row)
+    if corrupt == "none":
+        pk.Solver(prob).close()
+        return
+    with pytest.raises(pk.PCDNError) as ei:
+        pk.Solver(prob)
+    assert ei.value.status == pk.PCDN_ERR_INVALID
