@@ -262,7 +262,10 @@ void pcdn_destroy(pcdn_ctx *ctx);
 
 /* One-call host API: copies HOST arrays (pinned recommended) to the device, trains with
  * pcdn_solve and copies w back to w_out (host fp64[n]).  Allocates and frees its own device
- * memory (stream-ordered).  f_star <= 0 with eps > 0 is invalid.  info: host, nullable. */
+ * memory (stream-ordered).  f_star <= 0 with eps > 0 is invalid.  info: host, nullable.
+ * csr_row_ptr, csr_col_idx, csr_val may all be NULL: the CSR is then built on the device from
+ * the CSC (a stable radix sort of the nonzeros by row: every row lists its columns ascending),
+ * which halves the bytes copied over PCIe.  Passing some but not all of them is invalid. */
 int pcdn_train_host(int64_t s, int64_t n, int64_t nnz,
                     const int64_t *csc_col_ptr, const int32_t *csc_row_idx, const float *csc_val,
                     const int64_t *csr_row_ptr, const int32_t *csr_col_idx, const float *csr_val,

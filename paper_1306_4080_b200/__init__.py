@@ -181,7 +181,8 @@ def pcdn_destroy(ctx):
 
 def pcdn_train_host(col_ptr, row_idx, val, row_ptr, col_idx, csr_val, y, c, loss, P, eps, f_star, seed,
                     max_outer, stream=None, w_out=None):
-    """Host (numpy, ideally pinned) arrays in, w out: the one-call end-to-end API."""
+    """Host (numpy, ideally pinned) arrays in, w out: the one-call end-to-end API.  row_ptr,
+    col_idx, csr_val may all be None: the CSR is then built on the device from the CSC."""
     s, n, nnz = int(y.shape[0]), int(col_ptr.shape[0] - 1), int(col_ptr[-1])
     w = np.zeros(n, dtype=np.float64) if w_out is None else w_out
     inf = pcdn_solve_info()

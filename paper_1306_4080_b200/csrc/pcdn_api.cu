@@ -3,6 +3,7 @@
 // Host side only marshals arguments, carves the caller's workspace and enqueues the kernels
 // of pcdn_kernels.cuh on the context stream; every step of the path runs on the device.
 #include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 #include <chrono>
@@ -1464,6 +1465,81 @@ int pcdn_shard_loss(pcdn_ctx *ctx, double *loss_out)
     return PCDN_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// CSR from CSC on the device (pcdn_train_host with csr_* = NULL): the nonzeros in CSC order
+// (columns ascending) are stably sorted by row, so every row lists its columns ascending -- the
+// CSR a host would build.  Pairs: key = row, value = column << 32 | value bits.
+__global__ void k_csc_pairs(int64_t n, const int64_t *__restrict__ col_ptr, const float *__restrict__ val,
+                            unsigned long long *pairs)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t j = gw; j < n; j += nw)
+        for (int64_t p = col_ptr[j] + lane; p < col_ptr[j + 1]; p += 32)
+            pairs[p] = ((unsigned long long)(uint32_t)j << 32) | (unsigned long long)__float_as_uint(val[p]);
+}
+
+__global__ void k_csr_from_sorted(int64_t s, int64_t nnz, const int32_t *__restrict__ rows,
+                                  const unsigned long long *__restrict__ pairs, int64_t *row_ptr, int32_t *col_idx,
+                                  float *csr_val)
+{
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t p = tid; p < nnz; p += nth) {
+        const unsigned long long v = pairs[p];
+        col_idx[p] = (int32_t)(v >> 32);
+        csr_val[p] = __uint_as_float((uint32_t)(v & 0xffffffffull));
+    }
+    for (int64_t i = tid; i <= s; i += nth) {   // row_ptr[i] = first sorted position with row >= i
+        int64_t lo = 0, hi = nnz;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (rows[mid] < i) lo = mid + 1; else hi = mid;
+        }
+        row_ptr[i] = lo;
+    }
+}
+
+int device_csr(int64_t s, int64_t n, int64_t nnz, const int64_t *col_ptr, const int32_t *row_idx, const float *val,
+               int64_t *row_ptr, int32_t *col_idx, float *csr_val, cudaStream_t st)
+{
+    int32_t *rows = nullptr;
+    unsigned long long *pa = nullptr, *pb = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    int bits = 1;
+    while ((1ll << bits) < s) bits++;
+    int rc = PCDN_OK;
+    const int64_t m = nnz > 0 ? nnz : 1;
+    if (cudaMallocAsync(&rows, sizeof(int32_t) * m, st) != cudaSuccess ||
+        cudaMallocAsync(&pa, sizeof(unsigned long long) * m, st) != cudaSuccess ||
+        cudaMallocAsync(&pb, sizeof(unsigned long long) * m, st) != cudaSuccess)
+        rc = PCDN_ERR_NOMEM;
+    if (rc == PCDN_OK && nnz > 0) {
+        k_csc_pairs<<<grid1d(n * 32), 256, 0, st>>>(n, col_ptr, val, pa);
+        if (cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, row_idx, rows, pa, pb, (int)nnz, 0, bits, st) !=
+                cudaSuccess ||
+            cudaMallocAsync(&tmp, tmp_bytes ? tmp_bytes : 1, st) != cudaSuccess ||
+            cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, row_idx, rows, pa, pb, (int)nnz, 0, bits, st) !=
+                cudaSuccess)
+            rc = PCDN_ERR_CUDA;
+    }
+    if (rc == PCDN_OK) {
+        k_csr_from_sorted<<<grid1d(std::max(nnz, s + 1)), 256, 0, st>>>(s, nnz, rows, pb, row_ptr, col_idx, csr_val);
+        if (cudaGetLastError() != cudaSuccess) rc = PCDN_ERR_CUDA;
+    }
+    if (tmp) cudaFreeAsync(tmp, st);
+    if (rows) cudaFreeAsync(rows, st);
+    if (pa) cudaFreeAsync(pa, st);
+    if (pb) cudaFreeAsync(pb, st);
+    return rc;
+}
+}  // namespace
+
+extern "C" {
+
 int pcdn_train_host(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_ptr, const int32_t *csc_row_idx,
                     const float *csc_val, const int64_t *csr_row_ptr, const int32_t *csr_col_idx,
                     const float *csr_val, const int8_t *y, double c, int loss, int64_t P, double eps, double f_star,
@@ -1471,7 +1547,11 @@ int pcdn_train_host(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_pt
 {
     if (loss == PCDN_LOSS_SQUARED) return PCDN_ERR_INVALID;   // needs targets: use pcdn_create + pcdn_set_targets
     pcdn_ctx *ctx = nullptr;  // for CU() error text only
-    if (s < 1 || n < 1 || nnz < 0 || !csc_col_ptr || !csr_row_ptr || !y || !w_out) return PCDN_ERR_INVALID;
+    if (s < 1 || n < 1 || nnz < 0 || !csc_col_ptr || !y || !w_out) return PCDN_ERR_INVALID;
+    if (nnz > INT32_MAX) return PCDN_ERR_INVALID;   // 32-bit indices (row_idx, col_idx)
+    // csr_* all NULL: the CSR is built on the device from the CSC (not copied, not re-checked)
+    const bool csr_dev = !csr_row_ptr && !csr_col_idx && !csr_val;
+    if (!csr_dev && (!csr_row_ptr || (nnz > 0 && (!csr_col_idx || !csr_val)))) return PCDN_ERR_INVALID;
     if (eps > 0 && !(f_star > 0)) return PCDN_ERR_INVALID;
     cudaStream_t st = (cudaStream_t)cuda_stream;
     {
@@ -1503,6 +1583,9 @@ int pcdn_train_host(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_pt
             break;
         }
     }
+    if (rc == PCDN_OK && csr_dev)
+        rc = device_csr(s, n, nnz, (const int64_t *)d[0], (const int32_t *)d[1], (const float *)d[2], (int64_t *)d[3],
+                        (int32_t *)d[4], (float *)d[5], st);
     if (rc == PCDN_OK) {
         rc = pcdn_create(s, n, nnz, (const int64_t *)d[0], (const int32_t *)d[1], (const float *)d[2],
                          (const int64_t *)d[3], (const int32_t *)d[4], (const float *)d[5], (const int8_t *)d[6], c,

@@ -433,6 +433,33 @@ def test_train_host_matches_oracle(pk, cfg, loss):
     with pytest.raises(pk.PCDNError) as ei:
         pk.pcdn_train_host(*arrs, prob.c, prob.loss, prob.P, 1e-3, -1.0, prob.seed, 60)
     assert ei.value.status == pk.PCDN_ERR_INVALID
+    # the CSR built on the device (csr_* = None, as bench.py's e2e call): the same CSR, so the
+    # same run bit for bit
+    st2, inf2, w2 = pk.pcdn_train_host(arrs[0], arrs[1], arrs[2], None, None, None, arrs[6], prob.c, prob.loss,
+                                       prob.P, 1e-3, fstar, prob.seed, 60)
+    assert st2 == pk.PCDN_OK and inf2.outer_iters == inf.outer_iters and inf2.steps == inf.steps
+    assert np.array_equal(w2.view(np.uint64), w.view(np.uint64)) and inf2.F == inf.F
+    with pytest.raises(pk.PCDNError) as ei:   # some but not all CSR arrays
+        pk.pcdn_train_host(arrs[0], arrs[1], arrs[2], arrs[3], None, None, arrs[6], prob.c, prob.loss, prob.P, 1e-3,
+                           fstar, prob.seed, 60)
+    assert ei.value.status == pk.PCDN_ERR_INVALID
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (3, 700), (2000, 3), (513, 129)])
+def test_device_csr_build(pk, shape):
+    """The CSR that pcdn_train_host builds on the device from the CSC (stable radix sort by row)
+    gives bit-identical results to the host CSR, including empty rows / columns and a single
+    sample or feature."""
+    s_, n_ = shape
+    prob = synth.tiny(77 + s_, s_, n_, density=0.3, loss=LOSS_L2SVM, c=2.0, empty_cols=min(2, n_ - 1) if n_ > 2 else 0)
+    arrs = [np.ascontiguousarray(getattr(prob, k), dtype=dt) for k, dt in
+            (("col_ptr", np.int64), ("row_idx", np.int32), ("val", np.float32), ("row_ptr", np.int64),
+             ("col_idx", np.int32), ("csr_val", np.float32), ("y", np.int8))]
+    P = max(1, n_ // 3)
+    a = pk.pcdn_train_host(*arrs, prob.c, prob.loss, P, 0.0, 1.0, 5, 3)
+    b = pk.pcdn_train_host(arrs[0], arrs[1], arrs[2], None, None, None, arrs[6], prob.c, prob.loss, P, 0.0, 1.0, 5, 3)
+    assert a[0] == b[0] and a[1].steps == b[1].steps and a[1].F == b[1].F
+    assert np.array_equal(a[2].view(np.uint64), b[2].view(np.uint64))
 
 
 def test_knob_validation(pk):
