@@ -582,6 +582,9 @@ int choose_mode(const pcdn_ctx *ctx, int64_t P)
 // The side stream that builds the next outer iteration's lists beside the cluster-resident kernel:
 // one per device for the whole process (creating a stream per context cost ~0.2-0.8 ms in the
 // one-call host API); contexts order their own work on it with events.
+// set by pcdn_train_host around its pcdn_create call when it built the CSR from the CSC itself
+static thread_local bool g_csr_trusted = false;
+
 static cudaStream_t shared_side_stream()
 {
     static std::mutex mu;
@@ -835,7 +838,8 @@ int pcdn_create(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_ptr, c
                                                                loss == PCDN_LOSS_SQUARED ? nullptr : y,
                                                                ctx->at<int>(L.status), ctx->at<long long>(L.err_idx),
                                                                ctx->at<int>(L.err_what));
-    k_validate_transpose<<<grid1d(s * 32), 256, 0, ctx->stream>>>(s, csc_col_ptr, csc_row_idx, csc_val, csr_row_ptr,
+    // (skipped for a CSR the library built itself from this CSC: pcdn_train_host with csr_* = NULL)
+    if (!g_csr_trusted) k_validate_transpose<<<grid1d(s * 32), 256, 0, ctx->stream>>>(s, csc_col_ptr, csc_row_idx, csc_val, csr_row_ptr,
                                                              csr_col_idx, csr_val, ctx->at<int>(L.status),
                                                              ctx->at<long long>(L.err_idx), ctx->at<int>(L.err_what));
     {
@@ -1587,9 +1591,11 @@ int pcdn_train_host(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_pt
         rc = device_csr(s, n, nnz, (const int64_t *)d[0], (const int32_t *)d[1], (const float *)d[2], (int64_t *)d[3],
                         (int32_t *)d[4], (float *)d[5], st);
     if (rc == PCDN_OK) {
+        g_csr_trusted = csr_dev;
         rc = pcdn_create(s, n, nnz, (const int64_t *)d[0], (const int32_t *)d[1], (const float *)d[2],
                          (const int64_t *)d[3], (const int32_t *)d[4], (const float *)d[5], (const int8_t *)d[6], c,
                          loss, d[7], ws, st, &ctx);
+        g_csr_trusted = false;
         if (rc == PCDN_OK && eps > 0) rc = pcdn_set_reference(ctx, f_star);
         if (rc == PCDN_OK) {
             rc = pcdn_solve(ctx, P, eps, seed, max_outer, info);
