@@ -91,7 +91,7 @@ def lib():
         L.ora_solve.restype = C.c_int
         L.ora_solve.argtypes = [C.POINTER(_Prob), C.c_void_p, C.c_void_p, C.c_int64, C.c_double,
                                 C.c_double, C.c_uint64, C.c_int32, C.c_void_p, C.c_void_p,
-                                C.c_void_p, C.c_int64, C.POINTER(_SolveInfo)]
+                                C.c_void_p, C.c_int64, C.POINTER(_SolveInfo), C.c_void_p]
         L.ora_cdn.restype = C.c_int
         L.ora_cdn.argtypes = [C.POINTER(_Prob), C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32,
                               C.c_void_p, C.c_int64, C.POINTER(C.c_double)]
@@ -229,14 +229,16 @@ class Oracle:
         qt = np.zeros(max(cap, 1), dtype=np.int32)
         Ft = np.zeros(max(cap, 1))
         oF = np.zeros(max(max_outer, 1))
+        mt = np.zeros(max(cap, 1))
         info = _SolveInfo()
         rc = lib().ora_solve(C.byref(self.pb), _p(w), _p(z), int(P), float(eps), float(fstar),
                              seed & 0xFFFFFFFFFFFFFFFF, int(max_outer), _p(qt), _p(Ft), _p(oF), cap,
-                             C.byref(info))
+                             C.byref(info), _p(mt))
         ns = min(int(info.steps), cap)
         return dict(rc=rc, w=w, z=z, F=info.F, gap=info.gap, outer=int(info.outer_iters),
                     steps=int(info.steps), nnz=int(info.nnz_processed), touched=int(info.touched_total), null_steps=int(info.null_steps),
-                    q_trace=qt[:ns].copy(), F_trace=Ft[:ns].copy(), outer_F=oF[:int(info.outer_iters)].copy())
+                    q_trace=qt[:ns].copy(), F_trace=Ft[:ns].copy(), outer_F=oF[:int(info.outer_iters)].copy(),
+                    margin_trace=mt[:ns].copy())
 
     def scdn(self, Pbar, seed=0, max_outer=10, w0=None):
         """Alg.2 (Shotgun CDN), synchronous reading Z27: the F trace has one entry per iteration."""

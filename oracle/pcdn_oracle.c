@@ -485,9 +485,12 @@ typedef struct {
     double gap;
 } ora_solve_info;
 
+/* margin_trace (nullable): per step, the smallest relative margin of its decisions -- the Eq.5
+ * branch tests, the accepted Armijo test and the rejected one before it (reading Z22).  A GPU
+ * decision may differ from the oracle's only where this is below the tie threshold. */
 int ora_solve(const ora_prob *pb, double *w, double *z, int64_t P, double eps, double fstar,
               uint64_t seed, int32_t max_outer, int32_t *q_trace, double *F_trace,
-              double *outer_F, int64_t trace_cap, ora_solve_info *info)
+              double *outer_F, int64_t trace_cap, ora_solve_info *info, double *margin_trace)
 {
     const int64_t s = pb->s, n = pb->n;
     if (P < 1 || P > n) return ORA_ERR_INVALID;
@@ -519,6 +522,12 @@ int ora_solve(const ora_prob *pb, double *w, double *z, int64_t P, double eps, d
             if (steps < trace_cap) {
                 if (q_trace) q_trace[steps] = o.q;
                 if (F_trace) F_trace[steps] = st.F;
+                if (margin_trace) {
+                    double m = o.margin_d;
+                    if (o.q >= 0 && o.margin_accept < m) m = o.margin_accept;
+                    if (o.margin_prev < m) m = o.margin_prev;
+                    margin_trace[steps] = m;
+                }
             }
             steps++;
             if (o.q < 0) nulls++;

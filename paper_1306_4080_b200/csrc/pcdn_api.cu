@@ -21,6 +21,7 @@
 #include "pcdn_resident.cuh"
 #include "pcdn_dense.cuh"
 #include "pcdn_shard.cuh"
+#include "pcdn_sparse.cuh"
 
 using namespace pcdn;
 
@@ -32,11 +33,15 @@ constexpr size_t ALIGN = 256;
 
 inline size_t align_up(size_t x) { return (x + ALIGN - 1) & ~(ALIGN - 1); }
 
+// chunk descriptors a list set can need: chunks hold >= SP_CHMIN nonzeros, one partial chunk per column
+inline size_t chunk_capacity(int64_t n, int64_t nnz) { return (size_t)(nnz / SP_CHMIN + n + 1); }
+
 // per-outer-iteration lists (partition, column descriptors, heavy / full column lists); two sets
 // so that the lists of outer iteration k+1 can be built while the step kernel of k runs
 struct Lists {
     size_t order, hdesc, flag, fflag, fpos, flist, tiles3, colinfo, hpos, hlist, hlen, hstart, tiles1, tiles2, nheavy;
     size_t lb, ticket;   // k_prep_lists: tile states (zeroed at create) and its ticket pair
+    size_t cpos, cdesc, ccount;   // the sparse kernel's chunk lists (ccount: reference build only)
 };
 
 struct HostMirror {  // the readback block: device copy in the workspace, pinned host copy
@@ -55,7 +60,8 @@ static_assert(sizeof(HostMirror) % 8 == 0, "k_obj copies the read-back block in 
 
 struct Layout {
     size_t ydummy, w, z, coef, cnt, bits, rec, dxg, tlist, seen, dk, deltak, gk, hk, part, hpart, counters, info, F, Fcopy,
-        status, err_idx, err_what, stop, ticket, mirror, bar, objp, prof, tl, dbg_dx, dbg_mark, rec2, rslot, ovf_cnt, part_gh, total;
+        status, err_idx, err_what, stop, ticket, mirror, bar, objp, prof, tl, dbg_dx, dbg_mark, rec2, rslot, ovf_cnt, part_gh,
+        cslot, sbits, ccnt, dflag, cpart, total;
     Lists ls[2];
 };
 
@@ -100,6 +106,9 @@ Layout make_layout(int64_t s, int64_t n, int64_t nnz)
         S.nheavy = take(sizeof(int64_t));
         S.lb = take(sizeof(LbTile) * (size_t)((n + PL_TILE - 1) / PL_TILE + 1));
         S.ticket = take(sizeof(unsigned) * 2);
+        S.cpos = take(sizeof(int64_t) * (n + 1));
+        S.cdesc = take(sizeof(int4) * chunk_capacity(n, nnz));
+        S.ccount = take(sizeof(int32_t) * n);
     }
     L.seen = take(sizeof(uint32_t) * ((n + 31) / 32));
     L.dk = take(sizeof(double) * n);
@@ -130,6 +139,14 @@ Layout make_layout(int64_t s, int64_t n, int64_t nnz)
     L.ovf_cnt = take(sizeof(int) * 16);
     // dense kernel (only when every column is full): partial (g, h) per CTA per bundle column
     L.part_gh = take(nnz == s * n ? sizeof(double) * 2 * (size_t)n * DENSE_GMAX : 0);
+    // sparse kernel (pcdn_sparse.cuh): CSR offset of each CSC nonzero, the written-slot bitmap over
+    // those offsets (its records live in `rec`, 8 B at each offset), heavy-column arrival counters,
+    // stamped directions and chunk partials
+    L.cslot = take(sizeof(uint32_t) * nnz);
+    L.sbits = take(sizeof(uint32_t) * (nnz / 32 + 2));
+    L.ccnt = take(sizeof(int) * n);
+    L.dflag = take(sizeof(DFlag) * n);
+    L.cpart = take(sizeof(double2) * chunk_capacity(n, nnz));
     L.total = off + ALIGN;  // slack for base alignment
     return L;
 }
@@ -194,6 +211,7 @@ struct pcdn_ctx {
     int64_t trace_cap = 0;
     cudaEvent_t ev[10] = {};   // 0-3 single calls / solve span, 4-7 step spans (ring of 2), 8-9 readbacks
     int64_t launches = 0;
+    unsigned long long stamp = 1;   // sparse kernel: step stamps handed out so far (never reused)
     char err[512] = {0};
 
     template <typename T>
@@ -265,6 +283,18 @@ int build_heavy(pcdn_ctx *ctx, int64_t ntot, int buf, cudaStream_t st)
     k_full_compact<<<grid1d(ntot), 256, 0, st>>>(ctx->at<int64_t>(S.fpos), ntot, ctx->at<int32_t>(S.flist));
     ctx->launches++;
     CU(cudaGetLastError());
+    // the sparse kernel's chunks: counts per position, their scan, the descriptors
+    k_chunk_count<<<grid1d(ntot), 256, 0, st>>>(ctx->at<int4>(S.colinfo), ntot, ctx->heavy_eff,
+                                                ctx->at<int32_t>(S.ccount));
+    ctx->launches++;
+    CU(cudaGetLastError());
+    rc = scan<int32_t>(ctx, ctx->at<int32_t>(S.ccount), ntot, nullptr, ctx->at<int64_t>(S.cpos),
+                       ctx->at<int64_t>(S.tiles3), nullptr, st);
+    if (rc) return rc;
+    k_chunk_compact<<<grid1d(ntot), 256, 0, st>>>(ctx->at<int64_t>(S.cpos), ctx->at<int64_t>(S.hpos),
+                                                  ctx->at<int4>(S.colinfo), ntot, ctx->s, ctx->at<int4>(S.cdesc));
+    ctx->launches++;
+    CU(cudaGetLastError());
     return PCDN_OK;
 }
 
@@ -284,6 +314,8 @@ int prep_outer(pcdn_ctx *ctx, uint64_t seed, int64_t k, int buf, cudaStream_t st
         o.hlist = ctx->at<int32_t>(S.hlist);
         o.flist = ctx->at<int32_t>(S.flist);
         o.hdesc = ctx->at<int4>(S.hdesc);
+        o.cpos = ctx->at<int64_t>(S.cpos);
+        o.cdesc = ctx->at<int4>(S.cdesc);
         o.lb = ctx->at<LbTile>(S.lb);
         o.ticket = ctx->at<unsigned>(S.ticket);
         const int64_t ntiles = (ctx->n + PL_TILE - 1) / PL_TILE;
@@ -364,6 +396,18 @@ int reset_status(pcdn_ctx *ctx)
 // Launch the persistent step kernel over `nsteps` bundles of the positions in ctx->order.
 int choose_mode(const pcdn_ctx *ctx, int64_t P);
 int heavy_for_mode(const pcdn_ctx *ctx, int mode);
+
+// the sparse HBM-state kernel (pcdn_sparse.cuh): one cluster (mode 1) or the cooperative grid (mode 2)
+const void *sparse_kernel(bool cluster, int loss)
+{
+    if (cluster)
+        return loss == LOSS_LOGISTIC ? (const void *)k_step_sparse<ClusterSync, LOSS_LOGISTIC>
+               : loss == LOSS_L2SVM  ? (const void *)k_step_sparse<ClusterSync, LOSS_L2SVM>
+                                     : (const void *)k_step_sparse<ClusterSync, LOSS_SQ>;
+    return loss == LOSS_LOGISTIC ? (const void *)k_step_sparse<GridSync, LOSS_LOGISTIC>
+           : loss == LOSS_L2SVM  ? (const void *)k_step_sparse<GridSync, LOSS_L2SVM>
+                                 : (const void *)k_step_sparse<GridSync, LOSS_SQ>;
+}
 
 const void *dense_kernel(int loss)
 {
@@ -466,6 +510,16 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
     a.pflag = ctx->at<int32_t>(L.ls[1].flag);
     a.pfflag = ctx->at<int32_t>(L.ls[1].fflag);
     a.outers_done = ctx->at<int64_t>(L.counters) + 5;
+    a.cslot = ctx->at<uint32_t>(L.cslot);
+    a.sbits = ctx->at<uint32_t>(L.sbits);
+    a.rv = ctx->at<double>(L.rec);
+    a.cdesc = ctx->at<int4>(S.cdesc);
+    a.cpos = ctx->at<int64_t>(S.cpos);
+    a.cpart = ctx->at<double2>(L.cpart);
+    a.ccnt = ctx->at<int>(L.ccnt);
+    a.dflag = ctx->at<DFlag>(L.dflag);
+    a.stamp0 = ctx->stamp;
+    ctx->stamp += (unsigned long long)nsteps + 1ull;
     if (!ctx->bar_clean) CU(cudaMemsetAsync(a.bar, 0, sizeof(unsigned long long), ctx->stream));
     ctx->bar_clean = false;
     // cluster mode for steps small enough that 16 SMs keep up (hardware barrier, ~0.2 us);
@@ -500,9 +554,10 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
         // scattered at random every step while CSC and records stream through L2; a persisting
         // access-policy window keeps the state resident
         cudaLaunchConfig_t cfg{};
+        const bool sparse = mode != 5;
         cfg.gridDim = dim3(mode == 1 ? ctx->Gc : ctx->G);
         cfg.blockDim = dim3(NT);
-        cfg.dynamicSmemBytes = ctx->smem;
+        cfg.dynamicSmemBytes = sparse ? sizeof(SpSmem) : ctx->smem;
         cfg.stream = ctx->stream;
         cudaLaunchAttribute at[2];
         int na = 0;
@@ -547,21 +602,25 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
         }
         cfg.attrs = at;
         cfg.numAttrs = na;
-        if (mode == 1) CU(cudaLaunchKernelEx(&cfg, k_step<ClusterSync>, a));
-        else CU(cudaLaunchKernelEx(&cfg, k_step<GridSync>, a));
+        if (mode == 5) CU(cudaLaunchKernelEx(&cfg, k_step<GridSync>, a));
+        else {
+            void *kargs[] = {&a};
+            CU(cudaLaunchKernelExC(&cfg, sparse_kernel(mode == 1, ctx->loss), kargs));
+        }
     }
     ctx->launches++;
     return PCDN_OK;
 }
 
 // launch mode of the step kernel for bundles of size P (see pcdn_set_launch)
-// Columns longer than this are split nnz-balanced over every warp of the launch (heavy lists).
-// The HBM-state kernels (modes 1, 2) reduce columns up to CTA_LEN nonzeros inside one CTA (no grid
-// exchange); the cluster-resident kernel splits everything above a warp's 128.
+// Columns longer than this are "heavy": the sparse kernel (modes 1, 2) reduces them in chunks of
+// about this many nonzeros over several warps; the legacy grid kernel (mode 5) splits them
+// nnz-balanced over every warp of the launch and reduces shorter ones of up to CTA_LEN inside one
+// CTA; the cluster-resident kernel splits everything above a warp's 128.
 int heavy_for_mode(const pcdn_ctx *ctx, int mode)
 {
     if (ctx->heavy_len > 0) return ctx->heavy_len;
-    return (mode == 1 || mode == 2) ? CTA_LEN : MED_LEN;
+    return (mode == 1 || mode == 2) ? SP_CH : mode == 5 ? CTA_LEN : MED_LEN;
 }
 
 int choose_mode(const pcdn_ctx *ctx, int64_t P)
@@ -576,6 +635,8 @@ int choose_mode(const pcdn_ctx *ctx, int64_t P)
         if (ctx->res_G >= 2 && est_nb <= 65536.0) mode = 3;
         else mode = (ctx->Gc >= 2 && est_nb <= 16384.0 && P <= 2 * NW * ctx->Gc) ? 1 : 2;
     }
+    // the sparse kernel addresses CSR offsets in 32 bits
+    if ((mode == 1 || mode == 2) && ctx->nnz >= (int64_t)UINT32_MAX) mode = 5;
     return mode;
 }
 
@@ -619,7 +680,9 @@ static void preload_kernels()
         (const void *)k_scan_reduce<int32_t, int64_t>, (const void *)k_scan_reduce<int64_t, int64_t>,
         (const void *)k_scan_apply<int32_t, int64_t>, (const void *)k_scan_apply<int64_t, int64_t>,
         (const void *)k_scan_tiles<int64_t>, (const void *)k_heavy_compact, (const void *)k_step<GridSync>,
-        (const void *)k_step<ClusterSync>, res_kernel(LOSS_LOGISTIC, false), res_kernel(LOSS_L2SVM, false),
+        sparse_kernel(true, LOSS_LOGISTIC), sparse_kernel(true, LOSS_L2SVM), sparse_kernel(true, LOSS_SQ),
+        sparse_kernel(false, LOSS_LOGISTIC), sparse_kernel(false, LOSS_L2SVM), sparse_kernel(false, LOSS_SQ),
+        (const void *)k_chunk_count, (const void *)k_chunk_compact, res_kernel(LOSS_LOGISTIC, false), res_kernel(LOSS_L2SVM, false),
         res_kernel(LOSS_SQ, false), res_kernel(LOSS_LOGISTIC, true), res_kernel(LOSS_L2SVM, true),
         res_kernel(LOSS_SQ, true), dense_kernel(LOSS_LOGISTIC), dense_kernel(LOSS_L2SVM), dense_kernel(LOSS_SQ),
         (const void *)k_set_z, (const void *)k_obj_partial, (const void *)k_obj_final, (const void *)k_obj, (const void *)k_prep_lists, (const void *)k_solve_init, (const void *)k_validate,
@@ -642,12 +705,16 @@ int configure_launch(pcdn_ctx *ctx)
     if (!coop) return set_err(ctx, PCDN_ERR_CUDA, "device does not support cooperative launch");
     ctx->smem = sizeof(StepSmem);
     const void *kg = (const void *)k_step<GridSync>;
-    const void *kc = (const void *)k_step<ClusterSync>;
+    const void *kc = sparse_kernel(true, ctx->loss);
+    const void *ks = sparse_kernel(false, ctx->loss);
     CU(cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem));
-    CU(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem));
+    CU(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SpSmem)));
+    CU(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SpSmem)));
     CU(cudaFuncSetAttribute(kc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    int occ = 0;
+    int occ = 0, occs = 0;
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kg, NT, ctx->smem));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occs, ks, NT, sizeof(SpSmem)));
+    if (occs < occ) occ = occs;   // one grid size serves both grid kernels
     if (occ < 1) return set_err(ctx, PCDN_ERR_CUDA, "step kernel cannot be resident (smem %zu)", ctx->smem);
     int maxg = ctx->num_sms * occ;
     if (maxg > GMAX) maxg = GMAX;
@@ -657,7 +724,7 @@ int configure_launch(pcdn_ctx *ctx)
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(16);
         cfg.blockDim = dim3(NT);
-        cfg.dynamicSmemBytes = ctx->smem;
+        cfg.dynamicSmemBytes = sizeof(SpSmem);
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
         at[0].val.clusterDim.x = 16;
@@ -665,7 +732,7 @@ int configure_launch(pcdn_ctx *ctx)
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        if (cudaOccupancyMaxPotentialClusterSize(&maxc, k_step<ClusterSync>, &cfg) != cudaSuccess) {
+        if (cudaOccupancyMaxPotentialClusterSize(&maxc, kc, &cfg) != cudaSuccess) {
             cudaGetLastError();
             maxc = 0;
         }
@@ -838,10 +905,12 @@ int pcdn_create(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_ptr, c
                                                                loss == PCDN_LOSS_SQUARED ? nullptr : y,
                                                                ctx->at<int>(L.status), ctx->at<long long>(L.err_idx),
                                                                ctx->at<int>(L.err_what));
-    // (skipped for a CSR the library built itself from this CSC: pcdn_train_host with csr_* = NULL)
-    if (!g_csr_trusted) k_validate_transpose<<<grid1d(s * 32), 256, 0, ctx->stream>>>(s, csc_col_ptr, csc_row_idx, csc_val, csr_row_ptr,
-                                                             csr_col_idx, csr_val, ctx->at<int>(L.status),
-                                                             ctx->at<long long>(L.err_idx), ctx->at<int>(L.err_what));
+    // the CSR/CSC consistency check and the sparse kernel's CSC -> CSR offset map (values not
+    // compared for a CSR the library built itself from this CSC: pcdn_train_host with csr_* = NULL)
+    k_validate_transpose<<<grid1d(s * 32), 256, 0, ctx->stream>>>(s, csc_col_ptr, csc_row_idx, csc_val, csr_row_ptr,
+                                                                   csr_col_idx, csr_val, g_csr_trusted ? 0 : 1,
+                                                                   ctx->at<uint32_t>(L.cslot), ctx->at<int>(L.status),
+                                                                   ctx->at<long long>(L.err_idx), ctx->at<int>(L.err_what));
     {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail(set_err(ctx, PCDN_ERR_CUDA, "validate launch: %s", cudaGetErrorString(e)));
@@ -939,7 +1008,7 @@ int pcdn_set_debug(pcdn_ctx *ctx, int on)
 int pcdn_set_launch(pcdn_ctx *ctx, int mode, int ctas, int heavy_len)
 {
     if (!ctx) return PCDN_ERR_INVALID;
-    if (mode < 0 || mode > 4 || ctas < 0 || heavy_len < 0 || (mode == 1 && ctas > 16) ||
+    if (mode < 0 || mode > 5 || ctas < 0 || heavy_len < 0 || (mode == 1 && ctas > 16) ||
         (mode == 3 && (ctas > 16 || (ctas & (ctas - 1)) != 0)))
         return set_err(ctx, PCDN_ERR_INVALID, "invalid launch knobs");
     ctx->mode_req = mode;
@@ -1475,14 +1544,14 @@ namespace {
 // CSR from CSC on the device (pcdn_train_host with csr_* = NULL): the nonzeros in CSC order
 // (columns ascending) are stably sorted by row, so every row lists its columns ascending -- the
 // CSR a host would build.  Pairs: key = row, value = column << 32 | value bits.
-__global__ void k_csc_pairs(int64_t n, const int64_t *__restrict__ col_ptr, const float *__restrict__ val,
+__global__ void k_csc_pairs(int64_t n, int64_t nnz, const int64_t *__restrict__ col_ptr, const float *__restrict__ val,
                             unsigned long long *pairs)
 {
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t j = gw; j < n; j += nw)
-        for (int64_t p = col_ptr[j] + lane; p < col_ptr[j + 1]; p += 32)
+    for (int64_t j = gw; j < n; j += nw)   // (the CSC was validated first; the bounds only guard)
+        for (int64_t p = max(col_ptr[j], (int64_t)0) + lane; p < min(col_ptr[j + 1], nnz); p += 32)
             pairs[p] = ((unsigned long long)(uint32_t)j << 32) | (unsigned long long)__float_as_uint(val[p]);
 }
 
@@ -1516,13 +1585,37 @@ int device_csr(int64_t s, int64_t n, int64_t nnz, const int64_t *col_ptr, const 
     int bits = 1;
     while ((1ll << bits) < s) bits++;
     int rc = PCDN_OK;
+    // the CSC first (col_ptr monotone within [0, nnz], row indices in range, finite values): the
+    // pair build below indexes by col_ptr, so a broken one must be refused before it runs
+    {
+        struct Chk {
+            int status, what;
+            long long idx;
+        } *chk = nullptr, h{};
+        if (cudaMallocAsync(&chk, sizeof(Chk), st) != cudaSuccess) return PCDN_ERR_NOMEM;
+        if (cudaMemsetAsync(chk, 0, sizeof(Chk), st) != cudaSuccess ||
+            cudaMemsetAsync(&chk->idx, 0x7f, sizeof(long long), st) != cudaSuccess)
+            rc = PCDN_ERR_CUDA;
+        if (rc == PCDN_OK) {
+            k_validate<<<grid1d(n), 256, 0, st>>>(s, n, nnz, col_ptr, row_idx, val, nullptr, nullptr, nullptr, nullptr,
+                                                  &chk->status, &chk->idx, &chk->what);
+            if (cudaGetLastError() != cudaSuccess ||
+                cudaMemcpyAsync(&h, chk, sizeof(Chk), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+                cudaStreamSynchronize(st) != cudaSuccess)
+                rc = PCDN_ERR_CUDA;
+            else if (h.status)
+                rc = PCDN_ERR_INVALID;
+        }
+        cudaFreeAsync(chk, st);
+        if (rc != PCDN_OK) return rc;
+    }
     const int64_t m = nnz > 0 ? nnz : 1;
     if (cudaMallocAsync(&rows, sizeof(int32_t) * m, st) != cudaSuccess ||
         cudaMallocAsync(&pa, sizeof(unsigned long long) * m, st) != cudaSuccess ||
         cudaMallocAsync(&pb, sizeof(unsigned long long) * m, st) != cudaSuccess)
         rc = PCDN_ERR_NOMEM;
     if (rc == PCDN_OK && nnz > 0) {
-        k_csc_pairs<<<grid1d(n * 32), 256, 0, st>>>(n, col_ptr, val, pa);
+        k_csc_pairs<<<grid1d(n * 32), 256, 0, st>>>(n, nnz, col_ptr, val, pa);
         if (cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, row_idx, rows, pa, pb, (int)nnz, 0, bits, st) !=
                 cudaSuccess ||
             cudaMallocAsync(&tmp, tmp_bytes ? tmp_bytes : 1, st) != cudaSuccess ||
@@ -1552,6 +1645,7 @@ int pcdn_train_host(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_pt
     if (loss == PCDN_LOSS_SQUARED) return PCDN_ERR_INVALID;   // needs targets: use pcdn_create + pcdn_set_targets
     pcdn_ctx *ctx = nullptr;  // for CU() error text only
     if (s < 1 || n < 1 || nnz < 0 || !csc_col_ptr || !y || !w_out) return PCDN_ERR_INVALID;
+    if (nnz > 0 && (!csc_row_idx || !csc_val)) return PCDN_ERR_INVALID;
     if (nnz > INT32_MAX) return PCDN_ERR_INVALID;   // 32-bit indices (row_idx, col_idx)
     // csr_* all NULL: the CSR is built on the device from the CSC (not copied, not re-checked)
     const bool csr_dev = !csr_row_ptr && !csr_col_idx && !csr_val;

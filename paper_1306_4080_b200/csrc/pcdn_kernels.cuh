@@ -59,6 +59,11 @@ struct __align__(16) HPart {  // CTA partial of a heavy column crossing CTA boun
     double pad;
 };
 
+struct DFlag {   // a finished heavy column's direction d_j, published with the step's stamp
+    unsigned long long stamp;
+    double d;
+};
+
 struct StepArgs {
     // problem (immutable during the kernel)
     int64_t s, n;
@@ -130,6 +135,16 @@ struct StepArgs {
     double *objp;                 // [3 * OBJ_NB] objective partials
     int32_t *pflag, *pfflag;      // scratch for perm_positions
     int64_t *outers_done;
+    // sparse kernel (pcdn_sparse.cuh): records at the CSR slot of each nonzero, heavy columns in chunks
+    const uint32_t *cslot;   // CSR offset of each CSC nonzero [nnz]
+    uint32_t *sbits;         // written-slot bitmap over the CSR offsets (zero between steps)
+    double *rv;              // record value d_j x_ij at the CSR offset of (i, j)
+    const int4 *cdesc;       // chunk descriptors of the list set (chunk_decode)
+    const int64_t *cpos;     // chunks before each position [ntot+1]
+    double2 *cpart;          // chunk partials (g, h) by chunk index within the step
+    int *ccnt;               // arrivals per heavy entry (zero between steps)
+    DFlag *dflag;            // finished direction per heavy entry, stamped
+    unsigned long long stamp0;   // step t of this launch publishes stamp0 + t + 1
     // sync
     unsigned long long *bar;
     int *status;
@@ -399,6 +414,53 @@ __device__ __forceinline__ int64_t colinfo_p0(const int4 &ci)
     return (int64_t)(((uint64_t)(uint32_t)ci.w << 32) | (uint64_t)(uint32_t)ci.z);
 }
 
+// Chunks of the sparse step kernel (pcdn_sparse.cuh): a column longer than heavy_len is reduced by
+// whole CTAs in chunks of SP_CTA_MUL * max(heavy_len, SP_CHMIN) nonzeros (a warp's share of a chunk
+// is then about a medium column), the last chunk to arrive finishes the column.  So the
+// descriptor array of a list set needs at most nnz/SP_CHMIN + n entries; a column has at most
+// SP_NCHMAX chunks (the finishing warp sums <= 16 partials per lane).
+constexpr int SP_CHMIN = 4;
+constexpr int SP_CTA_MUL = 16;
+constexpr int SP_NCHMAX = 512;
+__host__ __device__ __forceinline__ int chunk_count(int64_t len, int heavy_len)
+{
+    if (len <= heavy_len) return 0;
+    const int64_t ch = (int64_t)SP_CTA_MUL * (heavy_len > SP_CHMIN ? heavy_len : SP_CHMIN);
+    const int64_t c = (len + ch - 1) / ch;
+    return (int)(c < SP_NCHMAX ? c : SP_NCHMAX);
+}
+// descriptor of chunk c of nch of heavy entry e over nonzeros [pb, pb + clen):
+// (e, c | nch << 10 | full << 20, pb lo, pb hi (8 bits) | clen << 8)
+__host__ __device__ __forceinline__ int64_t chunk_begin(int64_t cs, int64_t len, int c, int nch)
+{
+    return cs + (int64_t)c * len / nch;
+}
+__device__ __forceinline__ void write_chunks(int4 *out, int32_t e, int nch, int64_t cs, int64_t len, bool full)
+{
+    for (int c = 0; c < nch; c++) {
+        const int64_t pb = chunk_begin(cs, len, c, nch), pe = chunk_begin(cs, len, c + 1, nch);
+        out[c] = make_int4(e, c | (nch << 10) | ((full ? 1 : 0) << 20), (int)(uint32_t)(pb & 0xffffffffLL),
+                           (int)(uint32_t)(((uint64_t)pb >> 32) & 0xffu) | (int)((uint32_t)(pe - pb) << 8));
+    }
+}
+struct ChunkDesc {
+    int32_t e;
+    int c, nch;
+    bool full;
+    int64_t pb, len;
+};
+__device__ __forceinline__ ChunkDesc chunk_decode(const int4 &d)
+{
+    ChunkDesc r;
+    r.e = d.x;
+    r.c = d.y & 1023;
+    r.nch = (d.y >> 10) & 1023;
+    r.full = ((d.y >> 20) & 1) != 0;
+    r.pb = (int64_t)(((uint64_t)((uint32_t)d.w & 0xffu) << 32) | (uint64_t)(uint32_t)d.z);
+    r.len = (int64_t)((uint32_t)d.w >> 8);
+    return r;
+}
+
 // order[t] = pi_k(t); flag[t] = column length > heavy_len; fflag[t] = column is full (holds a
 // nonzero in every row: its entry for row i sits at col_ptr[j] + i); colinfo[t] (nullable)
 // (t0, stride: this thread's first position and the stride; by default the grid-stride order)
@@ -591,6 +653,27 @@ __global__ void k_heavy_compact(const int64_t *__restrict__ hpos, int64_t ntot, 
     }
 }
 
+// chunk counts per position (the reference build of the sparse kernel's chunk lists)
+__global__ void k_chunk_count(const int4 *__restrict__ colinfo, int64_t ntot, int heavy_len, int32_t *cnt)
+{
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntot; t += (int64_t)gridDim.x * blockDim.x)
+        cnt[t] = chunk_count(colinfo[t].y, heavy_len);
+}
+
+// chunk descriptors of every heavy position (cpos = exclusive scan of k_chunk_count, hpos = heavy
+// entry numbers)
+__global__ void k_chunk_compact(const int64_t *__restrict__ cpos, const int64_t *__restrict__ hpos,
+                                const int4 *__restrict__ colinfo, int64_t ntot, int64_t s, int4 *cdesc)
+{
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntot; t += (int64_t)gridDim.x * blockDim.x) {
+        const int nch = (int)(cpos[t + 1] - cpos[t]);
+        if (nch > 0) {
+            const int4 ci = colinfo[t];
+            write_chunks(cdesc + cpos[t], (int32_t)hpos[t], nch, colinfo_p0(ci), ci.y, ci.y == s);
+        }
+    }
+}
+
 // a0 in one launch: the permutation pi_k of a whole outer iteration and the lists the step kernels
 // read -- column descriptors, heavy-column lists (hpos, hlist, hdesc, hstart) and full-column
 // lists (fpos, flist) -- with the three position-order prefix sums taken by a single-pass scan
@@ -599,10 +682,11 @@ __global__ void k_heavy_compact(const int64_t *__restrict__ hpos, int64_t ntot, 
 // launches.  Tile states carry the launch's epoch, so they need no clearing between launches; the
 // last tile to finish re-arms the ticket.
 constexpr int PL_NT = 256, PL_PER = 2, PL_TILE = PL_NT * PL_PER;
+constexpr int PL_Q = 4;   // prefix sums of the list build: heavy count, heavy nnz, full count, chunk count
 struct alignas(64) LbTile {
-    long long agg[3];   // (heavy count, heavy nnz, full count) of the tile
-    long long inc[3];   // the same, inclusive of every earlier tile
-    unsigned flag;      // epoch << 2 | 1 (agg valid) or | 2 (inc valid)
+    long long agg[PL_Q];   // the tile's sums
+    long long inc[PL_Q];   // the same, inclusive of every earlier tile
+    unsigned flag;         // epoch << 2 | 1 (agg valid) or | 2 (inc valid)
 };
 struct PrepLists {
     int32_t *order;
@@ -610,6 +694,8 @@ struct PrepLists {
     int64_t *hpos, *hstart, *fpos, *nheavy;
     int32_t *hlist, *flist;
     int4 *hdesc;
+    int64_t *cpos;   // chunks of the sparse kernel before each position [n+1]
+    int4 *cdesc;     // chunk descriptors (chunk_desc)
     LbTile *lb;
     unsigned *ticket;   // [0] next tile, [1] tiles done
 };
@@ -618,8 +704,8 @@ __global__ void __launch_bounds__(PL_NT) k_prep_lists(uint64_t seed, int64_t k, 
                                                       unsigned epoch, PrepLists o)
 {
     __shared__ unsigned s_tile;
-    __shared__ long long s_w[3][PL_NT / 32];
-    __shared__ long long s_pre[3];
+    __shared__ long long s_w[PL_Q][PL_NT / 32];
+    __shared__ long long s_pre[PL_Q];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned ntiles = (unsigned)((n + PL_TILE - 1) / PL_TILE);
     if (tid == 0) s_tile = atomicAdd(&o.ticket[0], 1u);
@@ -629,7 +715,7 @@ __global__ void __launch_bounds__(PL_NT) k_prep_lists(uint64_t seed, int64_t k, 
     // this thread's PL_PER consecutive positions
     int32_t jv[PL_PER];
     int64_t p0v[PL_PER], lenv[PL_PER];
-    long long v[3] = {0, 0, 0};
+    long long v[PL_Q] = {0, 0, 0, 0};
     const int64_t tb = (int64_t)tile * PL_TILE + (int64_t)tid * PL_PER;
 #pragma unroll
     for (int e = 0; e < PL_PER; e++) {
@@ -648,26 +734,27 @@ __global__ void __launch_bounds__(PL_NT) k_prep_lists(uint64_t seed, int64_t k, 
             if (len > heavy_len) {
                 v[0] += 1;
                 v[1] += len;
+                v[3] += chunk_count(len, heavy_len);
             }
             if (len == s) v[2] += 1;
         }
     }
     // block exclusive scan of v (warp shuffles, then the warp totals)
-    long long inc[3] = {v[0], v[1], v[2]};
+    long long inc[PL_Q] = {v[0], v[1], v[2], v[3]};
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
 #pragma unroll
-        for (int q = 0; q < 3; q++) {
+        for (int q = 0; q < PL_Q; q++) {
             const long long u = __shfl_up_sync(0xffffffffu, inc[q], d);
             if (lane >= d) inc[q] += u;
         }
     }
     if (lane == 31)
-        for (int q = 0; q < 3; q++) s_w[q][warp] = inc[q];
+        for (int q = 0; q < PL_Q; q++) s_w[q][warp] = inc[q];
     __syncthreads();
-    long long wpre[3] = {0, 0, 0}, tot[3] = {0, 0, 0};
+    long long wpre[PL_Q] = {0, 0, 0, 0}, tot[PL_Q] = {0, 0, 0, 0};
     for (int w2 = 0; w2 < PL_NT / 32; w2++)
-        for (int q = 0; q < 3; q++) {
+        for (int q = 0; q < PL_Q; q++) {
             if (w2 < warp) wpre[q] += s_w[q][w2];
             tot[q] += s_w[q][w2];
         }
@@ -675,18 +762,18 @@ __global__ void __launch_bounds__(PL_NT) k_prep_lists(uint64_t seed, int64_t k, 
     if (warp == 0) {
         LbTile &me = o.lb[tile];
         if (lane == 0) {
-            for (int q = 0; q < 3; q++) me.agg[q] = tot[q];
+            for (int q = 0; q < PL_Q; q++) me.agg[q] = tot[q];
             if (tile == 0)
-                for (int q = 0; q < 3; q++) me.inc[q] = tot[q];
+                for (int q = 0; q < PL_Q; q++) me.inc[q] = tot[q];
             __threadfence();
             *(volatile unsigned *)&me.flag = (epoch << 2) | (tile == 0 ? 2u : 1u);
         }
-        long long pre[3] = {0, 0, 0};
+        long long pre[PL_Q] = {0, 0, 0, 0};
         long long base = (long long)tile - 1;
         while (base >= 0) {
             const long long i = base - lane;
             unsigned st = 2u;   // before tile 0: an inclusive sum of zero
-            long long val[3] = {0, 0, 0};
+            long long val[PL_Q] = {0, 0, 0, 0};
             if (i >= 0) {
                 const volatile unsigned *fp = &o.lb[i].flag;
                 unsigned fl;
@@ -696,11 +783,11 @@ __global__ void __launch_bounds__(PL_NT) k_prep_lists(uint64_t seed, int64_t k, 
                 st = fl & 3u;
                 __threadfence();
                 const long long *src = st == 2u ? o.lb[i].inc : o.lb[i].agg;
-                for (int q = 0; q < 3; q++) val[q] = __ldcg(&src[q]);
+                for (int q = 0; q < PL_Q; q++) val[q] = __ldcg(&src[q]);
             }
             const unsigned pm = __ballot_sync(0xffffffffu, st == 2u);
             const int lp = pm ? __ffs(pm) - 1 : 32;   // the nearest tile with an inclusive sum
-            for (int q = 0; q < 3; q++) {
+            for (int q = 0; q < PL_Q; q++) {
                 long long x = lane <= lp ? val[q] : 0;
                 for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
                 pre[q] += x;
@@ -710,30 +797,34 @@ __global__ void __launch_bounds__(PL_NT) k_prep_lists(uint64_t seed, int64_t k, 
         }
         if (lane == 0) {
             if (tile != 0) {
-                for (int q = 0; q < 3; q++) me.inc[q] = pre[q] + tot[q];
+                for (int q = 0; q < PL_Q; q++) me.inc[q] = pre[q] + tot[q];
                 __threadfence();
                 *(volatile unsigned *)&me.flag = (epoch << 2) | 2u;
             }
-            for (int q = 0; q < 3; q++) s_pre[q] = pre[q];
+            for (int q = 0; q < PL_Q; q++) s_pre[q] = pre[q];
         }
     }
     __syncthreads();
-    long long run[3];
-    for (int q = 0; q < 3; q++) run[q] = s_pre[q] + wpre[q] + inc[q] - v[q];   // exclusive, at tb
+    long long run[PL_Q];
+    for (int q = 0; q < PL_Q; q++) run[q] = s_pre[q] + wpre[q] + inc[q] - v[q];   // exclusive, at tb
 #pragma unroll
     for (int e = 0; e < PL_PER; e++) {
         const int64_t t = tb + e;
         if (t >= n) break;
         o.hpos[t] = run[0];
         o.fpos[t] = run[2];
+        o.cpos[t] = run[3];
         const int64_t len = lenv[e];
         if (len > heavy_len) {
             const int64_t cs = p0v[e];
             o.hlist[run[0]] = (int32_t)t;
             o.hdesc[run[0]] = make_int4((int)t, jv[e], (int)(uint32_t)(cs & 0xffffffffLL), (int)(cs >> 32));
             o.hstart[run[0]] = run[1];
+            const int nch = chunk_count(len, heavy_len);
+            write_chunks(o.cdesc + run[3], (int32_t)run[0], nch, cs, len, len == s);
             run[0] += 1;
             run[1] += len;
+            run[3] += nch;
         }
         if (len == s) {
             o.flist[run[2]] = (int32_t)t;
@@ -742,6 +833,7 @@ __global__ void __launch_bounds__(PL_NT) k_prep_lists(uint64_t seed, int64_t k, 
         if (t == n - 1) {   // the totals
             o.hpos[n] = run[0];
             o.fpos[n] = run[2];
+            o.cpos[n] = run[3];
             o.hstart[run[0]] = run[1];
             *o.nheavy = run[0];
         }
@@ -806,20 +898,40 @@ struct StepSmem {
     double sv[NHW][HB];
 };
 
-// Warp-level gh over columns' nonzeros [p0, p1): lanes strided, fixed xor tree.  The loop is
-// unrolled so several independent gathers are in flight per lane (the per-lane summation order is
-// unchanged).  full_base >= 0: the column is full, its row index is p - full_base (no index load).
+// Warp-level gh over columns' nonzeros [p0, p1): lanes strided, fixed xor tree.  The nonzeros of a
+// lane are taken in batches of B: the B index/value loads, then the B gathers they address, all in
+// flight together (a plain unrolled loop left each gather waiting on its own index load); the
+// per-lane summation order (ascending p) is unchanged.  full_base >= 0: the column is full, its
+// row index is p - full_base (no index load).
+template <int B = 8>
 __device__ __forceinline__ void col_gh(const StepArgs &a, int64_t p0, int64_t p1, int lane, double &gs, double &hs,
                                        int64_t full_base = -1)
 {
     double g = 0.0, h = 0.0;
-#pragma unroll 8
-    for (int64_t p = p0 + lane; p < p1; p += 32) {
-        const int32_t i = full_base >= 0 ? (int32_t)(p - full_base) : __ldg(&a.row_idx[p]);
-        const double x = (double)__ldg(&a.val[p]);
-        const double2 cf = ldcg(&a.coef[i]);
-        g += x * cf.x;
-        h += (x * x) * cf.y;
+    for (int64_t pb = p0 + lane; pb < p1; pb += 32 * B) {
+        int32_t ri[B];
+        float xv[B];
+#pragma unroll
+        for (int e = 0; e < B; e++) {
+            const int64_t p = pb + 32 * e;
+            ri[e] = -1;
+            xv[e] = 0.f;
+            if (p < p1) {
+                ri[e] = full_base >= 0 ? (int32_t)(p - full_base) : __ldg(&a.row_idx[p]);
+                xv[e] = __ldg(&a.val[p]);
+            }
+        }
+        double2 cf[B];
+#pragma unroll
+        for (int e = 0; e < B; e++) cf[e] = ri[e] >= 0 ? ldcg(&a.coef[ri[e]]) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int e = 0; e < B; e++) {
+            if (ri[e] >= 0) {
+                const double x = (double)xv[e];
+                g += x * cf[e].x;
+                h += (x * x) * cf[e].y;
+            }
+        }
     }
     gs = warp_sum(g);
     hs = warp_sum(h);
@@ -2216,7 +2328,7 @@ __global__ void k_validate(int64_t s, int64_t n, int64_t nnz, const int64_t *__r
             if (!isfinite(val[p])) fail(6, p);
         }
     }
-    for (int64_t i = t0; i < s; i += stride) {
+    for (int64_t i = t0; row_ptr && i < s; i += stride) {   // (row_ptr == NULL: the CSC alone)
         const int64_t a0 = row_ptr[i], a1 = row_ptr[i + 1];
         if (i == 0 && a0 != 0) fail(7, 0);
         if (i == s - 1 && a1 != nnz) fail(8, i);
@@ -2234,12 +2346,17 @@ __global__ void k_validate(int64_t s, int64_t n, int64_t nnz, const int64_t *__r
     }
 }
 
-// CSR/CSC consistency: every CSR nonzero (i, j, v) must be found in column j by binary search.
+// CSR/CSC consistency: every CSR nonzero (i, j, v) must be found in column j by binary search
+// (check == 0: a CSR the library built from this CSC itself -- found, values not compared).  The
+// search also gives the sparse kernel's map cslot[CSC offset] = CSR offset of the same nonzero.
+// Runs after k_validate on the same stream: if that refused the arrays (indices may point anywhere)
+// this kernel does nothing.
 __global__ void k_validate_transpose(int64_t s, const int64_t *__restrict__ col_ptr, const int32_t *__restrict__ row_idx,
                                      const float *__restrict__ val, const int64_t *__restrict__ row_ptr,
                                      const int32_t *__restrict__ col_idx, const float *__restrict__ csr_val,
-                                     int *status, long long *err_idx, int *err_what)
+                                     int check, uint32_t *cslot, int *status, long long *err_idx, int *err_what)
 {
+    if (ldcg(status)) return;
     // one warp per row, lanes over its nonzeros: the binary searches of a row run side by side
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -2252,9 +2369,11 @@ __global__ void k_validate_transpose(int64_t s, const int64_t *__restrict__ col_
                 const int64_t mid = (lo + hi) >> 1;
                 if (row_idx[mid] < i) lo = mid + 1; else hi = mid;
             }
-            if (lo >= col_ptr[j + 1] || row_idx[lo] != i || val[lo] != csr_val[p]) {
+            if (lo >= col_ptr[j + 1] || row_idx[lo] != i || (check && val[lo] != csr_val[p])) {
                 atomicMax(status, 1);
                 if (atomicMin(err_idx, (long long)p) > (long long)p) atomicExch(err_what, 14);
+            } else {
+                cslot[lo] = (uint32_t)p;
             }
         }
     }

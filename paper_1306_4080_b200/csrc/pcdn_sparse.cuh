@@ -1,0 +1,745 @@
+// pcdn_sparse.cuh -- the HBM-state bundle-step kernel for large sparse problems (launch modes 1-2;
+// config 5, kdda-shaped: s = 2*10^6 samples, n = 2*10^7 features, P = 4096).
+//
+// One persistent launch runs every bundle step of an outer iteration (Alg.3 l.5-11, PAPER.md:
+// 168-178).  The per-sample state (z_i, the cached factors (G_i, H_i)) lives in HBM/L2.  Per step:
+//
+//   A   g_j, h_j (Eq.13; App. A.2), d_j (Eq.5)
+//       and the Delta terms (Eq.7) for every bundle column, then one record d_j x_ij per nonzero of
+//       a column with d_j != 0 (Alg.4 l.1): stored at the CSR offset of (i, j) --
+//       a fixed slot, so no returning atomic and no per-sample record list -- plus a bit in the
+//       written-slot bitmap and a bit in the touched-sample bitmap (fire-and-forget reductions).
+//         short columns (<= SP_SHORT nonzeros): one lane, in row order;
+//         medium columns (<= heavy_len): one warp;
+//         heavy columns: nch chunks over nch warps; each publishes its partial (g, h) and bumps
+//         the column's arrival counter, the last to arrive sums the partials in chunk order,
+//         finishes the column and publishes d_j with the step's stamp; the chunk warps then wait
+//         for it and scatter their records.  No grid barrier inside phase A.
+//   [grid barrier]
+//   C   row-block owners: the touched set T (bitmap, ascending), d'x_i = the sum of the sample's
+//       written slots in CSR (ascending column) order -- a fixed order, no sort, no float atomics
+//       -- then the loss changes of a window of Armijo candidates (Eq.12), the L1 term and Delta
+//       over the CTA's bundle share -> one partial row
+//   [grid barrier]
+//   D   every CTA sums the partial rows in the same fixed order and takes the same decision
+//       (Eq.6, first passing q, further windows, q_max -> null step, reading Z10), commits its
+//       samples (z, factors) and its bundle share of w, clears its bitmaps
+//   [grid barrier]
+//
+// Summation orders differ from the oracle's (reading Z21: any fixed order); decisions and T are
+// compared bit-exact, floats with the condition-aware 1e-9 bar.
+#pragma once
+#include "pcdn_kernels.cuh"
+
+namespace pcdn {
+
+constexpr int SP_SHORT = 8;     // columns with <= SP_SHORT nonzeros are reduced by one lane
+constexpr int SP_CH = 256;      // default heavy_len of the sparse kernel: longer columns go in chunks
+constexpr int SP_FOLD = 4;      // record loads of one sample in flight together in the fold
+
+struct SpPlan {
+    int64_t c0, c1;     // the step's chunks [c0, c1) of cdesc
+    int64_t f_lo, nf;   // the step's full columns: entries [f_lo, f_lo + nf) of flist
+};
+
+struct SpSmem {
+    SpPlan plan[2];   // this and the next step (by step parity), computed a step ahead
+    double red[NW][32];
+    double tot[32];
+    int64_t scan_w[NW];
+    int64_t nT;
+    double F;
+    long long cnt[4];
+    long long pacc[16];
+    int dec_q, dec_bad;
+    double dec_alpha, dec_lhs, dec_rhs, dec_Delta, dec_nT;
+    double fd[FMAX];
+    int64_t fcp[FMAX];
+    double dxd[TSM];
+    int64_t row_base;
+    int32_t tl[TSM];
+};
+
+__device__ __forceinline__ int atom_add_acq_rel(int *p, int v)
+{
+    int old;
+    asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void st_release(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// record d_j x_ij of nonzero (i, j) at CSR offset `slot` (a3)
+__device__ __forceinline__ void sp_emit(const StepArgs &a, int32_t i, uint32_t slot, double v)
+{
+    __stcg(&a.rv[slot], v);
+    atomicOr(&a.sbits[slot >> 5], 1u << (slot & 31));
+    atomicOr(&a.bits[i >> 5], 1u << (i & 31));
+}
+
+__device__ __forceinline__ void sp_store_dir(const StepArgs &a, int64_t k, const Dir &r)
+{
+    a.dk[k] = r.d;
+    a.deltak[k] = r.delta;
+    if (a.g_out) {
+        a.g_out[k] = r.g;
+        a.h_out[k] = r.h;
+    }
+    if (a.d_out) a.d_out[k] = r.d;
+}
+
+// warp: g/h over nonzeros [p0, p1) then, for d != 0, the records (a column of <= heavy_len or a chunk)
+__device__ __forceinline__ void sp_scatter(const StepArgs &a, int64_t p0, int64_t p1, int lane, double d)
+{
+    constexpr int B = 8;
+    for (int64_t pb = p0 + lane; pb < p1; pb += 32 * B) {
+        int32_t ri[B];
+        uint32_t sl[B];
+        float xv[B];
+#pragma unroll
+        for (int e = 0; e < B; e++) {
+            const int64_t p = pb + 32 * e;
+            ri[e] = -1;
+            if (p < p1) {
+                ri[e] = __ldg(&a.row_idx[p]);
+                sl[e] = __ldg(&a.cslot[p]);
+                xv[e] = __ldg(&a.val[p]);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < B; e++)
+            if (ri[e] >= 0) sp_emit(a, ri[e], sl[e], d * (double)xv[e]);
+    }
+}
+
+// fold of sample i's records: the written slots of its CSR segment [r0, r1), ascending; up to
+// SP_FOLD slots of a word are loaded together (static register indices), summed in slot order
+__device__ __forceinline__ double sp_fold(const StepArgs &a, int64_t r0, int64_t r1)
+{
+    double dx = 0.0;
+    if (r1 <= r0) return dx;
+    const int64_t w0 = r0 >> 5, w1 = (r1 - 1) >> 5;
+    for (int64_t wd = w0; wd <= w1; wd++) {
+        uint32_t m = ldcg(&a.sbits[wd]);
+        if (wd == w0) m &= 0xffffffffu << (r0 & 31);
+        if (wd == w1) m &= 0xffffffffu >> (31 - ((r1 - 1) & 31));
+        while (m) {
+            uint32_t sl[SP_FOLD];
+#pragma unroll
+            for (int r = 0; r < SP_FOLD; r++) {
+                sl[r] = m ? (uint32_t)(wd * 32 + __ffs(m) - 1) : 0xffffffffu;
+                m &= m - 1;
+            }
+            double v[SP_FOLD];
+#pragma unroll
+            for (int r = 0; r < SP_FOLD; r++) v[r] = sl[r] != 0xffffffffu ? ldcg(&a.rv[sl[r]]) : 0.0;
+#pragma unroll
+            for (int r = 0; r < SP_FOLD; r++)
+                if (sl[r] != 0xffffffffu) dx += v[r];
+        }
+    }
+    return dx;
+}
+
+// One Armijo window over q0 .. q0+NQ-1 (Eq.6 with Eq.12 from retained quantities); window 0 also
+// folds d'x_i.  Then the grid barrier and the decision taken identically by every CTA.
+template <int NQ, int LOSS, class Sync>
+__device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &sy, WinState &ws, const int32_t *Tl,
+                                          int64_t nT, int64_t k0, int64_t pb0, int64_t pb1, int G, int c, int tid,
+                                          int lane, int warp, const ShareReg &sh, RowReg &rr, const DenseInfo &di,
+                                          bool prof, long long &tprev, long long *ctal, long long tstep)
+{
+    using LY = WinLayout<NQ>;
+    constexpr int W = LY::W;
+    double alpha0 = 1.0;
+    for (int q = 0; q < ws.q0; q++) alpha0 *= a.beta;
+    double acc[W];
+#pragma unroll
+    for (int q = 0; q < W; q++) acc[q] = 0.0;
+    for (int64_t li = tid; li < nT; li += NT) {
+        const int32_t i = Tl[li];
+        const double zi = ldcg(&a.z[i]);
+        const double cg = ldcg(&a.coef[i]).x;
+        const int yi = a.y[i];
+        double dx;
+        if (ws.win == 0) {
+            const int64_t r0 = __ldg(&a.row_ptr[i]), r1 = __ldg(&a.row_ptr[i + 1]);
+            dx = sp_fold(a, r0, r1);
+            if (di.any) {   // full columns, from CSC in bundle order (then the records)
+                const int64_t li2 = i - sm.row_base;
+                dx = (nT <= TSM ? sm.dxd[li2] : dense_dx(a, sm.fd, sm.fcp, di, k0, i)) + dx;
+            }
+            a.dxg[i] = dx;
+            if (li == tid) {
+                rr.i = i;
+                rr.yi = yi;
+                rr.zi = zi;
+                rr.dx = dx;
+                rr.has_dx = 1;
+            }
+        } else {
+            dx = li == tid ? rr.dx : ldcg(&a.dxg[i]);
+        }
+        double al = alpha0;
+#pragma unroll
+        for (int q = 0; q < NQ; q++) {
+            acc[q] += loss_change(LOSS, zi, yi, cg, dx, al);
+            al *= a.beta;
+        }
+    }
+    // L1 part of Eq.12 and Delta over this CTA's share of the bundle
+    for (int64_t kk = pb0 + tid; kk < pb1; kk += NT) {
+        const bool reg = kk == sh.kk;
+        const double wj = reg ? sh.wj : ldcg(&a.w[__ldg(&a.order[kk])]);
+        const double d = reg ? sh.d : ldcg(&a.dk[kk - k0]);
+        double al = alpha0;
+#pragma unroll
+        for (int q = 0; q < NQ; q++) {
+            acc[NQ + q] += fabs(wj + al * d) - fabs(wj) + a.mu * al * d * (wj + 0.5 * al * d);
+            al *= a.beta;
+        }
+        acc[LY::DELTA] += reg ? sh.delta : ldcg(&a.deltak[kk - k0]);
+    }
+    if (tid == 0) acc[LY::NTOUCH] = (double)nT;
+    if (ctal && ws.win == 0) {   // profiling mode 2: this CTA's fold + line-search time
+        __syncthreads();
+        if (tid == 0) ctal[1] += clock64() - tstep;
+    }
+    constexpr int SPL = 32 / W;
+    {
+        const double tot = xreduce<W>(acc, lane);
+        if ((lane % SPL) == 0) sm.red[warp][lane / SPL] = tot;
+    }
+    double *part = a.part + (int64_t)(ws.win & 1) * G * NPART;
+    __syncthreads();
+    if (warp == 0 && lane < W) {
+        double s = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < NW; w2++) s += sm.red[w2][lane];
+        part[(int64_t)c * NPART + lane] = s;
+    }
+    if (prof) {
+        const long long now = clock64();
+        sm.pacc[3] += now - tprev;
+        tprev = now;
+    }
+    sy.sync();
+    if (prof) {
+        const long long now = clock64();
+        sm.pacc[4] += now - tprev;
+        tprev = now;
+    }
+    grid_totals<W>(part, G, sm.red, sm.tot, lane, warp);
+    if (warp == 0 && lane == 0) {
+        const double Dl = sm.tot[LY::DELTA];
+        int qa = -1, badl = 0;
+        double al = alpha0, la = 0.0, ra = 0.0, alpha_a = 0.0;
+#pragma unroll
+        for (int q = 0; q < NQ; q++) {
+            if (qa < 0 && !badl) {
+                const double lhs = sm.tot[NQ + q] + a.c * sm.tot[q];
+                const double rhs = a.sigma * al * Dl;
+                if (!isfinite(lhs) || !isfinite(Dl)) {
+                    badl = 1;
+                } else if (lhs <= rhs) {
+                    qa = ws.q0 + q;
+                    alpha_a = al;
+                    la = lhs;
+                    ra = rhs;
+                }
+                al *= a.beta;
+            }
+        }
+        sm.dec_q = qa;
+        sm.dec_bad = badl;
+        sm.dec_alpha = alpha_a;
+        sm.dec_lhs = la;
+        sm.dec_rhs = ra;
+        sm.dec_Delta = Dl;
+        sm.dec_nT = sm.tot[LY::NTOUCH];
+    }
+    __syncthreads();
+    ws.qacc = sm.dec_q;
+    ws.bad = sm.dec_bad;
+    ws.alpha = sm.dec_alpha;
+    ws.lhs = sm.dec_lhs;
+    ws.rhs = sm.dec_rhs;
+    ws.Delta = sm.dec_Delta;
+    ws.nT_tot = sm.dec_nT;
+    ws.win++;
+    __syncthreads();   // sm.dec_* / sm.red / sm.tot are reused by the next window
+    if (prof) {
+        const long long now = clock64();
+        sm.pacc[5] += now - tprev;
+        tprev = now;
+    }
+}
+
+__device__ __forceinline__ void sp_plan(const StepArgs &a, int64_t k0, int64_t k1, SpPlan *out)
+{
+    SpPlan p;
+    p.c0 = __ldg(&a.cpos[k0]);
+    p.c1 = __ldg(&a.cpos[k1]);
+    p.f_lo = __ldg(&a.fpos[k0]);
+    p.nf = __ldg(&a.fpos[k1]) - p.f_lo;
+    *out = p;
+}
+
+template <class Sync, int LOSS>
+__global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
+{
+    if (a.stop && ldcg(a.stop)) return;   // the solve already ended (queued ahead; grid-uniform)
+    Sync sy(a.bar);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SpSmem &sm = *reinterpret_cast<SpSmem *>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x, c = blockIdx.x;
+    const int64_t nwords = (a.s + 31) >> 5;
+    const int64_t wb = (int64_t)c * nwords / G, we = (int64_t)(c + 1) * nwords / G;
+    const int64_t row_base = wb * 32;
+    if (tid == 0) sm.row_base = row_base;
+    int prev_q = 0;
+    const int64_t pbs0 = (int64_t)c * a.P / G, pbs1 = (int64_t)(c + 1) * a.P / G;
+    const int64_t gw = (int64_t)c * NW + warp;
+
+    long long tprev = 0;
+    const bool prof = a.prof != nullptr && c == 0 && tid == 0;
+    if (tid < 16) sm.pacc[tid] = 0;
+#define SP_MARK(i)                                \
+    do {                                          \
+        if (prof) {                               \
+            const long long now_ = clock64();     \
+            sm.pacc[i] += now_ - tprev;           \
+            tprev = now_;                         \
+        }                                         \
+    } while (0)
+    if (c == 0 && tid == 0) {
+        sm.F = ldcg(a.F);
+        for (int i = 0; i < 4; i++) sm.cnt[i] = 0;
+    }
+    if (tid == 0 && a.nsteps > 0) sp_plan(a, 0, min(a.P, a.ntot), &sm.plan[0]);
+    __syncthreads();
+    long long *const ctal = (a.tl && c < 512) ? a.tl + (int64_t)c * 8 : nullptr;   // per-CTA phase sums (profiling mode 2)
+    long long tstep = 0;
+    for (int64_t t = 0; t < a.nsteps; t++) {
+        if (prof) tprev = clock64();
+        if (ctal && tid == 0) tstep = clock64();
+        const int64_t k0 = t * a.P;
+        const int64_t k1 = min(k0 + a.P, a.ntot);
+        const int64_t Pt = k1 - k0;
+        const unsigned long long stamp = a.stamp0 + (unsigned long long)t + 1ull;
+        const SpPlan pl = sm.plan[t & 1];
+
+        // ---------------- phase A: short and medium columns (a1, a2, a3) ----------------------
+        // The step's heavy-column chunks go to the top GH CTAs (one chunk per CTA at a time, all
+        // 16 warps), the short and medium columns to the warps of the others.
+        const int64_t C0 = pl.c0, NCH = pl.c1 - pl.c0;
+        const int GH = NCH > 0 ? (int)max((int64_t)1, min((int64_t)(G / 2), NCH)) : 0;
+        const int GL = max(1, G - GH);
+        if (c < GL) {
+            const int64_t NWL = (int64_t)GL * NW;
+            const int cw = (int)min((int64_t)32, max((int64_t)1, (Pt + NWL - 1) / NWL));
+            for (int64_t ch = gw;; ch += NWL) {
+                const int64_t kb = k0 + ch * cw;
+                if (kb >= k1) break;
+                const int64_t kk = kb + lane;
+                const int4 ci = (lane < cw && kk < k1) ? __ldg(&a.colinfo[kk]) : make_int4(0, -1, 0, 0);
+                const int len = ci.y;
+                if (len >= 0 && len <= SP_SHORT && len <= a.heavy_len) {
+                    const int32_t j = ci.x;
+                    const int64_t p0 = colinfo_p0(ci);
+                    int32_t ri[SP_SHORT];
+                    uint32_t sl[SP_SHORT];
+                    float xv[SP_SHORT];
+#pragma unroll
+                    for (int e = 0; e < SP_SHORT; e++) {
+                        ri[e] = 0;
+                        sl[e] = 0;
+                        xv[e] = 0.f;
+                        if (e < len) {
+                            ri[e] = __ldg(&a.row_idx[p0 + e]);
+                            sl[e] = __ldg(&a.cslot[p0 + e]);
+                            xv[e] = __ldg(&a.val[p0 + e]);
+                        }
+                    }
+                    const double wj = ldcg(&a.w[j]);
+                    double2 cf[SP_SHORT];
+#pragma unroll
+                    for (int e = 0; e < SP_SHORT; e++) cf[e] = e < len ? ldcg(&a.coef[ri[e]]) : make_double2(0.0, 0.0);
+                    double g = 0.0, h = 0.0;
+#pragma unroll
+                    for (int e = 0; e < SP_SHORT; e++) {
+                        if (e < len) {
+                            const double x = (double)xv[e];
+                            g += x * cf[e].x;
+                            h += (x * x) * cf[e].y;
+                        }
+                    }
+                    const Dir r = finish_feature(a, g, h, wj);
+                    sp_store_dir(a, kk - k0, r);
+                    if (r.d != 0.0 && len != a.s) {   // full columns are folded from CSC (dense_dx)
+#pragma unroll
+                        for (int e = 0; e < SP_SHORT; e++)
+                            if (e < len) sp_emit(a, ri[e], sl[e], r.d * (double)xv[e]);
+                    }
+                }
+                unsigned med = __ballot_sync(0xffffffffu, len > SP_SHORT && len <= a.heavy_len);
+                while (med) {
+                    const int src = __ffs(med) - 1;
+                    med &= med - 1;
+                    const int32_t j = __shfl_sync(0xffffffffu, ci.x, src);
+                    const int ml = __shfl_sync(0xffffffffu, len, src);
+                    const int lo = __shfl_sync(0xffffffffu, ci.z, src), hi = __shfl_sync(0xffffffffu, ci.w, src);
+                    const int64_t p0 = (int64_t)(((uint64_t)(uint32_t)hi << 32) | (uint64_t)(uint32_t)lo);
+                    const int64_t p1 = p0 + ml;
+                    double gs, hs;
+                    col_gh(a, p0, p1, lane, gs, hs);
+                    const Dir r = finish_feature(a, gs, hs, ldcg(&a.w[j]));
+                    if (lane == 0) sp_store_dir(a, kb + src - k0, r);
+                    if (r.d != 0.0 && ml != a.s) sp_scatter(a, p0, p1, lane, r.d);
+                }
+            }
+        }
+        SP_MARK(8);
+
+        // ---------------- phase A, heavy columns: one chunk per CTA at a time (A1) ------------------
+        // The CTA's warps split the chunk's nonzeros evenly, their partials are added in warp
+        // order.  A one-chunk column is finished and scattered at once; a longer one publishes the
+        // chunk's partial and bumps the column's arrival counter -- the last chunk to arrive sums
+        // the partials in chunk order, finishes the column and publishes d_j with the step's stamp
+        // (A2 below scatters the other chunks).  Every partial is published before any CTA waits,
+        // so no wait can block a partial another column needs.
+        const bool heavy_cta = c >= G - GH;
+        if (heavy_cta) {
+            for (int64_t q = G - 1 - c; q < NCH; q += GH) {
+                const ChunkDesc cd = chunk_decode(__ldg(&a.cdesc[C0 + q]));
+                const int64_t w0 = cd.pb + (int64_t)warp * cd.len / NW, w1 = cd.pb + (int64_t)(warp + 1) * cd.len / NW;
+                double gs, hs;
+                col_gh(a, w0, w1, lane, gs, hs);
+                if (lane == 0) {
+                    sm.red[warp][0] = gs;
+                    sm.red[warp][1] = hs;
+                }
+                __syncthreads();
+                if (warp == 0) {
+                    double g = 0.0, h = 0.0;
+#pragma unroll
+                    for (int w2 = 0; w2 < NW; w2++) {
+                        g += sm.red[w2][0];
+                        h += sm.red[w2][1];
+                    }
+                    int fin = cd.nch == 1;
+                    if (!fin) {
+                        if (lane == 0) {
+                            __stcg(&a.cpart[q], make_double2(g, h));
+                            fin = atom_add_acq_rel(&a.ccnt[cd.e], 1) == cd.nch - 1;
+                        }
+                        fin = __shfl_sync(0xffffffffu, fin, 0);
+                        __syncwarp();
+                        if (fin) {   // the last chunk: the column's partials in chunk order, a fixed tree
+                            if (lane == 0) a.ccnt[cd.e] = 0;   // re-armed: the entry recurs only in a later launch
+                            g = 0.0;
+                            h = 0.0;
+                            const int64_t qb = q - cd.c;
+                            for (int u = lane; u < cd.nch; u += 32) {
+                                const double2 v = __ldcg(&a.cpart[qb + u]);
+                                g += v.x;
+                                h += v.y;
+                            }
+                            g = warp_sum(g);
+                            h = warp_sum(h);
+                        }
+                    }
+                    if (fin) {
+                        const int4 hd = __ldg(&a.hdesc[cd.e]);   // (position, j, col_ptr[j])
+                        const Dir r = finish_feature(a, g, h, ldcg(&a.w[hd.y]));
+                        if (lane == 0) {
+                            sp_store_dir(a, hd.x - k0, r);
+                            if (cd.nch > 1) {
+                                __stcg(&a.dflag[cd.e].d, r.d);
+                                st_release(&a.dflag[cd.e].stamp, stamp);
+                            }
+                            sm.tot[0] = r.d;
+                        }
+                    }
+                }
+                __syncthreads();
+                if (cd.nch == 1) {
+                    const double d = sm.tot[0];
+                    if (d != 0.0 && !cd.full) sp_scatter(a, w0, w1, lane, d);
+                }
+                __syncthreads();   // sm.red / sm.tot reused by the next chunk
+            }
+        }
+        SP_MARK(9);
+        // ---------------- phase A, heavy columns: records once d_j is published (A2) --------------
+        if (heavy_cta) {
+            for (int64_t q = G - 1 - c; q < NCH; q += GH) {
+                const ChunkDesc cd = chunk_decode(__ldg(&a.cdesc[C0 + q]));
+                if (cd.nch == 1 || cd.full) continue;
+                if (tid == 0) {
+                    const long long t0 = clock64();
+                    while (ld_acquire(&a.dflag[cd.e].stamp) != stamp) {
+                        if (clock64() - t0 > 8000000000LL) __trap();   // a broken protocol: fail, do not hang
+                        __nanosleep(32);
+                    }
+                    sm.tot[0] = __ldcg(&a.dflag[cd.e].d);
+                }
+                __syncthreads();
+                const double d = sm.tot[0];
+                const int64_t w0 = cd.pb + (int64_t)warp * cd.len / NW, w1 = cd.pb + (int64_t)(warp + 1) * cd.len / NW;
+                if (d != 0.0) sp_scatter(a, w0, w1, lane, d);
+                __syncthreads();
+            }
+        }
+        SP_MARK(0);
+        if (ctal) {   // profiling mode 2: this CTA's phase-A time (all its warps done)
+            __syncthreads();
+            if (tid == 0) ctal[0] += clock64() - tstep;
+        }
+        sy.sync();
+        SP_MARK(1);
+        if (ctal && tid == 0) tstep = clock64();
+
+        const bool fullP = Pt == a.P;
+        const int64_t pb0 = k0 + (fullP ? pbs0 : (int64_t)c * Pt / G);
+        const int64_t pb1 = k0 + (fullP ? pbs1 : (int64_t)(c + 1) * Pt / G);
+        ShareReg sh;
+        sh.kk = -1;
+        if (pb0 + tid < pb1) {   // loads issued here, consumed by the line search
+            sh.kk = pb0 + tid;
+            sh.j = __ldg(&a.order[sh.kk]);
+            sh.wj = ldcg(&a.w[sh.j]);
+            sh.d = ldcg(&a.dk[sh.kk - k0]);
+            sh.delta = ldcg(&a.deltak[sh.kk - k0]);
+        }
+        RowReg rr;
+        rr.i = -1;
+        rr.has_dx = 0;
+
+        // ---------------- the step's full columns (dense_dx) ------------------------------------
+        DenseInfo di;
+        di.f_lo = pl.f_lo;
+        di.nf = pl.nf;
+        di.any = false;
+        if (di.nf > 0) {
+            int any = 0;
+            for (int64_t e = tid; e < di.nf; e += NT) {
+                const int32_t kk = __ldg(&a.flist[di.f_lo + e]);
+                const double d = ldcg(&a.dk[kk - k0]);
+                if (e < FMAX) {
+                    sm.fd[e] = d;
+                    sm.fcp[e] = __ldg(&a.col_ptr[__ldg(&a.order[kk])]);
+                }
+                any |= d != 0.0;
+            }
+            di.any = __syncthreads_or(any) != 0;
+        }
+
+        // ---------------- phase C1: touched set of this CTA's row block -------------------------
+        if (di.any) {   // a full column with d_j != 0 touches every sample (reading Z8)
+            const int64_t nrows = min(a.s, we * 32) - row_base;
+            int32_t *Tw = nrows <= TSM ? sm.tl : a.tlist + row_base;
+            for (int64_t li = tid; li < nrows; li += NT) Tw[li] = (int32_t)(row_base + li);
+            if (tid == 0) sm.nT = nrows > 0 ? nrows : 0;
+            __syncthreads();
+        } else {
+            const int64_t nwc = we - wb;
+            const int64_t wpt = (nwc + NT - 1) / NT;
+            const int64_t w0 = wb + (int64_t)tid * wpt, w1 = min(we, w0 + wpt);
+            uint32_t wv[WREG];
+            unsigned cntb = 0;
+#pragma unroll
+            for (int r = 0; r < WREG; r++) {
+                wv[r] = (w0 + r < w1) ? ldcg(&a.bits[w0 + r]) : 0u;
+                cntb += __popc(wv[r]);
+            }
+            for (int64_t wi = w0 + WREG; wi < w1; wi++) cntb += __popc(ldcg(&a.bits[wi]));
+            unsigned incl = 0;
+            const unsigned lemask = 0xffffffffu >> (31 - lane);
+#pragma unroll
+            for (int b = 0; b < 16; b++) {
+                const unsigned m = __ballot_sync(0xffffffffu, (cntb >> b) & 1u);
+                if (!m && (b >= 8)) break;
+                incl += (unsigned)__popc(m & lemask) << b;
+            }
+            const unsigned wtot = __reduce_add_sync(0xffffffffu, cntb);
+            if (lane == 0) sm.scan_w[warp] = wtot;
+            __syncthreads();
+            const unsigned sw = lane < NW ? (unsigned)sm.scan_w[lane] : 0u;
+            const unsigned woff = __reduce_add_sync(0xffffffffu, lane < warp ? sw : 0u);
+            const unsigned total = __reduce_add_sync(0xffffffffu, sw);
+            int32_t *Tw = total <= (unsigned)TSM ? sm.tl : a.tlist + row_base;
+            if (cntb) {
+                int64_t pos = (int64_t)woff + incl - cntb;
+#pragma unroll
+                for (int r = 0; r < WREG; r++) {
+                    uint32_t m = wv[r];
+                    while (m) {
+                        const int b = __ffs(m) - 1;
+                        m &= m - 1;
+                        Tw[pos++] = (int32_t)((w0 + r) * 32 + b);
+                    }
+                }
+                for (int64_t wi = w0 + WREG; wi < w1; wi++) {
+                    uint32_t m = ldcg(&a.bits[wi]);
+                    while (m) {
+                        const int b = __ffs(m) - 1;
+                        m &= m - 1;
+                        Tw[pos++] = (int32_t)(wi * 32 + b);
+                    }
+                }
+            }
+            if (tid == 0) sm.nT = total;
+            __syncthreads();
+        }
+        const int64_t nT = sm.nT;
+        const int32_t *Tl = nT <= TSM ? sm.tl : a.tlist + row_base;
+        if (di.any && nT <= TSM) {
+            // the full columns' d'x part of every row of the block, (row, column chunk) per thread so
+            // that a column's loads are coalesced over rows; chunk partials added in chunk order
+            const int R = (int)nT;
+            const int C = R >= NT ? 1 : (int)min((int64_t)(NT / max(R, 1)), di.nf);
+            double *dpart = &sm.red[0][0];   // NW*32 = NT doubles
+            for (int r0 = 0; r0 < R; r0 += NT) {
+                const int tt = tid;
+                if (C == 1) {
+                    if (r0 + tt < R) sm.dxd[r0 + tt] = dense_dx(a, sm.fd, sm.fcp, di, k0, row_base + r0 + tt);
+                } else if (tt < R * C) {
+                    const int r = tt % R, chn = tt / R;
+                    const int64_t e0 = (int64_t)chn * di.nf / C, e1 = (int64_t)(chn + 1) * di.nf / C;
+                    const int64_t i = row_base + r;
+                    double part = 0.0;
+                    for (int64_t e = e0; e < e1; e++) {
+                        double d;
+                        int64_t cp;
+                        if (e < FMAX) {
+                            d = sm.fd[e];
+                            cp = sm.fcp[e];
+                        } else {
+                            const int32_t kk = __ldg(&a.flist[di.f_lo + e]);
+                            d = ldcg(&a.dk[kk - k0]);
+                            cp = __ldg(&a.col_ptr[__ldg(&a.order[kk])]);
+                        }
+                        if (d != 0.0) part += d * (double)__ldg(&a.val[cp + i]);
+                    }
+                    dpart[tt] = part;
+                }
+            }
+            if (C > 1) {
+                __syncthreads();
+                for (int r = tid; r < R; r += NT) {
+                    double x = 0.0;
+                    for (int chn = 0; chn < C; chn++) x += dpart[chn * R + r];
+                    sm.dxd[r] = x;
+                }
+            }
+            __syncthreads();
+        }
+        SP_MARK(2);
+        if (ctal && tid == 0) {
+            ctal[2] += nT;
+            ctal[3] += clock64() - tstep;
+        }
+
+        // ---------------- phase C2+C3: fold d'x_i (a3) and the Armijo windows (a4) --------------
+        WinState ws;
+        ws.q0 = 0;
+        ws.nq = prev_q <= 1 ? 2 : QW;
+        ws.qacc = -1;
+        ws.bad = 0;
+        ws.win = 0;
+        while (true) {
+            if (ws.nq <= 2)
+                sp_window<2, LOSS>(a, sm, sy, ws, Tl, nT, k0, pb0, pb1, G, c, tid, lane, warp, sh, rr, di, prof, tprev, ctal, tstep);
+            else
+                sp_window<QW, LOSS>(a, sm, sy, ws, Tl, nT, k0, pb0, pb1, G, c, tid, lane, warp, sh, rr, di, prof, tprev, ctal, tstep);
+            if (ws.qacc >= 0 || ws.bad) break;
+            ws.q0 += ws.nq;
+            if (ws.q0 > a.qmax) break;
+            ws.nq = QW;
+        }
+        int qacc = ws.qacc;
+        const bool bad = ws.bad != 0;
+        if (qacc > a.qmax) qacc = -1;   // window overshoot past q_max counts as exhausted
+        const double alpha_acc = qacc < 0 ? 0.0 : ws.alpha;   // null step (Z10)
+        prev_q = qacc < 0 ? QW : qacc;
+
+        // ---------------- commit (a5): this CTA's samples and bundle share; clear the bitmaps -----
+        // (every fold of the step finished before the decision's barrier, so the written-slot words
+        // can be cleared here even where two samples' segments share a word)
+        for (int64_t li = tid; li < nT; li += NT) {
+            const bool reg = li == tid && rr.i >= 0;
+            const int32_t i = reg ? rr.i : Tl[li];
+            const double dx = reg ? rr.dx : ldcg(&a.dxg[i]);
+            if (qacc >= 0) {
+                const double zi = reg ? rr.zi : ldcg(&a.z[i]);
+                const int yi = reg ? rr.yi : (int)a.y[i];
+                const double zn = zi + alpha_acc * dx;
+                a.z[i] = zn;
+                const double2 cfo = LOSS == LOSS_SQ ? ldcg(&a.coef[i]) : make_double2(0.0, 0.0);
+                a.coef[i] = coef_next(LOSS, cfo, zn, alpha_acc * dx, yi);
+            }
+            const int64_t r0 = __ldg(&a.row_ptr[i]), r1 = __ldg(&a.row_ptr[i + 1]);
+            if (r1 > r0)
+                for (int64_t wd = r0 >> 5; wd <= ((r1 - 1) >> 5); wd++) a.sbits[wd] = 0u;
+            if (a.debug) {
+                a.dbg_dx[i] = dx;
+                a.dbg_mark[i] = 1;
+            }
+        }
+        for (int64_t wi = wb + tid; wi < we; wi += NT) a.bits[wi] = 0u;
+        if (qacc >= 0) {
+            for (int64_t kb = pb0 + tid; kb < pb1; kb += NT) {
+                const bool reg = kb == sh.kk;
+                const int32_t j = reg ? sh.j : __ldg(&a.order[kb]);
+                const double wj = reg ? sh.wj : ldcg(&a.w[j]);
+                const double d = reg ? sh.d : ldcg(&a.dk[kb - k0]);
+                a.w[j] = wj + alpha_acc * d;
+            }
+        }
+        SP_MARK(6);
+        if (c == 0 && tid == 0) {
+            double F = sm.F;
+            if (qacc >= 0) F = F + ws.lhs;
+            sm.F = F;
+            *a.F = F;
+            if (bad) atomicMax(a.status, 3);
+            a.info[0] = (double)qacc;
+            a.info[1] = alpha_acc;
+            a.info[2] = ws.Delta;
+            a.info[3] = ws.lhs;
+            a.info[4] = ws.rhs;
+            a.info[5] = F;
+            a.info[7] = ws.nT_tot;
+            const int64_t gstep = a.trace_off + t;
+            if (gstep < a.trace_cap) {
+                if (a.q_trace) a.q_trace[gstep] = qacc;
+                if (a.F_trace) a.F_trace[gstep] = F;
+            }
+            sm.cnt[0] += 1;
+            sm.cnt[1] += qacc < 0 ? 1 : 0;
+            sm.cnt[2] += (int64_t)ws.nT_tot;
+            sm.cnt[3] += Pt;
+        }
+        sy.arrive();
+        // the next step's plan, while the barrier completes
+        if (tid == NT - 1 && k1 < a.ntot) sp_plan(a, k1, min(k1 + a.P, a.ntot), &sm.plan[(t + 1) & 1]);
+        sy.wait();
+        SP_MARK(7);
+        if (bad) break;
+    }
+    if (c == 0 && tid == 0) {
+        a.counters[0] += sm.cnt[0];
+        a.counters[1] += sm.cnt[1];
+        a.counters[3] += sm.cnt[2];
+        a.counters[4] += sm.cnt[3];
+    }
+    if (prof)
+        for (int i = 0; i < 16; i++) a.prof[i] += sm.pacc[i];
+#undef SP_MARK
+}
+
+}  // namespace pcdn

@@ -23,6 +23,7 @@ ap.add_argument("--modes", default="0")
 ap.add_argument("--outer", type=int, default=1)
 ap.add_argument("--profile", action="store_true")
 ap.add_argument("--heavy", type=int, default=0, help="heavy_len launch knob (0 = keep)")
+ap.add_argument("--ctas", default="0", help="comma list of CTA counts (launch knob; 0 = all co-resident)")
 ap.add_argument("--l2", type=int, default=1, help="persisting-L2 window of the HBM-state kernels (pcdn_set_l2_persist)")
 args = ap.parse_args()
 t0 = time.time()
@@ -33,10 +34,10 @@ pk.pcdn_set_l2_persist(s.ctx, args.l2)
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
 Ps = [int(x) for x in args.P.split(",") if x] or [prob.P]
-for P in Ps:
-    for mode in [int(m) for m in args.modes.split(",")]:
+for P, mode, ctas in [(P, int(m), int(g)) for P in Ps for m in args.modes.split(",") for g in args.ctas.split(",")]:
+    if True:
         try:
-            s.set_launch(mode, 0, args.heavy)
+            s.set_launch(mode, ctas, args.heavy)
         except pk.PCDNError as e:
             print(json.dumps({"P": P, "mode": mode, "error": str(e)}), flush=True)
             continue
@@ -52,7 +53,7 @@ for P in Ps:
         steps = r["steps"]
         kms = r["t_step_kernel_ms"]
         gbs = r["alg_bytes"] / (kms / 1e3) / 1e9
-        out = {"cfg": args.cfg, "P": P, "mode_req": mode, "mode_used": used, "heavy_len": args.heavy, "outer": r["outer_iters"],
+        out = {"cfg": args.cfg, "P": P, "mode_req": mode, "ctas": ctas, "mode_used": used, "heavy_len": args.heavy, "outer": r["outer_iters"],
                "steps": steps, "step_us": 1e3 * kms / steps, "kernel_ms_per_outer": kms / max(1, r["outer_iters"]),
                "gpu_ms_per_outer": r["t_gpu_ms"] / max(1, r["outer_iters"]),
                "alg_bytes_per_step": r["alg_bytes"] / steps, "kernel_alg_GBs": gbs, "frac_measured_hbm": gbs / peak,

@@ -2,7 +2,7 @@
 
 Bars (BASELINE.json north_star):
   * partitions, touched sets T and accepted q: bit-exact (decisions whose oracle margin is below
-    1e-9 are ties, reported but not failed -- reading Z22);
+    1e-12 relative are ties, listed at the end of the run but not failed -- reading Z22);
   * from the same state: g, h, d, Delta, d'x, LHS and F within 1e-9, condition-aware
     (|gpu - ora| <= 1e-9 * max(|ora|, sum|terms|), reading Z21);
   * solves: final F within 1e-6 relative, w within 1e-5 max-norm, q traces equal.
@@ -14,12 +14,13 @@ import pytest
 
 import oracle
 import synth
+from conftest import excuse_tie
 from synth import LOSS_L2SVM, LOSS_LOGISTIC
 
 pytestmark = pytest.mark.gpu
 
 RTOL = 1e-9
-TIE = 1e-9
+TIE = 1e-12   # a decision whose oracle margin is below 1e-12 (relative) is a tie
 
 
 @pytest.fixture(scope="module")
@@ -59,6 +60,7 @@ def _compare_step(g, o, ties):
         assert g["n_touched"] == o["T"].size
     else:
         ties.append(("d", o["margin_d"]))
+        excuse_tie("step: Eq.5 branch / d = 0 test", o["margin_d"])
     assert g["bundle_nnz"] == o["bundle_nnz"]
     if decisive_d and np.all(o["d"] == 0):      # zero direction: 0 <= 0 exactly at q = 0 (Z9)
         assert np.all(g["d"] == 0) and g["q"] == 0 and g["lhs"] == 0 and g["n_touched"] == 0
@@ -71,6 +73,7 @@ def _compare_step(g, o, ties):
         _close(g["F"], o["F_after"], o["lhs_abs"] + abs(o["F_after"]) * 1e-3, "F")
     else:
         ties.append(("q", o["margin_accept"], o["margin_prev"]))
+        excuse_tie("step: Armijo test", min(o["margin_accept"], o["margin_prev"], o["margin_d"]))
 
 
 def _random_state(rng, n, scale=0.3, density=0.3):
@@ -150,7 +153,7 @@ def test_step_parity_configs(pk, cfg, loss):
         for B in _step_cases(prob, rng, sizes=[1, prob.P, 4 * prob.P]):
             s.set_w(w)
             _compare_step(s.step(B), o.step(w, B), ties)
-    assert len(ties) <= 1, ties
+    assert not ties, ties   # configs 1-2: no decision may be excused
     s.close()
 
 
@@ -191,14 +194,25 @@ def test_objective_and_state_injection(pk):
 
 # ----------------------------------------------------------------------------- solve parity
 def _compare_solve(gs, os_, ws_gpu, what, ftrace_rtol=RTOL):
+    """q traces equal step for step (bit-exact decisions), the F trace within the per-step bar, the
+    final F within 1e-6 and w within 1e-5 (north-star bars).  A first q difference at a step whose
+    oracle margin (the smallest of its Eq.5 / Armijo decision margins) is below TIE is a tie
+    (reading Z22): it is listed, the traces are compared up to it, and the final bars still hold."""
     qg, qo = gs["q_trace"], os_["q_trace"]
     m = min(qg.size, qo.size)
     div = np.nonzero(qg[:m] != qo[:m])[0]
-    assert div.size == 0, f"{what}: q traces diverge first at step {div[0]} (gpu {qg[div[0]]}, ora {qo[div[0]]})"
-    assert gs["steps"] == os_["steps"] and gs["outer_iters"] == os_["outer"]
+    if div.size:
+        k = int(div[0])
+        margin = os_["margin_trace"][k]
+        assert margin <= TIE, f"{what}: q traces diverge first at step {k} (gpu {qg[k]}, ora {qo[k]}, margin {margin:.3g})"
+        excuse_tie(f"{what}: solve step {k} q gpu {qg[k]} ora {qo[k]}", margin)
+        m = k
+    else:
+        assert gs["steps"] == os_["steps"] and gs["outer_iters"] == os_["outer"]
     assert abs(gs["F"] - os_["F"]) <= 1e-6 * abs(os_["F"]), (gs["F"], os_["F"])
     assert np.max(np.abs(ws_gpu - os_["w"])) <= 1e-5
-    _close(gs["F_trace"], os_["F_trace"], np.abs(os_["F_trace"]) * 1e-3, what + " F trace", rtol=ftrace_rtol)
+    _close(gs["F_trace"][:m], os_["F_trace"][:m], np.abs(os_["F_trace"][:m]) * 1e-3, what + " F trace",
+           rtol=ftrace_rtol)
 
 
 @pytest.mark.parametrize("loss", [LOSS_LOGISTIC, LOSS_L2SVM])
@@ -277,7 +291,7 @@ def test_step_parity_large_configs(pk, cfg, mode):
         B2 = rng.choice(prob.n, size=P, replace=False).astype(np.int32)
         s.set_w(w1)
         _compare_step(s.step(B2), o.step(w1, B2), ties)
-    assert len(ties) <= 1, ties
+    assert not ties, ties   # configs 3-4: no decision may be excused
     s.close()
 
 
