@@ -170,10 +170,10 @@ int pcdn_set_debug(pcdn_ctx *ctx, int on);
  * columns of 129..2048 nonzeros are reduced by one CTA, 128 for mode 3). */
 int pcdn_set_launch(pcdn_ctx *ctx, int mode, int ctas, int heavy_len);
 
-/* Sample-sharded step: data larger than one GPU.  Each rank
- * creates a context over ITS rows (their CSC/CSR, labels / targets); w and the partition stream
- * are replicated.  One PCDN bundle step (Alg.3 l.6-10 with Alg.4) is then, on every rank, for the
- * same device bundle[P] (distinct feature indices; not validated here):
+/* Sample-sharded step: data larger than one
+ * GPU.  Each rank creates a context over ITS rows (their CSC/CSR, labels / targets); w and the
+ * partition stream are replicated.  One PCDN bundle step (Alg.3 l.6-10 with Alg.4) is then, on
+ * every rank, for the same device bundle[P] (distinct feature indices; not validated here):
  *   pcdn_shard_gh          -> gh_out (DEVICE fp64[2P]): sum_i x_ij G_i, sum_i x_ij^2 H_i over the
  *                             local samples (Eq.13 / App. A.2 factors, before the factor c);
  *   caller: sum gh over the ranks (in rank order, for bit-identical results on every rank);
@@ -184,20 +184,40 @@ int pcdn_set_launch(pcdn_ctx *ctx, int mode, int ctas, int heavy_len);
  *                             out[6+q] = the bundle's separable-term change, out[12] = Delta --
  *                             both only if with_l1 (exactly one rank), else 0.  first = 1 for the
  *                             step's first window (folds d'x_i), 0 for later windows;
- *   caller: sum out over the ranks; accept the first q with out[6+q] + c out[q] <= sigma alpha
- *           out[12] (Eq.6); none in the window -> the next window (q0 += 6, first = 0);
- *   pcdn_shard_commit      w_B += alpha d_B (every rank), z and the factors of the local touched
- *                             samples (alpha = 0: a null step, records cleared).  Synchronizes.
- *   pcdn_shard_loss        -> loss_out (host): c sum_i phi_i over the local samples (the caller
- *                             adds ||w||_1 (+ mu/2 ||w||^2) once: Eq.1 at an outer boundary).
+ *   caller: sum out over the ranks (rank order);
+ *   pcdn_shard_decide      the Eq.6 decision of the window from the rank-summed totals tot (DEVICE
+ *                             fp64[13]), on the device with the context's sigma, beta, q_max
+ *                             (pcdn_set_armijo): the first q with out[6+q] + c out[q] <= sigma
+ *                             alpha out[12]; recorded in the context and copied to *out (host):
+ *                             q (-1: none in this window), next (1: run the window at q0 + 6; 0
+ *                             with q = -1: q_max passed, a null step, reading Z10), alpha, LHS,
+ *                             RHS, Delta, and the maintained objective F after the step.
+ *                             PCDN_ERR_NUMERIC for non-finite totals.  Synchronizes;
+ *   pcdn_shard_commit      with the recorded decision: w_B += alpha d_B (every rank), z and the
+ *                             factors of the local touched samples, F += LHS (q = -1: a null
+ *                             step, records cleared).  Synchronizes.
+ * At an outer boundary (reading Z23):
+ *   pcdn_shard_loss        -> loss_out (DEVICE fp64[1]): c sum_i phi_i over the local samples;
+ *   caller: sum loss_out over the ranks (rank order);
+ *   pcdn_shard_objective   F = the summed loss (DEVICE fp64[1]) + ||w||_1 + mu/2 ||w||^2 on the
+ *                             device; becomes the maintained F and is copied to *F_out (host).
  * The kernels never wait on another rank (the caller's collectives sit between the calls).
- * Returns PCDN_ERR_INVALID for null pointers, P outside [1, n], q0 < 0, alpha < 0 / not finite. */
+ * Returns PCDN_ERR_INVALID for null pointers, P outside [1, n], q0 < 0. */
+typedef struct {
+    int32_t q;      /* accepted Armijo index, -1 if none in the window */
+    int32_t next;   /* 1: no candidate passed and q0 + 6 <= q_max -- run the next window */
+    double alpha, lhs, rhs, Delta;
+    double F;       /* maintained objective after the step (before it, for q = -1) */
+} pcdn_shard_decision;
+
 int pcdn_shard_gh(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, double *gh_out);
 int pcdn_shard_direction(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, const double *gh);
 int pcdn_shard_line_search(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, int q0, int first, int with_l1,
                            double *out);
-int pcdn_shard_commit(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, double alpha);
+int pcdn_shard_decide(pcdn_ctx *ctx, const double *tot, int q0, pcdn_shard_decision *out);
+int pcdn_shard_commit(pcdn_ctx *ctx, const int32_t *bundle, int64_t P);
 int pcdn_shard_loss(pcdn_ctx *ctx, double *loss_out);
+int pcdn_shard_objective(pcdn_ctx *ctx, const double *loss_sum, double *F_out);
 
 /* SCDN baseline (Alg.2 Shotgun CDN; reading Z27): with
  * on != 0, pcdn_bundle_step / pcdn_solve run SCDN instead of PCDN -- each feature of a bundle (of

@@ -57,7 +57,7 @@ class _StepOut(C.Structure):
 class _SolveInfo(C.Structure):
     _fields_ = [("outer_iters", C.c_int32), ("status", C.c_int32), ("steps", C.c_int64),
                 ("nnz_processed", C.c_int64), ("touched_total", C.c_int64),
-                ("null_steps", C.c_int64), ("F", C.c_double), ("gap", C.c_double)]
+                ("null_steps", C.c_int64), ("F", C.c_double), ("gap", C.c_double), ("t_steps", C.c_double)]
 
 
 _lib = None
@@ -91,7 +91,7 @@ def lib():
         L.ora_solve.restype = C.c_int
         L.ora_solve.argtypes = [C.POINTER(_Prob), C.c_void_p, C.c_void_p, C.c_int64, C.c_double,
                                 C.c_double, C.c_uint64, C.c_int32, C.c_void_p, C.c_void_p,
-                                C.c_void_p, C.c_int64, C.POINTER(_SolveInfo), C.c_void_p]
+                                C.c_void_p, C.c_int64, C.POINTER(_SolveInfo), C.c_void_p, C.c_int64]
         L.ora_cdn.restype = C.c_int
         L.ora_cdn.argtypes = [C.POINTER(_Prob), C.c_void_p, C.c_void_p, C.c_uint64, C.c_int32,
                               C.c_void_p, C.c_int64, C.POINTER(C.c_double)]
@@ -221,7 +221,9 @@ class Oracle:
         return res
 
     # --- Alg.3 driver ---
-    def solve(self, P, eps=0.0, fstar=1.0, seed=0, max_outer=10, w0=None, trace_cap=None):
+    def solve(self, P, eps=0.0, fstar=1.0, seed=0, max_outer=10, w0=None, trace_cap=None, max_steps=0):
+        """Alg.3 from w0 (default 0).  max_steps > 0 stops after that many bundle steps (a bounded
+        CPU timing sample; rc = BUDGET)."""
         w = np.zeros(self.n) if w0 is None else np.array(w0, dtype=np.float64, copy=True)
         z = np.zeros(self.s)
         b = -(-self.n // int(P))
@@ -233,12 +235,12 @@ class Oracle:
         info = _SolveInfo()
         rc = lib().ora_solve(C.byref(self.pb), _p(w), _p(z), int(P), float(eps), float(fstar),
                              seed & 0xFFFFFFFFFFFFFFFF, int(max_outer), _p(qt), _p(Ft), _p(oF), cap,
-                             C.byref(info), _p(mt))
+                             C.byref(info), _p(mt), int(max_steps))
         ns = min(int(info.steps), cap)
         return dict(rc=rc, w=w, z=z, F=info.F, gap=info.gap, outer=int(info.outer_iters),
                     steps=int(info.steps), nnz=int(info.nnz_processed), touched=int(info.touched_total), null_steps=int(info.null_steps),
                     q_trace=qt[:ns].copy(), F_trace=Ft[:ns].copy(), outer_F=oF[:int(info.outer_iters)].copy(),
-                    margin_trace=mt[:ns].copy())
+                    margin_trace=mt[:ns].copy(), t_steps=float(info.t_steps))
 
     def scdn(self, Pbar, seed=0, max_outer=10, w0=None):
         """Alg.2 (Shotgun CDN), synchronous reading Z27: the F trace has one entry per iteration."""

@@ -40,6 +40,7 @@
  * intrinsics).
  */
 #include <math.h>
+#include <time.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -483,14 +484,18 @@ typedef struct {
     int64_t null_steps;
     double F;
     double gap;
+    double t_steps;   /* wall seconds inside the bundle steps (timing only; the CPU baseline's rate) */
 } ora_solve_info;
 
 /* margin_trace (nullable): per step, the smallest relative margin of its decisions -- the Eq.5
  * branch tests, the accepted Armijo test and the rejected one before it (reading Z22).  A GPU
- * decision may differ from the oracle's only where this is below the tie threshold. */
+ * decision may differ from the oracle's only where this is below the tie threshold.
+ * max_steps > 0: stop after that many bundle steps (a bounded timing sample of the CPU baseline;
+ * the outer iteration in progress is not finished, no outer refresh, rc = ORA_BUDGET). */
 int ora_solve(const ora_prob *pb, double *w, double *z, int64_t P, double eps, double fstar,
               uint64_t seed, int32_t max_outer, int32_t *q_trace, double *F_trace,
-              double *outer_F, int64_t trace_cap, ora_solve_info *info, double *margin_trace)
+              double *outer_F, int64_t trace_cap, ora_solve_info *info, double *margin_trace,
+              int64_t max_steps)
 {
     const int64_t s = pb->s, n = pb->n;
     if (P < 1 || P > n) return ORA_ERR_INVALID;
@@ -505,6 +510,7 @@ int ora_solve(const ora_prob *pb, double *w, double *z, int64_t P, double eps, d
     ora_compute_z(pb, w, z);
     st.F = ora_objective(pb, z, w);
     int64_t steps = 0, nnzp = 0, touched = 0, nulls = 0;
+    double t_steps = 0.0;
     int rc = ORA_BUDGET;
     int32_t k;
     double gap = INFINITY;
@@ -513,8 +519,13 @@ int ora_solve(const ora_prob *pb, double *w, double *z, int64_t P, double eps, d
     for (k = 0; k < max_outer; k++) {
         ora_permutation(seed, k, n, perm);                        /* Alg.3 l.4, Eq.8 */
         for (int64_t t0 = 0; t0 < n; t0 += P) {                   /* Alg.3 l.5 */
+            if (max_steps > 0 && steps >= max_steps) goto done;
             int64_t Pt = (n - t0) < P ? (n - t0) : P;
+            struct timespec ta, tb;
+            clock_gettime(CLOCK_MONOTONIC, &ta);
             int r = ora_bundle_step(pb, &st, perm + t0, Pt, 0, &o);
+            clock_gettime(CLOCK_MONOTONIC, &tb);
+            t_steps += (double)(tb.tv_sec - ta.tv_sec) + 1e-9 * (double)(tb.tv_nsec - ta.tv_nsec);
             if (r != ORA_OK) {
                 rc = r;
                 goto done;
@@ -560,6 +571,7 @@ done:
         info->null_steps = nulls;
         info->F = st.F;
         info->gap = eps > 0.0 ? (st.F - fstar) / fstar : NAN;
+        info->t_steps = t_steps;
     }
     free(st.dx);
     free(st.dxa);

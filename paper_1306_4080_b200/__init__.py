@@ -185,6 +185,21 @@ def pcdn_train_host(col_ptr, row_idx, val, row_ptr, col_idx, csr_val, y, c, loss
     col_idx, csr_val may all be None: the CSR is then built on the device from the CSC."""
     s, n, nnz = int(y.shape[0]), int(col_ptr.shape[0] - 1), int(col_ptr[-1])
     w = np.zeros(n, dtype=np.float64) if w_out is None else w_out
+
+    def _want(a, dt, size, what, optional=False):
+        if a is None and optional:
+            return
+        if not isinstance(a, np.ndarray) or a.dtype != dt or a.ndim != 1 or a.size != size or not a.flags.c_contiguous:
+            raise PCDNError(PCDN_ERR_INVALID, f"pcdn_train_host: {what} must be a contiguous {np.dtype(dt).name}[{size}]")
+
+    _want(col_ptr, np.int64, n + 1, "col_ptr")
+    _want(row_idx, np.int32, nnz, "row_idx")
+    _want(val, np.float32, nnz, "val")
+    _want(y, np.int8, s, "y")
+    _want(row_ptr, np.int64, s + 1, "row_ptr", optional=True)
+    _want(col_idx, np.int32, nnz, "col_idx", optional=True)
+    _want(csr_val, np.float32, nnz, "csr_val", optional=True)
+    _want(w, np.float64, n, "w_out")
     inf = pcdn_solve_info()
     st = lib().pcdn_train_host(s, n, nnz, _ptr(col_ptr), _ptr(row_idx), _ptr(val), _ptr(row_ptr), _ptr(col_idx),
                                _ptr(csr_val), _ptr(y), float(c), int(loss), int(P), float(eps), float(f_star),
@@ -323,6 +338,6 @@ class Solver:
 
 # sample-sharded step (NEXT #2): C-ABI wrappers and the rank-level driver
 from .sharded import (  # noqa: E402,F401
-    ShardedSolver, pcdn_shard_commit, pcdn_shard_direction, pcdn_shard_gh, pcdn_shard_line_search, pcdn_shard_loss,
-    rank_order_sum,
+    ShardedSolver, pcdn_shard_commit, pcdn_shard_decide, pcdn_shard_direction, pcdn_shard_gh, pcdn_shard_line_search,
+    pcdn_shard_loss, pcdn_shard_objective, rank_order_sum,
 )

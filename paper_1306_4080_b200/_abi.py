@@ -41,6 +41,11 @@ class pcdn_solve_info(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class pcdn_shard_decision(C.Structure):
+    _fields_ = [("q", C.c_int32), ("next", C.c_int32), ("alpha", C.c_double), ("lhs", C.c_double),
+                ("rhs", C.c_double), ("Delta", C.c_double), ("F", C.c_double)]
+
+
 P = C.c_void_p
 I64 = C.c_int64
 # name -> (restype, argtypes), exactly the functions declared in include/pcdn.h
@@ -70,8 +75,10 @@ SIGNATURES = {
     "pcdn_shard_gh": (C.c_int, [P, C.c_void_p, C.c_int64, C.c_void_p]),
     "pcdn_shard_direction": (C.c_int, [P, C.c_void_p, C.c_int64, C.c_void_p]),
     "pcdn_shard_line_search": (C.c_int, [P, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_void_p]),
-    "pcdn_shard_commit": (C.c_int, [P, C.c_void_p, C.c_int64, C.c_double]),
-    "pcdn_shard_loss": (C.c_int, [P, C.POINTER(C.c_double)]),
+    "pcdn_shard_decide": (C.c_int, [P, C.c_void_p, C.c_int, C.POINTER(pcdn_shard_decision)]),
+    "pcdn_shard_commit": (C.c_int, [P, C.c_void_p, C.c_int64]),
+    "pcdn_shard_loss": (C.c_int, [P, C.c_void_p]),
+    "pcdn_shard_objective": (C.c_int, [P, C.c_void_p, C.POINTER(C.c_double)]),
     "pcdn_set_profile": (C.c_int, [P, C.c_int]),
     "pcdn_phase_cycles": (C.c_int, [P, P, C.POINTER(C.c_int32)]),
     "pcdn_warp_timeline": (C.c_int, [P, P]),

@@ -640,31 +640,37 @@ int choose_mode(const pcdn_ctx *ctx, int64_t P)
     return mode;
 }
 
-// The side stream that builds the next outer iteration's lists beside the cluster-resident kernel:
-// one per device for the whole process (creating a stream per context cost ~0.2-0.8 ms in the
-// one-call host API); contexts order their own work on it with events.
+// The side stream that builds the next outer iteration's lists beside the cluster-resident kernel.
+// Streams come from a per-device pool of SIDE_POOL, handed out round-robin to contexts (creating a
+// stream per context cost ~0.2-0.8 ms in the one-call host API); a context orders its own work on
+// its side stream with events, so contexts on different pool streams overlap independently (up to
+// SIDE_POOL concurrently active contexts per device; beyond that two contexts share a stream and
+// their list builds queue behind each other -- results are unchanged).
 // set by pcdn_train_host around its pcdn_create call when it built the CSR from the CSC itself
 static thread_local bool g_csr_trusted = false;
 
 static cudaStream_t shared_side_stream()
 {
+    constexpr int SIDE_POOL = 8;
     static std::mutex mu;
-    static cudaStream_t streams[64] = {};
-    static bool tried[64] = {};
+    static cudaStream_t streams[64][SIDE_POOL] = {};
+    static bool tried[64][SIDE_POOL] = {};
+    static unsigned next[64] = {};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
         cudaGetLastError();
         return nullptr;
     }
     std::lock_guard<std::mutex> lock(mu);
-    if (!tried[dev]) {
-        tried[dev] = true;
-        if (cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess) {
+    const unsigned k = next[dev]++ % SIDE_POOL;
+    if (!tried[dev][k]) {
+        tried[dev][k] = true;
+        if (cudaStreamCreateWithFlags(&streams[dev][k], cudaStreamNonBlocking) != cudaSuccess) {
             cudaGetLastError();
-            streams[dev] = nullptr;
+            streams[dev][k] = nullptr;
         }
     }
-    return streams[dev];
+    return streams[dev][k];
 }
 
 // Load every kernel of the library once per process.  Under CUDA's default lazy module loading
@@ -687,7 +693,8 @@ static void preload_kernels()
         res_kernel(LOSS_SQ, true), dense_kernel(LOSS_LOGISTIC), dense_kernel(LOSS_L2SVM), dense_kernel(LOSS_SQ),
         (const void *)k_set_z, (const void *)k_obj_partial, (const void *)k_obj_final, (const void *)k_obj, (const void *)k_prep_lists, (const void *)k_solve_init, (const void *)k_validate,
         (const void *)k_validate_transpose, (const void *)k_check_finite, (const void *)k_sh_gh, (const void *)k_sh_dir,
-        (const void *)k_sh_ls, (const void *)k_sh_ls_long, (const void *)k_sh_ls_final, (const void *)k_sh_commit};
+        (const void *)k_sh_ls, (const void *)k_sh_ls_long, (const void *)k_sh_ls_final, (const void *)k_sh_commit,
+        (const void *)k_sh_decide, (const void *)k_sh_add_loss};
     for (const void *f : fns) {
         cudaFuncAttributes fa;
         if (cudaFuncGetAttributes(&fa, f) != cudaSuccess) cudaGetLastError();
@@ -1454,6 +1461,7 @@ static StepArgs shard_args(pcdn_ctx *ctx, int64_t P)
     a.dk = ctx->at<double>(L.dk);
     a.deltak = ctx->at<double>(L.deltak);
     a.part = ctx->at<double>(L.part);
+    a.F = ctx->at<double>(L.F);
     a.P = P;
     a.status = ctx->at<int>(L.status);
     return a;
@@ -1506,11 +1514,36 @@ int pcdn_shard_line_search(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, int 
     return PCDN_OK;
 }
 
-int pcdn_shard_commit(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, double alpha)
+int pcdn_shard_decide(pcdn_ctx *ctx, const double *tot, int q0, pcdn_shard_decision *out)
 {
-    if (!ctx || !bundle || P < 1 || P > ctx->n || !(alpha >= 0) || !std::isfinite(alpha)) return PCDN_ERR_INVALID;
+    if (!ctx || !tot || q0 < 0) return PCDN_ERR_INVALID;
     PCDN_NEED_TARGETS(ctx);
-    k_sh_commit<<<shard_blocks(ctx->s, SH_NT), SH_NT, 0, ctx->stream>>>(shard_args(ctx, P), bundle, P, alpha);
+    int rc;
+    if ((rc = reset_status(ctx))) return rc;
+    k_sh_decide<<<1, 32, 0, ctx->stream>>>(shard_args(ctx, 1), tot, q0, ctx->at<double>(ctx->L.info));
+    ctx->launches++;
+    CU(cudaGetLastError());
+    if ((rc = readback(ctx))) return rc;
+    const double *v = ctx->hm->info;
+    if (out) {
+        out->q = (int32_t)v[0];
+        out->next = (int32_t)v[1];
+        out->alpha = v[2];
+        out->lhs = v[3];
+        out->rhs = v[4];
+        out->Delta = v[5];
+        out->F = v[6];
+    }
+    if (ctx->hm->status == 3) return set_err(ctx, PCDN_ERR_NUMERIC, "non-finite line-search quantities");
+    return PCDN_OK;
+}
+
+int pcdn_shard_commit(pcdn_ctx *ctx, const int32_t *bundle, int64_t P)
+{
+    if (!ctx || !bundle || P < 1 || P > ctx->n) return PCDN_ERR_INVALID;
+    PCDN_NEED_TARGETS(ctx);
+    k_sh_commit<<<shard_blocks(ctx->s, SH_NT), SH_NT, 0, ctx->stream>>>(shard_args(ctx, P), bundle, P,
+                                                                       ctx->at<double>(ctx->L.info));
     ctx->launches++;
     CU(cudaGetLastError());
     int rc;
@@ -1523,18 +1556,33 @@ int pcdn_shard_loss(pcdn_ctx *ctx, double *loss_out)
 {
     if (!ctx || !loss_out) return PCDN_ERR_INVALID;
     PCDN_NEED_TARGETS(ctx);
-    // c * sum_i phi_i of the local samples (Eq.1 without the separable terms): F with w's terms
-    // removed -- evaluate F(z, w = 0 view) by the objective kernels on the copy slot
+    // c * sum_i phi_i of the local samples (Eq.1 without the separable terms) into loss_out (device)
     const Layout &L = ctx->L;
     k_obj_partial<<<OBJ_NB, 256, 0, ctx->stream>>>(ctx->s, 0, ctx->at<double>(L.z), ctx->y, ctx->at<double>(L.w),
                                                    ctx->loss, ctx->at<double>(L.objp), ctx->t);
-    k_obj_final<<<1, OBJ_NB, 0, ctx->stream>>>(ctx->at<double>(L.objp), ctx->c, 0.0, ctx->at<double>(L.Fcopy), nullptr, -1.0, 0.0,
+    k_obj_final<<<1, OBJ_NB, 0, ctx->stream>>>(ctx->at<double>(L.objp), ctx->c, 0.0, loss_out, nullptr, -1.0, 0.0,
                                                nullptr, nullptr);
     ctx->launches += 2;
     CU(cudaGetLastError());
+    return PCDN_OK;
+}
+
+int pcdn_shard_objective(pcdn_ctx *ctx, const double *loss_sum, double *F_out)
+{
+    if (!ctx || !loss_sum || !F_out) return PCDN_ERR_INVALID;
+    PCDN_NEED_TARGETS(ctx);
+    // ||w||_1 + mu/2 ||w||^2 over the replicated w, then + the rank-summed loss: the maintained F
+    const Layout &L = ctx->L;
+    k_obj_partial<<<OBJ_NB, 256, 0, ctx->stream>>>(0, ctx->n, ctx->at<double>(L.z), ctx->y, ctx->at<double>(L.w),
+                                                   ctx->loss, ctx->at<double>(L.objp), ctx->t);
+    k_obj_final<<<1, OBJ_NB, 0, ctx->stream>>>(ctx->at<double>(L.objp), ctx->c, ctx->mu, ctx->at<double>(L.F), nullptr,
+                                               -1.0, 0.0, nullptr, nullptr);
+    k_sh_add_loss<<<1, 32, 0, ctx->stream>>>(ctx->at<double>(L.F), loss_sum, ctx->at<double>(L.Fcopy));
+    ctx->launches += 3;
+    CU(cudaGetLastError());
     CU(cudaMemcpyAsync(&ctx->hm->Fcopy, ctx->at<double>(L.Fcopy), sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
-    *loss_out = ctx->hm->Fcopy;
+    *F_out = ctx->hm->Fcopy;
     return PCDN_OK;
 }
 

@@ -215,9 +215,52 @@ __global__ void k_sh_ls_final(StepArgs a, const int32_t *__restrict__ bundle, in
     }
 }
 
-// commit with the accepted alpha (0: a null step -- the records are only cleared)
-__global__ void k_sh_commit(StepArgs a, const int32_t *__restrict__ bundle, int64_t P, double alpha)
+// The Eq.6 decision of one window from the rank-summed totals tot[13] (tot[q]: c-free loss changes,
+// tot[6+q]: separable terms, tot[12]: Delta) for candidates alpha = beta^(q0+q): the first q with
+// LHS = tot[6+q] + c tot[q] <= sigma alpha Delta (alpha by repeated multiplication, reading Z11),
+// candidates past q_max not taken (reading Z10).  dec[0] q (-1: none in this window), dec[1]
+// next (1: run the window at q0 + 6), dec[2..6] alpha, LHS, RHS, Delta, the maintained F after
+// the step.  Every rank holds the same totals, so every rank takes the same decision.
+__global__ void k_sh_decide(StepArgs a, const double *__restrict__ tot, int q0, double *dec)
 {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const double Delta = tot[2 * SH_W];
+    double al = 1.0;
+    for (int q = 0; q < q0; q++) al *= a.beta;
+    int qa = -1, bad = 0;
+    double la = 0.0, ra = 0.0, alpha = 0.0;
+    for (int q = 0; q < SH_W && q0 + q <= a.qmax; q++) {
+        const double lhs = tot[SH_W + q] + a.c * tot[q];
+        const double rhs = a.sigma * al * Delta;
+        if (!isfinite(lhs) || !isfinite(Delta)) {
+            bad = 1;
+            break;
+        }
+        if (lhs <= rhs) {
+            qa = q0 + q;
+            alpha = al;
+            la = lhs;
+            ra = rhs;
+            break;
+        }
+        al *= a.beta;
+    }
+    if (bad) atomicMax(a.status, 3);
+    const double F = *a.F;
+    dec[0] = (double)qa;
+    dec[1] = (qa < 0 && !bad && q0 + SH_W <= a.qmax) ? 1.0 : 0.0;
+    dec[2] = alpha;
+    dec[3] = la;
+    dec[4] = ra;
+    dec[5] = Delta;
+    dec[6] = qa >= 0 ? F + la : F;
+}
+
+// commit with the recorded decision (q < 0: a null step -- the records are only cleared) and the
+// maintained F (reading Z23)
+__global__ void k_sh_commit(StepArgs a, const int32_t *__restrict__ bundle, int64_t P, const double *__restrict__ dec)
+{
+    const double alpha = dec[0] >= 0.0 ? dec[2] : 0.0;
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = tid; i < a.s; i += nth) {
         if (a.cnt[i] == 0) continue;
@@ -232,6 +275,18 @@ __global__ void k_sh_commit(StepArgs a, const int32_t *__restrict__ bundle, int6
     for (int64_t wi = tid; wi < (a.s + 31) / 32; wi += nth) a.bits[wi] = 0u;
     if (alpha != 0.0)
         for (int64_t kk = tid; kk < P; kk += nth) a.w[bundle[kk]] += alpha * a.dk[kk];
+    if (tid == 0) *a.F = dec[6];
+}
+
+// F at an outer boundary: the rank-summed c sum_i phi_i plus the separable terms of the replicated
+// w (||w||_1 + mu/2 ||w||^2, by k_obj_partial/k_obj_final over w alone into *F first)
+__global__ void k_sh_add_loss(double *F, const double *__restrict__ loss_sum, double *F_copy)
+{
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        const double v = loss_sum[0] + *F;
+        *F = v;
+        *F_copy = v;
+    }
 }
 
 }  // namespace pcdn

@@ -16,8 +16,9 @@ import ctypes as C
 
 import numpy as np
 
-from . import PCDN_BUDGET, PCDN_ERR_NUMERIC, PCDN_OK, PCDNError, Solver, check, lib, pcdn_permutation
+from . import PCDN_BUDGET, PCDN_OK, Solver, check, lib, pcdn_permutation
 from . import _ptr
+from ._abi import pcdn_shard_decision
 
 W = 6   # candidates per line-search window (pcdn_shard_line_search)
 
@@ -35,19 +36,32 @@ def pcdn_shard_line_search(ctx, bundle, P, q0, first, with_l1, out):
                                                    _ptr(out)))
 
 
-def pcdn_shard_commit(ctx, bundle, P, alpha):
-    return check(ctx, lib().pcdn_shard_commit(ctx, _ptr(bundle), int(P), float(alpha)))
+def pcdn_shard_decide(ctx, tot, q0):
+    """The Eq.6 decision of one window from the rank-summed totals (on the device, with the
+    context's Armijo constants); returns the pcdn_shard_decision."""
+    d = pcdn_shard_decision()
+    check(ctx, lib().pcdn_shard_decide(ctx, _ptr(tot), int(q0), C.byref(d)))
+    return d
 
 
-def pcdn_shard_loss(ctx):
+def pcdn_shard_commit(ctx, bundle, P):
+    return check(ctx, lib().pcdn_shard_commit(ctx, _ptr(bundle), int(P)))
+
+
+def pcdn_shard_loss(ctx, loss_out):
+    return check(ctx, lib().pcdn_shard_loss(ctx, _ptr(loss_out)))
+
+
+def pcdn_shard_objective(ctx, loss_sum):
     v = C.c_double()
-    check(ctx, lib().pcdn_shard_loss(ctx, C.byref(v)))
+    check(ctx, lib().pcdn_shard_objective(ctx, _ptr(loss_sum), C.byref(v)))
     return v.value
 
 
 def rank_order_sum(t, group=None):
-    """Sum of `t` over the ranks of `group`, added in rank order (identical bits on every rank).
-    CPU tensors for gloo, device tensors for NCCL; world 1 (group None) returns t."""
+    """Sum of `t` over the ranks of `group`, added in rank order (identical bits on every rank): a
+    deterministic all-reduce.  gloo takes CPU tensors, NCCL device tensors (the input's device);
+    the result is on t's device.  World 1 (group None) returns t."""
     if group is None:
         return t
     import torch
@@ -63,7 +77,9 @@ def rank_order_sum(t, group=None):
 
 
 class ShardedSolver:
-    """One rank's share of a sample-sharded PCDN solve (the shard's rows; global n)."""
+    """One rank's share of a sample-sharded PCDN solve (the shard's rows; global n).  The Armijo
+    constants (sigma, beta, gamma, q_max keywords) go to the context (pcdn_set_armijo); every
+    decision is taken on the device from the rank-summed totals."""
 
     def __init__(self, shard, group=None, **kw):
         import torch
@@ -75,73 +91,55 @@ class ShardedSolver:
             import torch.distributed as dist
             self.rank = dist.get_rank(group)
         self.sol = Solver(shard, **kw)
-        self.ctx, self.n, self.c = self.sol.ctx, self.sol.n, self.sol.c
-        self.mu = 0.0
-        self.beta, self.sigma, self.qmax = 0.5, 0.01, 50
+        self.ctx, self.n = self.sol.ctx, self.sol.n
         dev = self.sol.device
         self.gh = torch.zeros(2 * self.n, dtype=torch.float64, device=dev)
         self.out = torch.zeros(2 * W + 1, dtype=torch.float64, device=dev)
+        self.loss = torch.zeros(1, dtype=torch.float64, device=dev)
         self.F = self.objective()
 
     def set_elastic(self, mu):
         self.sol.set_elastic(mu)
-        self.mu = float(mu)
         self.F = self.objective()
 
     def objective(self):
-        """Eq.1: the ranks' local losses summed in rank order, plus the separable terms of w."""
-        w = self.sol.w().cpu().numpy()
-        loss = rank_order_sum(self.torch.tensor([pcdn_shard_loss(self.ctx)], dtype=self.torch.float64),
-                              self.group)
-        return float(loss[0]) + float(np.sum(np.abs(w))) + 0.5 * self.mu * float(np.dot(w, w))
+        """Eq.1 at an outer boundary: the ranks' local losses (device) summed in rank order, then F
+        with the separable terms of w on the device (it becomes the maintained F)."""
+        pcdn_shard_loss(self.ctx, self.loss)
+        return pcdn_shard_objective(self.ctx, rank_order_sum(self.loss, self.group))
 
     def step(self, bundle):
-        """One bundle step; returns (q, alpha, lhs) -- q = -1 for a null step (reading Z10)."""
+        """One bundle step; returns the pcdn_shard_decision (q = -1: a null step, reading Z10)."""
         P = int(bundle.numel())
         gh = self.gh[:2 * P]
         pcdn_shard_gh(self.ctx, bundle, P, gh)
         gh.copy_(rank_order_sum(gh, self.group))
         pcdn_shard_direction(self.ctx, bundle, P, gh)
-        q0, first, qacc, alpha_acc, lhs_acc = 0, 1, -1, 0.0, 0.0
-        while q0 <= self.qmax:
+        q0, first = 0, 1
+        while True:
             pcdn_shard_line_search(self.ctx, bundle, P, q0, first, self.rank == 0, self.out)
-            tot = rank_order_sum(self.out, self.group).cpu().numpy()
-            Delta = tot[2 * W]
-            al = self.beta ** 0
-            for _ in range(q0):
-                al *= self.beta
-            for q in range(W):
-                lhs = tot[W + q] + self.c * tot[q]
-                if not (np.isfinite(lhs) and np.isfinite(Delta)):
-                    raise PCDNError(PCDN_ERR_NUMERIC, "non-finite line-search quantities")
-                if q0 + q > self.qmax:
-                    break
-                if lhs <= self.sigma * al * Delta:
-                    qacc, alpha_acc, lhs_acc = q0 + q, al, lhs
-                    break
-                al *= self.beta
-            if qacc >= 0:
+            dec = pcdn_shard_decide(self.ctx, rank_order_sum(self.out, self.group), q0)
+            if dec.q >= 0 or not dec.next:
                 break
-            q0 += W
-            first = 0
-        pcdn_shard_commit(self.ctx, bundle, P, alpha_acc)
-        if qacc >= 0:
-            self.F += lhs_acc
-        return qacc, alpha_acc, lhs_acc
+            q0, first = q0 + W, 0
+        pcdn_shard_commit(self.ctx, bundle, P)
+        self.F = dec.F
+        return dec
 
     def solve(self, P, seed=0, max_outer=10, eps=0.0, fstar=None, trace=False):
-        """Alg.3 with the Eq.14 stop test at outer boundaries (F refreshed there, reading Z23)."""
+        """Alg.3 with the Eq.14 stop test at outer boundaries (F refreshed there, reading Z23).  The
+        stop test compares the device-computed F with F* (the same value on every rank)."""
         torch = self.torch
         perm = torch.empty(self.n, dtype=torch.int32, device=self.sol.device)
         qs, Fs, steps, status, outer = [], [], 0, PCDN_BUDGET, 0
         for k in range(max_outer):
             pcdn_permutation(self.ctx, seed, k, perm)
             for t0 in range(0, self.n, P):
-                q, _, _ = self.step(perm[t0:min(t0 + P, self.n)])
+                dec = self.step(perm[t0:min(t0 + P, self.n)])
                 steps += 1
                 if trace:
-                    qs.append(q)
-                    Fs.append(self.F)
+                    qs.append(dec.q)
+                    Fs.append(dec.F)
             self.F = self.objective()
             outer = k + 1
             if eps > 0 and fstar is not None and (self.F - fstar) / fstar <= eps:

@@ -858,3 +858,101 @@ def test_csr_csc_consistency_check(pk, corrupt):
     with pytest.raises(pk.PCDNError) as ei:
         pk.Solver(prob)
     assert ei.value.status == pk.PCDN_ERR_INVALID
+
+
+# ----------------------------------------------------------------------------- invalid inputs
+def test_train_host_refuses_broken_csc_before_building_csr(pk):
+    """pcdn_train_host with csr_* = None builds the CSR from the CSC on the device: a CSC whose
+    col_ptr is not monotone, or whose row indices are out of range, is refused with
+    PCDN_ERR_INVALID before the pair build runs (no write past the nnz-sized buffers, no crash),
+    and the process's CUDA context stays usable."""
+    prob = synth.tiny(41, 30, 3, density=0.5, c=2.0, P=2)
+    cp = np.ascontiguousarray(prob.col_ptr, dtype=np.int64)
+    ri = np.ascontiguousarray(prob.row_idx, dtype=np.int32)
+    va = np.ascontiguousarray(prob.val, dtype=np.float32)
+    y = np.ascontiguousarray(prob.y, dtype=np.int8)
+    nnz = int(cp[-1])
+    bad = cp.copy()
+    bad[1] = nnz + 7          # col_ptr[1] beyond nnz: not monotone, out of range
+    for cpa, ria in ((bad, ri), (cp, np.where(np.arange(nnz) == 3, prob.s + 1000, ri).astype(np.int32))):
+        with pytest.raises(pk.PCDNError) as ei:
+            pk.pcdn_train_host(cpa, ria, va, None, None, None, y, prob.c, prob.loss, 2, 0.0, 1.0, 1, 2)
+        assert ei.value.status == pk.PCDN_ERR_INVALID
+    # wrong dtype / length of an array: refused by the binding
+    with pytest.raises(pk.PCDNError) as ei:
+        pk.pcdn_train_host(cp, ri.astype(np.int64), va, None, None, None, y, prob.c, prob.loss, 2, 0.0, 1.0, 1, 2)
+    assert ei.value.status == pk.PCDN_ERR_INVALID
+    st, inf, w = pk.pcdn_train_host(cp, ri, va, None, None, None, y, prob.c, prob.loss, 2, 0.0, 1.0, 1, 2)
+    assert st == pk.PCDN_BUDGET
+    ref = oracle.Oracle(prob).solve(2, seed=1, max_outer=2)
+    assert np.max(np.abs(w - ref["w"])) <= 1e-9
+
+
+@pytest.mark.parametrize("corrupt", ["col_idx_out_of_range", "row_ptr_past_nnz"])
+def test_create_refuses_out_of_range_csr(pk, corrupt):
+    """A CSR with a column index far out of range or a row_ptr beyond nnz is refused by k_validate
+    with PCDN_ERR_INVALID; the transpose check that runs after it reads nothing out of bounds (it
+    exits when the status is raised), so the context creation fails cleanly and the device stays
+    usable for the next context."""
+    prob = synth.tiny(43, 40, 12, density=0.3, c=2.0, P=3)
+    if corrupt == "col_idx_out_of_range":
+        prob.col_idx = prob.col_idx.copy()
+        prob.col_idx[5] = prob.n + 1000
+    else:
+        prob.row_ptr = prob.row_ptr.copy()
+        prob.row_ptr[7:] = prob.row_ptr[7:] + 10 ** 6
+    with pytest.raises(pk.PCDNError) as ei:
+        pk.Solver(prob)
+    assert ei.value.status == pk.PCDN_ERR_INVALID
+    good = synth.tiny(43, 40, 12, density=0.3, c=2.0, P=3)
+    s = _solver(pk, good)
+    r = s.solve(3, seed=1, max_outer=2, trace=True)
+    _compare_solve(r, oracle.Oracle(good).solve(3, seed=1, max_outer=2), s.w().cpu().numpy(), "after refusal")
+    s.close()
+
+
+# ----------------------------------------------------------------------------- non-default Armijo constants
+ARMIJO_ND = dict(sigma=0.3, beta=0.7, gamma=0.5, q_max=80)
+
+
+@pytest.mark.parametrize("loss", [LOSS_LOGISTIC, LOSS_L2SVM])
+@pytest.mark.parametrize("launch", [(0, 0, 0), (1, 4, 0), (1, 16, 2), (2, 0, 0), (2, 3, 1), (3, 0, 0), (3, 16, 1),
+                                    (5, 0, 0), (5, 3, 2)])
+def test_nondefault_armijo_parity(pk, loss, launch):
+    """pcdn_set_armijo(sigma=0.3, beta=0.7, gamma=0.5, q_max=80) (Eq.6-7, PAPER.md:113-121) in every
+    launch mode: steps from injected states (g, h, d, Delta with the gamma term, T, dx, q, alpha =
+    0.7^q, LHS) and short solves against the oracle with the same constants."""
+    rng = np.random.default_rng(55 + loss)
+    ties = []
+    for case in (0, 2, 4):
+        prob = synth.tiny(loss=loss, c=3.0, P=5, **TINY[case])
+        s = pk.Solver(prob, **ARMIJO_ND)
+        if launch[0] or launch[1] or launch[2]:
+            s.set_launch(*launch)
+        o = oracle.Oracle(prob, sigma=0.3, beta=0.7, gamma=0.5, qmax=80)
+        for rep in range(2):
+            w = _random_state(rng, prob.n, scale=0.5 * (rep + 1))
+            for B in _step_cases(prob, rng, nb=3):
+                s.set_w(w)
+                _compare_step(s.step(B), o.step(w, B), ties)
+        s.reset()
+        gs = s.solve(5, seed=7, max_outer=5, trace=True)
+        os_ = o.solve(5, seed=7, max_outer=5)
+        _compare_solve(gs, os_, s.w().cpu().numpy(), f"armijo {launch} case {case}")
+        s.close()
+    assert len(ties) <= 2, ties
+
+
+@pytest.mark.parametrize("loss", [LOSS_LOGISTIC, LOSS_L2SVM])
+def test_nondefault_armijo_dense_kernel(pk, loss):
+    """The dense row-block kernel (mode 4, speculative commit alpha_s = beta^{previous q}) with
+    sigma=0.3, beta=0.7, gamma=0.5: a solve whose accepted q varies, against the oracle."""
+    prob = synth.tiny(31, 40, 200, density=1.0, loss=loss, c=10.0, P=50)
+    s = pk.Solver(prob, **ARMIJO_ND)
+    s.set_launch(4, 3, 0)
+    o = oracle.Oracle(prob, sigma=0.3, beta=0.7, gamma=0.5, qmax=80)
+    gs = s.solve(50, seed=3, max_outer=4, trace=True)
+    os_ = o.solve(50, seed=3, max_outer=4)
+    assert np.unique(os_["q_trace"]).size >= 2
+    _compare_solve(gs, os_, s.w().cpu().numpy(), "armijo dense", ftrace_rtol=1e-7)
+    s.close()

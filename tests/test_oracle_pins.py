@@ -436,6 +436,175 @@ def test_permutation_pairwise_independence(oracle_mod):
     assert np.all(np.diag(cnt) == 0)
 
 
+def np_mix64(x):
+    """SplitMix64's 64-bit finalizer (reading Z2), numpy uint64 (wrapping arithmetic)."""
+    x = np.asarray(x, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        x = x ^ (x >> np.uint64(30))
+        x = x * np.uint64(0xBF58476D1CE4E5B9)
+        x = x ^ (x >> np.uint64(27))
+        x = x * np.uint64(0x94D049BB133111EB)
+        x = x ^ (x >> np.uint64(31))
+    return x
+
+
+def np_permutation(seed, k, n):
+    """pi_k written out from DESIGN.md reading Z2, independently of oracle/: an 8-round balanced
+    Feistel network on 2*hb bits, hb = ceil(ceil(log2 n) / 2) (>= 1), keyed by
+    kk = mix64(mix64(seed ^ 0x6A09E667F3BCC909) ^ k) with round keys mix64(kk + (r+1) * golden64),
+    round function (L, R) -> (R, L ^ (mix64(key_r ^ R) & mask)), then cycle walking (re-encrypt
+    until the value is < n).  Vectorised over all positions t."""
+    bits = 0
+    while bits < 63 and (1 << bits) < n:
+        bits += 1
+    hb = max(1, (bits + 1) // 2)
+    mask = np.uint64((1 << hb) - 1)
+    kk = int(np_mix64(np_mix64(np.uint64((seed ^ 0x6A09E667F3BCC909) & (2**64 - 1))) ^ np.uint64(k)))
+    keys = [np_mix64(np.uint64((kk + (r + 1) * 0x9E3779B97F4A7C15) & (2**64 - 1))) for r in range(8)]
+
+    def enc(x):
+        L, R = x >> np.uint64(hb), x & mask
+        for r in range(8):
+            L, R = R, L ^ (np_mix64(keys[r] ^ R) & mask)
+        return (L << np.uint64(hb)) | R
+
+    x = enc(np.arange(n, dtype=np.uint64))
+    bad = np.nonzero(x >= np.uint64(n))[0]
+    while bad.size:
+        x[bad] = enc(x[bad])
+        bad = bad[x[bad] >= np.uint64(n)]
+    return x.astype(np.int64)
+
+
+def test_permutation_matches_independent_feistel(oracle_mod):
+    """Reading Z2 pinned against an independent numpy implementation of the documented
+    construction (not a call into oracle/), including a seed >= 2^63 and n = 10^6."""
+    for seed, k, n in ((0, 0, 1), (0, 0, 2), (3, 1, 5), (7, 3, 64), (12345, 7, 1000), (2**63 + 5, 11, 4097),
+                       (1, 2, 65537), (2, 0, 1000000)):
+        np.testing.assert_array_equal(oracle_mod.permutation(seed, k, n), np_permutation(seed, k, n),
+                                      err_msg=f"seed={seed} k={k} n={n}")
+
+
+def test_permutation_known_answer_vectors(oracle_mod):
+    """tests/golden/perm_kat.json (scripts/make_perm_kat.py, from oracle/ when it was pinned):
+    the oracle still produces the stored vectors, up to n = 2*10^7 (config 5); the numpy
+    re-implementation agrees with them where it is cheap."""
+    import hashlib
+    kat = json.load(open(os.path.join(GOLD, "perm_kat.json")))
+    for c in kat["cases"]:
+        seed, k, n = int(c["seed"]), c["k"], c["n"]
+        pi = oracle_mod.permutation(seed, k, n)
+        assert pi[:16].tolist() == c["head"] and pi[-4:].tolist() == c["tail"], (seed, k, n)
+        assert hashlib.sha256(pi.astype("<i4").tobytes()).hexdigest() == c["sha256"], (seed, k, n)
+        if n <= 50000:
+            assert np_permutation(seed, k, n)[:16].tolist() == c["head"]
+
+
+# ------------------------------------------------------------------ non-default Armijo constants
+ARMIJO = [(0.01, 0.5, 0.0), (0.3, 0.7, 0.5), (0.1, 0.9, 0.9)]
+
+
+@pytest.mark.parametrize("loss", LOSSES)
+@pytest.mark.parametrize("gamma", [0.3, 0.9])
+def test_delta_gamma_term_at_zero(oracle_mod, loss, gamma):
+    """Eq.7 with gamma > 0.  At w = 0 every coordinate of Eq.5's d lies on one
+    side of the kink (d_j = -(g_j+1)/h_j >= 0, -(g_j-1)/h_j <= 0, or 0), so the proof of Lemma 1(c)
+     holds with equality: Delta = (gamma - 1) sum_j h_j d_j^2.  Both sides from
+    independent numpy closed forms at w = 0: g = -(c/2) X'y, h = (c/4) lambda (LR); g = -2c X'y,
+    h = 2c lambda (SVM).  A dropped or sign-flipped gamma term fails this."""
+    for seed in range(4):
+        p = synth.tiny(300 + seed, 40, 12, density=0.4, loss=loss, c=float(1 + 2 * seed))
+        X = p.dense()
+        yv = p.y.astype(np.float64)
+        lam = np.sum(X ** 2, axis=0)
+        if loss == LOSS_LOGISTIC:
+            g, h = -(p.c / 2) * (X.T @ yv), (p.c / 4) * lam
+        else:
+            g, h = -2 * p.c * (X.T @ yv), 2 * p.c * lam
+        h = np.maximum(h, 1e-12)
+        d = np.where(g + 1 <= 0, -(g + 1) / h, np.where(g - 1 >= 0, -(g - 1) / h, 0.0))
+        o = oracle_mod.Oracle(p, gamma=gamma)
+        B = np.arange(p.n)
+        r = o.step(np.zeros(p.n), B)
+        want = (gamma - 1) * np.sum(h * d * d)
+        assert np.any(d != 0)
+        assert math.isclose(r["Delta"], want, rel_tol=1e-12, abs_tol=1e-14), (r["Delta"], want)
+        # and Lemma 1(c) as an inequality from a random state
+        w = np.random.default_rng(seed).normal(size=p.n) * 0.4
+        r = o.step(w, B)
+        assert r["Delta"] <= (gamma - 1) * np.sum(r["h"] * r["d"] ** 2) + 1e-12 * (1 + abs(r["Delta"]))
+
+
+@pytest.mark.parametrize("loss", LOSSES)
+@pytest.mark.parametrize("sigma,beta,gamma", ARMIJO)
+def test_line_search_nondefault_constants(oracle_mod, loss, sigma, beta, gamma):
+    """Eq.6 with non-default sigma, beta, gamma: the incremental decision (Eq.12)
+    equals the direct one, the accepted alpha = beta^q (repeated multiplication, Z11) passes and
+    the previous candidate fails when re-checked with an independent numpy F, and Delta includes
+    gamma sum h d^2."""
+    rng = np.random.default_rng(int(sigma * 100) + int(beta * 10) + loss)
+    checked = 0
+    for seed in range(20):
+        Xc = rng.normal(size=(30, 2)) @ rng.normal(size=(2, 12)) + 0.05 * rng.normal(size=(30, 12))
+        p = synth.from_dense(Xc, np.where(rng.random(30) < 0.5, 1, -1), c=float(rng.choice([3, 30])), loss=loss)
+        X = p.dense()
+        o = oracle_mod.Oracle(p, sigma=sigma, beta=beta, gamma=gamma)
+        w = rng.normal(size=p.n) * 0.5
+        B = rng.choice(p.n, size=int(rng.integers(2, p.n + 1)), replace=False)
+        r0, r1 = o.step(w, B, mode=0), o.step(w, B, mode=1)
+        assert r0["rc"] == 0 and r0["q"] == r1["q"]
+        Fw = np_F(p, w, X)
+        # Delta: g d + gamma h d^2 + |w+d| - |w| over the bundle, g and h from numpy
+        gn = np_grad(p, w, X)[B]
+        Delta = np.sum(gn * r0["d"] + gamma * r0["h"] * r0["d"] ** 2 + np.abs(w[B] + r0["d"]) - np.abs(w[B]))
+        assert math.isclose(r0["Delta"], Delta, rel_tol=1e-9, abs_tol=1e-9)
+
+        def alpha(q):
+            a = 1.0
+            for _ in range(q):
+                a *= beta
+            return a
+
+        def dec(q):
+            wn = w.copy()
+            wn[B] += alpha(q) * r0["d"]
+            return np_F(p, wn, X) - Fw, sigma * alpha(q) * r0["Delta"]
+
+        assert r0["alpha"] == alpha(r0["q"])
+        lhs, rhs = dec(r0["q"])
+        assert lhs <= rhs + 1e-10 * (1 + abs(lhs))
+        if r0["q"] > 0:
+            lhs, rhs = dec(r0["q"] - 1)
+            assert lhs > rhs - 1e-10 * (1 + abs(lhs))
+            checked += 1
+    assert checked >= 3
+
+
+@pytest.mark.parametrize("loss", LOSSES)
+@pytest.mark.parametrize("sigma,beta,gamma", ARMIJO)
+def test_theorem1_bound_nondefault_constants(oracle_mod, loss, sigma, beta, gamma):
+    """Theorem 1 with reading Z14's corrected constant and the
+    paper's (1 - sigma + sigma gamma) factor: alpha >= min(1, beta * 2 h_min (1 - sigma + sigma
+    gamma) / (theta c sum_{j in B} lambda_j)) for non-default sigma, beta, gamma."""
+    theta = 0.25 if loss == LOSS_LOGISTIC else 2.0
+    rng = np.random.default_rng(170 + loss)
+    for seed in range(40):
+        X = rng.normal(size=(30, 3)) @ rng.normal(size=(3, 10)) + 0.05 * rng.normal(size=(30, 10))
+        y = np.where(rng.random(30) < 0.5, 1, -1)
+        c = float(rng.choice([0.1, 1, 10, 100]))
+        p = synth.from_dense(X, y, c=c, loss=loss)
+        lam = np.sum(p.dense() ** 2, axis=0)
+        w = rng.normal(size=10) * 0.1
+        B = rng.choice(10, size=int(rng.integers(2, 11)), replace=False)
+        r = oracle_mod.Oracle(p, sigma=sigma, beta=beta, gamma=gamma).step(w, B)
+        nz = r["d"] != 0
+        if not nz.any():
+            continue
+        hmin = np.min(r["h"][nz])
+        bound = min(1.0, beta * 2 * hmin * (1 - sigma + sigma * gamma) / (theta * c * np.sum(lam[B])))
+        assert r["alpha"] >= bound * (1 - 1e-12)
+
+
 # ------------------------------------------------------------------ solve (Alg.3)
 def test_one_dimensional_closed_forms(oracle_mod):
     """s=1,x=1,y=+1: LR w*=ln(c-1), F*=c ln(c/(c-1)) + ln(c-1); SVM w*=1-1/(2c), F*=1-1/(4c),
