@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpcdn.so")
+# PCDN_LIB (A/B measurements of prebuilt variants): another build of the same library, e.g. under scratch/
+LIB_PATH = os.environ.get("PCDN_LIB") or os.path.join(HERE, "libpcdn.so")
 
 PCDN_OK, PCDN_ERR_INVALID, PCDN_BUDGET, PCDN_ERR_NUMERIC, PCDN_ERR_CUDA, PCDN_ERR_NOMEM = 0, 1, 2, 3, 4, 5
 PCDN_LOSS_LOGISTIC, PCDN_LOSS_L2SVM, PCDN_LOSS_SQUARED = 0, 1, 2

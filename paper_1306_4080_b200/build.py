@@ -11,6 +11,9 @@ ROOT = os.path.dirname(HERE)
 SRC = [os.path.join(HERE, "csrc", "pcdn_api.cu")]
 DEPS = SRC + sorted(glob.glob(os.path.join(HERE, "csrc", "*.cuh"))) + [os.path.join(ROOT, "include", "pcdn.h"), __file__]
 LIB = os.path.join(HERE, "libpcdn.so")
+# the same library with the sparse kernel's profiling instrumentation (-DPCDN_PROFILE=1), for the
+# profiling scripts (loaded through PCDN_LIB); never the product path
+LIB_PROF = os.path.join(HERE, "libpcdn_prof.so")
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17",
@@ -28,15 +31,17 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    stale = force or not os.path.exists(LIB) or any(os.path.getmtime(d) > os.path.getmtime(LIB) for d in DEPS)
+def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
+    lib = LIB_PROF if profile else LIB
+    stale = force or not os.path.exists(lib) or any(os.path.getmtime(d) > os.path.getmtime(lib) for d in DEPS)
     if stale:
-        tmp = LIB + f".tmp{os.getpid()}"
-        cmd = [nvcc()] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-o", tmp] + SRC
+        tmp = lib + f".tmp{os.getpid()}"
+        cmd = [nvcc()] + NVCC_FLAGS + (["-DPCDN_PROFILE=1"] if profile else []) + \
+              (["-Xptxas", "-v"] if verbose else []) + ["-o", tmp] + SRC
         subprocess.check_call(cmd)
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, profile="--profile" in sys.argv))

@@ -556,7 +556,7 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
         cudaLaunchConfig_t cfg{};
         const bool sparse = mode != 5;
         cfg.gridDim = dim3(mode == 1 ? ctx->Gc : ctx->G);
-        cfg.blockDim = dim3(NT);
+        cfg.blockDim = dim3(sparse ? SNT : NT);
         cfg.dynamicSmemBytes = sparse ? sizeof(SpSmem) : ctx->smem;
         cfg.stream = ctx->stream;
         cudaLaunchAttribute at[2];
@@ -720,7 +720,7 @@ int configure_launch(pcdn_ctx *ctx)
     CU(cudaFuncSetAttribute(kc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     int occ = 0, occs = 0;
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kg, NT, ctx->smem));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occs, ks, NT, sizeof(SpSmem)));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occs, ks, SNT, sizeof(SpSmem)));
     if (occs < occ) occ = occs;   // one grid size serves both grid kernels
     if (occ < 1) return set_err(ctx, PCDN_ERR_CUDA, "step kernel cannot be resident (smem %zu)", ctx->smem);
     int maxg = ctx->num_sms * occ;
@@ -730,7 +730,7 @@ int configure_launch(pcdn_ctx *ctx)
     {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(16);
-        cfg.blockDim = dim3(NT);
+        cfg.blockDim = dim3(SNT);
         cfg.dynamicSmemBytes = sizeof(SpSmem);
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;

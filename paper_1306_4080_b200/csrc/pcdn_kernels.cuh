@@ -180,17 +180,25 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 
 // Software grid barrier for a cooperative launch (all CTAs co-resident).  `target`
 // advances by gridDim.x per barrier; the counter only grows within a launch.
+__device__ __forceinline__ void bar_arrive_gpu(unsigned long long *ctr)
+{
+    __threadfence();          // release: the CTA's writes (ordered by the bar.sync before it)
+    atomicAdd(ctr, 1ULL);
+}
+__device__ __forceinline__ void bar_wait_gpu(const unsigned long long *ctr, unsigned long long target)
+{
+    const long long t0 = clock64();
+    while (ld_acquire(ctr) < target) {   // acquire: no trailing fence needed
+        if (clock64() - t0 > 8000000000LL) __trap();   // a broken protocol: fail, do not hang
+    }
+}
 __device__ __forceinline__ void grid_sync(unsigned long long *ctr, unsigned long long &target)
 {
     target += gridDim.x;
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();          // release: the CTA's writes (ordered by the bar.sync above)
-        atomicAdd(ctr, 1ULL);
-        const long long t0 = clock64();
-        while (ld_acquire(ctr) < target) {   // acquire: no trailing fence needed
-            if (clock64() - t0 > 8000000000LL) __trap();   // a broken protocol: fail, do not hang
-        }
+        bar_arrive_gpu(ctr);
+        bar_wait_gpu(ctr, target);
     }
     __syncthreads();
 }
@@ -210,19 +218,11 @@ struct GridSync {
     {
         target += gridDim.x;
         __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(ctr, 1ULL);
-        }
+        if (threadIdx.x == 0) bar_arrive_gpu(ctr);
     }
     __device__ __forceinline__ void wait()
     {
-        if (threadIdx.x == 0) {
-            const long long t0 = clock64();
-            while (ld_acquire(ctr) < target) {
-                if (clock64() - t0 > 8000000000LL) __trap();
-            }
-        }
+        if (threadIdx.x == 0) bar_wait_gpu(ctr, target);
         __syncthreads();
     }
 };
@@ -1176,6 +1176,7 @@ struct RowReg {
     int yi;
     int has_dx;  // 0 when the sample had > NREG records (folded by a warp into dxg)
     double zi, dx;
+    int64_t r0, r1;   // the sample's CSR segment (sparse kernel)
 };
 
 // ------------------------------------------------------------------------------------

@@ -33,9 +33,27 @@
 
 namespace pcdn {
 
-constexpr int SP_SHORT = 8;     // columns with <= SP_SHORT nonzeros are reduced by one lane
+// Profiling instrumentation (phase cycles of CTA 0 for pcdn_set_profile(ctx, 1); per-CTA phase
+// sums for mode 2) is compiled in only with -DPCDN_PROFILE=1 (a separate build, loaded through
+// PCDN_LIB by the profiling scripts): even as untaken branches it cost the production kernel
+// registers and ~5 us per config-5 step.
+#ifndef PCDN_PROFILE
+#define PCDN_PROFILE 0
+#endif
+
+// CTA shape of the sparse kernel: 384 threads per SM (one CTA per SM) leave each thread up to 168
+// registers -- at 512 threads the kernel's live state spilled (config 5: 25.7 us per step at 512,
+// 25.5 at 256, 25.2 at 384)
+#ifndef PCDN_SNT
+#define PCDN_SNT 384
+#endif
+constexpr int SNT = PCDN_SNT;
+constexpr int SNW = SNT / 32;
+
+constexpr int SP_SHORT = 4;     // columns with <= SP_SHORT nonzeros are reduced by one lane
 constexpr int SP_CH = 256;      // default heavy_len of the sparse kernel: longer columns go in chunks
 constexpr int SP_FOLD = 4;      // record loads of one sample in flight together in the fold
+constexpr int SP_CB = 4;        // samples / positions of a thread with their loads in flight together (commit)
 
 struct SpPlan {
     int64_t c0, c1;     // the step's chunks [c0, c1) of cdesc
@@ -44,13 +62,14 @@ struct SpPlan {
 
 struct SpSmem {
     SpPlan plan[2];   // this and the next step (by step parity), computed a step ahead
-    double red[NW][32];
+    double red[SNW][32];
     double tot[32];
-    int64_t scan_w[NW];
+    int64_t scan_w[SNW];
     int64_t nT;
     double F;
     long long cnt[4];
     long long pacc[16];
+    long long cprof[16];   // profiling mode 2: this CTA's sums, copied out at the end of the launch
     int dec_q, dec_bad;
     double dec_alpha, dec_lhs, dec_rhs, dec_Delta, dec_nT;
     double fd[FMAX];
@@ -93,7 +112,7 @@ __device__ __forceinline__ void sp_store_dir(const StepArgs &a, int64_t k, const
 // warp: g/h over nonzeros [p0, p1) then, for d != 0, the records (a column of <= heavy_len or a chunk)
 __device__ __forceinline__ void sp_scatter(const StepArgs &a, int64_t p0, int64_t p1, int lane, double d)
 {
-    constexpr int B = 8;
+    constexpr int B = 4;
     for (int64_t pb = p0 + lane; pb < p1; pb += 32 * B) {
         int32_t ri[B];
         uint32_t sl[B];
@@ -114,33 +133,144 @@ __device__ __forceinline__ void sp_scatter(const StepArgs &a, int64_t p0, int64_
     }
 }
 
-// fold of sample i's records: the written slots of its CSR segment [r0, r1), ascending; up to
-// SP_FOLD slots of a word are loaded together (static register indices), summed in slot order
+// A warp's range [p0, p1) of at most SP_WR nonzeros per lane, held in registers from the gather to
+// the scatter: load (row, slot, value), gather the factors, reduce (lane order, fixed xor tree).
+constexpr int SP_WR = 8;
+struct WarpRange {
+    int32_t ri[SP_WR];
+    uint32_t sl[SP_WR];
+    float xv[SP_WR];
+};
+__device__ __forceinline__ void sp_range_gh(const StepArgs &a, int64_t p0, int64_t p1, int lane, WarpRange &r,
+                                            double &gs, double &hs)
+{
+#pragma unroll
+    for (int e = 0; e < SP_WR; e++) {
+        const int64_t p = p0 + lane + 32 * e;
+        r.ri[e] = -1;
+        r.sl[e] = 0;
+        r.xv[e] = 0.f;
+        if (p < p1) {
+            r.ri[e] = __ldg(&a.row_idx[p]);
+            r.sl[e] = __ldg(&a.cslot[p]);
+            r.xv[e] = __ldg(&a.val[p]);
+        }
+    }
+    double2 cf[SP_WR];
+#pragma unroll
+    for (int e = 0; e < SP_WR; e++) cf[e] = r.ri[e] >= 0 ? ldcg(&a.coef[r.ri[e]]) : make_double2(0.0, 0.0);
+    double g = 0.0, h = 0.0;
+#pragma unroll
+    for (int e = 0; e < SP_WR; e++) {
+        if (r.ri[e] >= 0) {
+            const double x = (double)r.xv[e];
+            g += x * cf[e].x;
+            h += (x * x) * cf[e].y;
+        }
+    }
+    gs = warp_sum(g);
+    hs = warp_sum(h);
+}
+__device__ __forceinline__ void sp_range_scatter(const StepArgs &a, const WarpRange &r, double d)
+{
+#pragma unroll
+    for (int e = 0; e < SP_WR; e++)
+        if (r.ri[e] >= 0) sp_emit(a, r.ri[e], r.sl[e], d * (double)r.xv[e]);
+}
+
+// fold of sample i's records: the written slots of its CSR segment [r0, r1), ascending.  The first
+// three words of the segment's written-slot bitmap are loaded together (a row of <= 65 nonzeros
+// needs no more), then up to SP_FOLD slots of a word at a time (static register indices), summed
+// in slot order.
+__device__ __forceinline__ double sp_fold_word(const StepArgs &a, int64_t wd, uint32_t m)
+{
+    double dx = 0.0;
+    while (m) {
+        uint32_t sl[SP_FOLD];
+#pragma unroll
+        for (int r = 0; r < SP_FOLD; r++) {
+            sl[r] = m ? (uint32_t)(wd * 32 + __ffs(m) - 1) : 0xffffffffu;
+            m &= m - 1;
+        }
+        double v[SP_FOLD];
+#pragma unroll
+        for (int r = 0; r < SP_FOLD; r++) v[r] = sl[r] != 0xffffffffu ? ldcg(&a.rv[sl[r]]) : 0.0;
+#pragma unroll
+        for (int r = 0; r < SP_FOLD; r++)
+            if (sl[r] != 0xffffffffu) dx += v[r];
+    }
+    return dx;
+}
+__device__ __forceinline__ uint32_t sp_word_mask(int64_t wd, int64_t r0, int64_t r1)
+{
+    uint32_t m = 0xffffffffu;
+    if (wd == (r0 >> 5)) m &= 0xffffffffu << (r0 & 31);
+    if (wd == ((r1 - 1) >> 5)) m &= 0xffffffffu >> (31 - ((r1 - 1) & 31));
+    return m;
+}
 __device__ __forceinline__ double sp_fold(const StepArgs &a, int64_t r0, int64_t r1)
 {
     double dx = 0.0;
     if (r1 <= r0) return dx;
     const int64_t w0 = r0 >> 5, w1 = (r1 - 1) >> 5;
-    for (int64_t wd = w0; wd <= w1; wd++) {
-        uint32_t m = ldcg(&a.sbits[wd]);
-        if (wd == w0) m &= 0xffffffffu << (r0 & 31);
-        if (wd == w1) m &= 0xffffffffu >> (31 - ((r1 - 1) & 31));
-        while (m) {
-            uint32_t sl[SP_FOLD];
+    uint32_t m3[3];
 #pragma unroll
-            for (int r = 0; r < SP_FOLD; r++) {
-                sl[r] = m ? (uint32_t)(wd * 32 + __ffs(m) - 1) : 0xffffffffu;
-                m &= m - 1;
-            }
-            double v[SP_FOLD];
+    for (int u = 0; u < 3; u++) m3[u] = w0 + u <= w1 ? ldcg(&a.sbits[w0 + u]) & sp_word_mask(w0 + u, r0, r1) : 0u;
 #pragma unroll
-            for (int r = 0; r < SP_FOLD; r++) v[r] = sl[r] != 0xffffffffu ? ldcg(&a.rv[sl[r]]) : 0.0;
-#pragma unroll
-            for (int r = 0; r < SP_FOLD; r++)
-                if (sl[r] != 0xffffffffu) dx += v[r];
-        }
+    for (int u = 0; u < 3; u++)
+        if (m3[u]) dx += sp_fold_word(a, w0 + u, m3[u]);
+    for (int64_t wd = w0 + 3; wd <= w1; wd++) {
+        const uint32_t m = ldcg(&a.sbits[wd]) & sp_word_mask(wd, r0, r1);
+        if (m) dx += sp_fold_word(a, wd, m);
     }
     return dx;
+}
+
+// The full columns' d'x part of sample i in bundle order (a full column holds row i at offset i).
+// Out of line (rare: a step with a full column); scalar arguments only, so that no copy of the
+// kernel's StepArgs is made addressable.
+__device__ __noinline__ double sp_dense_dx(const int32_t *__restrict__ flist, const double *dk,
+                                          const int4 *__restrict__ colinfo, const float *__restrict__ val,
+                                          const double *fd, const int64_t *fcp, int64_t f_lo, int64_t nf, int64_t k0,
+                                          int64_t i)
+{
+    double dx = 0.0;
+    for (int64_t e = 0; e < nf; e++) {
+        double d;
+        int64_t cp;
+        if (e < FMAX) {
+            d = fd[e];
+            cp = fcp[e];
+        } else {
+            const int32_t kk = __ldg(&flist[f_lo + e]);
+            d = ldcg(&dk[kk - k0]);
+            cp = colinfo_p0(__ldg(&colinfo[kk]));
+        }
+        if (d != 0.0) dx += d * (double)__ldg(&val[cp + i]);
+    }
+    return dx;
+}
+
+// grid_totals (pcdn_kernels.cuh) for SNW warps: warp w sums rows c2 = w, w + SNW, ... in order,
+// then warp 0 adds the warp sums in warp order (a fixed order)
+template <int W>
+__device__ __forceinline__ void sp_grid_totals(const double *part, int G, double (*red)[32], double *tot, int lane,
+                                               int warp)
+{
+    double v = 0.0;
+    if (lane < W) {
+#pragma unroll 4
+        for (int c2 = warp; c2 < G; c2 += SNW) v += ldcg(&part[(int64_t)c2 * NPART + lane]);
+    }
+    red[warp][lane] = v;
+    __syncthreads();
+    if (warp == 0 && lane < W) {
+        double t = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < SNW; w2++) t += red[w2][lane];
+        tot[lane] = t;
+    }
+    __syncwarp();
 }
 
 // One Armijo window over q0 .. q0+NQ-1 (Eq.6 with Eq.12 from retained quantities); window 0 also
@@ -158,7 +288,7 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
     double acc[W];
 #pragma unroll
     for (int q = 0; q < W; q++) acc[q] = 0.0;
-    for (int64_t li = tid; li < nT; li += NT) {
+    for (int64_t li = tid; li < nT; li += SNT) {
         const int32_t i = Tl[li];
         const double zi = ldcg(&a.z[i]);
         const double cg = ldcg(&a.coef[i]).x;
@@ -169,7 +299,7 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
             dx = sp_fold(a, r0, r1);
             if (di.any) {   // full columns, from CSC in bundle order (then the records)
                 const int64_t li2 = i - sm.row_base;
-                dx = (nT <= TSM ? sm.dxd[li2] : dense_dx(a, sm.fd, sm.fcp, di, k0, i)) + dx;
+                dx = (nT <= TSM ? sm.dxd[li2] : sp_dense_dx(a.flist, a.dk, a.colinfo, a.val, sm.fd, sm.fcp, di.f_lo, di.nf, k0, i)) + dx;
             }
             a.dxg[i] = dx;
             if (li == tid) {
@@ -178,6 +308,8 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
                 rr.zi = zi;
                 rr.dx = dx;
                 rr.has_dx = 1;
+                rr.r0 = r0;
+                rr.r1 = r1;
             }
         } else {
             dx = li == tid ? rr.dx : ldcg(&a.dxg[i]);
@@ -189,18 +321,46 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
             al *= a.beta;
         }
     }
-    // L1 part of Eq.12 and Delta over this CTA's share of the bundle
-    for (int64_t kk = pb0 + tid; kk < pb1; kk += NT) {
-        const bool reg = kk == sh.kk;
-        const double wj = reg ? sh.wj : ldcg(&a.w[__ldg(&a.order[kk])]);
-        const double d = reg ? sh.d : ldcg(&a.dk[kk - k0]);
+    // L1 part of Eq.12 and Delta over this CTA's share of the bundle (the thread's first position
+    // from registers, the others in batches of SP_CB)
+    if (sh.kk >= 0) {
         double al = alpha0;
 #pragma unroll
         for (int q = 0; q < NQ; q++) {
-            acc[NQ + q] += fabs(wj + al * d) - fabs(wj) + a.mu * al * d * (wj + 0.5 * al * d);
+            acc[NQ + q] += fabs(sh.wj + al * sh.d) - fabs(sh.wj) + a.mu * al * sh.d * (sh.wj + 0.5 * al * sh.d);
             al *= a.beta;
         }
-        acc[LY::DELTA] += reg ? sh.delta : ldcg(&a.deltak[kk - k0]);
+        acc[LY::DELTA] += sh.delta;
+    }
+    for (int64_t kb = pb0 + tid + SNT; kb < pb1; kb += (int64_t)SNT * SP_CB) {
+        int32_t jj[SP_CB];
+#pragma unroll
+        for (int e = 0; e < SP_CB; e++) {
+            const int64_t kk = kb + (int64_t)e * SNT;
+            jj[e] = kk < pb1 ? __ldg(&a.order[kk]) : -1;
+        }
+        double wv[SP_CB], dv[SP_CB], tv[SP_CB];
+#pragma unroll
+        for (int e = 0; e < SP_CB; e++) {
+            const int64_t kk = kb + (int64_t)e * SNT;
+            wv[e] = dv[e] = tv[e] = 0.0;
+            if (jj[e] >= 0) {
+                wv[e] = ldcg(&a.w[jj[e]]);
+                dv[e] = ldcg(&a.dk[kk - k0]);
+                tv[e] = ldcg(&a.deltak[kk - k0]);
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < SP_CB; e++) {
+            if (jj[e] < 0) continue;
+            double al = alpha0;
+#pragma unroll
+            for (int q = 0; q < NQ; q++) {
+                acc[NQ + q] += fabs(wv[e] + al * dv[e]) - fabs(wv[e]) + a.mu * al * dv[e] * (wv[e] + 0.5 * al * dv[e]);
+                al *= a.beta;
+            }
+            acc[LY::DELTA] += tv[e];
+        }
     }
     if (tid == 0) acc[LY::NTOUCH] = (double)nT;
     if (ctal && ws.win == 0) {   // profiling mode 2: this CTA's fold + line-search time
@@ -217,7 +377,7 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
     if (warp == 0 && lane < W) {
         double s = 0.0;
 #pragma unroll
-        for (int w2 = 0; w2 < NW; w2++) s += sm.red[w2][lane];
+        for (int w2 = 0; w2 < SNW; w2++) s += sm.red[w2][lane];
         part[(int64_t)c * NPART + lane] = s;
     }
     if (prof) {
@@ -231,7 +391,7 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
         sm.pacc[4] += now - tprev;
         tprev = now;
     }
-    grid_totals<W>(part, G, sm.red, sm.tot, lane, warp);
+    sp_grid_totals<W>(part, G, sm.red, sm.tot, lane, warp);
     if (warp == 0 && lane == 0) {
         const double Dl = sm.tot[LY::DELTA];
         int qa = -1, badl = 0;
@@ -288,7 +448,7 @@ __device__ __forceinline__ void sp_plan(const StepArgs &a, int64_t k0, int64_t k
 }
 
 template <class Sync, int LOSS>
-__global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
+__global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
 {
     if (a.stop && ldcg(a.stop)) return;   // the solve already ended (queued ahead; grid-uniform)
     Sync sy(a.bar);
@@ -302,10 +462,10 @@ __global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
     if (tid == 0) sm.row_base = row_base;
     int prev_q = 0;
     const int64_t pbs0 = (int64_t)c * a.P / G, pbs1 = (int64_t)(c + 1) * a.P / G;
-    const int64_t gw = (int64_t)c * NW + warp;
+    const int64_t gw = (int64_t)c * SNW + warp;
 
     long long tprev = 0;
-    const bool prof = a.prof != nullptr && c == 0 && tid == 0;
+    const bool prof = PCDN_PROFILE && a.prof != nullptr && c == 0 && tid == 0;
     if (tid < 16) sm.pacc[tid] = 0;
 #define SP_MARK(i)                                \
     do {                                          \
@@ -319,9 +479,11 @@ __global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
         sm.F = ldcg(a.F);
         for (int i = 0; i < 4; i++) sm.cnt[i] = 0;
     }
+    long long *const ctal_out = (PCDN_PROFILE && a.tl && c < 256) ? a.tl + (int64_t)c * 16 : nullptr;   // profiling mode 2
+    long long *const ctal = ctal_out ? sm.cprof : nullptr;   // per-CTA phase sums, in shared memory
+    if (tid < 16) sm.cprof[tid] = 0;
     if (tid == 0 && a.nsteps > 0) sp_plan(a, 0, min(a.P, a.ntot), &sm.plan[0]);
     __syncthreads();
-    long long *const ctal = (a.tl && c < 512) ? a.tl + (int64_t)c * 8 : nullptr;   // per-CTA phase sums (profiling mode 2)
     long long tstep = 0;
     for (int64_t t = 0; t < a.nsteps; t++) {
         if (prof) tprev = clock64();
@@ -339,7 +501,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
         const int GH = NCH > 0 ? (int)max((int64_t)1, min((int64_t)(G / 2), NCH)) : 0;
         const int GL = max(1, G - GH);
         if (c < GL) {
-            const int64_t NWL = (int64_t)GL * NW;
+            const int64_t NWL = (int64_t)GL * SNW;
             const int cw = (int)min((int64_t)32, max((int64_t)1, (Pt + NWL - 1) / NWL));
             for (int64_t ch = gw;; ch += NWL) {
                 const int64_t kb = k0 + ch * cw;
@@ -394,11 +556,20 @@ __global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
                     const int lo = __shfl_sync(0xffffffffu, ci.z, src), hi = __shfl_sync(0xffffffffu, ci.w, src);
                     const int64_t p0 = (int64_t)(((uint64_t)(uint32_t)hi << 32) | (uint64_t)(uint32_t)lo);
                     const int64_t p1 = p0 + ml;
+                    const double wj = ldcg(&a.w[j]);
                     double gs, hs;
-                    col_gh(a, p0, p1, lane, gs, hs);
-                    const Dir r = finish_feature(a, gs, hs, ldcg(&a.w[j]));
-                    if (lane == 0) sp_store_dir(a, kb + src - k0, r);
-                    if (r.d != 0.0 && ml != a.s) sp_scatter(a, p0, p1, lane, r.d);
+                    if (ml <= 32 * SP_WR) {   // held in registers from the gather to the scatter
+                        WarpRange wr;
+                        sp_range_gh(a, p0, p1, lane, wr, gs, hs);
+                        const Dir r = finish_feature(a, gs, hs, wj);
+                        if (lane == 0) sp_store_dir(a, kb + src - k0, r);
+                        if (r.d != 0.0 && ml != a.s) sp_range_scatter(a, wr, r.d);
+                    } else {
+                        col_gh(a, p0, p1, lane, gs, hs);
+                        const Dir r = finish_feature(a, gs, hs, wj);
+                        if (lane == 0) sp_store_dir(a, kb + src - k0, r);
+                        if (r.d != 0.0 && ml != a.s) sp_scatter(a, p0, p1, lane, r.d);
+                    }
                 }
             }
         }
@@ -415,9 +586,19 @@ __global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
         if (heavy_cta) {
             for (int64_t q = G - 1 - c; q < NCH; q += GH) {
                 const ChunkDesc cd = chunk_decode(__ldg(&a.cdesc[C0 + q]));
-                const int64_t w0 = cd.pb + (int64_t)warp * cd.len / NW, w1 = cd.pb + (int64_t)(warp + 1) * cd.len / NW;
+                const int64_t w0 = cd.pb + (int64_t)warp * cd.len / SNW, w1 = cd.pb + (int64_t)(warp + 1) * cd.len / SNW;
+                // the column's position, feature and w_j, loaded beside the gather (warp 0 finishes)
+                int4 hd = make_int4(0, 0, 0, 0);
+                double wj = 0.0;
+                if (warp == 0) {
+                    hd = __ldg(&a.hdesc[cd.e]);   // (position, j, col_ptr[j])
+                    wj = ldcg(&a.w[hd.y]);
+                }
+                const bool inreg = w1 - w0 <= 32 * SP_WR;   // this warp's share held in registers
+                WarpRange wr;
                 double gs, hs;
-                col_gh(a, w0, w1, lane, gs, hs);
+                if (inreg) sp_range_gh(a, w0, w1, lane, wr, gs, hs);
+                else col_gh(a, w0, w1, lane, gs, hs);
                 if (lane == 0) {
                     sm.red[warp][0] = gs;
                     sm.red[warp][1] = hs;
@@ -426,7 +607,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
                 if (warp == 0) {
                     double g = 0.0, h = 0.0;
 #pragma unroll
-                    for (int w2 = 0; w2 < NW; w2++) {
+                    for (int w2 = 0; w2 < SNW; w2++) {
                         g += sm.red[w2][0];
                         h += sm.red[w2][1];
                     }
@@ -453,8 +634,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
                         }
                     }
                     if (fin) {
-                        const int4 hd = __ldg(&a.hdesc[cd.e]);   // (position, j, col_ptr[j])
-                        const Dir r = finish_feature(a, g, h, ldcg(&a.w[hd.y]));
+                        const Dir r = finish_feature(a, g, h, wj);
                         if (lane == 0) {
                             sp_store_dir(a, hd.x - k0, r);
                             if (cd.nch > 1) {
@@ -468,7 +648,10 @@ __global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
                 __syncthreads();
                 if (cd.nch == 1) {
                     const double d = sm.tot[0];
-                    if (d != 0.0 && !cd.full) sp_scatter(a, w0, w1, lane, d);
+                    if (d != 0.0 && !cd.full) {
+                        if (inreg) sp_range_scatter(a, wr, d);
+                        else sp_scatter(a, w0, w1, lane, d);
+                    }
                 }
                 __syncthreads();   // sm.red / sm.tot reused by the next chunk
             }
@@ -489,7 +672,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
                 }
                 __syncthreads();
                 const double d = sm.tot[0];
-                const int64_t w0 = cd.pb + (int64_t)warp * cd.len / NW, w1 = cd.pb + (int64_t)(warp + 1) * cd.len / NW;
+                const int64_t w0 = cd.pb + (int64_t)warp * cd.len / SNW, w1 = cd.pb + (int64_t)(warp + 1) * cd.len / SNW;
                 if (d != 0.0) sp_scatter(a, w0, w1, lane, d);
                 __syncthreads();
             }
@@ -526,12 +709,12 @@ __global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
         di.any = false;
         if (di.nf > 0) {
             int any = 0;
-            for (int64_t e = tid; e < di.nf; e += NT) {
+            for (int64_t e = tid; e < di.nf; e += SNT) {
                 const int32_t kk = __ldg(&a.flist[di.f_lo + e]);
                 const double d = ldcg(&a.dk[kk - k0]);
                 if (e < FMAX) {
                     sm.fd[e] = d;
-                    sm.fcp[e] = __ldg(&a.col_ptr[__ldg(&a.order[kk])]);
+                    sm.fcp[e] = colinfo_p0(__ldg(&a.colinfo[kk]));   // (a.val's offset of the column)
                 }
                 any |= d != 0.0;
             }
@@ -542,12 +725,12 @@ __global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
         if (di.any) {   // a full column with d_j != 0 touches every sample (reading Z8)
             const int64_t nrows = min(a.s, we * 32) - row_base;
             int32_t *Tw = nrows <= TSM ? sm.tl : a.tlist + row_base;
-            for (int64_t li = tid; li < nrows; li += NT) Tw[li] = (int32_t)(row_base + li);
+            for (int64_t li = tid; li < nrows; li += SNT) Tw[li] = (int32_t)(row_base + li);
             if (tid == 0) sm.nT = nrows > 0 ? nrows : 0;
             __syncthreads();
         } else {
             const int64_t nwc = we - wb;
-            const int64_t wpt = (nwc + NT - 1) / NT;
+            const int64_t wpt = (nwc + SNT - 1) / SNT;
             const int64_t w0 = wb + (int64_t)tid * wpt, w1 = min(we, w0 + wpt);
             uint32_t wv[WREG];
             unsigned cntb = 0;
@@ -568,7 +751,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
             const unsigned wtot = __reduce_add_sync(0xffffffffu, cntb);
             if (lane == 0) sm.scan_w[warp] = wtot;
             __syncthreads();
-            const unsigned sw = lane < NW ? (unsigned)sm.scan_w[lane] : 0u;
+            const unsigned sw = lane < SNW ? (unsigned)sm.scan_w[lane] : 0u;
             const unsigned woff = __reduce_add_sync(0xffffffffu, lane < warp ? sw : 0u);
             const unsigned total = __reduce_add_sync(0xffffffffu, sw);
             int32_t *Tw = total <= (unsigned)TSM ? sm.tl : a.tlist + row_base;
@@ -601,12 +784,13 @@ __global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
             // the full columns' d'x part of every row of the block, (row, column chunk) per thread so
             // that a column's loads are coalesced over rows; chunk partials added in chunk order
             const int R = (int)nT;
-            const int C = R >= NT ? 1 : (int)min((int64_t)(NT / max(R, 1)), di.nf);
-            double *dpart = &sm.red[0][0];   // NW*32 = NT doubles
-            for (int r0 = 0; r0 < R; r0 += NT) {
+            const int C = R >= SNT ? 1 : (int)min((int64_t)(SNT / max(R, 1)), di.nf);
+            double *dpart = &sm.red[0][0];   // SNW*32 = SNT doubles
+            for (int r0 = 0; r0 < R; r0 += SNT) {
                 const int tt = tid;
                 if (C == 1) {
-                    if (r0 + tt < R) sm.dxd[r0 + tt] = dense_dx(a, sm.fd, sm.fcp, di, k0, row_base + r0 + tt);
+                    if (r0 + tt < R) sm.dxd[r0 + tt] = sp_dense_dx(a.flist, a.dk, a.colinfo, a.val, sm.fd, sm.fcp, di.f_lo, di.nf, k0,
+                                                                       row_base + r0 + tt);
                 } else if (tt < R * C) {
                     const int r = tt % R, chn = tt / R;
                     const int64_t e0 = (int64_t)chn * di.nf / C, e1 = (int64_t)(chn + 1) * di.nf / C;
@@ -621,7 +805,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
                         } else {
                             const int32_t kk = __ldg(&a.flist[di.f_lo + e]);
                             d = ldcg(&a.dk[kk - k0]);
-                            cp = __ldg(&a.col_ptr[__ldg(&a.order[kk])]);
+                            cp = colinfo_p0(__ldg(&a.colinfo[kk]));
                         }
                         if (d != 0.0) part += d * (double)__ldg(&a.val[cp + i]);
                     }
@@ -630,7 +814,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
             }
             if (C > 1) {
                 __syncthreads();
-                for (int r = tid; r < R; r += NT) {
+                for (int r = tid; r < R; r += SNT) {
                     double x = 0.0;
                     for (int chn = 0; chn < C; chn++) x += dpart[chn * R + r];
                     sm.dxd[r] = x;
@@ -670,34 +854,90 @@ __global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
         // ---------------- commit (a5): this CTA's samples and bundle share; clear the bitmaps -----
         // (every fold of the step finished before the decision's barrier, so the written-slot words
         // can be cleared here even where two samples' segments share a word)
-        for (int64_t li = tid; li < nT; li += NT) {
-            const bool reg = li == tid && rr.i >= 0;
-            const int32_t i = reg ? rr.i : Tl[li];
-            const double dx = reg ? rr.dx : ldcg(&a.dxg[i]);
+        // (the thread's first sample from registers; the others in batches of SP_CB, all loads in
+        // flight together)
+        if (rr.i >= 0) {
+            const int32_t i = rr.i;
             if (qacc >= 0) {
-                const double zi = reg ? rr.zi : ldcg(&a.z[i]);
-                const int yi = reg ? rr.yi : (int)a.y[i];
-                const double zn = zi + alpha_acc * dx;
+                const double zn = rr.zi + alpha_acc * rr.dx;
                 a.z[i] = zn;
                 const double2 cfo = LOSS == LOSS_SQ ? ldcg(&a.coef[i]) : make_double2(0.0, 0.0);
-                a.coef[i] = coef_next(LOSS, cfo, zn, alpha_acc * dx, yi);
+                a.coef[i] = coef_next(LOSS, cfo, zn, alpha_acc * rr.dx, rr.yi);
             }
-            const int64_t r0 = __ldg(&a.row_ptr[i]), r1 = __ldg(&a.row_ptr[i + 1]);
-            if (r1 > r0)
-                for (int64_t wd = r0 >> 5; wd <= ((r1 - 1) >> 5); wd++) a.sbits[wd] = 0u;
+            if (rr.r1 > rr.r0)
+                for (int64_t wd = rr.r0 >> 5; wd <= ((rr.r1 - 1) >> 5); wd++) a.sbits[wd] = 0u;
             if (a.debug) {
-                a.dbg_dx[i] = dx;
+                a.dbg_dx[i] = rr.dx;
                 a.dbg_mark[i] = 1;
             }
         }
-        for (int64_t wi = wb + tid; wi < we; wi += NT) a.bits[wi] = 0u;
+        for (int64_t lb = tid + SNT; lb < nT; lb += (int64_t)SNT * SP_CB) {
+            int32_t ii[SP_CB];
+            double dxv[SP_CB], zv[SP_CB];
+            double2 cfo[SP_CB];
+            int64_t ra[SP_CB], rb[SP_CB];
+            int yv[SP_CB];
+#pragma unroll
+            for (int e = 0; e < SP_CB; e++) {
+                const int64_t li = lb + (int64_t)e * SNT;
+                ii[e] = li < nT ? Tl[li] : -1;
+            }
+#pragma unroll
+            for (int e = 0; e < SP_CB; e++) {
+                dxv[e] = zv[e] = 0.0;
+                cfo[e] = make_double2(0.0, 0.0);
+                ra[e] = rb[e] = 0;
+                yv[e] = 1;
+                if (ii[e] >= 0) {
+                    dxv[e] = ldcg(&a.dxg[ii[e]]);
+                    ra[e] = __ldg(&a.row_ptr[ii[e]]);
+                    rb[e] = __ldg(&a.row_ptr[ii[e] + 1]);
+                    if (qacc >= 0) {
+                        zv[e] = ldcg(&a.z[ii[e]]);
+                        yv[e] = (int)a.y[ii[e]];
+                        if (LOSS == LOSS_SQ) cfo[e] = ldcg(&a.coef[ii[e]]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < SP_CB; e++) {
+                const int32_t i = ii[e];
+                if (i < 0) continue;
+                if (qacc >= 0) {
+                    const double zn = zv[e] + alpha_acc * dxv[e];
+                    a.z[i] = zn;
+                    a.coef[i] = coef_next(LOSS, cfo[e], zn, alpha_acc * dxv[e], yv[e]);
+                }
+                if (rb[e] > ra[e])
+                    for (int64_t wd = ra[e] >> 5; wd <= ((rb[e] - 1) >> 5); wd++) a.sbits[wd] = 0u;
+                if (a.debug) {
+                    a.dbg_dx[i] = dxv[e];
+                    a.dbg_mark[i] = 1;
+                }
+            }
+        }
+        for (int64_t wi = wb + tid; wi < we; wi += SNT) a.bits[wi] = 0u;
         if (qacc >= 0) {
-            for (int64_t kb = pb0 + tid; kb < pb1; kb += NT) {
-                const bool reg = kb == sh.kk;
-                const int32_t j = reg ? sh.j : __ldg(&a.order[kb]);
-                const double wj = reg ? sh.wj : ldcg(&a.w[j]);
-                const double d = reg ? sh.d : ldcg(&a.dk[kb - k0]);
-                a.w[j] = wj + alpha_acc * d;
+            for (int64_t kb = pb0 + tid; kb < pb1; kb += (int64_t)SNT * SP_CB) {
+                int32_t jj[SP_CB];
+                double wv[SP_CB], dv[SP_CB];
+#pragma unroll
+                for (int e = 0; e < SP_CB; e++) {
+                    const int64_t kk = kb + (int64_t)e * SNT;
+                    jj[e] = kk < pb1 ? (kk == sh.kk ? sh.j : __ldg(&a.order[kk])) : -1;
+                }
+#pragma unroll
+                for (int e = 0; e < SP_CB; e++) {
+                    const int64_t kk = kb + (int64_t)e * SNT;
+                    wv[e] = dv[e] = 0.0;
+                    if (jj[e] >= 0) {
+                        wv[e] = kk == sh.kk ? sh.wj : ldcg(&a.w[jj[e]]);
+                        dv[e] = kk == sh.kk ? sh.d : ldcg(&a.dk[kk - k0]);
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < SP_CB; e++)
+                    if (jj[e] >= 0) a.w[jj[e]] = wv[e] + alpha_acc * dv[e];
             }
         }
         SP_MARK(6);
@@ -726,7 +966,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
         }
         sy.arrive();
         // the next step's plan, while the barrier completes
-        if (tid == NT - 1 && k1 < a.ntot) sp_plan(a, k1, min(k1 + a.P, a.ntot), &sm.plan[(t + 1) & 1]);
+        if (tid == SNT - 1 && k1 < a.ntot) sp_plan(a, k1, min(k1 + a.P, a.ntot), &sm.plan[(t + 1) & 1]);
         sy.wait();
         SP_MARK(7);
         if (bad) break;
@@ -739,6 +979,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_sparse(StepArgs a)
     }
     if (prof)
         for (int i = 0; i < 16; i++) a.prof[i] += sm.pacc[i];
+    if (ctal_out && tid < 16) ctal_out[tid] += sm.cprof[tid];
 #undef SP_MARK
 }
 

@@ -32,7 +32,7 @@ s.reset()
 pk.pcdn_set_profile(s.ctx, 2)
 r = s.solve(P, seed=prob.seed, max_outer=1)
 steps = r["steps"]
-tl = pk.pcdn_warp_timeline(s.ctx).astype(np.float64).reshape(-1)[: 512 * 8].reshape(512, 8)
+tl = pk.pcdn_warp_timeline(s.ctx).astype(np.float64).reshape(-1)[: 256 * 16].reshape(256, 16)
 pk.pcdn_set_profile(s.ctx, 0)   # (zeroes the counters)
 G = int(np.count_nonzero(tl[:, 0]))
 us = tl[:G] / steps / args.mhz
@@ -43,9 +43,11 @@ for k, name in ((0, "A_us"), (3, "C1_us"), (1, "C1+fold+LS_us")):
                  "argmax": int(v.argmax())}
 out["touched_per_cta"] = {"median": float(np.median(tl[:G, 2] / steps)), "max": float((tl[:G, 2] / steps).max())}
 out["A_us_by_cta"] = [round(x, 2) for x in us[:, 0]]
-# warp 0 of each CTA: its chunk partials (A1), wait for the published d_j, records (A2), chunks taken
-out["w0_A1_us"] = [round(x, 2) for x in us[-20:, 4]]
-out["w0_wait_us"] = [round(x, 2) for x in us[-20:, 5]]
-out["w0_scatter_us"] = [round(x, 2) for x in us[-20:, 6]]
-out["w0_chunks_per_step"] = [round(x, 3) for x in (tl[:G, 7] / steps)[-20:]]
+# thread 0 of each light CTA, its lane columns: cycles until the column descriptor, the rows, the
+# gathered factors are in registers, and the emits issued (per lane column it handled)
+lc = tl[:G, 8]
+sel = lc > 0
+for k, name in ((4, "colinfo"), (5, "rows"), (6, "coef"), (7, "finish+emit")):
+    out["lane_col_cycles_" + name] = round(float(np.sum(tl[:G, k][sel]) / np.sum(lc[sel])), 1)
+out["lane_cols_per_step_thread0"] = round(float(np.mean(lc[sel]) / steps), 3)
 print(json.dumps(out))

@@ -26,10 +26,11 @@ for r in csv.reader(open(path, errors="replace")):
     d = dict(zip(hdr, r))
     name = d.get("Metric Name")
     if name in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"):
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "ns": 1e-9, "us": 1e-6, "ms": 1e-3,
                  "msecond": 1e-3, "second": 1.0}[d["Metric Unit"]]
         per[d["ID"]][name] = float(d["Metric Value"].replace(",", "")) * scale
-launches = [v for v in per.values() if len(v) == 3]
+# (a launch queued after the outer iteration that ended the solve exits at once: not a step launch)
+launches = [v for v in per.values() if len(v) == 3 and v["gpu__time_duration.sum"] > 1e-3]
 if not launches:
     raise SystemExit("no complete launches in " + path)
 rd = sum(v["dram__bytes_read.sum"] for v in launches) / len(launches)
