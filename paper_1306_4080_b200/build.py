@@ -14,6 +14,9 @@ LIB = os.path.join(HERE, "libpcdn.so")
 # the same library with the sparse kernel's profiling instrumentation (-DPCDN_PROFILE=1), for the
 # profiling scripts (loaded through PCDN_LIB); never the product path
 LIB_PROF = os.path.join(HERE, "libpcdn_prof.so")
+# ... and with device-side bounds / protocol checks (-DPCDN_CHECKS=1): the GPU tests run against it
+# (scripts/checked_run.sh) in place of compute-sanitizer, which is closed on this pool
+LIB_CHECKED = os.path.join(HERE, "libpcdn_checked.so")
 
 NVCC_FLAGS = [
     "-O3", "-std=c++17",
@@ -31,12 +34,12 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
-    lib = LIB_PROF if profile else LIB
+def build(force: bool = False, verbose: bool = False, profile: bool = False, checks: bool = False) -> str:
+    lib = LIB_CHECKED if checks else LIB_PROF if profile else LIB
     stale = force or not os.path.exists(lib) or any(os.path.getmtime(d) > os.path.getmtime(lib) for d in DEPS)
     if stale:
         tmp = lib + f".tmp{os.getpid()}"
-        cmd = [nvcc()] + NVCC_FLAGS + (["-DPCDN_PROFILE=1"] if profile else []) + \
+        cmd = [nvcc()] + NVCC_FLAGS + (["-DPCDN_PROFILE=1"] if profile else []) + (["-DPCDN_CHECKS=1"] if checks else []) + \
               (["-Xptxas", "-v"] if verbose else []) + ["-o", tmp] + SRC
         subprocess.check_call(cmd)
         os.replace(tmp, lib)
@@ -44,4 +47,5 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False) -> 
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, profile="--profile" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, profile="--profile" in sys.argv,
+                checks="--checks" in sys.argv))

@@ -19,9 +19,31 @@
 //   a6  k_obj_*          F_c(w) from (z, w) with a fixed-order two-level reduction (Eq.1)
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace pcdn {
+
+// Checked build (-DPCDN_CHECKS=1, libpcdn_checked.so): device-side bounds and protocol checks that
+// trap with the failing condition.  compute-sanitizer is closed on this pool; the GPU test suite
+// runs against this build instead (scripts/checked_run.sh).  The product build compiles them out.
+#ifndef PCDN_CHECKS
+#define PCDN_CHECKS 0
+#endif
+#if PCDN_CHECKS
+#define PCDN_CHECK(cond)                                                                          \
+    do {                                                                                          \
+        if (!(cond)) {                                                                            \
+            printf("PCDN_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                            \
+            __trap();                                                                             \
+        }                                                                                         \
+    } while (0)
+#else
+#define PCDN_CHECK(cond) \
+    do {                 \
+    } while (0)
+#endif
 
 constexpr int NT = 512;            // threads per CTA of the step kernel
 constexpr int NW = NT / 32;        // warps per CTA
@@ -420,7 +442,7 @@ __device__ __forceinline__ int64_t colinfo_p0(const int4 &ci)
 // descriptor array of a list set needs at most nnz/SP_CHMIN + n entries; a column has at most
 // SP_NCHMAX chunks (the finishing warp sums <= 16 partials per lane).
 constexpr int SP_CHMIN = 4;
-constexpr int SP_CTA_MUL = 16;
+constexpr int SP_CTA_MUL = 12;   // = the warps of a sparse-kernel CTA (pcdn_sparse.cuh)
 constexpr int SP_NCHMAX = 512;
 __host__ __device__ __forceinline__ int chunk_count(int64_t len, int heavy_len)
 {

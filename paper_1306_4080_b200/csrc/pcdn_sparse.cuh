@@ -54,6 +54,8 @@ constexpr int SP_SHORT = 4;     // columns with <= SP_SHORT nonzeros are reduced
 constexpr int SP_CH = 256;      // default heavy_len of the sparse kernel: longer columns go in chunks
 constexpr int SP_FOLD = 4;      // record loads of one sample in flight together in the fold
 constexpr int SP_CB = 4;        // samples / positions of a thread with their loads in flight together (commit)
+constexpr int SP_MQ = 256;      // per-CTA queue of a step's medium columns (one warp each, after the lane sweep)
+static_assert(SP_CTA_MUL == SNW, "a heavy chunk is one warp-register range (32 * SP_WR) per warp of the CTA");
 
 struct SpPlan {
     int64_t c0, c1;     // the step's chunks [c0, c1) of cdesc
@@ -72,6 +74,9 @@ struct SpSmem {
     long long cprof[16];   // profiling mode 2: this CTA's sums, copied out at the end of the launch
     int dec_q, dec_bad;
     double dec_alpha, dec_lhs, dec_rhs, dec_Delta, dec_nT;
+    int nmq;               // medium columns of this CTA in this step, queued by the lane sweep
+    int4 mq[SP_MQ];        // their column descriptors ...
+    int32_t mqk[SP_MQ];    // ... and bundle positions (relative to the step)
     double fd[FMAX];
     int64_t fcp[FMAX];
     double dxd[TSM];
@@ -93,6 +98,8 @@ __device__ __forceinline__ void st_release(unsigned long long *p, unsigned long 
 // record d_j x_ij of nonzero (i, j) at CSR offset `slot` (a3)
 __device__ __forceinline__ void sp_emit(const StepArgs &a, int32_t i, uint32_t slot, double v)
 {
+    PCDN_CHECK(i >= 0 && i < a.s);
+    PCDN_CHECK(slot >= (uint32_t)__ldg(&a.row_ptr[i]) && slot < (uint32_t)__ldg(&a.row_ptr[i + 1]));
     __stcg(&a.rv[slot], v);
     atomicOr(&a.sbits[slot >> 5], 1u << (slot & 31));
     atomicOr(&a.bits[i >> 5], 1u << (i & 31));
@@ -178,12 +185,35 @@ __device__ __forceinline__ void sp_range_scatter(const StepArgs &a, const WarpRa
         if (r.ri[e] >= 0) sp_emit(a, r.ri[e], r.sl[e], d * (double)r.xv[e]);
 }
 
+// A medium column (SP_SHORT < length <= heavy_len) by one warp: g/h (Eq.13), d_j (Eq.5), the Delta
+// term, and its records; k = the column's bundle position within the step
+__device__ __forceinline__ void sp_medium_column(const StepArgs &a, const int4 ci, int64_t k, int lane)
+{
+    const int ml = ci.y;
+    const int64_t p0 = colinfo_p0(ci), p1 = p0 + ml;
+    const double wj = ldcg(&a.w[ci.x]);
+    double gs, hs;
+    if (ml <= 32 * SP_WR) {   // held in registers from the gather to the scatter
+        WarpRange wr;
+        sp_range_gh(a, p0, p1, lane, wr, gs, hs);
+        const Dir r = finish_feature(a, gs, hs, wj);
+        if (lane == 0) sp_store_dir(a, k, r);
+        if (r.d != 0.0 && ml != a.s) sp_range_scatter(a, wr, r.d);
+    } else {
+        col_gh(a, p0, p1, lane, gs, hs);
+        const Dir r = finish_feature(a, gs, hs, wj);
+        if (lane == 0) sp_store_dir(a, k, r);
+        if (r.d != 0.0 && ml != a.s) sp_scatter(a, p0, p1, lane, r.d);
+    }
+}
+
 // fold of sample i's records: the written slots of its CSR segment [r0, r1), ascending.  The first
 // three words of the segment's written-slot bitmap are loaded together (a row of <= 65 nonzeros
 // needs no more), then up to SP_FOLD slots of a word at a time (static register indices), summed
 // in slot order.
 __device__ __forceinline__ double sp_fold_word(const StepArgs &a, int64_t wd, uint32_t m)
 {
+    PCDN_CHECK(wd >= 0 && wd <= (int64_t)(a.row_ptr[a.s] >> 5));
     double dx = 0.0;
     while (m) {
         uint32_t sl[SP_FOLD];
@@ -290,6 +320,7 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
     for (int q = 0; q < W; q++) acc[q] = 0.0;
     for (int64_t li = tid; li < nT; li += SNT) {
         const int32_t i = Tl[li];
+        PCDN_CHECK(i >= 0 && i < a.s);
         const double zi = ldcg(&a.z[i]);
         const double cg = ldcg(&a.coef[i]).x;
         const int yi = a.y[i];
@@ -482,6 +513,7 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
     long long *const ctal_out = (PCDN_PROFILE && a.tl && c < 256) ? a.tl + (int64_t)c * 16 : nullptr;   // profiling mode 2
     long long *const ctal = ctal_out ? sm.cprof : nullptr;   // per-CTA phase sums, in shared memory
     if (tid < 16) sm.cprof[tid] = 0;
+    if (tid == 0) sm.nmq = 0;
     if (tid == 0 && a.nsteps > 0) sp_plan(a, 0, min(a.P, a.ntot), &sm.plan[0]);
     __syncthreads();
     long long tstep = 0;
@@ -509,6 +541,7 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
                 const int64_t kk = kb + lane;
                 const int4 ci = (lane < cw && kk < k1) ? __ldg(&a.colinfo[kk]) : make_int4(0, -1, 0, 0);
                 const int len = ci.y;
+                PCDN_CHECK(len < 0 || (ci.x >= 0 && ci.x < a.n && colinfo_p0(ci) + len <= a.col_ptr[a.n]));
                 if (len >= 0 && len <= SP_SHORT && len <= a.heavy_len) {
                     const int32_t j = ci.x;
                     const int64_t p0 = colinfo_p0(ci);
@@ -547,32 +580,31 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
                             if (e < len) sp_emit(a, ri[e], sl[e], r.d * (double)xv[e]);
                     }
                 }
+                // medium columns go to the CTA's queue (a warp each below), so that no warp reduces
+                // two of them one after the other; beyond the queue the warp takes them itself
                 unsigned med = __ballot_sync(0xffffffffu, len > SP_SHORT && len <= a.heavy_len);
+                if (med) {
+                    int base = 0;
+                    if (lane == 0) base = atomicAdd(&sm.nmq, __popc(med));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    const int slot = base + __popc(med & ((1u << lane) - 1u));
+                    if (((med >> lane) & 1u) && slot < SP_MQ) {
+                        sm.mq[slot] = ci;
+                        sm.mqk[slot] = (int32_t)(kk - k0);
+                    }
+                    med &= __ballot_sync(0xffffffffu, ((med >> lane) & 1u) && slot >= SP_MQ);
+                }
                 while (med) {
                     const int src = __ffs(med) - 1;
                     med &= med - 1;
-                    const int32_t j = __shfl_sync(0xffffffffu, ci.x, src);
-                    const int ml = __shfl_sync(0xffffffffu, len, src);
-                    const int lo = __shfl_sync(0xffffffffu, ci.z, src), hi = __shfl_sync(0xffffffffu, ci.w, src);
-                    const int64_t p0 = (int64_t)(((uint64_t)(uint32_t)hi << 32) | (uint64_t)(uint32_t)lo);
-                    const int64_t p1 = p0 + ml;
-                    const double wj = ldcg(&a.w[j]);
-                    double gs, hs;
-                    if (ml <= 32 * SP_WR) {   // held in registers from the gather to the scatter
-                        WarpRange wr;
-                        sp_range_gh(a, p0, p1, lane, wr, gs, hs);
-                        const Dir r = finish_feature(a, gs, hs, wj);
-                        if (lane == 0) sp_store_dir(a, kb + src - k0, r);
-                        if (r.d != 0.0 && ml != a.s) sp_range_scatter(a, wr, r.d);
-                    } else {
-                        col_gh(a, p0, p1, lane, gs, hs);
-                        const Dir r = finish_feature(a, gs, hs, wj);
-                        if (lane == 0) sp_store_dir(a, kb + src - k0, r);
-                        if (r.d != 0.0 && ml != a.s) sp_scatter(a, p0, p1, lane, r.d);
-                    }
+                    const int4 cm = make_int4(__shfl_sync(0xffffffffu, ci.x, src), __shfl_sync(0xffffffffu, ci.y, src),
+                                              __shfl_sync(0xffffffffu, ci.z, src), __shfl_sync(0xffffffffu, ci.w, src));
+                    sp_medium_column(a, cm, kb + src - k0, lane);
                 }
             }
         }
+        __syncthreads();
+        for (int q = warp; q < min(sm.nmq, SP_MQ); q += SNW) sp_medium_column(a, sm.mq[q], sm.mqk[q], lane);
         SP_MARK(8);
 
         // ---------------- phase A, heavy columns: one chunk per CTA at a time (A1) ------------------
@@ -586,6 +618,8 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
         if (heavy_cta) {
             for (int64_t q = G - 1 - c; q < NCH; q += GH) {
                 const ChunkDesc cd = chunk_decode(__ldg(&a.cdesc[C0 + q]));
+                PCDN_CHECK(cd.e >= 0 && cd.e < a.n && cd.c < cd.nch && cd.nch >= 1 && cd.nch <= SP_NCHMAX);
+                PCDN_CHECK(cd.pb >= 0 && cd.len >= 1 && cd.pb + cd.len <= a.col_ptr[a.n]);
                 const int64_t w0 = cd.pb + (int64_t)warp * cd.len / SNW, w1 = cd.pb + (int64_t)(warp + 1) * cd.len / SNW;
                 // the column's position, feature and w_j, loaded beside the gather (warp 0 finishes)
                 int4 hd = make_int4(0, 0, 0, 0);
@@ -615,7 +649,9 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
                     if (!fin) {
                         if (lane == 0) {
                             __stcg(&a.cpart[q], make_double2(g, h));
-                            fin = atom_add_acq_rel(&a.ccnt[cd.e], 1) == cd.nch - 1;
+                            const int old = atom_add_acq_rel(&a.ccnt[cd.e], 1);
+                            PCDN_CHECK(old >= 0 && old < cd.nch);   // arrivals of this step only
+                            fin = old == cd.nch - 1;
                         }
                         fin = __shfl_sync(0xffffffffu, fin, 0);
                         __syncwarp();
@@ -635,6 +671,7 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
                     }
                     if (fin) {
                         const Dir r = finish_feature(a, g, h, wj);
+                        PCDN_CHECK(hd.x >= k0 && hd.x < k1);
                         if (lane == 0) {
                             sp_store_dir(a, hd.x - k0, r);
                             if (cd.nch > 1) {
@@ -684,6 +721,7 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
         }
         sy.sync();
         SP_MARK(1);
+        if (tid == 0) sm.nmq = 0;   // every warp left the medium-column queue before the barrier
         if (ctal && tid == 0) tstep = clock64();
 
         const bool fullP = Pt == a.P;

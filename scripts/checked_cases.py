@@ -1,10 +1,11 @@
-"""Small cases of every launch mode for compute-sanitizer (memcheck / racecheck / synccheck /
-initcheck): one bundle step from an injected state and a two-outer-iteration solve per mode and
-loss on a tiny fixture and on config 1, plus SCDN, elastic net, Lasso, the dense kernel and the
-sample-sharded step.  Prints one line per case; exits non-zero if a result leaves the oracle's
-north-star bars (the sanitizer's own report is the point of the run).
+"""Small cases of every launch mode for the checked build (libpcdn_checked.so, device-side bounds and
+protocol checks; compute-sanitizer is closed on this pool): one bundle step from an injected state
+and a two-outer-iteration solve per mode and loss on a tiny fixture and on config 1, plus SCDN,
+elastic net, Lasso, the dense kernel, the sample-sharded step and the one-call host API.  Prints one
+line per case; exits non-zero if a result leaves the oracle's north-star bars (a failed check traps
+the kernel and the CUDA error ends the run).
 
-usage: compute-sanitizer --tool memcheck python scripts/sanitize_cases.py [--quick]"""
+usage: PCDN_LIB=paper_1306_4080_b200/libpcdn_checked.so python scripts/checked_cases.py [--quick]"""
 import os
 import sys
 
