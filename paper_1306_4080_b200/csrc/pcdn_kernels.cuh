@@ -1199,6 +1199,7 @@ struct RowReg {
     int has_dx;  // 0 when the sample had > NREG records (folded by a warp into dxg)
     double zi, dx;
     int64_t r0, r1;   // the sample's CSR segment (sparse kernel)
+    double cg;        // the sample's cached G before the step (sparse kernel: speculative commit)
 };
 
 // ------------------------------------------------------------------------------------
@@ -1257,6 +1258,7 @@ __device__ __forceinline__ void grid_totals(const double *part, int G, double (*
 
 struct WinState {
     int q0, nq, qacc, bad, win;
+    int nospec;       // sparse kernel: some CTA did not commit speculatively in this window
     unsigned tmask;   // cluster-resident kernel: owned samples (bit r) touched in this step
     double alpha, lhs, rhs, Delta, nT_tot;
 };
@@ -1290,9 +1292,9 @@ __device__ __forceinline__ double dense_dx(const StepArgs &a, const double *fd, 
 }
 
 template <int NQ>
-struct WinLayout {  // packed partial slots: Ls[0,NQ) L1[NQ,2NQ) Delta |T|
-    static constexpr int W = 2 * NQ + 2 <= 8 ? 8 : (2 * NQ + 2 <= 16 ? 16 : 32);
-    static constexpr int DELTA = 2 * NQ, NTOUCH = 2 * NQ + 1;
+struct WinLayout {  // packed partial slots: Ls[0,NQ) L1[NQ,2NQ) Delta |T| [no-speculation count]
+    static constexpr int W = 2 * NQ + 3 <= 8 ? 8 : (2 * NQ + 3 <= 16 ? 16 : 32);
+    static constexpr int DELTA = 2 * NQ, NTOUCH = 2 * NQ + 1, NOSPEC = 2 * NQ + 2;
 };
 
 // the full columns' d'x part of sample i: from the dense pass (the block's rows are T when a

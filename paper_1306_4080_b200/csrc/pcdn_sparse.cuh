@@ -72,7 +72,7 @@ struct SpSmem {
     long long cnt[4];
     long long pacc[16];
     long long cprof[16];   // profiling mode 2: this CTA's sums, copied out at the end of the launch
-    int dec_q, dec_bad;
+    int dec_q, dec_bad, dec_nospec;
     double dec_alpha, dec_lhs, dec_rhs, dec_Delta, dec_nT;
     int nmq;               // medium columns of this CTA in this step, queued by the lane sweep
     int4 mq[SP_MQ];        // their column descriptors ...
@@ -309,6 +309,7 @@ template <int NQ, int LOSS, class Sync>
 __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &sy, WinState &ws, const int32_t *Tl,
                                           int64_t nT, int64_t k0, int64_t pb0, int64_t pb1, int G, int c, int tid,
                                           int lane, int warp, const ShareReg &sh, RowReg &rr, const DenseInfo &di,
+                                          bool spec, double alpha_s, int64_t wb, int64_t we,
                                           bool prof, long long &tprev, long long *ctal, long long tstep)
 {
     using LY = WinLayout<NQ>;
@@ -321,9 +322,12 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
     for (int64_t li = tid; li < nT; li += SNT) {
         const int32_t i = Tl[li];
         PCDN_CHECK(i >= 0 && i < a.s);
-        const double zi = ldcg(&a.z[i]);
-        const double cg = ldcg(&a.coef[i]).x;
-        const int yi = a.y[i];
+        // (the thread's first sample from registers after window 0: its z / G may already hold the
+        // speculative commit)
+        const bool rg = ws.win > 0 && li == tid;
+        const double zi = rg ? rr.zi : ldcg(&a.z[i]);
+        const double cg = rg ? rr.cg : ldcg(&a.coef[i]).x;
+        const int yi = rg ? rr.yi : a.y[i];
         double dx;
         if (ws.win == 0) {
             const int64_t r0 = __ldg(&a.row_ptr[i]), r1 = __ldg(&a.row_ptr[i + 1]);
@@ -341,6 +345,7 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
                 rr.has_dx = 1;
                 rr.r0 = r0;
                 rr.r1 = r1;
+                rr.cg = cg;
             }
         } else {
             dx = li == tid ? rr.dx : ldcg(&a.dxg[i]);
@@ -393,7 +398,24 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
             acc[LY::DELTA] += tv[e];
         }
     }
-    if (tid == 0) acc[LY::NTOUCH] = (double)nT;
+    if (tid == 0) {
+        acc[LY::NTOUCH] = (double)nT;
+        acc[LY::NOSPEC] = spec ? 0.0 : 1.0;
+    }
+    // speculative commit (a5) with alpha_s = beta^{previous q}: this CTA's samples (one per thread,
+    // in registers) and the clearing of its bitmaps, before the barrier -- the decision after it
+    // confirms (no third barrier) or corrects it (the kernel redoes the commit from registers)
+    if (spec && ws.win == 0) {
+        if (rr.i >= 0) {
+            const int32_t i = rr.i;
+            const double zn = rr.zi + alpha_s * rr.dx;
+            a.z[i] = zn;
+            a.coef[i] = coef_next(LOSS, make_double2(rr.cg, 2.0), zn, alpha_s * rr.dx, rr.yi);
+            if (rr.r1 > rr.r0)
+                for (int64_t wd = rr.r0 >> 5; wd <= ((rr.r1 - 1) >> 5); wd++) a.sbits[wd] = 0u;
+        }
+        for (int64_t wi = wb + tid; wi < we; wi += SNT) a.bits[wi] = 0u;
+    }
     if (ctal && ws.win == 0) {   // profiling mode 2: this CTA's fold + line-search time
         __syncthreads();
         if (tid == 0) ctal[1] += clock64() - tstep;
@@ -450,6 +472,7 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
         sm.dec_rhs = ra;
         sm.dec_Delta = Dl;
         sm.dec_nT = sm.tot[LY::NTOUCH];
+        sm.dec_nospec = sm.tot[LY::NOSPEC] != 0.0;
     }
     __syncthreads();
     ws.qacc = sm.dec_q;
@@ -459,6 +482,7 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
     ws.rhs = sm.dec_rhs;
     ws.Delta = sm.dec_Delta;
     ws.nT_tot = sm.dec_nT;
+    ws.nospec = sm.dec_nospec;
     ws.win++;
     __syncthreads();   // sm.dec_* / sm.red / sm.tot are reused by the next window
     if (prof) {
@@ -492,6 +516,7 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
     const int64_t row_base = wb * 32;
     if (tid == 0) sm.row_base = row_base;
     int prev_q = 0;
+    int q_spec = 0;   // the speculative commit's q: the last accepted one (the dense kernel's rule)
     const int64_t pbs0 = (int64_t)c * a.P / G, pbs1 = (int64_t)(c + 1) * a.P / G;
     const int64_t gw = (int64_t)c * SNW + warp;
 
@@ -723,6 +748,8 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
         SP_MARK(1);
         if (tid == 0) sm.nmq = 0;   // every warp left the medium-column queue before the barrier
         if (ctal && tid == 0) tstep = clock64();
+        // the next step's plan (read after this step's decision)
+        if (tid == SNT - 1 && k1 < a.ntot) sp_plan(a, k1, min(k1 + a.P, a.ntot), &sm.plan[(t + 1) & 1]);
 
         const bool fullP = Pt == a.P;
         const int64_t pb0 = k0 + (fullP ? pbs0 : (int64_t)c * Pt / G);
@@ -873,11 +900,19 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
         ws.qacc = -1;
         ws.bad = 0;
         ws.win = 0;
+        ws.nospec = 0;
+        // speculative commit (a5) before the decision's barrier: one touched sample per thread, no
+        // full column (then T is the whole block)
+        const bool spec = nT <= SNT && !di.any;
+        double alpha_s = 1.0;
+        for (int q = 0; q < q_spec; q++) alpha_s *= a.beta;
         while (true) {
             if (ws.nq <= 2)
-                sp_window<2, LOSS>(a, sm, sy, ws, Tl, nT, k0, pb0, pb1, G, c, tid, lane, warp, sh, rr, di, prof, tprev, ctal, tstep);
+                sp_window<2, LOSS>(a, sm, sy, ws, Tl, nT, k0, pb0, pb1, G, c, tid, lane, warp, sh, rr, di, spec, alpha_s,
+                                   wb, we, prof, tprev, ctal, tstep);
             else
-                sp_window<QW, LOSS>(a, sm, sy, ws, Tl, nT, k0, pb0, pb1, G, c, tid, lane, warp, sh, rr, di, prof, tprev, ctal, tstep);
+                sp_window<QW, LOSS>(a, sm, sy, ws, Tl, nT, k0, pb0, pb1, G, c, tid, lane, warp, sh, rr, di, spec, alpha_s,
+                                    wb, we, prof, tprev, ctal, tstep);
             if (ws.qacc >= 0 || ws.bad) break;
             ws.q0 += ws.nq;
             if (ws.q0 > a.qmax) break;
@@ -888,73 +923,90 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
         if (qacc > a.qmax) qacc = -1;   // window overshoot past q_max counts as exhausted
         const double alpha_acc = qacc < 0 ? 0.0 : ws.alpha;   // null step (Z10)
         prev_q = qacc < 0 ? QW : qacc;
-
-        // ---------------- commit (a5): this CTA's samples and bundle share; clear the bitmaps -----
-        // (every fold of the step finished before the decision's barrier, so the written-slot words
-        // can be cleared here even where two samples' segments share a word)
-        // (the thread's first sample from registers; the others in batches of SP_CB, all loads in
-        // flight together)
-        if (rr.i >= 0) {
-            const int32_t i = rr.i;
-            if (qacc >= 0) {
+        // the speculation hit: every CTA that could speculate did, with the accepted q -- then no
+        // third barrier (the w commit below reads registers only: P <= SNT * G)
+        const bool hit = !bad && qacc >= 0 && qacc == q_spec;
+        const bool skip3 = hit && !ws.nospec && a.P <= (int64_t)SNT * G;
+        if (qacc >= 0) q_spec = qacc;
+        if (spec) {
+            // correct a missed speculation from registers (alpha_acc = 0: the state before the step)
+            if (!hit && rr.i >= 0) {
                 const double zn = rr.zi + alpha_acc * rr.dx;
-                a.z[i] = zn;
-                const double2 cfo = LOSS == LOSS_SQ ? ldcg(&a.coef[i]) : make_double2(0.0, 0.0);
-                a.coef[i] = coef_next(LOSS, cfo, zn, alpha_acc * rr.dx, rr.yi);
+                a.z[rr.i] = zn;
+                a.coef[rr.i] = coef_next(LOSS, make_double2(rr.cg, 2.0), zn, alpha_acc * rr.dx, rr.yi);
             }
-            if (rr.r1 > rr.r0)
-                for (int64_t wd = rr.r0 >> 5; wd <= ((rr.r1 - 1) >> 5); wd++) a.sbits[wd] = 0u;
-            if (a.debug) {
-                a.dbg_dx[i] = rr.dx;
-                a.dbg_mark[i] = 1;
+            if (a.debug && rr.i >= 0) {
+                a.dbg_dx[rr.i] = rr.dx;
+                a.dbg_mark[rr.i] = 1;
             }
-        }
-        for (int64_t lb = tid + SNT; lb < nT; lb += (int64_t)SNT * SP_CB) {
-            int32_t ii[SP_CB];
-            double dxv[SP_CB], zv[SP_CB];
-            double2 cfo[SP_CB];
-            int64_t ra[SP_CB], rb[SP_CB];
-            int yv[SP_CB];
-#pragma unroll
-            for (int e = 0; e < SP_CB; e++) {
-                const int64_t li = lb + (int64_t)e * SNT;
-                ii[e] = li < nT ? Tl[li] : -1;
-            }
-#pragma unroll
-            for (int e = 0; e < SP_CB; e++) {
-                dxv[e] = zv[e] = 0.0;
-                cfo[e] = make_double2(0.0, 0.0);
-                ra[e] = rb[e] = 0;
-                yv[e] = 1;
-                if (ii[e] >= 0) {
-                    dxv[e] = ldcg(&a.dxg[ii[e]]);
-                    ra[e] = __ldg(&a.row_ptr[ii[e]]);
-                    rb[e] = __ldg(&a.row_ptr[ii[e] + 1]);
-                    if (qacc >= 0) {
-                        zv[e] = ldcg(&a.z[ii[e]]);
-                        yv[e] = (int)a.y[ii[e]];
-                        if (LOSS == LOSS_SQ) cfo[e] = ldcg(&a.coef[ii[e]]);
-                    }
-                }
-            }
-#pragma unroll
-            for (int e = 0; e < SP_CB; e++) {
-                const int32_t i = ii[e];
-                if (i < 0) continue;
+        } else {   // the commit (a5) of a CTA that could not speculate
+            // ---------------- commit (a5): this CTA's samples and bundle share; clear the bitmaps -----
+            // (every fold of the step finished before the decision's barrier, so the written-slot words
+            // can be cleared here even where two samples' segments share a word)
+            // (the thread's first sample from registers; the others in batches of SP_CB, all loads in
+            // flight together)
+            if (rr.i >= 0) {
+                const int32_t i = rr.i;
                 if (qacc >= 0) {
-                    const double zn = zv[e] + alpha_acc * dxv[e];
+                    const double zn = rr.zi + alpha_acc * rr.dx;
                     a.z[i] = zn;
-                    a.coef[i] = coef_next(LOSS, cfo[e], zn, alpha_acc * dxv[e], yv[e]);
+                    const double2 cfo = LOSS == LOSS_SQ ? ldcg(&a.coef[i]) : make_double2(0.0, 0.0);
+                    a.coef[i] = coef_next(LOSS, cfo, zn, alpha_acc * rr.dx, rr.yi);
                 }
-                if (rb[e] > ra[e])
-                    for (int64_t wd = ra[e] >> 5; wd <= ((rb[e] - 1) >> 5); wd++) a.sbits[wd] = 0u;
+                if (rr.r1 > rr.r0)
+                    for (int64_t wd = rr.r0 >> 5; wd <= ((rr.r1 - 1) >> 5); wd++) a.sbits[wd] = 0u;
                 if (a.debug) {
-                    a.dbg_dx[i] = dxv[e];
+                    a.dbg_dx[i] = rr.dx;
                     a.dbg_mark[i] = 1;
                 }
             }
+            for (int64_t lb = tid + SNT; lb < nT; lb += (int64_t)SNT * SP_CB) {
+                int32_t ii[SP_CB];
+                double dxv[SP_CB], zv[SP_CB];
+                double2 cfo[SP_CB];
+                int64_t ra[SP_CB], rb[SP_CB];
+                int yv[SP_CB];
+    #pragma unroll
+                for (int e = 0; e < SP_CB; e++) {
+                    const int64_t li = lb + (int64_t)e * SNT;
+                    ii[e] = li < nT ? Tl[li] : -1;
+                }
+    #pragma unroll
+                for (int e = 0; e < SP_CB; e++) {
+                    dxv[e] = zv[e] = 0.0;
+                    cfo[e] = make_double2(0.0, 0.0);
+                    ra[e] = rb[e] = 0;
+                    yv[e] = 1;
+                    if (ii[e] >= 0) {
+                        dxv[e] = ldcg(&a.dxg[ii[e]]);
+                        ra[e] = __ldg(&a.row_ptr[ii[e]]);
+                        rb[e] = __ldg(&a.row_ptr[ii[e] + 1]);
+                        if (qacc >= 0) {
+                            zv[e] = ldcg(&a.z[ii[e]]);
+                            yv[e] = (int)a.y[ii[e]];
+                            if (LOSS == LOSS_SQ) cfo[e] = ldcg(&a.coef[ii[e]]);
+                        }
+                    }
+                }
+    #pragma unroll
+                for (int e = 0; e < SP_CB; e++) {
+                    const int32_t i = ii[e];
+                    if (i < 0) continue;
+                    if (qacc >= 0) {
+                        const double zn = zv[e] + alpha_acc * dxv[e];
+                        a.z[i] = zn;
+                        a.coef[i] = coef_next(LOSS, cfo[e], zn, alpha_acc * dxv[e], yv[e]);
+                    }
+                    if (rb[e] > ra[e])
+                        for (int64_t wd = ra[e] >> 5; wd <= ((rb[e] - 1) >> 5); wd++) a.sbits[wd] = 0u;
+                    if (a.debug) {
+                        a.dbg_dx[i] = dxv[e];
+                        a.dbg_mark[i] = 1;
+                    }
+                }
+            }
+            for (int64_t wi = wb + tid; wi < we; wi += SNT) a.bits[wi] = 0u;
         }
-        for (int64_t wi = wb + tid; wi < we; wi += SNT) a.bits[wi] = 0u;
         if (qacc >= 0) {
             for (int64_t kb = pb0 + tid; kb < pb1; kb += (int64_t)SNT * SP_CB) {
                 int32_t jj[SP_CB];
@@ -1002,10 +1054,8 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
             sm.cnt[2] += (int64_t)ws.nT_tot;
             sm.cnt[3] += Pt;
         }
-        sy.arrive();
-        // the next step's plan, while the barrier completes
-        if (tid == SNT - 1 && k1 < a.ntot) sp_plan(a, k1, min(k1 + a.P, a.ntot), &sm.plan[(t + 1) & 1]);
-        sy.wait();
+        if (!skip3) sy.sync();
+        else __syncthreads();   // (sm.plan, written after the first barrier, before its use)
         SP_MARK(7);
         if (bad) break;
     }
