@@ -703,7 +703,7 @@ __global__ void k_chunk_compact(const int64_t *__restrict__ cpos, const int64_t 
 // inclusive sums; integer sums, so exact).  The output equals k_perm + build_heavy's twelve
 // launches.  Tile states carry the launch's epoch, so they need no clearing between launches; the
 // last tile to finish re-arms the ticket.
-constexpr int PL_NT = 256, PL_PER = 2, PL_TILE = PL_NT * PL_PER;
+constexpr int PL_NT = 256, PL_PER = 8, PL_TILE = PL_NT * PL_PER;   // (8 positions per thread: their col_ptr loads in flight together)
 constexpr int PL_Q = 4;   // prefix sums of the list build: heavy count, heavy nnz, full count, chunk count
 struct alignas(64) LbTile {
     long long agg[PL_Q];   // the tile's sums
@@ -740,16 +740,20 @@ __global__ void __launch_bounds__(PL_NT) k_prep_lists(uint64_t seed, int64_t k, 
     long long v[PL_Q] = {0, 0, 0, 0};
     const int64_t tb = (int64_t)tile * PL_TILE + (int64_t)tid * PL_PER;
 #pragma unroll
+    for (int e = 0; e < PL_PER; e++) jv[e] = tb + e < n ? (int32_t)feistel_perm(f, n, tb + e) : 0;
+    int64_t p1v[PL_PER];
+#pragma unroll
+    for (int e = 0; e < PL_PER; e++) {
+        p0v[e] = tb + e < n ? __ldg(&col_ptr[jv[e]]) : 0;
+        p1v[e] = tb + e < n ? __ldg(&col_ptr[jv[e] + 1]) : -1;
+    }
+#pragma unroll
     for (int e = 0; e < PL_PER; e++) {
         const int64_t t = tb + e;
-        jv[e] = 0;
-        p0v[e] = 0;
         lenv[e] = -1;
         if (t < n) {
-            const int32_t j = (int32_t)feistel_perm(f, n, t);
-            const int64_t p0 = __ldg(&col_ptr[j]), len = __ldg(&col_ptr[j + 1]) - p0;
-            jv[e] = j;
-            p0v[e] = p0;
+            const int32_t j = jv[e];
+            const int64_t p0 = p0v[e], len = p1v[e] - p0;
             lenv[e] = len;
             o.order[t] = j;
             o.colinfo[t] = make_colinfo(j, p0, len);
