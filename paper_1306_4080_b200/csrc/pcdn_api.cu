@@ -907,7 +907,7 @@ int pcdn_create(int64_t s, int64_t n, int64_t nnz, const int64_t *csc_col_ptr, c
     }
     if ((rc = reset_status(ctx))) return fail(rc);
     const Layout &L = ctx->L;
-    k_validate<<<grid1d(32 * (s > n ? s : n)), 256, 0, ctx->stream>>>(s, n, nnz, csc_col_ptr, csc_row_idx, csc_val,
+    k_validate<<<grid1d(std::max(nnz, s > n ? s : n)), 256, 0, ctx->stream>>>(s, n, nnz, csc_col_ptr, csc_row_idx, csc_val,
                                                                csr_row_ptr, csr_col_idx, csr_val,
                                                                loss == PCDN_LOSS_SQUARED ? nullptr : y,
                                                                ctx->at<int>(L.status), ctx->at<long long>(L.err_idx),
@@ -1645,7 +1645,7 @@ int device_csr(int64_t s, int64_t n, int64_t nnz, const int64_t *col_ptr, const 
             cudaMemsetAsync(&chk->idx, 0x7f, sizeof(long long), st) != cudaSuccess)
             rc = PCDN_ERR_CUDA;
         if (rc == PCDN_OK) {
-            k_validate<<<grid1d(32 * n), 256, 0, st>>>(s, n, nnz, col_ptr, row_idx, val, nullptr, nullptr, nullptr, nullptr,
+            k_validate<<<grid1d(std::max(nnz, n)), 256, 0, st>>>(s, n, nnz, col_ptr, row_idx, val, nullptr, nullptr, nullptr, nullptr,
                                                   &chk->status, &chk->idx, &chk->what);
             if (cudaGetLastError() != cudaSuccess ||
                 cudaMemcpyAsync(&h, chk, sizeof(Chk), cudaMemcpyDeviceToHost, st) != cudaSuccess ||

@@ -2329,50 +2329,63 @@ __global__ void k_check_finite(const double *__restrict__ t, int64_t s, int *sta
         }
 }
 
-// Input validation: code 1 + first offending index.  A warp per column (per row),
-// lanes over its nonzeros: a thread per column had left config 5's 1.96M-nonzero column to one
-// thread (0.36 s of a create).
+// is p the first offset of a segment of ptr[0..m] (ptr nondecreasing)?  (binary search)
+__device__ __forceinline__ bool seg_start(const int64_t *__restrict__ ptr, int64_t m, int64_t p)
+{
+    int64_t lo = 0, hi = m;   // first k with ptr[k] >= p
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (ptr[mid] < p) lo = mid + 1; else hi = mid;
+    }
+    return lo <= m && ptr[lo] == p;
+}
+
+// Input validation: code 1 + first offending index.  The pointer arrays a thread
+// per entry; the nonzeros flat over the whole array (coalesced): an index not above its
+// predecessor is an error unless it starts a segment (binary search in the pointer array) -- a
+// thread or warp per column had left config 5's 1.96M-nonzero column to one of them (0.36 s).
 __global__ void k_validate(int64_t s, int64_t n, int64_t nnz, const int64_t *__restrict__ col_ptr,
                            const int32_t *__restrict__ row_idx, const float *__restrict__ val,
                            const int64_t *__restrict__ row_ptr, const int32_t *__restrict__ col_idx,
                            const float *__restrict__ csr_val, const int8_t *__restrict__ y,
                            int *status, long long *err_idx, int *err_what)
 {
-    const int lane = threadIdx.x & 31;
-    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     auto fail = [&](int what, int64_t idx) {
         atomicMax(status, 1);
         if (atomicMin(err_idx, (long long)idx) > (long long)idx) atomicExch(err_what, what);
     };
-    for (int64_t j = gw; j < n; j += nwp) {
+    bool cbad = false, rbad = false;   // this thread saw a broken pointer array (flat checks then stop)
+    for (int64_t j = t0; j < n; j += stride) {
         const int64_t a0 = col_ptr[j], a1 = col_ptr[j + 1];
-        if (lane == 0) {
-            if (j == 0 && a0 != 0) fail(1, 0);
-            if (j == n - 1 && a1 != nnz) fail(2, j);
-            if (a1 < a0 || a0 < 0 || a1 > nnz) fail(3, j);
-        }
-        if (a1 < a0 || a0 < 0 || a1 > nnz) continue;
-        for (int64_t p = a0 + lane; p < a1; p += 32) {
-            const int32_t r = row_idx[p];
-            if (r < 0 || r >= s) fail(4, p);
-            if (p > a0 && r <= row_idx[p - 1]) fail(5, p);
-            if (!isfinite(val[p])) fail(6, p);
+        if (j == 0 && a0 != 0) fail(1, 0);
+        if (j == n - 1 && a1 != nnz) fail(2, j);
+        if (a1 < a0 || a0 < 0 || a1 > nnz) {
+            fail(3, j);
+            cbad = true;
         }
     }
-    for (int64_t i = gw; row_ptr && i < s; i += nwp) {   // (row_ptr == NULL: the CSC alone)
+    for (int64_t i = t0; row_ptr && i < s; i += stride) {   // (row_ptr == NULL: the CSC alone)
         const int64_t a0 = row_ptr[i], a1 = row_ptr[i + 1];
-        if (lane == 0) {
-            if (i == 0 && a0 != 0) fail(7, 0);
-            if (i == s - 1 && a1 != nnz) fail(8, i);
-            if (a1 < a0 || a0 < 0 || a1 > nnz) fail(9, i);
-            if (y && y[i] != 1 && y[i] != -1) fail(13, i);   // labels unused by the squared loss
+        if (i == 0 && a0 != 0) fail(7, 0);
+        if (i == s - 1 && a1 != nnz) fail(8, i);
+        if (a1 < a0 || a0 < 0 || a1 > nnz) {
+            fail(9, i);
+            rbad = true;
         }
-        if (a1 < a0 || a0 < 0 || a1 > nnz) continue;
-        for (int64_t p = a0 + lane; p < a1; p += 32) {
+        if (y && y[i] != 1 && y[i] != -1) fail(13, i);   // labels unused by the squared loss
+    }
+    if (cbad || rbad) return;
+    for (int64_t p = t0; p < nnz; p += stride) {
+        const int32_t r = row_idx[p];
+        if (r < 0 || r >= s) fail(4, p);
+        if (p > 0 && r <= row_idx[p - 1] && !seg_start(col_ptr, n, p)) fail(5, p);
+        if (!isfinite(val[p])) fail(6, p);
+        if (row_ptr) {
             const int32_t cidx = col_idx[p];
             if (cidx < 0 || cidx >= n) fail(10, p);
-            if (p > a0 && cidx <= col_idx[p - 1]) fail(11, p);
+            if (p > 0 && cidx <= col_idx[p - 1] && !seg_start(row_ptr, s, p)) fail(11, p);
             if (!isfinite(csr_val[p])) fail(12, p);
         }
     }
