@@ -55,6 +55,7 @@ constexpr int SP_CH = 256;      // default heavy_len of the sparse kernel: longe
 constexpr int SP_FOLD = 4;      // record loads of one sample in flight together in the fold
 constexpr int SP_CB = 4;        // samples / positions of a thread with their loads in flight together (commit)
 constexpr int SP_MQ = 256;      // per-CTA queue of a step's medium columns (one warp each, after the lane sweep)
+constexpr int SP_GT_ROWS = 160; // grids up to this many CTAs read every partial row in one batch of loads
 static_assert(SP_CTA_MUL == SNW, "a heavy chunk is one warp-register range (32 * SP_WR) per warp of the CTA");
 
 struct SpPlan {
@@ -82,6 +83,7 @@ struct SpSmem {
     double dxd[TSM];
     int64_t row_base;
     int32_t tl[TSM];
+    double pv[SP_GT_ROWS * 16];   // the partial rows of every CTA (sp_grid_totals), up to SP_GT_ROWS CTAs
 };
 
 __device__ __forceinline__ int atom_add_acq_rel(int *p, int v)
@@ -281,18 +283,43 @@ __device__ __noinline__ double sp_dense_dx(const int32_t *__restrict__ flist, co
     return dx;
 }
 
-// grid_totals (pcdn_kernels.cuh) for SNW warps: warp w sums rows c2 = w, w + SNW, ... in order,
-// then warp 0 adds the warp sums in warp order (a fixed order)
+// Totals of the G partial rows part[c2][0..W) in a fixed order, into tot[0..W) (valid for every
+// thread after the call).  Up to SP_GT_ROWS CTAs: every thread loads its share of the G x W values
+// in one batch (a single L2 round trip), then warp q sums slot q over the rows (lane-strided, a
+// fixed xor tree).  Beyond: warp w sums rows w, w + SNW, ... and warp 0 the warp sums.
 template <int W>
-__device__ __forceinline__ void sp_grid_totals(const double *part, int G, double (*red)[32], double *tot, int lane,
-                                               int warp)
+__device__ __forceinline__ void sp_grid_totals(const double *part, int G, double (*red)[32], double *tot, double *pv,
+                                               int tid, int lane, int warp)
 {
-    double v = 0.0;
+    if (G <= SP_GT_ROWS) {
+        constexpr int K = (SP_GT_ROWS * W + SNT - 1) / SNT;   // values per thread
+        double v[K];
+#pragma unroll
+        for (int e = 0; e < K; e++) {
+            const int idx = tid + e * SNT;
+            v[e] = idx < G * W ? ldcg(&part[(int64_t)(idx / W) * NPART + (idx % W)]) : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < K; e++) {
+            const int idx = tid + e * SNT;
+            if (idx < G * W) pv[idx] = v[e];
+        }
+        __syncthreads();
+        for (int q = warp; q < W; q += SNW) {
+            double x = 0.0;
+            for (int r = lane; r < G; r += 32) x += pv[r * W + q];
+            x = warp_sum(x);
+            if (lane == 0) tot[q] = x;
+        }
+        __syncthreads();
+        return;
+    }
+    double x = 0.0;
     if (lane < W) {
 #pragma unroll 4
-        for (int c2 = warp; c2 < G; c2 += SNW) v += ldcg(&part[(int64_t)c2 * NPART + lane]);
+        for (int c2 = warp; c2 < G; c2 += SNW) x += ldcg(&part[(int64_t)c2 * NPART + lane]);
     }
-    red[warp][lane] = v;
+    red[warp][lane] = x;
     __syncthreads();
     if (warp == 0 && lane < W) {
         double t = 0.0;
@@ -300,7 +327,7 @@ __device__ __forceinline__ void sp_grid_totals(const double *part, int G, double
         for (int w2 = 0; w2 < SNW; w2++) t += red[w2][lane];
         tot[lane] = t;
     }
-    __syncwarp();
+    __syncthreads();
 }
 
 // One Armijo window over q0 .. q0+NQ-1 (Eq.6 with Eq.12 from retained quantities); window 0 also
@@ -444,7 +471,7 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
         sm.pacc[4] += now - tprev;
         tprev = now;
     }
-    sp_grid_totals<W>(part, G, sm.red, sm.tot, lane, warp);
+    sp_grid_totals<W>(part, G, sm.red, sm.tot, sm.pv, tid, lane, warp);
     if (warp == 0 && lane == 0) {
         const double Dl = sm.tot[LY::DELTA];
         int qa = -1, badl = 0;
