@@ -193,6 +193,8 @@ __device__ __forceinline__ HPart ld_hpart(const HPart *p)
     return r;
 }
 
+__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long *p)
 {
     unsigned long long v;

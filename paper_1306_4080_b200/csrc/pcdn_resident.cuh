@@ -540,10 +540,6 @@ __device__ __forceinline__ void res_stage_cols(const StepArgs &a, ResFixed &fx, 
 // descriptors, the row / value lines and w_j of the NW x R_RP staged columns), issued by one warp
 // during the fold, where the upper warps idle when the step touches fewer samples than threads:
 // the staging after the partial-row send then hits L2 instead of HBM.
-__device__ __forceinline__ void prefetch_l2(const void *p)
-{
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
 __device__ __forceinline__ void res_l2_prefetch_next(const StepArgs &a, int64_t kb, int64_t ke, int c, int G, int lane)
 {
     const int64_t GN = (int64_t)G * NW;

@@ -330,6 +330,7 @@ __device__ __forceinline__ void sp_grid_totals(const double *part, int G, double
     __syncthreads();
 }
 
+
 // One Armijo window over q0 .. q0+NQ-1 (Eq.6 with Eq.12 from retained quantities); window 0 also
 // folds d'x_i.  Then the grid barrier and the decision taken identically by every CTA.
 template <int NQ, int LOSS, class Sync>
