@@ -924,7 +924,10 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
         // ---------------- phase C2+C3: fold d'x_i (a3) and the Armijo windows (a4) --------------
         WinState ws;
         ws.q0 = 0;
-        ws.nq = prev_q <= 1 ? 2 : QW;
+        // the first window: one candidate after a step that accepted q = 0 (almost every step at the
+        // configured P: the second candidate's loss changes would sit on every step's critical path),
+        // two after q = 1, six otherwise
+        ws.nq = prev_q == 0 ? 1 : prev_q <= 1 ? 2 : QW;
         ws.qacc = -1;
         ws.bad = 0;
         ws.win = 0;
@@ -935,7 +938,10 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
         double alpha_s = 1.0;
         for (int q = 0; q < q_spec; q++) alpha_s *= a.beta;
         while (true) {
-            if (ws.nq <= 2)
+            if (ws.nq == 1)
+                sp_window<1, LOSS>(a, sm, sy, ws, Tl, nT, k0, pb0, pb1, G, c, tid, lane, warp, sh, rr, di, spec, alpha_s,
+                                   wb, we, prof, tprev, ctal, tstep);
+            else if (ws.nq <= 2)
                 sp_window<2, LOSS>(a, sm, sy, ws, Tl, nT, k0, pb0, pb1, G, c, tid, lane, warp, sh, rr, di, spec, alpha_s,
                                    wb, we, prof, tprev, ctal, tstep);
             else

@@ -22,6 +22,7 @@ ap.add_argument("--P", type=int, default=1)
 ap.add_argument("--modes", default="1,2,3,5")
 ap.add_argument("--s", type=int, default=20000)
 ap.add_argument("--n", type=int, default=200000)
+ap.add_argument("--profile", action="store_true", help="phase cycles of CTA 0 (needs PCDN_LIB=.../libpcdn_prof.so)")
 args = ap.parse_args()
 s_, n_ = args.s, args.n
 rng = np.random.default_rng(0)
@@ -48,8 +49,15 @@ for mode in [int(m) for m in args.modes.split(",")]:
     s.reset()
     s.solve(args.P, seed=1, max_outer=1)
     s.reset()
+    if args.profile:
+        pk.pcdn_set_profile(s.ctx, 1)
     r = s.solve(args.P, seed=1, max_outer=1)
-    used = pk.pcdn_phase_cycles(s.ctx)[1]
-    print(json.dumps({"mode_req": mode, "mode_used": used, "P": args.P, "steps": r["steps"],
-                      "step_us": 1e3 * r["t_step_kernel_ms"] / r["steps"], "nnz": int(r["nnz_processed"])}), flush=True)
+    cyc, used = pk.pcdn_phase_cycles(s.ctx)
+    if args.profile:
+        pk.pcdn_set_profile(s.ctx, 0)
+    out = {"mode_req": mode, "mode_used": used, "P": args.P, "steps": r["steps"],
+           "step_us": 1e3 * r["t_step_kernel_ms"] / r["steps"], "nnz": int(r["nnz_processed"])}
+    if args.profile:
+        out["phase_cycles"] = (cyc / r["steps"]).round().tolist()
+    print(json.dumps(out), flush=True)
 s.close()
