@@ -13,6 +13,9 @@ import paper_1306_4080_b200 as pk  # noqa: E402
 
 NAMES = ["A rest", "sync1", "C1 touched set", "C2 fold+LS loops", "C3 reduce+xbar", "decide",
          "commit", "sync3", "A light", "A' search", "A' rounds", "A' gridsync"]
+# k_step_sparse (launch modes 1, 2): its SP_MARK slots
+SPARSE_NAMES = ["A2 heavy scatter", "sync1", "C1 touched set", "fold+LS", "sync2", "decide", "commit", "sync3",
+                "A light+medium", "A1 heavy chunks"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
@@ -39,10 +42,11 @@ for mode in [int(m) for m in args.modes.split(",")]:
         cyc, m = pk.pcdn_phase_cycles(s.ctx)
         pk.pcdn_set_profile(s.ctx, 0)
         steps = r["steps"]
-        us = cyc[:len(NAMES)] / steps / args.mhz
+        names = SPARSE_NAMES if m in (1, 2) else NAMES
+        us = cyc[:len(names)] / steps / args.mhz
         key = f"mode{m}_ctas{ctas}"
-        res[key] = dict(step_us_kernel=r["t_step_kernel_ms"] * 1e3 / steps, phases_us=dict(zip(NAMES, us.round(3).tolist())),
+        res[key] = dict(step_us_kernel=r["t_step_kernel_ms"] * 1e3 / steps, phases_us=dict(zip(names, us.round(3).tolist())),
                         steps=steps)
         print(key, f"kernel {r['t_step_kernel_ms']*1e3/steps:.2f} us/step |",
-              " ".join(f"{n}={u:.2f}" for n, u in zip(NAMES, us)), flush=True)
+              " ".join(f"{n}={u:.2f}" for n, u in zip(names, us)), flush=True)
 print(json.dumps(res))

@@ -24,7 +24,7 @@ ap.add_argument("--outer", type=int, default=1)
 ap.add_argument("--profile", action="store_true")
 ap.add_argument("--heavy", type=int, default=0, help="heavy_len launch knob (0 = keep)")
 ap.add_argument("--ctas", default="0", help="comma list of CTA counts (launch knob; 0 = all co-resident)")
-ap.add_argument("--l2", type=int, default=1, help="persisting-L2 window of the HBM-state kernels (pcdn_set_l2_persist)")
+ap.add_argument("--l2", type=int, default=0, help="persisting-L2 window of the HBM-state kernels (pcdn_set_l2_persist; the library default is off)")
 args = ap.parse_args()
 t0 = time.time()
 prob = synth.config(args.cfg, loss=args.loss)
