@@ -152,7 +152,8 @@ int pcdn_set_trace(pcdn_ctx *ctx, int32_t *q_trace, double *F_trace, int64_t cap
 /* Debug flags.  on & 1: record T and d'x of each step (for pcdn_last_touched).  on & 2: build
  * each outer iteration's lists with the reference sequence of launches (k_perm, device-wide
  * scans, compactions) instead of the single-pass k_prep_lists -- a test knob; the lists are
- * identical. */
+ * identical.  on & 4: the dense kernel as one launch per outer iteration (test knob; results
+ * bit-identical). */
 int pcdn_set_debug(pcdn_ctx *ctx, int on);
 
 /* Launch knobs (results stay within fp64 rounding-order differences; for a fixed setting they

@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
     bool inflight = false;   // a tile copy was issued and not yet waited for (for step inflight_t)
     int64_t inflight_t = 0;
     long long tprev = 0;
-    const bool prof = a.prof != nullptr && c == 0 && tid == 0;
+    const bool prof = PCDN_PROFILE && a.prof != nullptr && c == 0 && tid == 0;
 #define DPROF(i)                                 \
     do {                                         \
         if (prof) {                              \
@@ -386,6 +386,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
             wcount++;
             sy.sync();
         }
+        DPROF(13);
         if (qacc > a.qmax) qacc = -1;
         if (qacc < 0) alpha_acc = 0.0;
         prev_q = qacc < 0 ? QW : qacc;
@@ -416,6 +417,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
                 }
             }
         }
+        DPROF(14);
         if (c == 0 && tid == 0) {
             double F = sm.F;
             if (qacc >= 0) F = F + lhs_acc;
@@ -480,6 +482,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
         dense_gphase(a, tile, sm.coef[pend && pend_any ? cc ^ 1 : cc], k0, Pt, r0, R, Rs, c, part_gh, tid);
         DPROF(6);
         sy.arrive();   // B1: the g/h partials of this step and the line-search partials of the last
+        DPROF(10);
         // the next step's tile, issued while the barrier completes (in the background of this
         // step's remaining phases)
         if (use_tile && t + 1 < a.nsteps) {
@@ -565,6 +568,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
             any |= d != 0.0;
         }
         const bool dense_any = __syncthreads_or(any) != 0;
+        DPROF(11);
         if (dense_any) {
             const int C = R >= NT ? 1 : (int)min(NT / max(R, 1), Pt);
             for (int rb = 0; rb < R; rb += NT) {
@@ -600,6 +604,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_dense(StepArgs a)
                     sm.dpart[tid] = x;
                 }
             }
+            DPROF(12);
             if (C > 1) {
                 __syncthreads();
                 for (int r = tid; r < R; r += NT) {

@@ -27,6 +27,12 @@ namespace pcdn {
 // Checked build (-DPCDN_CHECKS=1, libpcdn_checked.so): device-side bounds and protocol checks that
 // trap with the failing condition.  compute-sanitizer is closed on this pool; the GPU test suite
 // runs against this build instead (scripts/checked_run.sh).  The product build compiles them out.
+// Profiling instrumentation (pcdn_set_profile phase cycles, pcdn_warp_timeline) is compiled into
+// the step kernels only with -DPCDN_PROFILE=1 (libpcdn_prof.so, loaded through PCDN_LIB by the
+// profiling scripts): even as untaken branches it costs the product kernels registers and time.
+#ifndef PCDN_PROFILE
+#define PCDN_PROFILE 0
+#endif
 #ifndef PCDN_CHECKS
 #define PCDN_CHECKS 0
 #endif
@@ -1499,7 +1505,7 @@ __global__ void __launch_bounds__(NT, Sync::kMinBlocks) k_step(StepArgs a)
     const int64_t pbs0 = (int64_t)c * a.P / G, pbs1 = (int64_t)(c + 1) * a.P / G;
 
     long long tprev = 0;
-    const bool prof = a.prof != nullptr && c == 0 && tid == 0;
+    const bool prof = PCDN_PROFILE && a.prof != nullptr && c == 0 && tid == 0;
     if (tid < 16) sm.pacc[tid] = 0;
 #define PROF_MARK(i)                              \
     do {                                          \

@@ -973,7 +973,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
     R.my_ovf = fx.ovf_base[c];
 
     ResProf pr;
-    pr.on = a.prof != nullptr && c == 0 && tid == 0;
+    pr.on = PCDN_PROFILE && a.prof != nullptr && c == 0 && tid == 0;
     pr.t = 0;
     const bool prof = pr.on;
 #define PROF_MARK(i) pr.mark(fx, i)
@@ -986,7 +986,7 @@ __global__ void __launch_bounds__(NT, 1) k_step_res(StepArgs a)
     for (int64_t t = 0; t < a.nsteps; t++) {
         pr.start();
         R.cb = (int)(t & 1);
-        R.tl = (a.tl && c == 0 && t < TL_STEPS) ? a.tl + (t * NW + warp) * TL_PTS : nullptr;
+        R.tl = (PCDN_PROFILE && a.tl && c == 0 && t < TL_STEPS) ? a.tl + (t * NW + warp) * TL_PTS : nullptr;
         RTL(R, 0);
         const int64_t k0 = t * a.P;
         const int64_t k1 = min(k0 + a.P, a.ntot);

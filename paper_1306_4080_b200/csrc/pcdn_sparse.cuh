@@ -34,12 +34,8 @@
 namespace pcdn {
 
 // Profiling instrumentation (phase cycles of CTA 0 for pcdn_set_profile(ctx, 1); per-CTA phase
-// sums for mode 2) is compiled in only with -DPCDN_PROFILE=1 (a separate build, loaded through
-// PCDN_LIB by the profiling scripts): even as untaken branches it cost the production kernel
-// registers and ~5 us per config-5 step.
-#ifndef PCDN_PROFILE
-#define PCDN_PROFILE 0
-#endif
+// sums for mode 2) is compiled in only with -DPCDN_PROFILE=1 (pcdn_kernels.cuh): even as untaken
+// branches it cost the production kernel registers and ~5 us per config-5 step.
 
 // CTA shape of the sparse kernel: 384 threads per SM (one CTA per SM) leave each thread up to 168
 // registers -- at 512 threads the kernel's live state spilled (config 5: 25.7 us per step at 512,
@@ -240,6 +236,19 @@ __device__ __forceinline__ uint32_t sp_word_mask(int64_t wd, int64_t r0, int64_t
     if (wd == ((r1 - 1) >> 5)) m &= 0xffffffffu >> (31 - ((r1 - 1) & 31));
     return m;
 }
+// Clear sample i's written-slot bits (its CSR segment [r0, r1)) before the decision's barrier (the
+// speculative commit): a word shared with a neighbouring sample's segment -- which another thread,
+// or another CTA at a block boundary, may not have folded yet -- loses only this sample's bits.
+// (Clearing whole words here lost a neighbour's records whenever its fold ran later.)
+__device__ __forceinline__ void sp_clear_own_slots(const StepArgs &a, int64_t r0, int64_t r1)
+{
+    if (r1 <= r0) return;
+    for (int64_t wd = r0 >> 5; wd <= ((r1 - 1) >> 5); wd++) {
+        const uint32_t m = sp_word_mask(wd, r0, r1);
+        if (m == 0xffffffffu) a.sbits[wd] = 0u;
+        else atomicAnd(&a.sbits[wd], ~m);
+    }
+}
 __device__ __forceinline__ double sp_fold(const StepArgs &a, int64_t r0, int64_t r1)
 {
     double dx = 0.0;
@@ -439,8 +448,7 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
             const double zn = rr.zi + alpha_s * rr.dx;
             a.z[i] = zn;
             a.coef[i] = coef_next(LOSS, make_double2(rr.cg, 2.0), zn, alpha_s * rr.dx, rr.yi);
-            if (rr.r1 > rr.r0)
-                for (int64_t wd = rr.r0 >> 5; wd <= ((rr.r1 - 1) >> 5); wd++) a.sbits[wd] = 0u;
+            sp_clear_own_slots(a, rr.r0, rr.r1);
         }
         for (int64_t wi = wb + tid; wi < we; wi += SNT) a.bits[wi] = 0u;
     }

@@ -17,6 +17,10 @@ NAMES = ["A rest", "sync1", "C1 touched set", "C2 fold+LS loops", "C3 reduce+xba
 SPARSE_NAMES = ["A2 heavy scatter", "sync1", "C1 touched set", "fold+LS", "sync2", "decide", "commit", "sync3",
                 "A light+medium", "A1 heavy chunks"]
 
+# k_step_dense (launch mode 4): its DPROF slots (in order along a step)
+DENSE_NAMES = ["B1 fence+prefetch issue", "B1 wait", "D finish cols", "B2", "X d'x", "LS", "G", "-", "tile wait",
+               "resolve tail(commit+F)", "B1 arrive", "X dk load+or", "X chunks", "resolve decide", "resolve commit z/w"]
+
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--P", type=int, default=None)
@@ -42,7 +46,7 @@ for mode in [int(m) for m in args.modes.split(",")]:
         cyc, m = pk.pcdn_phase_cycles(s.ctx)
         pk.pcdn_set_profile(s.ctx, 0)
         steps = r["steps"]
-        names = SPARSE_NAMES if m in (1, 2) else NAMES
+        names = SPARSE_NAMES if m in (1, 2) else DENSE_NAMES if m == 4 else NAMES
         us = cyc[:len(names)] / steps / args.mhz
         key = f"mode{m}_ctas{ctas}"
         res[key] = dict(step_us_kernel=r["t_step_kernel_ms"] * 1e3 / steps, phases_us=dict(zip(names, us.round(3).tolist())),

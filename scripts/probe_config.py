@@ -24,6 +24,7 @@ ap.add_argument("--outer", type=int, default=1)
 ap.add_argument("--profile", action="store_true")
 ap.add_argument("--heavy", type=int, default=0, help="heavy_len launch knob (0 = keep)")
 ap.add_argument("--ctas", default="0", help="comma list of CTA counts (launch knob; 0 = all co-resident)")
+ap.add_argument("--debug", default="0", help="comma list of pcdn_set_debug values (e.g. 8: no next-step staging)")
 ap.add_argument("--l2", type=int, default=0, help="persisting-L2 window of the HBM-state kernels (pcdn_set_l2_persist; the library default is off)")
 args = ap.parse_args()
 t0 = time.time()
@@ -34,8 +35,10 @@ pk.pcdn_set_l2_persist(s.ctx, args.l2)
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
 Ps = [int(x) for x in args.P.split(",") if x] or [prob.P]
-for P, mode, ctas in [(P, int(m), int(g)) for P in Ps for m in args.modes.split(",") for g in args.ctas.split(",")]:
+for P, mode, ctas, dbg in [(P, int(m), int(g), int(d)) for P in Ps for m in args.modes.split(",") for g in args.ctas.split(",")
+                           for d in args.debug.split(",")]:
     if True:
+        pk.pcdn_set_debug(s.ctx, dbg)
         try:
             s.set_launch(mode, ctas, args.heavy)
         except pk.PCDNError as e:
@@ -53,7 +56,7 @@ for P, mode, ctas in [(P, int(m), int(g)) for P in Ps for m in args.modes.split(
         steps = r["steps"]
         kms = r["t_step_kernel_ms"]
         gbs = r["alg_bytes"] / (kms / 1e3) / 1e9
-        out = {"cfg": args.cfg, "P": P, "mode_req": mode, "ctas": ctas, "mode_used": used, "heavy_len": args.heavy, "outer": r["outer_iters"],
+        out = {"cfg": args.cfg, "P": P, "debug": dbg, "mode_req": mode, "ctas": ctas, "mode_used": used, "heavy_len": args.heavy, "outer": r["outer_iters"],
                "steps": steps, "step_us": 1e3 * kms / steps, "kernel_ms_per_outer": kms / max(1, r["outer_iters"]),
                "gpu_ms_per_outer": r["t_gpu_ms"] / max(1, r["outer_iters"]),
                "alg_bytes_per_step": r["alg_bytes"] / steps, "kernel_alg_GBs": gbs, "frac_measured_hbm": gbs / peak,
