@@ -33,6 +33,116 @@
 
 namespace pcdn {
 
+// L2 eviction priorities of this kernel's accesses (PTX .L2::cache_hint with a createpolicy
+// policy).  PCDN_L2_STREAM: the once-per-outer-iteration streams (CSC row indices, values, CSR
+// slots) and the records (dead after the fold); PCDN_L2_STATE: the per-sample state gathered at
+// random every step (z, the cached factors, row pointers, bitmaps, d'x).  0 = plain accesses,
+// 1 = evict_first, 2 = evict_last, 3 = evict_normal.  Config 5 (LR, P = 4096 / 10^5 / 10^6, one
+// outer iteration; profiles/r2c/l2a_*, l2b_*): plain 21.47 / 86.2 / 506 us per step, streams
+// evict_first 21.11 / 83.7, state evict_last 20.88 / 83.6, both 20.65 / 80.6 / 495 us; records
+// evict_normal with both 20.86 / 82.8.
+#ifndef PCDN_L2_STREAM
+#define PCDN_L2_STREAM 1
+#endif
+#ifndef PCDN_L2_STATE
+#define PCDN_L2_STATE 2
+#endif
+#ifndef PCDN_L2_REC
+#define PCDN_L2_REC PCDN_L2_STREAM
+#endif
+template <int K>
+__device__ __forceinline__ uint64_t l2pol()
+{
+    uint64_t p = 0;
+    if (K == 1) asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    if (K == 2) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    if (K == 3) asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// read-only streams (non-coherent path)
+template <int K>
+__device__ __forceinline__ int32_t ldro(const int32_t *p)
+{
+    if (K == 0) return __ldg(p);
+    int32_t v;
+    asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(l2pol<K>()));
+    return v;
+}
+template <int K>
+__device__ __forceinline__ uint32_t ldro(const uint32_t *p)
+{
+    if (K == 0) return __ldg(p);
+    uint32_t v;
+    asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(l2pol<K>()));
+    return v;
+}
+template <int K>
+__device__ __forceinline__ float ldro(const float *p)
+{
+    if (K == 0) return __ldg(p);
+    float v;
+    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(l2pol<K>()));
+    return v;
+}
+template <int K>
+__device__ __forceinline__ int64_t ldro(const int64_t *p)
+{
+    if (K == 0) return __ldg((const long long *)p);
+    int64_t v;
+    asm("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(l2pol<K>()));
+    return v;
+}
+// mutable state (L2-coherent .cg loads; volatile: never merged or moved across the kernel's barriers)
+template <int K>
+__device__ __forceinline__ double ldst(const double *p)
+{
+    if (K == 0) return __ldcg(p);
+    double v;
+    asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2pol<K>()));
+    return v;
+}
+template <int K>
+__device__ __forceinline__ double2 ldst(const double2 *p)
+{
+    if (K == 0) return __ldcg(p);
+    double2 v;
+    asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(l2pol<K>()));
+    return v;
+}
+template <int K>
+__device__ __forceinline__ uint32_t ldst(const uint32_t *p)
+{
+    if (K == 0) return __ldcg(p);
+    uint32_t v;
+    asm volatile("ld.global.cg.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(l2pol<K>()));
+    return v;
+}
+template <int K>
+__device__ __forceinline__ void stst(double *p, double v)
+{
+    if (K == 0) { *p = v; return; }
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(l2pol<K>()) : "memory");
+}
+template <int K>
+__device__ __forceinline__ void stst(double2 *p, double2 v)
+{
+    if (K == 0) { *p = v; return; }
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(l2pol<K>()) : "memory");
+}
+template <int K>
+__device__ __forceinline__ void stcg_rec(double *p, double v)
+{
+    if (K == 0) { __stcg(p, v); return; }
+    asm volatile("st.global.cg.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(l2pol<K>()) : "memory");
+}
+template <int K>
+__device__ __forceinline__ void red_or(uint32_t *p, uint32_t v)
+{
+    if (K == 0) { atomicOr(p, v); return; }
+    asm volatile("red.global.or.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(l2pol<K>()) : "memory");
+}
+constexpr int SK = PCDN_L2_STREAM, TK = PCDN_L2_STATE, RK = PCDN_L2_REC;
+
 // Profiling instrumentation (phase cycles of CTA 0 for pcdn_set_profile(ctx, 1); per-CTA phase
 // sums for mode 2) is compiled in only with -DPCDN_PROFILE=1 (pcdn_kernels.cuh): even as untaken
 // branches it cost the production kernel registers and ~5 us per config-5 step.
@@ -98,9 +208,9 @@ __device__ __forceinline__ void sp_emit(const StepArgs &a, int32_t i, uint32_t s
 {
     PCDN_CHECK(i >= 0 && i < a.s);
     PCDN_CHECK(slot >= (uint32_t)__ldg(&a.row_ptr[i]) && slot < (uint32_t)__ldg(&a.row_ptr[i + 1]));
-    __stcg(&a.rv[slot], v);
-    atomicOr(&a.sbits[slot >> 5], 1u << (slot & 31));
-    atomicOr(&a.bits[i >> 5], 1u << (i & 31));
+    stcg_rec<RK>(&a.rv[slot], v);
+    red_or<TK>(&a.sbits[slot >> 5], 1u << (slot & 31));
+    red_or<TK>(&a.bits[i >> 5], 1u << (i & 31));
 }
 
 __device__ __forceinline__ void sp_store_dir(const StepArgs &a, int64_t k, const Dir &r)
@@ -127,9 +237,9 @@ __device__ __forceinline__ void sp_scatter(const StepArgs &a, int64_t p0, int64_
             const int64_t p = pb + 32 * e;
             ri[e] = -1;
             if (p < p1) {
-                ri[e] = __ldg(&a.row_idx[p]);
-                sl[e] = __ldg(&a.cslot[p]);
-                xv[e] = __ldg(&a.val[p]);
+                ri[e] = ldro<SK>(&a.row_idx[p]);
+                sl[e] = ldro<SK>(&a.cslot[p]);
+                xv[e] = ldro<SK>(&a.val[p]);
             }
         }
 #pragma unroll
@@ -156,14 +266,14 @@ __device__ __forceinline__ void sp_range_gh(const StepArgs &a, int64_t p0, int64
         r.sl[e] = 0;
         r.xv[e] = 0.f;
         if (p < p1) {
-            r.ri[e] = __ldg(&a.row_idx[p]);
-            r.sl[e] = __ldg(&a.cslot[p]);
-            r.xv[e] = __ldg(&a.val[p]);
+            r.ri[e] = ldro<SK>(&a.row_idx[p]);
+            r.sl[e] = ldro<SK>(&a.cslot[p]);
+            r.xv[e] = ldro<SK>(&a.val[p]);
         }
     }
     double2 cf[SP_WR];
 #pragma unroll
-    for (int e = 0; e < SP_WR; e++) cf[e] = r.ri[e] >= 0 ? ldcg(&a.coef[r.ri[e]]) : make_double2(0.0, 0.0);
+    for (int e = 0; e < SP_WR; e++) cf[e] = r.ri[e] >= 0 ? ldst<TK>(&a.coef[r.ri[e]]) : make_double2(0.0, 0.0);
     double g = 0.0, h = 0.0;
 #pragma unroll
     for (int e = 0; e < SP_WR; e++) {
@@ -222,7 +332,7 @@ __device__ __forceinline__ double sp_fold_word(const StepArgs &a, int64_t wd, ui
         }
         double v[SP_FOLD];
 #pragma unroll
-        for (int r = 0; r < SP_FOLD; r++) v[r] = sl[r] != 0xffffffffu ? ldcg(&a.rv[sl[r]]) : 0.0;
+        for (int r = 0; r < SP_FOLD; r++) v[r] = sl[r] != 0xffffffffu ? ldst<RK>(&a.rv[sl[r]]) : 0.0;
 #pragma unroll
         for (int r = 0; r < SP_FOLD; r++)
             if (sl[r] != 0xffffffffu) dx += v[r];
@@ -256,12 +366,12 @@ __device__ __forceinline__ double sp_fold(const StepArgs &a, int64_t r0, int64_t
     const int64_t w0 = r0 >> 5, w1 = (r1 - 1) >> 5;
     uint32_t m3[3];
 #pragma unroll
-    for (int u = 0; u < 3; u++) m3[u] = w0 + u <= w1 ? ldcg(&a.sbits[w0 + u]) & sp_word_mask(w0 + u, r0, r1) : 0u;
+    for (int u = 0; u < 3; u++) m3[u] = w0 + u <= w1 ? ldst<TK>(&a.sbits[w0 + u]) & sp_word_mask(w0 + u, r0, r1) : 0u;
 #pragma unroll
     for (int u = 0; u < 3; u++)
         if (m3[u]) dx += sp_fold_word(a, w0 + u, m3[u]);
     for (int64_t wd = w0 + 3; wd <= w1; wd++) {
-        const uint32_t m = ldcg(&a.sbits[wd]) & sp_word_mask(wd, r0, r1);
+        const uint32_t m = ldst<TK>(&a.sbits[wd]) & sp_word_mask(wd, r0, r1);
         if (m) dx += sp_fold_word(a, wd, m);
     }
     return dx;
@@ -362,18 +472,18 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
         // (the thread's first sample from registers after window 0: its z / G may already hold the
         // speculative commit)
         const bool rg = ws.win > 0 && li == tid;
-        const double zi = rg ? rr.zi : ldcg(&a.z[i]);
-        const double cg = rg ? rr.cg : ldcg(&a.coef[i]).x;
+        const double zi = rg ? rr.zi : ldst<TK>(&a.z[i]);
+        const double cg = rg ? rr.cg : ldst<TK>(&a.coef[i]).x;
         const int yi = rg ? rr.yi : a.y[i];
         double dx;
         if (ws.win == 0) {
-            const int64_t r0 = __ldg(&a.row_ptr[i]), r1 = __ldg(&a.row_ptr[i + 1]);
+            const int64_t r0 = ldro<TK>(&a.row_ptr[i]), r1 = ldro<TK>(&a.row_ptr[i + 1]);
             dx = sp_fold(a, r0, r1);
             if (di.any) {   // full columns, from CSC in bundle order (then the records)
                 const int64_t li2 = i - sm.row_base;
                 dx = (nT <= TSM ? sm.dxd[li2] : sp_dense_dx(a.flist, a.dk, a.colinfo, a.val, sm.fd, sm.fcp, di.f_lo, di.nf, k0, i)) + dx;
             }
-            a.dxg[i] = dx;
+            stst<TK>(&a.dxg[i], dx);
             if (li == tid) {
                 rr.i = i;
                 rr.yi = yi;
@@ -385,7 +495,7 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
                 rr.cg = cg;
             }
         } else {
-            dx = li == tid ? rr.dx : ldcg(&a.dxg[i]);
+            dx = li == tid ? rr.dx : ldst<TK>(&a.dxg[i]);
         }
         double al = alpha0;
 #pragma unroll
@@ -446,8 +556,8 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
         if (rr.i >= 0) {
             const int32_t i = rr.i;
             const double zn = rr.zi + alpha_s * rr.dx;
-            a.z[i] = zn;
-            a.coef[i] = coef_next(LOSS, make_double2(rr.cg, 2.0), zn, alpha_s * rr.dx, rr.yi);
+            stst<TK>(&a.z[i], zn);
+            stst<TK>(&a.coef[i], coef_next(LOSS, make_double2(rr.cg, 2.0), zn, alpha_s * rr.dx, rr.yi));
             sp_clear_own_slots(a, rr.r0, rr.r1);
         }
         for (int64_t wi = wb + tid; wi < we; wi += SNT) a.bits[wi] = 0u;
@@ -615,15 +725,15 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
                         sl[e] = 0;
                         xv[e] = 0.f;
                         if (e < len) {
-                            ri[e] = __ldg(&a.row_idx[p0 + e]);
-                            sl[e] = __ldg(&a.cslot[p0 + e]);
-                            xv[e] = __ldg(&a.val[p0 + e]);
+                            ri[e] = ldro<SK>(&a.row_idx[p0 + e]);
+                            sl[e] = ldro<SK>(&a.cslot[p0 + e]);
+                            xv[e] = ldro<SK>(&a.val[p0 + e]);
                         }
                     }
                     const double wj = ldcg(&a.w[j]);
                     double2 cf[SP_SHORT];
 #pragma unroll
-                    for (int e = 0; e < SP_SHORT; e++) cf[e] = e < len ? ldcg(&a.coef[ri[e]]) : make_double2(0.0, 0.0);
+                    for (int e = 0; e < SP_SHORT; e++) cf[e] = e < len ? ldst<TK>(&a.coef[ri[e]]) : make_double2(0.0, 0.0);
                     double g = 0.0, h = 0.0;
 #pragma unroll
                     for (int e = 0; e < SP_SHORT; e++) {
@@ -665,7 +775,15 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
             }
         }
         __syncthreads();
+        if (ctal && tid == 0) ctal[9] += clock64() - tstep;   // profiling mode 2: lane sweep done (all warps)
         for (int q = warp; q < min(sm.nmq, SP_MQ); q += SNW) sp_medium_column(a, sm.mq[q], sm.mqk[q], lane);
+        if (ctal) {   // profiling mode 2: medium columns done; the CTA's medium-column count
+            __syncthreads();
+            if (tid == 0) {
+                ctal[10] += clock64() - tstep;
+                ctal[12] += sm.nmq;
+            }
+        }
         SP_MARK(8);
 
         // ---------------- phase A, heavy columns: one chunk per CTA at a time (A1) ------------------
@@ -755,6 +873,10 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
             }
         }
         SP_MARK(9);
+        if (ctal) {   // profiling mode 2: heavy chunks reduced (A1)
+            __syncthreads();
+            if (tid == 0) ctal[11] += clock64() - tstep;
+        }
         // ---------------- phase A, heavy columns: records once d_j is published (A2) --------------
         if (heavy_cta) {
             for (int64_t q = G - 1 - c; q < NCH; q += GH) {
@@ -837,10 +959,10 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
             unsigned cntb = 0;
 #pragma unroll
             for (int r = 0; r < WREG; r++) {
-                wv[r] = (w0 + r < w1) ? ldcg(&a.bits[w0 + r]) : 0u;
+                wv[r] = (w0 + r < w1) ? ldst<TK>(&a.bits[w0 + r]) : 0u;
                 cntb += __popc(wv[r]);
             }
-            for (int64_t wi = w0 + WREG; wi < w1; wi++) cntb += __popc(ldcg(&a.bits[wi]));
+            for (int64_t wi = w0 + WREG; wi < w1; wi++) cntb += __popc(ldst<TK>(&a.bits[wi]));
             unsigned incl = 0;
             const unsigned lemask = 0xffffffffu >> (31 - lane);
 #pragma unroll
@@ -868,7 +990,7 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
                     }
                 }
                 for (int64_t wi = w0 + WREG; wi < w1; wi++) {
-                    uint32_t m = ldcg(&a.bits[wi]);
+                    uint32_t m = ldst<TK>(&a.bits[wi]);
                     while (m) {
                         const int b = __ffs(m) - 1;
                         m &= m - 1;
@@ -974,8 +1096,8 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
             // correct a missed speculation from registers (alpha_acc = 0: the state before the step)
             if (!hit && rr.i >= 0) {
                 const double zn = rr.zi + alpha_acc * rr.dx;
-                a.z[rr.i] = zn;
-                a.coef[rr.i] = coef_next(LOSS, make_double2(rr.cg, 2.0), zn, alpha_acc * rr.dx, rr.yi);
+                stst<TK>(&a.z[rr.i], zn);
+                stst<TK>(&a.coef[rr.i], coef_next(LOSS, make_double2(rr.cg, 2.0), zn, alpha_acc * rr.dx, rr.yi));
             }
             if (a.debug && rr.i >= 0) {
                 a.dbg_dx[rr.i] = rr.dx;
@@ -991,9 +1113,9 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
                 const int32_t i = rr.i;
                 if (qacc >= 0) {
                     const double zn = rr.zi + alpha_acc * rr.dx;
-                    a.z[i] = zn;
-                    const double2 cfo = LOSS == LOSS_SQ ? ldcg(&a.coef[i]) : make_double2(0.0, 0.0);
-                    a.coef[i] = coef_next(LOSS, cfo, zn, alpha_acc * rr.dx, rr.yi);
+                    stst<TK>(&a.z[i], zn);
+                    const double2 cfo = LOSS == LOSS_SQ ? ldst<TK>(&a.coef[i]) : make_double2(0.0, 0.0);
+                    stst<TK>(&a.coef[i], coef_next(LOSS, cfo, zn, alpha_acc * rr.dx, rr.yi));
                 }
                 if (rr.r1 > rr.r0)
                     for (int64_t wd = rr.r0 >> 5; wd <= ((rr.r1 - 1) >> 5); wd++) a.sbits[wd] = 0u;
@@ -1020,13 +1142,13 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
                     ra[e] = rb[e] = 0;
                     yv[e] = 1;
                     if (ii[e] >= 0) {
-                        dxv[e] = ldcg(&a.dxg[ii[e]]);
-                        ra[e] = __ldg(&a.row_ptr[ii[e]]);
-                        rb[e] = __ldg(&a.row_ptr[ii[e] + 1]);
+                        dxv[e] = ldst<TK>(&a.dxg[ii[e]]);
+                        ra[e] = ldro<TK>(&a.row_ptr[ii[e]]);
+                        rb[e] = ldro<TK>(&a.row_ptr[ii[e] + 1]);
                         if (qacc >= 0) {
-                            zv[e] = ldcg(&a.z[ii[e]]);
+                            zv[e] = ldst<TK>(&a.z[ii[e]]);
                             yv[e] = (int)a.y[ii[e]];
-                            if (LOSS == LOSS_SQ) cfo[e] = ldcg(&a.coef[ii[e]]);
+                            if (LOSS == LOSS_SQ) cfo[e] = ldst<TK>(&a.coef[ii[e]]);
                         }
                     }
                 }
@@ -1036,8 +1158,8 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
                     if (i < 0) continue;
                     if (qacc >= 0) {
                         const double zn = zv[e] + alpha_acc * dxv[e];
-                        a.z[i] = zn;
-                        a.coef[i] = coef_next(LOSS, cfo[e], zn, alpha_acc * dxv[e], yv[e]);
+                        stst<TK>(&a.z[i], zn);
+                        stst<TK>(&a.coef[i], coef_next(LOSS, cfo[e], zn, alpha_acc * dxv[e], yv[e]));
                     }
                     if (rb[e] > ra[e])
                         for (int64_t wd = ra[e] >> 5; wd <= ((rb[e] - 1) >> 5); wd++) a.sbits[wd] = 0u;

@@ -43,6 +43,11 @@ for k, name in ((0, "A_us"), (3, "C1_us"), (1, "C1+fold+LS_us")):
                  "argmax": int(v.argmax())}
 out["touched_per_cta"] = {"median": float(np.median(tl[:G, 2] / steps)), "max": float((tl[:G, 2] / steps).max())}
 out["A_us_by_cta"] = [round(x, 2) for x in us[:, 0]]
+# per-CTA points of phase A (cycles since the step began, mean per step): lane sweep done, medium
+# columns done, heavy chunks reduced; medium columns per step
+for k, name in ((9, "lane_done_us_by_cta"), (10, "medium_done_us_by_cta"), (11, "A1_done_us_by_cta")):
+    out[name] = [round(x, 2) for x in us[:, k]]
+out["medium_cols_by_cta"] = [round(x, 2) for x in tl[:G, 12] / steps]
 # thread 0 of each light CTA, its lane columns: cycles until the column descriptor, the rows, the
 # gathered factors are in registers, and the emits issued (per lane column it handled)
 lc = tl[:G, 8]
