@@ -142,6 +142,15 @@ __device__ __forceinline__ void red_or(uint32_t *p, uint32_t v)
     asm volatile("red.global.or.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(l2pol<K>()) : "memory");
 }
 constexpr int SK = PCDN_L2_STREAM, TK = PCDN_L2_STATE, RK = PCDN_L2_REC;
+// L2 prefetch (evict_last) of the next step's column descriptors and bundle positions after the
+// first barrier (1 = on).  Config 5 LR (profiles/r2c/l2pf_*): P = 4096 20.65 -> 20.54 us per step,
+// P = 10^5 80.5 -> 80.8; prefetching each light lane's next column rows / slots / values / w_j as
+// well (between the decision barrier's arrive and wait) measured 20.77 / 82.0.
+#ifndef PCDN_SP_L2PF
+#define PCDN_SP_L2PF 1
+#endif
+__device__ __forceinline__ void pf_l2_last(const void *p) { asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p)); }
+
 
 // Profiling instrumentation (phase cycles of CTA 0 for pcdn_set_profile(ctx, 1); per-CTA phase
 // sums for mode 2) is compiled in only with -DPCDN_PROFILE=1 (pcdn_kernels.cuh): even as untaken
@@ -710,6 +719,18 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
                 const int64_t kb = k0 + ch * cw;
                 if (kb >= k1) break;
                 const int64_t kk = kb + lane;
+                // profiling mode 2, thread 0 of the CTA: cycles from the start of its lane column until
+                // the descriptor, the rows / w_j, the gathered factors have arrived and the emits are
+                // issued (slots 4-7, cumulative; slot 8 counts its lane columns).  The volatile
+                // shared-memory write of a loaded value stalls until the load has returned.
+                const long long tq0 = (ctal && tid == 0) ? clock64() : 0;
+#define SP_PROBE(slot, dep)                                                       \
+    do {                                                                          \
+        if (ctal && tid == 0) {                                                   \
+            *reinterpret_cast<volatile long long *>(&sm.cprof[15]) = (long long)(dep); \
+            ctal[slot] += clock64() - tq0;                                        \
+        }                                                                         \
+    } while (0)
                 const int4 ci = (lane < cw && kk < k1) ? __ldg(&a.colinfo[kk]) : make_int4(0, -1, 0, 0);
                 const int len = ci.y;
                 PCDN_CHECK(len < 0 || (ci.x >= 0 && ci.x < a.n && colinfo_p0(ci) + len <= a.col_ptr[a.n]));
@@ -731,9 +752,12 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
                         }
                     }
                     const double wj = ldcg(&a.w[j]);
+                    SP_PROBE(4, len);
+                    SP_PROBE(5, ri[0] + (long long)__float_as_int(xv[0]) + (long long)sl[0] + __double_as_longlong(wj));
                     double2 cf[SP_SHORT];
 #pragma unroll
                     for (int e = 0; e < SP_SHORT; e++) cf[e] = e < len ? ldst<TK>(&a.coef[ri[e]]) : make_double2(0.0, 0.0);
+                    SP_PROBE(6, __double_as_longlong(cf[0].x) + __double_as_longlong(cf[len > 1 ? 1 : 0].y));
                     double g = 0.0, h = 0.0;
 #pragma unroll
                     for (int e = 0; e < SP_SHORT; e++) {
@@ -750,7 +774,10 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
                         for (int e = 0; e < SP_SHORT; e++)
                             if (e < len) sp_emit(a, ri[e], sl[e], r.d * (double)xv[e]);
                     }
+                    SP_PROBE(7, __double_as_longlong(r.d));
+                    if (ctal && tid == 0) ctal[8] += 1;
                 }
+#undef SP_PROBE
                 // medium columns go to the CTA's queue (a warp each below), so that no warp reduces
                 // two of them one after the other; beyond the queue the warp takes them itself
                 unsigned med = __ballot_sync(0xffffffffu, len > SP_SHORT && len <= a.heavy_len);
@@ -908,6 +935,13 @@ __global__ void __launch_bounds__(SNT, 1) k_step_sparse(StepArgs a)
         if (ctal && tid == 0) tstep = clock64();
         // the next step's plan (read after this step's decision)
         if (tid == SNT - 1 && k1 < a.ntot) sp_plan(a, k1, min(k1 + a.P, a.ntot), &sm.plan[(t + 1) & 1]);
+        if (PCDN_SP_L2PF && k1 < a.ntot) {   // the next step's descriptors and positions into L2
+            const int64_t n1 = min(k1 + a.P, a.ntot);
+            const int64_t gt = (int64_t)c * SNT + tid, lines = ((n1 - k1) * 16 + 127) / 128;
+            if (gt < lines) pf_l2_last(reinterpret_cast<const char *>(&a.colinfo[k1]) + 128 * gt);
+            else if (gt - lines < ((n1 - k1) * 4 + 127) / 128)
+                pf_l2_last(reinterpret_cast<const char *>(&a.order[k1]) + 128 * (gt - lines));
+        }
 
         const bool fullP = Pt == a.P;
         const int64_t pb0 = k0 + (fullP ? pbs0 : (int64_t)c * Pt / G);

@@ -22,6 +22,7 @@ timeout 900 python scripts/probe_config.py 5 --P 4096,29500,100000,1000000 --mod
 timeout 900 python scripts/probe_config.py 5 --loss 1 --P 4096,100000,1000000 --modes 2 --outer 1 > $OUT/pext_cfg5_svm.jsonl 2>&1
 timeout 1200 python scripts/p_sweep_cfg3.py 1,64,1024,8192 --oracle-p1 > $OUT/psweep_cfg3.jsonl 2>&1; echo "cfg3 sweep rc=$?"
 PCDN_LIB=paper_1306_4080_b200/libpcdn_prof.so timeout 900 python scripts/probe_config.py 5 --P 4096,100000 --modes 2 --outer 1 --profile > $OUT/phases_cfg5.jsonl 2>&1
+PCDN_LIB=paper_1306_4080_b200/libpcdn_prof.so timeout 600 python scripts/cta_profile.py 5 > $OUT/cta_cfg5.json 2>/dev/null
 ARGS="--steps 1 --warmup 0 --no-cpu-baseline --no-e2e"
 timeout 600 python bench.py $ARGS > $OUT/plain.json 2>&1; echo "plain rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
