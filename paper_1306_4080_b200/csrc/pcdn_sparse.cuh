@@ -149,6 +149,13 @@ constexpr int SK = PCDN_L2_STREAM, TK = PCDN_L2_STATE, RK = PCDN_L2_REC;
 #ifndef PCDN_SP_L2PF
 #define PCDN_SP_L2PF 1
 #endif
+// the window's decision taken by every thread from the totals (1) or by one thread and broadcast
+// through shared memory behind two more CTA barriers (0).  Config 5 LR P = 4096
+// (profiles/r2c/ab_c1/b_*): 20.55 -> 20.36 us per step.  (Deferring the line-search share's w_j
+// load and the next step's plan to after the touched-set scan measured 20.63.)
+#ifndef PCDN_SP_DECALL
+#define PCDN_SP_DECALL 1
+#endif
 __device__ __forceinline__ void pf_l2_last(const void *p) { asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p)); }
 
 
@@ -600,6 +607,41 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
         tprev = now;
     }
     sp_grid_totals<W>(part, G, sm.red, sm.tot, sm.pv, tid, lane, warp);
+#if PCDN_SP_DECALL
+    // every thread takes the decision itself from the totals (the same bits in every thread of
+    // every CTA): no broadcast through shared memory and no further CTA barrier (sm.tot is next
+    // written after the next window's first __syncthreads)
+    {
+        const double Dl = sm.tot[LY::DELTA];
+        int qa = -1, badl = 0;
+        double al = alpha0, la = 0.0, ra = 0.0, alpha_a = 0.0;
+#pragma unroll
+        for (int q = 0; q < NQ; q++) {
+            if (qa < 0 && !badl) {
+                const double lhs = sm.tot[NQ + q] + a.c * sm.tot[q];
+                const double rhs = a.sigma * al * Dl;
+                if (!isfinite(lhs) || !isfinite(Dl)) {
+                    badl = 1;
+                } else if (lhs <= rhs) {
+                    qa = ws.q0 + q;
+                    alpha_a = al;
+                    la = lhs;
+                    ra = rhs;
+                }
+                al *= a.beta;
+            }
+        }
+        ws.qacc = qa;
+        ws.bad = badl;
+        ws.alpha = alpha_a;
+        ws.lhs = la;
+        ws.rhs = ra;
+        ws.Delta = Dl;
+        ws.nT_tot = sm.tot[LY::NTOUCH];
+        ws.nospec = sm.tot[LY::NOSPEC] != 0.0;
+        ws.win++;
+    }
+#else
     if (warp == 0 && lane == 0) {
         const double Dl = sm.tot[LY::DELTA];
         int qa = -1, badl = 0;
@@ -640,6 +682,7 @@ __device__ __forceinline__ void sp_window(const StepArgs &a, SpSmem &sm, Sync &s
     ws.nospec = sm.dec_nospec;
     ws.win++;
     __syncthreads();   // sm.dec_* / sm.red / sm.tot are reused by the next window
+#endif
     if (prof) {
         const long long now = clock64();
         sm.pacc[5] += now - tprev;
