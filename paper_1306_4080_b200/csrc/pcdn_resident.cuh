@@ -39,6 +39,13 @@
 
 #include "pcdn_kernels.cuh"
 
+// the window's decision taken by every warp from the partial rows (1), or by warp 0 and broadcast
+// behind a CTA barrier (0).  profiles/r2c/ab_res: config 2 6.86 -> 6.75 us per step, config 3
+// (P = 1024) 19.63 -> 19.23.  (The same change in the dense kernel measured 17.17 -> 17.21: not taken.)
+#ifndef PCDN_RES_DECALL
+#define PCDN_RES_DECALL 1
+#endif
+
 namespace pcdn {
 
 namespace cgx = cooperative_groups;
@@ -808,6 +815,54 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
             }
         }
     };
+#if PCDN_RES_DECALL
+    pr.mark(fx, 4);
+    // every warp: the G partial rows (local now), the same fixed-order sums and the same decision
+    // (identical in every warp of every CTA: no broadcast, no CTA barrier), then the gather of the
+    // next step's first staged column (after the decision: its shared-memory reads must not queue
+    // behind remote loads).  part_in[buf] is refilled only after every CTA has received this CTA's
+    // next row, which its warps contribute to after this point.
+    {
+        double tot = 0.0;
+        if (lane < W) {
+            double v[16];
+#pragma unroll
+            for (int r = 0; r < 16; r++) v[r] = r < R.G ? fx.part_in[buf][r][lane] : 0.0;
+#pragma unroll
+            for (int r = 0; r < 16; r++) tot += v[r];
+        }
+        const double Dl = __shfl_sync(0xffffffffu, tot, LY::DELTA);
+        const double nTt = __shfl_sync(0xffffffffu, tot, LY::NTOUCH);
+        int qa = -1, badl = 0;
+        double al = alpha0, la = 0.0, ra = 0.0, alpha_a = 0.0;
+#pragma unroll
+        for (int q = 0; q < NQ; q++) {
+            const double Ls = __shfl_sync(0xffffffffu, tot, q);
+            const double L1 = __shfl_sync(0xffffffffu, tot, NQ + q);
+            if (qa < 0 && !badl) {
+                const double lhs = L1 + a.c * Ls;
+                const double rhs = a.sigma * al * Dl;
+                if (!isfinite(lhs) || (!a.scdn && !isfinite(Dl))) {
+                    badl = 1;
+                } else if (a.scdn || lhs <= rhs) {   // SCDN takes the combined step as it is (Z27)
+                    qa = ws.q0 + q;
+                    alpha_a = al;
+                    la = lhs;
+                    ra = rhs;
+                }
+                al *= a.beta;
+            }
+        }
+        ws.qacc = qa;
+        ws.bad = badl;
+        ws.alpha = alpha_a;
+        ws.lhs = la;
+        ws.rhs = ra;
+        ws.Delta = Dl;
+        ws.nT_tot = nTt;
+    }
+    prefetch();
+#else
     if (warp != 0) prefetch();
     pr.mark(fx, 4);
     // warp 0: the G partial rows (local now), fixed-order tree, decision; broadcast in the CTA
@@ -864,6 +919,7 @@ __device__ __forceinline__ void res_window(const StepArgs &a, const ResCtx &R, W
     ws.rhs = fx.dec_rhs[buf];
     ws.Delta = fx.dec_Delta[buf];
     ws.nT_tot = fx.dec_nT[buf];
+#endif
     if (ws.win == 0) RTL(R, 12);
     ws.win++;
     pr.mark(fx, 5);
