@@ -421,7 +421,9 @@ __device__ __noinline__ double sp_dense_dx(const int32_t *__restrict__ flist, co
 // Totals of the G partial rows part[c2][0..W) in a fixed order, into tot[0..W) (valid for every
 // thread after the call).  Up to SP_GT_ROWS CTAs: every thread loads its share of the G x W values
 // in one batch (a single L2 round trip), then warp q sums slot q over the rows (lane-strided, a
-// fixed xor tree).  Beyond: warp w sums rows w, w + SNW, ... and warp 0 the warp sums.
+// fixed xor tree).  Beyond: warp w sums rows w, w + SNW, ... and warp 0 the warp sums.  (Warp q
+// loading slot q of every row itself, without the shared-memory staging and its CTA barrier,
+// measured slower: config 5 LR P = 4096 20.37 -> 21.10 us per step, profiles/r2c/ab_gt.)
 template <int W>
 __device__ __forceinline__ void sp_grid_totals(const double *part, int G, double (*red)[32], double *tot, double *pv,
                                                int tid, int lane, int warp)
