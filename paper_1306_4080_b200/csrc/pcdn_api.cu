@@ -395,7 +395,7 @@ int reset_status(pcdn_ctx *ctx)
 
 // Launch the persistent step kernel over `nsteps` bundles of the positions in ctx->order.
 int choose_mode(const pcdn_ctx *ctx, int64_t P);
-int heavy_for_mode(const pcdn_ctx *ctx, int mode);
+int heavy_for_mode(const pcdn_ctx *ctx, int mode, int64_t P);
 
 // the sparse HBM-state kernel (pcdn_sparse.cuh): one cluster (mode 1) or the cooperative grid (mode 2)
 const void *sparse_kernel(bool cluster, int loss)
@@ -617,10 +617,22 @@ int launch_steps(pcdn_ctx *ctx, int buf, int64_t ntot, int64_t P, int64_t nsteps
 // about this many nonzeros over several warps; the legacy grid kernel (mode 5) splits them
 // nnz-balanced over every warp of the launch and reduces shorter ones of up to CTA_LEN inside one
 // CTA; the cluster-resident kernel splits everything above a warp's 128.
-int heavy_for_mode(const pcdn_ctx *ctx, int mode)
+int heavy_for_mode(const pcdn_ctx *ctx, int mode, int64_t P)
 {
     if (ctx->heavy_len > 0) return ctx->heavy_len;
-    return (mode == 1 || mode == 2) ? SP_CH : mode == 5 ? CTA_LEN : MED_LEN;
+    if (mode == 2) {
+        // Sparse grid kernel: when a step gives a CTA only a few columns, most of its 12 warps have
+        // none of their own, and a column of 65-256 nonzeros is reduced sooner as CTA chunks (all
+        // warps on one) than by one warp; with more work per CTA the chunks' CTA barriers cost more
+        // than they save.  B200 (profiles/r2d/heavy_len/), us per step at heavy_len 64 / 128 / 256:
+        // config 5 P = 4096 (111 bundle nonzeros per CTA) 19.43 / 19.68 / 20.38, P = 8192 22.65 / - /
+        // 23.82, P = 29,500 39.1 / 35.3 / 34.9, P = 1e5 94.4 / 83.6 / 80.9; config 3 P = 8192 (498
+        // per CTA, heavier columns) 33.6 / - / 32.0; one cluster (mode 1) P = 1024: 17.75 / - / 17.34.
+        const double per_cta = (double)ctx->nnz * (double)P / (double)ctx->n / (double)(ctx->G > 0 ? ctx->G : 1);
+        return per_cta <= 256.0 ? 64 : SP_CH;
+    }
+    if (mode == 1) return SP_CH;
+    return mode == 5 ? CTA_LEN : MED_LEN;
 }
 
 int choose_mode(const pcdn_ctx *ctx, int64_t P)
@@ -1164,7 +1176,7 @@ int pcdn_bundle_step(pcdn_ctx *ctx, const int32_t *bundle, int64_t P, pcdn_step_
     if ((rc = reset_status(ctx))) return rc;
     CU(cudaMemsetAsync(ctx->at<int64_t>(L.counters), 0, sizeof(int64_t) * 8, ctx->stream));
     const Lists &S = L.ls[0];
-    ctx->heavy_eff = heavy_for_mode(ctx, choose_mode(ctx, P));
+    ctx->heavy_eff = heavy_for_mode(ctx, choose_mode(ctx, P), P);
     k_bundle_prep<<<grid1d(P), 256, 0, ctx->stream>>>(bundle, P, ctx->n, ctx->s, ctx->col_ptr, ctx->heavy_eff,
                                                       ctx->at<int32_t>(S.order), ctx->at<int32_t>(S.flag),
                                                       ctx->at<int32_t>(S.fflag),
@@ -1249,7 +1261,7 @@ int pcdn_solve(pcdn_ctx *ctx, int64_t P, double eps, uint64_t seed, int32_t max_
     // the cluster-resident step kernel occupies one cluster of SMs: the next outer iteration's
     // partition and lists are then built concurrently on the side stream (double-buffered sets)
     const int smode = choose_mode(ctx, P);
-    ctx->heavy_eff = heavy_for_mode(ctx, smode);
+    ctx->heavy_eff = heavy_for_mode(ctx, smode, P);
     // the dense kernel needs only the permutation: k_obj computes it (no launch of its own)
     const bool overlap = ctx->side != nullptr && smode == 3;
     const bool lists = smode != 4;
