@@ -624,15 +624,18 @@ int heavy_for_mode(const pcdn_ctx *ctx, int mode, int64_t P)
         // Sparse grid kernel: when a step gives a CTA only a few columns, most of its 12 warps have
         // none of their own, and a column of 65-256 nonzeros is reduced sooner as CTA chunks (all
         // warps on one) than by one warp; with more work per CTA the chunks' CTA barriers cost more
-        // than they save.  B200 (profiles/r2d/heavy_len/), us per step at heavy_len 64 / 128 / 256:
-        // config 5 P = 4096 (111 bundle nonzeros per CTA) 19.43 / 19.68 / 20.38, P = 8192 22.65 / - /
-        // 23.82, P = 29,500 39.1 / 35.3 / 34.9, P = 1e5 94.4 / 83.6 / 80.9; config 3 P = 8192 (498
-        // per CTA, heavier columns) 33.6 / - / 32.0; one cluster (mode 1) P = 1024: 17.75 / - / 17.34.
+        // than they save.  B200 (profiles/r2d/heavy_len/, profiles/r2e/knobs/), us per step at
+        // heavy_len 64 / 128 / 256: config 5 P = 4096 (111 bundle nonzeros per CTA) 19.43 / 19.68 /
+        // 20.38, P = 8192 (221) 22.65 / - / 23.82, P = 16,384 (443) - / 27.45 / 28.48, P = 29,500 (797)
+        // 39.1 / 35.3 / 34.9, P = 1e5 94.4 / 83.6 / 80.9; config 3 P = 8192 (498) 33.9 / 31.05 / 32.4;
+        // one cluster (mode 1), config 5 P = 1024: 17.75 / - / 17.34.
         const double per_cta = (double)ctx->nnz * (double)P / (double)ctx->n / (double)(ctx->G > 0 ? ctx->G : 1);
-        return per_cta <= 256.0 ? 64 : SP_CH;
+        return per_cta <= 256.0 ? 64 : per_cta <= 640.0 ? 128 : SP_CH;
     }
     if (mode == 1) return SP_CH;
-    return mode == 5 ? CTA_LEN : MED_LEN;
+    // cluster-resident kernel: config 3 (P = 1024) 18.98 / 18.88 / 19.34 / 20.75 us per step at 64 / 96 /
+    // 128 / 192; config 2 has no column that long (6.75 us at any setting)
+    return mode == 5 ? CTA_LEN : mode == 3 ? 96 : MED_LEN;
 }
 
 int choose_mode(const pcdn_ctx *ctx, int64_t P)
