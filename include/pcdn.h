@@ -168,9 +168,9 @@ int pcdn_set_debug(pcdn_ctx *ctx, int on);
  * 4 dense row-block kernel (every column full).
  * heavy_len: column length above which a column leaves the one-warp path (0 = the library's
  * choice per mode and bundle size).  Modes 1-2 (the sparse kernel): longer columns are reduced by
- * whole CTAs in chunks of 12 * heavy_len nonzeros; default 256, and 64 in mode 2 when a step
- * brings a CTA at most 256 bundle nonzeros (nnz * P / n / CTAs).  Mode 3: split
- * over the cluster's warps above 128.  Mode 5 (the round-1 grid kernel): 2048, columns of
+ * whole CTAs in chunks of 12 * heavy_len nonzeros; default 256, and in mode 2 64 / 128 when a
+ * step brings a CTA at most 256 / 640 bundle nonzeros (nnz * P / n / CTAs).  Mode 3:
+ * split over the cluster's warps above 96.  Mode 5 (the round-1 grid kernel): 2048, columns of
  * 129..2048 nonzeros reduced inside one CTA, longer ones nnz-balanced over the launch's warps. */
 int pcdn_set_launch(pcdn_ctx *ctx, int mode, int ctas, int heavy_len);
 
